@@ -1,0 +1,210 @@
+/*
+ * vrs.h -- C ABI of libvrs: batched, relationally filtered, exact k-NN search
+ * on NVIDIA B200 (sm_100a).
+ *
+ * The operation is the paper's selection with a query vector, a similarity
+ * predicate and a relational predicate, evaluated predicate-first:
+ *
+ *   PAPER.md L285-L288 (Sec. 3):  sigma_{eps,v,theta_R}(R) <=> sigma_eps(v x sigma_{theta_R}(R))
+ *
+ * for a whole batch of query vectors at once ("batching both
+ * the data and query vectors"), one relational predicate per batch
+ * (late materialization), and eps = "the k best under a
+ * metric" (PAPER.md L350 top-k; result contract SPEC.md L141-L147).
+ *
+ * Conventions shared by every call
+ *  - Device pointers are CUDA device (or managed) memory of the current
+ *    device; host pointers are rejected with VRS_EINVAL unless the call says
+ *    otherwise.  Integers are little-endian, arrays are dense row-major.
+ *  - Every call that takes `cuda_stream` (a cudaStream_t; NULL = legacy
+ *    default stream) validates its arguments synchronously, enqueues all
+ *    device work on that stream and returns without synchronising.  Device
+ *    faults surface as VRS_ECUDA on a later call.
+ *  - On any error nothing is enqueued and vrs_last_error() describes it.
+ *  - Metrics (reading R1 in DESIGN.md):
+ *      VRS_L2      squared Euclidean distance sum_t (q_t - x_t)^2, best = smallest
+ *      VRS_IP      inner product sum_t q_t x_t, best = largest
+ *      VRS_COSINE  cosine SIMILARITY <q,x>/(|q||x|), best = largest
+ *                  ("dot product of two normalized input matrices")
+ *  - Results: row j of ids/dists holds the m = min(k, N_sel) best qualifying
+ *    rows of query j, best first, ties broken by the lower global row id
+ *    (SPEC.md L145, L177); entries m..k-1 are padding id = -1 and
+ *    dist = +inf (L2) or -inf (IP, COSINE).  ids are GLOBAL: row_offset + local row.
+ *    dists are computed exactly in fp32 from the fp32 inputs (the tensor-core
+ *    selection pass is re-scored).
+ */
+#ifndef VRS_H
+#define VRS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VRS_API __attribute__((visibility("default")))
+#else
+#define VRS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRS_ABI_VERSION 1
+/* Largest k vrs_search accepts (the selection pass over-fetches k + 16). */
+#define VRS_K_MAX 240
+/* Largest number of AND-ed clauses in one predicate. */
+#define VRS_MAX_CLAUSES 8
+
+typedef enum {
+  VRS_OK = 0,
+  VRS_EINVAL = 1,        /* bad argument: sizes, null / host pointer, enum value, d mismatch */
+  VRS_ENOTFOUND = 2,     /* a clause names an attribute index >= n_attrs */
+  VRS_EDEGENERATE = 3,   /* VRS_COSINE over a corpus holding a zero-norm row */
+  VRS_ENOMEM = 4,        /* the allocator returned NULL */
+  VRS_ECUDA = 5,         /* a CUDA runtime error (including asynchronous faults) */
+  VRS_ECOMM = 6,         /* reserved for collective errors raised by callers of vrs_merge */
+  VRS_EUNSUPPORTED = 7   /* k > VRS_K_MAX, too many clauses, or a device that is not sm_100 */
+} vrs_status;
+
+typedef enum { VRS_L2 = 0, VRS_IP = 1, VRS_COSINE = 2 } vrs_metric;
+
+typedef enum { VRS_ATTR_I32 = 0, VRS_ATTR_U8 = 1 } vrs_attr_type;
+
+/* One relational column: `data` is a device array of n entries (int32 or uint8). */
+typedef struct {
+  vrs_attr_type type;
+  const void *data;
+} vrs_attr;
+
+/* One clause of theta_R: lo <= attr[i] <= hi, compared as exact integers
+ * (uint8 as unsigned).  lo > hi selects nothing.  (reading R4;
+ * SPEC.md L48-L52 LT/LE/GT/GE/BETWEEN all map to one closed interval.) */
+typedef struct {
+  int32_t attr;
+  int64_t lo;
+  int64_t hi;
+} vrs_clause;
+
+/* theta_R = AND of the clauses; n_clauses == 0 (clauses may be NULL) selects every row. */
+typedef struct {
+  int32_t n_clauses;
+  const vrs_clause *clauses;
+} vrs_predicate;
+
+/* Optional stream-ordered allocator for the library's own device memory
+ * (norms at load, per-call scratch).  NULL => cudaMallocAsync / cudaFreeAsync. */
+typedef struct {
+  void *(*alloc)(size_t bytes, void *cuda_stream, void *ctx);
+  void (*free)(void *ptr, void *cuda_stream, void *ctx);
+  void *ctx;
+} vrs_allocator;
+
+typedef struct vrs_index vrs_index;
+
+/*
+ * vrs_load -- build an index over one (shard of a) relation R (PAPER.md L269,
+ * "column-store layout that stores both vector and relational data").
+ *   vectors : device fp32 [n x d], row-major, BORROWED: must stay valid and
+ *             unmodified until vrs_free.  16-byte aligned rows (d % 4 == 0 and a
+ *             16-byte aligned base) enable the vectorised / TMA paths; other
+ *             layouts run on the scalar-load scan path.
+ *   attrs   : n_attrs relational columns (device, n entries each), BORROWED.
+ *   row_offset : global id of local row 0 (row sharding).
+ *   alloc   : optional allocator (copied; its ctx must outlive the index).
+ * Computes per-row |x|^2 and 1/|x| once (the norm terms of PAPER.md L305, L790)
+ * on `cuda_stream` and waits for them (load is not on the search path).
+ * Errors: EINVAL (n < 1, n >= 2^31, d < 1, n_attrs < 0, null / host pointers,
+ * bad attr type), ENOMEM, ECUDA, EUNSUPPORTED (device is not sm_100).
+ */
+VRS_API vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
+                    int64_t row_offset, const vrs_allocator *alloc, void *cuda_stream, vrs_index **out);
+
+/*
+ * vrs_search -- sigma_{eps,v,theta_R}(R) for a batch of q query vectors.
+ *   queries : device fp32 [q x d] row-major (d must equal the loaded d).
+ *   pred    : theta_R (NULL => every row).
+ *   k       : 1..VRS_K_MAX.
+ *   ids     : device int64 [q x k] (output), dists: device fp32 [q x k] (output).
+ * q == 0 is a successful no-op.  A zero-norm COSINE query yields an all-padding
+ * row (documented deviation from SPEC.md L95: detecting it would need a host sync).
+ * Errors: EINVAL, ENOTFOUND, EDEGENERATE, EUNSUPPORTED, ENOMEM, ECUDA.
+ */
+VRS_API vrs_status vrs_search(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
+                      int32_t k, vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream);
+
+/* Path control for tests and the bench (vrs_search uses VRS_PATH_AUTO). */
+typedef enum {
+  VRS_PATH_AUTO = 0,  /* dispatch on (q, d): scan for small batches, tensor cores above */
+  VRS_PATH_SCAN = 1,  /* per-tuple fp32 FFMA scan over the selection */
+  VRS_PATH_GEMM = 2   /* batched tcgen05 tensor-core formulation */
+} vrs_path;
+
+typedef enum {
+  VRS_ROWS_AUTO = 0,    /* selectivity-driven choice between the two below */
+  VRS_ROWS_GATHER = 1,  /* compact the selection, deliver only qualifying rows (late materialization) */
+  VRS_ROWS_MASKED = 2   /* stream full row tiles, unqualified rows masked out by the bitmap */
+} vrs_rows;
+
+typedef struct {
+  int32_t path;      /* vrs_path */
+  int32_t rows;      /* vrs_rows */
+  int32_t reserved[6];
+} vrs_search_options;
+
+/* vrs_search with explicit options (opts == NULL => defaults). */
+VRS_API vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
+                         int32_t k, vrs_metric metric, int64_t *ids, float *dists,
+                         const vrs_search_options *opts, void *cuda_stream);
+
+/*
+ * vrs_search_host -- end-to-end call on HOST buffers: copies the queries
+ * host->device, runs vrs_search_ex, copies ids/dists device->host, and
+ * synchronises `cuda_stream` before returning.  h_queries / h_ids / h_dists
+ * are host memory (pinned memory makes the copies asynchronous DMA).
+ */
+VRS_API vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,
+                           const vrs_predicate *pred, int32_t k, vrs_metric metric, int64_t *h_ids,
+                           float *h_dists, const vrs_search_options *opts, void *cuda_stream);
+
+/*
+ * vrs_select -- the relational step alone, sigma_{theta_R}(R):
+ *   bitmap : device uint32 [ceil(n/32)], word w bit b <-> local row 32w+b,
+ *            LSB first, bits past n zero (output).
+ *   count  : device int64 [1], the number of qualifying rows (output).
+ *   ids    : optional device int32 [n] (NULL allowed): ascending qualifying local row ids.
+ * Bit-exact by construction (integer work).  Errors: EINVAL, ENOTFOUND, ECUDA.
+ */
+VRS_API vrs_status vrs_select(vrs_index *ix, const vrs_predicate *pred, uint32_t *bitmap, int64_t *count, int32_t *ids,
+                      void *cuda_stream);
+
+/*
+ * vrs_merge -- final step of a row-sharded search (north_star (4)): the top-k
+ * of the union of n_parts candidate lists, each the vrs_search output of one
+ * shard (same q, k, metric), as gathered by an all-gather.
+ *   cand_ids   : device int64 [n_parts x q x k] (padding id = -1 ignored)
+ *   cand_dists : device fp32  [n_parts x q x k]
+ *   ids, dists : device [q x k] outputs, same ordering / tie / padding rules.
+ * Exact: top-k(A u B) = top-k(top-k(A) u top-k(B)) under the total order (dist, id).
+ */
+VRS_API vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n_parts, int64_t q, int32_t k,
+                     vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream);
+
+/* Release the index's own memory (borrowed vectors / attrs are untouched). NULL is a no-op. */
+VRS_API vrs_status vrs_free(vrs_index *ix);
+
+/* Thread-local description of the last failure on this thread; valid until the next vrs_* call. */
+VRS_API const char *vrs_last_error(void);
+
+/* Introspection for tests / bench: which path the last vrs_search_ex on this
+ * thread took (vrs_path value) and how many kernels it enqueued. */
+VRS_API int32_t vrs_last_path(void);
+VRS_API int32_t vrs_last_launches(void);
+
+/* Loaded index properties. */
+VRS_API int64_t vrs_index_rows(const vrs_index *ix);
+VRS_API int32_t vrs_index_dim(const vrs_index *ix);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VRS_H */

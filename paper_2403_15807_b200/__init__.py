@@ -1,0 +1,159 @@
+"""paper_2403_15807_b200 -- B200-native filtered exact top-k vector search.
+
+The hot path of the scan-based access path of Sanca & Ailamaki,
+"Efficient Data Access Paths for Mixed Vector-Relational Search"
+(arxiv 2403.15807): sigma_{eps,v,theta_R}(R) <=> sigma_eps(v x sigma_{theta_R}(R))
+ for a batch of queries, on hand-written sm_100a CUDA
+kernels behind the C ABI in include/vrs.h.  This package is a thin binding:
+torch supplies device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (ATTR_I32, ATTR_U8, COSINE, EXPORTS, IP, K_MAX, L2, PATH_AUTO, PATH_GEMM, PATH_SCAN,
+                   ROWS_AUTO, ROWS_GATHER, ROWS_MASKED, VrsError)
+
+__all__ = ["Index", "merge", "VrsError", "L2", "IP", "COSINE", "PATH_AUTO", "PATH_SCAN", "PATH_GEMM",
+           "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "K_MAX", "last_path", "last_launches", "library"]
+
+METRICS = {"l2": L2, "ip": IP, "cos": COSINE, "cosine": COSINE}
+
+
+def library():
+    return _lib.load_library()
+
+
+def _metric(m):
+    return METRICS[m.lower()] if isinstance(m, str) else int(m)
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _options(path, rows):
+    if path is None and rows is None:
+        return None
+    o = _lib.SearchOptions()
+    o.path = PATH_AUTO if path is None else int(path)
+    o.rows = ROWS_AUTO if rows is None else int(rows)
+    return o
+
+
+def last_path() -> int:
+    return int(library().vrs_last_path())
+
+
+def last_launches() -> int:
+    return int(library().vrs_last_launches())
+
+
+class Index:
+    """vrs_load over one (shard of a) relation: fp32 vectors [n, d] and
+    int32 / uint8 attribute columns, all CUDA tensors (borrowed, kept alive here)."""
+
+    def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None):
+        lib = library()
+        if vectors.dtype != torch.float32 or vectors.dim() != 2 or not vectors.is_contiguous():
+            raise ValueError("vectors must be a contiguous float32 [n, d] tensor")
+        self.vectors = vectors
+        self.attrs = [a.contiguous() for a in attrs]
+        carr = (_lib.Attr * max(len(self.attrs), 1))()
+        for i, a in enumerate(self.attrs):
+            if a.dtype == torch.int32:
+                carr[i].type = ATTR_I32
+            elif a.dtype == torch.uint8:
+                carr[i].type = ATTR_U8
+            else:
+                raise ValueError(f"attribute {i}: dtype {a.dtype} (int32 or uint8 expected)")
+            carr[i].data = a.data_ptr()
+        h = ctypes.c_void_p()
+        n, d = vectors.shape
+        st = lib.vrs_load(_ptr(vectors), n, d, carr, len(self.attrs), int(row_offset), None, _stream(stream),
+                          ctypes.byref(h))
+        _lib.check(st, "vrs_load")
+        self._h = h
+        self.n, self.d, self.row_offset = int(n), int(d), int(row_offset)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            library().vrs_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, queries: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
+               out=None, stream=None):
+        """-> (ids int64 [q, k], dists float32 [q, k]) on the device (async on `stream`)."""
+        lib = library()
+        q = queries.shape[0]
+        d = queries.shape[1] if queries.dim() == 2 else self.d
+        dev = self.vectors.device
+        if out is None:
+            ids = torch.empty((q, k), dtype=torch.int64, device=dev)
+            dists = torch.empty((q, k), dtype=torch.float32, device=dev)
+        else:
+            ids, dists = out
+        pr, keep = _lib.make_predicate(pred)
+        st = lib.vrs_search_ex(self._h, _ptr(queries) if q else None, q, d, ctypes.byref(pr), int(k),
+                               _metric(metric), _ptr(ids) if q else None, _ptr(dists) if q else None,
+                               _options(path, rows), _stream(stream))
+        _lib.check(st, "vrs_search")
+        return ids, dists
+
+    def search_host(self, queries_h: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
+                    out=None, stream=None):
+        """End-to-end call on host buffers (H2D + search + D2H inside libvrs; synchronous)."""
+        lib = library()
+        q, d = queries_h.shape
+        if out is None:
+            ids = torch.empty((q, k), dtype=torch.int64, pin_memory=True)
+            dists = torch.empty((q, k), dtype=torch.float32, pin_memory=True)
+        else:
+            ids, dists = out
+        pr, keep = _lib.make_predicate(pred)
+        st = lib.vrs_search_host(self._h, _ptr(queries_h), q, d, ctypes.byref(pr), int(k), _metric(metric),
+                                 _ptr(ids), _ptr(dists), _options(path, rows), _stream(stream))
+        _lib.check(st, "vrs_search_host")
+        return ids, dists
+
+    def select(self, pred=None, with_ids: bool = False, stream=None):
+        """-> (bitmap uint32-as-int32 [ceil(n/32)], count int64 [1], ids int32 [n] or None); device tensors."""
+        lib = library()
+        dev = self.vectors.device
+        words = (self.n + 31) // 32
+        bitmap = torch.empty(words, dtype=torch.int32, device=dev)
+        count = torch.empty(1, dtype=torch.int64, device=dev)
+        ids = torch.empty(self.n, dtype=torch.int32, device=dev) if with_ids else None
+        pr, keep = _lib.make_predicate(pred)
+        st = lib.vrs_select(self._h, ctypes.byref(pr), _ptr(bitmap), _ptr(count), _ptr(ids), _stream(stream))
+        _lib.check(st, "vrs_select")
+        return bitmap, count, ids
+
+
+def merge(cand_ids: torch.Tensor, cand_dists: torch.Tensor, k: int, metric="l2", stream=None):
+    """vrs_merge: cand_* [parts, q, k] device tensors -> (ids [q, k], dists [q, k])."""
+    lib = library()
+    parts, q, kk = cand_ids.shape
+    if kk != k:
+        raise ValueError("candidate lists must have k entries")
+    ids = torch.empty((q, k), dtype=torch.int64, device=cand_ids.device)
+    dists = torch.empty((q, k), dtype=torch.float32, device=cand_ids.device)
+    ci, cd = cand_ids.contiguous(), cand_dists.contiguous()
+    st = lib.vrs_merge(_ptr(ci), _ptr(cd), parts, q, int(k), _metric(metric), _ptr(ids), _ptr(dists),
+                       _stream(stream))
+    _lib.check(st, "vrs_merge")
+    return ids, dists

@@ -1,0 +1,283 @@
+// scan.cu -- K6' norms at load and K2' the per-tuple scan path with fused top-k.
+//
+// K2' realises the paper's per-tuple strategies for small query batches
+// (1:1 / 1:N / N:1, "Explicit SIMD" L535) over the
+// late-materialized selection (L319): the qualifying rows, addressed through
+// the compacted id list (or the identity when theta_R is empty), are streamed
+// HBM -> shared memory with 16-byte cp.async (LDGSTS) in a 3-stage per-warp
+// ring; each lane owns one row and accumulates exact fp32 FFMA dot products
+// against up to QG queries held in shared memory (read as broadcasts).  The
+// score matrix never leaves the SM: each 256-row block's ranking keys go to a
+// small shared buffer, warp j keeps query j's running top-k' (threshold in a
+// register, warp-ballot append of rows that beat it, warp-cooperative bitonic
+// merge when the append buffer fills).  One sorted list per (CTA, query) is
+// written out; finalize.cu merges the lists and re-scores exactly.
+//
+// Roofline: HBM.  Algorithmic bytes per selected row: 4*d (vector) + 4 (id)
+// + 8 (norm terms); per call + 4*d*q (queries) + 12*q*k (results).
+#include <float.h>
+
+#include "vrs_kernels.cuh"
+
+namespace vrs {
+
+// ------------------------------------------------------------------ K6' norms
+// |x|^2 and 1/|x| per row (fp32), computed once at vrs_load (PAPER.md L305,
+// L790 "then normalized"); zero_flag records a zero-norm row (COSINE degenerate).
+__global__ void norms_kernel(const float *__restrict__ X, int64_t n, int32_t d, float *__restrict__ nx2,
+                             float *__restrict__ inv_nx, int32_t *__restrict__ zero_flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const float *x = X + row * d;
+  float s = 0.f;
+  for (int t = lane; t < d; t += 32) s = fmaf(x[t], x[t], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    nx2[row] = s;
+    inv_nx[row] = s > 0.f ? 1.0f / sqrtf(s) : 0.f;
+    if (!(s > 0.f)) atomicOr(zero_flag, 1);
+  }
+}
+
+cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *zero_flag,
+                         cudaStream_t stream) {
+  const int warps = 8;
+  norms_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, stream>>>(X, n, d, nx2, inv_nx, zero_flag);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- K2' scan
+constexpr int kScWarps = 8;
+constexpr int kScThreads = kScWarps * 32;
+constexpr int kScRows = kScThreads;  // rows per block iteration (one per lane)
+constexpr int kScKC = 32;            // fp32 columns per stage
+constexpr int kScStages = 3;
+constexpr int kScPad = kScKC + 4;    // padded row stride in the stage (conflict-free LDS.128)
+
+
+__host__ __device__ constexpr size_t scan_smem_bytes(int QG, int KPE, int dpad) {
+  return (size_t)QG * dpad * 4                        // queries
+         + (size_t)kScWarps * kScStages * 32 * kScPad * 4  // row stages
+         + (size_t)2 * QG * kScRows * 4                  // key double buffer
+         + (size_t)2 * kScRows * 4                       // row-id double buffer
+         + (size_t)QG * 2 * KPE * 8;                     // per-query list + append buffer
+}
+
+template <int QG, int KPE, bool VEC4>
+__global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = a.d;
+  const int dpad = (d + kScKC - 1) / kScKC * kScKC;
+  const int nk = dpad / kScKC;
+
+  float *q_s = smem;
+  float *stage = q_s + QG * dpad;
+  float *sc = stage + kScWarps * kScStages * 32 * kScPad;
+  int32_t *sid = reinterpret_cast<int32_t *>(sc + 2 * QG * kScRows);
+  float *lk = reinterpret_cast<float *>(sid + 2 * kScRows);
+  int32_t *li = reinterpret_cast<int32_t *>(lk + QG * 2 * KPE);
+
+  const int64_t q0 = (int64_t)blockIdx.y * QG;
+  const int nq = (int)(a.q - q0 < QG ? a.q - q0 : QG);
+
+  for (int i = threadIdx.x; i < QG * dpad; i += kScThreads) {
+    const int j = i / dpad, t = i - j * dpad;
+    q_s[i] = (j < nq && t < d) ? a.Q[(q0 + j) * d + t] : 0.f;
+  }
+  for (int i = threadIdx.x; i < QG * 2 * KPE; i += kScThreads) {
+    lk[i] = -INFINITY;
+    li[i] = -1;
+  }
+
+  const int64_t n_sel = a.ids ? *a.count : a.n;
+  int64_t chunk = (n_sel + a.P - 1) / a.P;
+  chunk = (chunk + kScRows - 1) / kScRows * kScRows;
+  const int64_t start = (int64_t)blockIdx.x * chunk;
+  const int64_t end = min(n_sel, start + chunk);
+  const int niter = end > start ? (int)((end - start + kScRows - 1) / kScRows) : 0;
+  __syncthreads();
+
+  float *wst = stage + warp * kScStages * 32 * kScPad;
+  const int total = niter * nk;
+
+  auto row_id = [&](int it, int r) -> int32_t {
+    const int64_t pos = start + (int64_t)it * kScRows + warp * 32 + r;
+    if (pos >= end) return -1;
+    return a.ids ? __ldg(a.ids + pos) : (int32_t)pos;
+  };
+  auto issue = [&](int t) {
+    const int it = t / nk, kc = t - it * nk;
+    float *buf = wst + (t % kScStages) * 32 * kScPad;
+    const int32_t myid = row_id(it, lane);
+    if constexpr (VEC4) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = (lane >> 3) + 4 * i;
+        const int32_t idr = __shfl_sync(0xffffffffu, myid, r);
+        const int col = kc * kScKC + (lane & 7) * 4;
+        const bool ok = idr >= 0 && col < d;
+        cp_async16(buf + r * kScPad + (lane & 7) * 4, ok ? (const void *)(a.X + (int64_t)idr * d + col) : a.X, ok);
+      }
+    } else {
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int32_t idr = __shfl_sync(0xffffffffu, myid, r);
+        const int col = kc * kScKC + lane;
+        const bool ok = idr >= 0 && col < d;
+        cp_async4(buf + r * kScPad + lane, ok ? (const void *)(a.X + (int64_t)idr * d + col) : a.X, ok);
+      }
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int t = 0; t < kScStages - 1; ++t) {
+    if (t < total) issue(t);
+    else cp_async_commit();
+  }
+
+  float acc[QG];
+#pragma unroll
+  for (int j = 0; j < QG; ++j) acc[j] = 0.f;
+  float tau = -INFINITY;  // warp j's running k'-th best key of query j
+  int cnt = 0;            // entries in warp j's append buffer
+  float *L = lk + warp * 2 * KPE;
+  int32_t *I = li + warp * 2 * KPE;
+
+  auto merge = [&]() {
+    for (int i = cnt + lane; i < KPE; i += 32) {
+      L[KPE + i] = -INFINITY;
+      I[KPE + i] = -1;
+    }
+    warp_bitonic_sort_desc(L, I, 2 * KPE);
+    tau = L[a.kprime - 1];
+    cnt = 0;
+  };
+
+  for (int t = 0; t < total; ++t) {
+    if (t + kScStages - 1 < total) issue(t + kScStages - 1);
+    else cp_async_commit();
+    cp_async_wait<kScStages - 1>();
+    __syncwarp();
+    const int kc = t % nk;
+    const float *buf = wst + (t % kScStages) * 32 * kScPad + lane * kScPad;
+    const float *qk = q_s + kc * kScKC;
+#pragma unroll
+    for (int c4 = 0; c4 < kScKC / 4; ++c4) {
+      const float4 rv = *reinterpret_cast<const float4 *>(buf + c4 * 4);
+#pragma unroll
+      for (int j = 0; j < QG; ++j) {
+        const float4 qv = *reinterpret_cast<const float4 *>(qk + j * dpad + c4 * 4);
+        acc[j] = fmaf(rv.x, qv.x, acc[j]);
+        acc[j] = fmaf(rv.y, qv.y, acc[j]);
+        acc[j] = fmaf(rv.z, qv.z, acc[j]);
+        acc[j] = fmaf(rv.w, qv.w, acc[j]);
+      }
+    }
+    __syncwarp();
+    if (kc == nk - 1) {
+      // ---- one 256-row block done: ranking keys -> shared, then per-query selection
+      const int it = t / nk, b = it & 1;
+      const int32_t myid = row_id(it, lane);
+      float nx2 = 0.f, inx = 0.f;
+      if (myid >= 0) {
+        nx2 = __ldg(a.nx2 + myid);
+        inx = __ldg(a.inv_nx + myid);
+      }
+#pragma unroll
+      for (int j = 0; j < QG; ++j) {
+        sc[(b * QG + j) * kScRows + warp * 32 + lane] =
+            (myid >= 0 && j < nq) ? rank_key(a.metric, acc[j], nx2, inx) : -INFINITY;
+        acc[j] = 0.f;
+      }
+      sid[b * kScRows + warp * 32 + lane] = myid;
+      __syncthreads();
+      if (warp < nq) {
+        const float *keys = sc + (b * QG + warp) * kScRows;
+        const int32_t *rid = sid + b * kScRows;
+#pragma unroll 1
+        for (int s = 0; s < kScRows / 32; ++s) {
+          const float key = keys[s * 32 + lane];
+          bool c = key > tau;
+          uint32_t mask = __ballot_sync(0xffffffffu, c);
+          if (mask) {
+            if (cnt + 32 > KPE) {
+              merge();
+              c = key > tau;
+              mask = __ballot_sync(0xffffffffu, c);
+            }
+            if (c) {
+              const int pos = cnt + __popc(mask & lanemask_lt());
+              L[KPE + pos] = key;
+              I[KPE + pos] = rid[s * 32 + lane];
+            }
+            cnt += __popc(mask);
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  if (warp < nq) {
+    if (cnt > 0) merge();
+    const int64_t o = ((int64_t)blockIdx.x * a.q + q0 + warp) * a.kprime;
+    for (int r = lane; r < a.kprime; r += 32) {
+      a.part_key[o + r] = L[r];
+      a.part_id[o + r] = I[r];
+    }
+  }
+}
+
+template <int QG, int KPE, bool VEC4>
+static cudaError_t launch_scan_t(const ScanArgs &a, int gy, cudaStream_t stream) {
+  const int dpad = (a.d + kScKC - 1) / kScKC * kScKC;
+  const size_t smem = scan_smem_bytes(QG, KPE, dpad);
+  auto fn = scan_topk_kernel<QG, KPE, VEC4>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<dim3(a.P, gy), kScThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int QG, int KPE>
+static cudaError_t launch_scan_v(const ScanArgs &a, int gy, bool vec4, cudaStream_t s) {
+  return vec4 ? launch_scan_t<QG, KPE, true>(a, gy, s) : launch_scan_t<QG, KPE, false>(a, gy, s);
+}
+
+template <int QG>
+static cudaError_t launch_scan_k(const ScanArgs &a, int kpe, int gy, bool vec4, cudaStream_t s) {
+  if (kpe <= 64) return launch_scan_v<QG, 64>(a, gy, vec4, s);
+  if (kpe <= 128) return launch_scan_v<QG, 128>(a, gy, vec4, s);
+  return launch_scan_v<QG, 256>(a, gy, vec4, s);
+}
+
+static constexpr size_t kSmemLimit = 227 * 1024;
+
+// Pick the query group size: the smallest of {1,2,4,8} covering q (8 for q > 8),
+// shrunk until the shared-memory plan fits.
+int scan_query_group(int64_t q, int d, int kpe) {
+  const int dpad = (d + kScKC - 1) / kScKC * kScKC;
+  int qg = q <= 1 ? 1 : q <= 2 ? 2 : q <= 4 ? 4 : 8;
+  const int kp = kpe <= 64 ? 64 : kpe <= 128 ? 128 : 256;
+  while (qg > 1 && scan_smem_bytes(qg, kp, dpad) > kSmemLimit) qg >>= 1;
+  if (scan_smem_bytes(qg, kp, dpad) > kSmemLimit) return 0;
+  return qg;
+}
+
+cudaError_t launch_scan(const ScanArgs &a, int qg, int kpe, cudaStream_t s, int *launches) {
+  const int gy = (int)((a.q + qg - 1) / qg);
+  const bool vec4 = (a.d % 4 == 0) && ((uintptr_t)a.X % 16 == 0);
+  if (launches) *launches += 1;
+  switch (qg) {
+    case 1: return launch_scan_k<1>(a, kpe, gy, vec4, s);
+    case 2: return launch_scan_k<2>(a, kpe, gy, vec4, s);
+    case 4: return launch_scan_k<4>(a, kpe, gy, vec4, s);
+    default: return launch_scan_k<8>(a, kpe, gy, vec4, s);
+  }
+}
+
+}  // namespace vrs

@@ -1,0 +1,411 @@
+// vrs_api.cu -- libvrs host engine and C ABI (include/vrs.h).
+//
+// Validation, the predicate's device form, per-call scratch (stream-ordered
+// allocator), path dispatch and stream ordering.  Every compute step runs in
+// the CUDA kernels of select.cu / scan.cu / gemm_tc.cu / finalize.cu; there is
+// no host or CPU fallback for any of them (a device that is not sm_100 gets
+// VRS_EUNSUPPORTED).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "vrs_kernels.cuh"
+
+
+using namespace vrs;
+
+struct vrs_index {
+  const float *X;
+  int64_t n;
+  int32_t d;
+  int32_t n_attrs;
+  vrs_attr attrs[64];
+  int64_t row_offset;
+  vrs_allocator alloc;
+  int32_t has_alloc;
+  float *nx2;
+  float *inv_nx;
+  int32_t has_zero_row;
+  int32_t device;
+  int32_t num_sms;
+};
+
+static thread_local char g_err[512];
+static thread_local int32_t g_last_path = 0;
+static thread_local int32_t g_last_launches = 0;
+
+static vrs_status fail(vrs_status st, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) return fail(VRS_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+static bool is_device_ptr(const void *p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static vrs_status check_device(int *dev_out, int *sms_out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int major = 0, minor = 0, sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (major != 10 || minor != 0)
+    return fail(VRS_EUNSUPPORTED, "device %d is sm_%d%d; libvrs is built for sm_100a only", dev, major, minor);
+  if (dev_out) *dev_out = dev;
+  if (sms_out) *sms_out = sms;
+  return VRS_OK;
+}
+
+// ---- scratch --------------------------------------------------------------------
+struct Scratch {
+  const vrs_allocator *alloc;
+  cudaStream_t stream;
+  void *ptr = nullptr;
+  ~Scratch() {
+    if (!ptr) return;
+    if (alloc) alloc->free(ptr, stream, alloc->ctx);
+    else cudaFreeAsync(ptr, stream);
+  }
+};
+
+static vrs_status scratch_alloc(Scratch &s, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (s.alloc) {
+    s.ptr = s.alloc->alloc(bytes, s.stream, s.alloc->ctx);
+    if (!s.ptr) return fail(VRS_ENOMEM, "allocator returned NULL for %zu bytes", bytes);
+    return VRS_OK;
+  }
+  static bool pool_tuned = false;
+  if (!pool_tuned) {  // keep freed scratch in the pool instead of returning it to the driver
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_tuned = true;
+  }
+  cudaError_t e = cudaMallocAsync(&s.ptr, bytes, s.stream);
+  if (e != cudaSuccess) {
+    s.ptr = nullptr;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? VRS_ENOMEM : VRS_ECUDA, "cudaMallocAsync(%zu): %s", bytes,
+                cudaGetErrorString(e));
+  }
+  return VRS_OK;
+}
+
+struct Carve {
+  char *base;
+  size_t off = 0;
+  explicit Carve(void *p) : base(static_cast<char *>(p)) {}
+  template <typename T>
+  T *take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T *p = reinterpret_cast<T *>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+static size_t carve_size(std::initializer_list<size_t> parts) {
+  size_t off = 0;
+  for (size_t b : parts) off = ((off + 255) & ~size_t(255)) + b;
+  return off + 256;
+}
+
+// ---- predicate ---------------------------------------------------------------------
+static vrs_status make_pred(const vrs_index *ix, const vrs_predicate *pred, PredDev *out) {
+  memset(out, 0, sizeof *out);
+  if (!pred || pred->n_clauses == 0) return VRS_OK;
+  if (pred->n_clauses < 0) return fail(VRS_EINVAL, "n_clauses < 0");
+  if (pred->n_clauses > VRS_MAX_CLAUSES)
+    return fail(VRS_EUNSUPPORTED, "%d clauses > VRS_MAX_CLAUSES (%d)", pred->n_clauses, VRS_MAX_CLAUSES);
+  if (!pred->clauses) return fail(VRS_EINVAL, "clauses is NULL with n_clauses > 0");
+  out->n = pred->n_clauses;
+  for (int c = 0; c < pred->n_clauses; ++c) {
+    const vrs_clause &cl = pred->clauses[c];
+    if (cl.attr < 0 || cl.attr >= ix->n_attrs)
+      return fail(VRS_ENOTFOUND, "clause %d names attribute %d; the index has %d", c, cl.attr, ix->n_attrs);
+    const vrs_attr &at = ix->attrs[cl.attr];
+    const int64_t tmin = at.type == VRS_ATTR_I32 ? INT32_MIN : 0;
+    const int64_t tmax = at.type == VRS_ATTR_I32 ? INT32_MAX : 255;
+    const int64_t lo = std::max(cl.lo, tmin), hi = std::min(cl.hi, tmax);
+    out->c[c].col = at.data;
+    out->c[c].type = at.type;
+    if (lo > hi) {
+      out->empty = 1;
+      out->c[c].lo = 1;
+      out->c[c].hi = 0;
+    } else {
+      out->c[c].lo = (int32_t)lo;
+      out->c[c].hi = (int32_t)hi;
+    }
+  }
+  return VRS_OK;
+}
+
+// ---- ABI ----------------------------------------------------------------------------
+extern "C" {
+
+const char *vrs_last_error(void) { return g_err; }
+int32_t vrs_last_path(void) { return g_last_path; }
+int32_t vrs_last_launches(void) { return g_last_launches; }
+int64_t vrs_index_rows(const vrs_index *ix) { return ix ? ix->n : -1; }
+int32_t vrs_index_dim(const vrs_index *ix) { return ix ? ix->d : -1; }
+
+vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
+                    int64_t row_offset, const vrs_allocator *alloc, void *cuda_stream, vrs_index **out) {
+  g_err[0] = 0;
+  if (!out) return fail(VRS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n >= (int64_t(1) << 31)) return fail(VRS_EINVAL, "n = %lld outside [1, 2^31)", (long long)n);
+  if (d < 1) return fail(VRS_EINVAL, "d = %d < 1", d);
+  if (n_attrs < 0 || n_attrs > 64) return fail(VRS_EINVAL, "n_attrs = %d outside [0, 64]", n_attrs);
+  if (n_attrs > 0 && !attrs) return fail(VRS_EINVAL, "attrs is NULL with n_attrs > 0");
+  if (row_offset < 0) return fail(VRS_EINVAL, "row_offset < 0");
+  if (alloc && (!alloc->alloc || !alloc->free)) return fail(VRS_EINVAL, "allocator without alloc/free");
+  int dev = 0, sms = 0;
+  vrs_status st = check_device(&dev, &sms);
+  if (st != VRS_OK) return st;
+  if (!is_device_ptr(vectors)) return fail(VRS_EINVAL, "vectors is not a device pointer");
+  for (int a = 0; a < n_attrs; ++a) {
+    if (attrs[a].type != VRS_ATTR_I32 && attrs[a].type != VRS_ATTR_U8)
+      return fail(VRS_EINVAL, "attribute %d has bad type %d", a, (int)attrs[a].type);
+    if (!is_device_ptr(attrs[a].data)) return fail(VRS_EINVAL, "attribute %d is not a device pointer", a);
+  }
+  vrs_index *ix = new vrs_index();
+  ix->X = vectors;
+  ix->n = n;
+  ix->d = d;
+  ix->n_attrs = n_attrs;
+  for (int a = 0; a < n_attrs; ++a) ix->attrs[a] = attrs[a];
+  ix->row_offset = row_offset;
+  ix->has_alloc = alloc != nullptr;
+  if (alloc) ix->alloc = *alloc;
+  ix->device = dev;
+  ix->num_sms = sms;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 4});
+  void *mem = nullptr;
+  if (alloc) {
+    mem = alloc->alloc(bytes, cuda_stream, alloc->ctx);
+    if (!mem) {
+      delete ix;
+      return fail(VRS_ENOMEM, "allocator returned NULL for %zu bytes", bytes);
+    }
+  } else if (cudaMalloc(&mem, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete ix;
+    return fail(VRS_ENOMEM, "cudaMalloc(%zu) failed", bytes);
+  }
+  Carve cv(mem);
+  ix->nx2 = cv.take<float>(n);
+  ix->inv_nx = cv.take<float>(n);
+  int32_t *zf = cv.take<int32_t>(1);
+  int32_t zero = 0;
+  cudaError_t e = cudaMemsetAsync(zf, 0, 4, stream);
+  if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&zero, zf, 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    vrs_free(ix);
+    return fail(VRS_ECUDA, "vrs_load norms: %s", cudaGetErrorString(e));
+  }
+  ix->has_zero_row = zero;
+  *out = ix;
+  return VRS_OK;
+}
+
+vrs_status vrs_free(vrs_index *ix) {
+  if (!ix) return VRS_OK;
+  if (ix->nx2) {
+    if (ix->has_alloc) ix->alloc.free(ix->nx2, nullptr, ix->alloc.ctx);
+    else cudaFree(ix->nx2);
+  }
+  delete ix;
+  return VRS_OK;
+}
+
+static int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
+                         int32_t k, vrs_metric metric, int64_t *ids, float *dists,
+                         const vrs_search_options *opts, void *cuda_stream) {
+  g_err[0] = 0;
+  g_last_launches = 0;
+  if (!ix) return fail(VRS_EINVAL, "index is NULL");
+  if (q < 0) return fail(VRS_EINVAL, "q < 0");
+  if (d != ix->d) return fail(VRS_EINVAL, "d = %d differs from the loaded d = %d", d, ix->d);
+  if (k < 1) return fail(VRS_EINVAL, "k = %d < 1", k);
+  if (metric != VRS_L2 && metric != VRS_IP && metric != VRS_COSINE)
+    return fail(VRS_EINVAL, "bad metric %d", (int)metric);
+  const int path_req = opts ? opts->path : VRS_PATH_AUTO;
+  const int rows_req = opts ? opts->rows : VRS_ROWS_AUTO;
+  if (path_req < VRS_PATH_AUTO || path_req > VRS_PATH_GEMM) return fail(VRS_EINVAL, "bad path option");
+  if (rows_req < VRS_ROWS_AUTO || rows_req > VRS_ROWS_MASKED) return fail(VRS_EINVAL, "bad rows option");
+  PredDev pd;
+  vrs_status st = make_pred(ix, pred, &pd);
+  if (st != VRS_OK) return st;
+  if (k > VRS_K_MAX) return fail(VRS_EUNSUPPORTED, "k = %d > VRS_K_MAX (%d)", k, VRS_K_MAX);
+  if (metric == VRS_COSINE && ix->has_zero_row)
+    return fail(VRS_EDEGENERATE, "COSINE over a corpus with a zero-norm row");
+  if (q == 0) return VRS_OK;
+  if (!is_device_ptr(queries) || !is_device_ptr(ids) || !is_device_ptr(dists))
+    return fail(VRS_EINVAL, "queries / ids / dists must be device pointers");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != ix->device) return fail(VRS_EINVAL, "current device %d differs from the index device %d", dev, ix->device);
+
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  const int32_t kprime = k + 16;  // over-fetch for the exact re-score
+  const int kpe = std::max(64, pow2_at_least(kprime));
+  const bool identity = (pd.n == 0);
+  const int64_t n = ix->n;
+
+  // path choice (A16: per-tuple for small batches, tensor formulation for large ones)
+  int path = path_req;
+  GemmPlan gp{0, 0, 0};
+  if (path != VRS_PATH_SCAN) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
+  if (path == VRS_PATH_AUTO) path = (q >= 8 && gp.ok) ? VRS_PATH_GEMM : VRS_PATH_SCAN;
+  if (path == VRS_PATH_GEMM && !gp.ok) return fail(VRS_EUNSUPPORTED, "tensor-core path does not support this shape");
+
+  int qg = 0, P = 0;
+  if (path == VRS_PATH_SCAN) {
+    qg = scan_query_group(q, d, kpe);
+    if (qg == 0) return fail(VRS_EUNSUPPORTED, "d = %d too large for the scan path", d);
+    const int64_t gy = (q + qg - 1) / qg;
+    const int64_t want = std::max<int64_t>(1, ix->num_sms / gy);
+    P = (int)std::min<int64_t>(want, std::max<int64_t>(1, (n + 255) / 256));
+  } else {
+    P = gp.P;
+  }
+  const size_t nwords = (size_t)((n + 31) / 32);
+  const size_t part_entries = (size_t)P * q * kprime;
+  Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
+                                   part_entries * 4, part_entries * 4,
+                                   path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0});
+  st = scratch_alloc(scr, bytes);
+  if (st != VRS_OK) return st;
+  Carve cv(scr.ptr);
+  uint32_t *bitmap = cv.take<uint32_t>(nwords);
+  int32_t *sel_ids = identity ? nullptr : cv.take<int32_t>((size_t)n);
+  int64_t *count = cv.take<int64_t>(1);
+  void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
+  float *part_key = cv.take<float>(part_entries);
+  int32_t *part_id = cv.take<int32_t>(part_entries);
+  void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
+
+  int launches = 0;
+  if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
+
+  if (path == VRS_PATH_SCAN) {
+    ScanArgs a{ix->X, n, d, sel_ids, count, queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime,
+               part_key, part_id, P};
+    CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
+  } else {
+    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_req == VRS_ROWS_MASKED ? 1 : 0,
+               queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
+    CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
+  }
+  FinalizeArgs f{part_key, part_id, P, kprime, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
+  CUDA_TRY(launch_finalize(f, stream, &launches));
+  g_last_path = path;
+  g_last_launches = launches;
+  return VRS_OK;
+}
+
+vrs_status vrs_search(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
+                      int32_t k, vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream) {
+  return vrs_search_ex(ix, queries, q, d, pred, k, metric, ids, dists, nullptr, cuda_stream);
+}
+
+vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,
+                           const vrs_predicate *pred, int32_t k, vrs_metric metric, int64_t *h_ids,
+                           float *h_dists, const vrs_search_options *opts, void *cuda_stream) {
+  g_err[0] = 0;
+  if (!ix) return fail(VRS_EINVAL, "index is NULL");
+  if (q < 0 || k < 1) return fail(VRS_EINVAL, "q < 0 or k < 1");
+  if (q == 0) return vrs_search_ex(ix, nullptr, 0, d, pred, k, metric, nullptr, nullptr, opts, cuda_stream);
+  if (!h_queries || !h_ids || !h_dists) return fail(VRS_EINVAL, "NULL host buffer");
+  if (d != ix->d) return fail(VRS_EINVAL, "d = %d differs from the loaded d = %d", d, ix->d);
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  Scratch io{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  const size_t qb = (size_t)q * d * 4, ib = (size_t)q * k * 8, db = (size_t)q * k * 4;
+  vrs_status st = scratch_alloc(io, carve_size({qb, ib, db}));
+  if (st != VRS_OK) return st;
+  Carve cv(io.ptr);
+  float *dq = cv.take<float>((size_t)q * d);
+  int64_t *di = cv.take<int64_t>((size_t)q * k);
+  float *dd = cv.take<float>((size_t)q * k);
+  CUDA_TRY(cudaMemcpyAsync(dq, h_queries, qb, cudaMemcpyHostToDevice, stream));
+  st = vrs_search_ex(ix, dq, q, d, pred, k, metric, di, dd, opts, cuda_stream);
+  if (st != VRS_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(h_ids, di, ib, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaMemcpyAsync(h_dists, dd, db, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  return VRS_OK;
+}
+
+vrs_status vrs_select(vrs_index *ix, const vrs_predicate *pred, uint32_t *bitmap, int64_t *count, int32_t *ids,
+                      void *cuda_stream) {
+  g_err[0] = 0;
+  if (!ix) return fail(VRS_EINVAL, "index is NULL");
+  PredDev pd;
+  vrs_status st = make_pred(ix, pred, &pd);
+  if (st != VRS_OK) return st;
+  if (!is_device_ptr(bitmap) || !is_device_ptr(count)) return fail(VRS_EINVAL, "bitmap / count must be device pointers");
+  if (ids && !is_device_ptr(ids)) return fail(VRS_EINVAL, "ids must be a device pointer");
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  st = scratch_alloc(scr, select_scratch_bytes(ix->n));
+  if (st != VRS_OK) return st;
+  int launches = 0;
+  CUDA_TRY(launch_select(pd, ix->n, bitmap, ids, count, scr.ptr, stream, &launches));
+  g_last_launches = launches;
+  return VRS_OK;
+}
+
+vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n_parts, int64_t q, int32_t k,
+                     vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream) {
+  g_err[0] = 0;
+  if (n_parts < 1 || q < 0 || k < 1) return fail(VRS_EINVAL, "n_parts < 1, q < 0 or k < 1");
+  if (metric != VRS_L2 && metric != VRS_IP && metric != VRS_COSINE)
+    return fail(VRS_EINVAL, "bad metric %d", (int)metric);
+  if (k > VRS_K_MAX) return fail(VRS_EUNSUPPORTED, "k = %d > VRS_K_MAX (%d)", k, VRS_K_MAX);
+  if (q == 0) return VRS_OK;
+  if (!is_device_ptr(cand_ids) || !is_device_ptr(cand_dists) || !is_device_ptr(ids) || !is_device_ptr(dists))
+    return fail(VRS_EINVAL, "vrs_merge buffers must be device pointers");
+  vrs_status st = check_device(nullptr, nullptr);
+  if (st != VRS_OK) return st;
+  int launches = 0;
+  MergeArgs a{cand_ids, cand_dists, n_parts, q, k, (int32_t)metric, ids, dists};
+  CUDA_TRY(launch_merge(a, (cudaStream_t)cuda_stream, &launches));
+  g_last_launches = launches;
+  return VRS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// vrs_internal.cuh -- device-side building blocks shared by the libvrs kernels.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md "Boundary").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "vrs.h"
+
+namespace vrs {
+
+constexpr int kSmCountB200 = 148;
+
+// One clause of theta_R in device form: the [lo, hi] interval clamped to the
+// column type's range (empty => the whole predicate selects nothing).
+struct ClauseDev {
+  const void *col;
+  int32_t type;  // VRS_ATTR_I32 / VRS_ATTR_U8
+  int32_t lo;
+  int32_t hi;
+};
+
+struct PredDev {
+  int32_t n;      // number of clauses (0 => all rows)
+  int32_t empty;  // some clause is empty after clamping => no row qualifies
+  ClauseDev c[VRS_MAX_CLAUSES];
+};
+
+// theta_R for one row (reading R4): AND of closed intervals.
+__device__ __forceinline__ bool eval_pred(const PredDev &p, int64_t row) {
+  if (p.empty) return false;
+  bool ok = true;
+#pragma unroll 1
+  for (int c = 0; c < p.n; ++c) {
+    int32_t v = (p.c[c].type == VRS_ATTR_I32) ? __ldg(static_cast<const int32_t *>(p.c[c].col) + row)
+                                              : (int32_t)__ldg(static_cast<const uint8_t *>(p.c[c].col) + row);
+    ok = ok && (p.c[c].lo <= v) && (v <= p.c[c].hi);
+  }
+  return ok;
+}
+
+// float -> uint32 whose unsigned order equals the float order (-inf < ... < +inf).
+__device__ __forceinline__ uint32_t ordered_u32(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- cp.async (LDGSTS) helpers -------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool valid) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  int n = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Ranking key used by the selection passes, larger = better for every metric
+// (DESIGN.md "Selection key"):  L2: 2<q,x> - |x|^2  (= |q|^2 - L2, same order),
+// IP: <q,x>,  COS: <q,x>/|x|  (1/|q| > 0 does not change the order).
+__device__ __forceinline__ float rank_key(int metric, float dot, float nx2, float inv_nx) {
+  if (metric == VRS_L2) return fmaf(2.0f, dot, -nx2);
+  if (metric == VRS_IP) return dot;
+  return dot * inv_nx;
+}
+
+// Candidate (key, id) total order: key descending, then id ascending.
+__device__ __forceinline__ bool cand_better(float ka, int32_t ia, float kb, int32_t ib) {
+  return (ka > kb) || (ka == kb && ia < ib);
+}
+
+// Warp-cooperative bitonic sort, descending in (key, -id), of n = 2^p entries
+// held in shared memory.  All 32 lanes must call it.
+__device__ __forceinline__ void warp_bitonic_sort_desc(float *key, int32_t *id, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncwarp();
+      for (int t = lane; t < (n >> 1); t += 32) {
+        int lo = 2 * t - (t & (stride - 1));
+        int hi = lo + stride;
+        bool desc = ((lo & size) == 0);  // direction of this bitonic half
+        float ka = key[lo], kb = key[hi];
+        int32_t ia = id[lo], ib = id[hi];
+        bool swap = desc ? cand_better(kb, ib, ka, ia) : cand_better(ka, ia, kb, ib);
+        if (swap) {
+          key[lo] = kb; key[hi] = ka;
+          id[lo] = ib;  id[hi] = ia;
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace vrs

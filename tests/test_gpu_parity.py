@@ -1,0 +1,190 @@
+"""GPU parity: libvrs (through the C ABI) vs the CPU oracle on seeded inputs.
+
+Sizes span several tiles and ragged tails; selectivities include 0, tiny,
+partial and 1; every metric and both distance paths.  Acceptance rules in
+tests/parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from parity import check_select, check_topk
+
+pytestmark = pytest.mark.gpu
+
+I32MIN, I32MAX = -(2 ** 31), 2 ** 31 - 1
+METRICS = {oracle.L2: "l2", oracle.IP: "ip", oracle.COS: "cos"}
+
+
+@pytest.fixture(scope="module")
+def vrs():
+    import paper_2403_15807_b200 as m
+    m.library()
+    return m
+
+
+def _data(n, d, seed=0, mod=1000, nattr=1, kind="gauss"):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    if kind == "norm":
+        X /= np.linalg.norm(X, axis=1, keepdims=True)
+    attrs = [rng.integers(0, mod, n).astype(np.int32)]
+    if nattr > 1:
+        attrs.append(rng.integers(0, 64, n).astype(np.uint8))
+    return X, attrs
+
+
+def _run(vrs, X, attrs, pred, Q, k, metric, path=None, rows=None, off=0):
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off)
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=path, rows=rows)
+    torch.cuda.synchronize()
+    return ids.cpu().numpy(), dists.cpu().numpy()
+
+
+# ------------------------------------------------------------------ selection
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1000, 1024, 1025, 10007, 250_001])
+def test_select_bit_exact(vrs, n):
+    X, attrs = _data(n, 4, seed=n, nattr=2)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    for pred in ([], [(0, I32MIN, 99)], [(0, 500, 499)], [(0, 100, 899), (1, 3, 40)], [(1, 0, 255)],
+                 [(0, -5, 10 ** 12)], [(0, 0, 0)], [(1, 200, 300)]):
+        bm, cnt, ids = ix.select(pred, with_ids=True)
+        torch.cuda.synchronize()
+        check_select(bm, cnt, ids, attrs, n, pred)
+
+
+def test_select_errors(vrs):
+    X, attrs = _data(100, 4)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    with pytest.raises(vrs.VrsError) as e:
+        ix.select([(3, 0, 1)])
+    assert e.value.status == 2    # ENOTFOUND
+
+
+# ------------------------------------------------------------------ search parity
+
+CASES = [
+    # n, d, q, k, metric, pred
+    (1, 8, 1, 1, oracle.L2, []),
+    (33, 8, 3, 5, oracle.IP, [(0, 0, 499)]),
+    (1000, 1, 2, 10, oracle.L2, []),
+    (1000, 127, 7, 10, oracle.IP, [(0, I32MIN, 99)]),
+    (4099, 128, 8, 10, oracle.L2, [(0, I32MIN, 99)]),
+    (4099, 128, 16, 64, oracle.COS, [(0, 0, 499)]),
+    (10007, 256, 1, 100, oracle.IP, []),
+    (10007, 256, 5, 240, oracle.L2, [(0, 0, 899)]),
+    (5000, 1027, 3, 10, oracle.COS, [(0, 0, 599)]),
+    (20000, 768, 2, 100, oracle.L2, [(0, I32MIN, 9)]),     # ~1 % selectivity
+    (20000, 64, 33, 50, oracle.IP, [(0, 0, 999)]),
+    (3000, 128, 9, 10, oracle.L2, [(0, 5000, 6000)]),      # selectivity 0 -> padding
+    (300, 128, 4, 240, oracle.IP, [(0, 0, 99)]),           # k > N_sel -> padding
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}-d{c[1]}-q{c[2]}-k{c[3]}-m{c[4]}")
+@pytest.mark.parametrize("path", [None, 1], ids=["auto", "scan"])
+def test_search_parity(vrs, case, path):
+    n, d, q, k, metric, pred = case
+    X, attrs = _data(n, d, seed=n + d, kind="norm" if metric == oracle.IP and d == 128 else "gauss")
+    Q = np.random.default_rng(q).standard_normal((q, d)).astype(np.float32)
+    gi, gd = _run(vrs, X, attrs, pred, Q, k, metric, path=path)
+    check_topk(gi, gd, X, attrs, pred, Q, k, metric)
+
+
+def test_row_offset_and_determinism(vrs):
+    X, attrs = _data(5000, 64, seed=3)
+    Q = np.random.default_rng(1).standard_normal((4, 64)).astype(np.float32)
+    pred = [(0, 0, 299)]
+    off = 123_456_789
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off)
+    Qd = torch.from_numpy(Q).cuda()
+    a = ix.search(Qd, pred, k=20, metric="l2")
+    b = ix.search(Qd, pred, k=20, metric="l2")
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])      # bit-identical repeats
+    check_topk(a[0].cpu().numpy(), a[1].cpu().numpy(), X, attrs, pred, Q, 20, oracle.L2, row_offset=off)
+
+
+def test_identical_vector_distance_zero(vrs):
+    X, attrs = _data(2000, 32, seed=5)
+    Q = X[[17, 1999, 0]].copy()
+    gi, gd = _run(vrs, X, attrs, [], Q, 3, oracle.L2)
+    assert gi[:, 0].tolist() == [17, 1999, 0] and (gd[:, 0] == 0).all()
+
+
+def test_q_zero_and_errors(vrs):
+    X, attrs = _data(100, 16)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    Qd = torch.zeros(2, 16, device="cuda")
+    ids, _ = ix.search(torch.zeros(0, 16, device="cuda"), [], k=5)     # q = 0: no-op
+    assert ids.shape == (0, 5)
+    cases = [
+        (dict(k=0), 1), (dict(k=241), 7), (dict(metric=9), 1), (dict(pred=[(1, 0, 1)]), 2),
+        (dict(pred=[(0, 0, 1)] * 9), 7),
+    ]
+    for kw, status in cases:
+        args = dict(pred=[], k=5, metric="l2")
+        args.update(kw)
+        with pytest.raises(vrs.VrsError) as e:
+            ix.search(Qd, **args)
+        assert e.value.status == status, kw
+    with pytest.raises(vrs.VrsError) as e:                  # host pointer
+        ix.search(torch.zeros(2, 16), [], k=5)
+    assert e.value.status == 1
+    with pytest.raises(vrs.VrsError) as e:                  # d mismatch
+        ix.search(torch.zeros(2, 8, device="cuda"), [], k=5)
+    assert e.value.status == 1
+    Z = X.copy()
+    Z[3] = 0
+    iz = vrs.Index(torch.from_numpy(Z).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    with pytest.raises(vrs.VrsError) as e:
+        iz.search(Qd + 1, [], k=5, metric="cos")
+    assert e.value.status == 3                              # EDEGENERATE
+    ids, d = ix.search(Qd, [], k=5, metric="cos")           # zero COSINE query -> padding
+    assert (ids == -1).all()
+
+
+def test_merge_matches_oracle(vrs):
+    rng = np.random.default_rng(12)
+    n, d, k, q = 6000, 48, 25, 6
+    X, attrs = _data(n, d, seed=12)
+    Q = rng.standard_normal((q, d)).astype(np.float32)
+    pred = [(0, 0, 699)]
+    cuts = [0, 1500, 3001, 4700, 6000]
+    for metric in (oracle.L2, oracle.IP, oracle.COS):
+        parts = []
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            parts.append(_run(vrs, X[r0:r1].copy(), [a[r0:r1].copy() for a in attrs], pred, Q, k, metric, off=r0))
+        ci = torch.from_numpy(np.stack([p[0] for p in parts])).cuda()
+        cd = torch.from_numpy(np.stack([p[1] for p in parts])).cuda()
+        mi, md = vrs.merge(ci, cd, k, METRICS[metric])
+        torch.cuda.synchronize()
+        oi, od = oracle.merge(ci.cpu().numpy(), cd.cpu().numpy(), k, metric)
+        assert (mi.cpu().numpy() == oi).all() and (md.cpu().numpy() == od).all()
+        check_topk(mi.cpu().numpy(), md.cpu().numpy(), X, attrs, pred, Q, k, metric)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_config_shaped_reduced(vrs, name):
+    """Each BASELINE config's distributions / predicate structure at a size the oracle finishes in seconds."""
+    cfg = datagen.CONFIGS[name]
+    n = {"c1": cfg.n, "c2": 60_000, "c3": 20_000, "c4": 8_000, "c5": 30_000}[name]
+    X, attrs = datagen.corpus(cfg, 0, n, "cpu", n=n)
+    Xn, an = X.numpy(), [a.numpy() for a in attrs]
+    for sel in cfg.sels:
+        pred = datagen.predicate(cfg, sel)
+        for q in cfg.qs:
+            qq = min(q, 64)
+            Q = datagen.queries(cfg, qq, "cpu").numpy()
+            gi, gd = _run(vrs, Xn, an, pred, Q, cfg.k, cfg.metric)
+            check_topk(gi, gd, Xn, an, pred, Q, cfg.k, cfg.metric)
+
+
+def test_search_host_end_to_end(vrs):
+    X, attrs = _data(3000, 64, seed=9)
+    Q = np.random.default_rng(2).standard_normal((5, 64)).astype(np.float32)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    ids, dists = ix.search_host(torch.from_numpy(Q).pin_memory(), [(0, 0, 499)], k=7, metric="ip")
+    check_topk(ids.numpy(), dists.numpy(), X, attrs, [(0, 0, 499)], Q, 7, oracle.IP)
