@@ -46,7 +46,7 @@ def _options(path, rows):
     o = _lib.SearchOptions()
     o.path = PATH_AUTO if path is None else int(path)
     o.rows = ROWS_AUTO if rows is None else int(rows)
-    return o
+    return ctypes.byref(o)
 
 
 def last_path() -> int:

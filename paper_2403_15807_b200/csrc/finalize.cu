@@ -180,13 +180,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs a) {
   const float *q = a.Q + j * a.d;
 
   auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    const int64_t p = c / a.kprime, r = c - p * a.kprime;
-    const int64_t o = (p * a.q + j) * a.kprime + r;
+    const int64_t p = c / a.kread, r = c - p * a.kread;
+    const int64_t o = (p * a.q + j) * a.stride + r;
     id = a.part_id[o];
     key = a.part_key[o];
     return id >= 0;
   };
-  const int m = block_select_top<int32_t>(get, (int64_t)a.P * a.kprime, a.kprime, s_id, s_key);
+  const int m = block_select_top<int32_t>(get, (int64_t)a.P * a.kread, a.kprime, s_id, s_key);
 
   // |q|^2 in fp64 (COSINE only)
   if (warp == 0) {

@@ -1,10 +1,519 @@
-// gemm_tc.cu -- K3' tcgen05 tensor-core path (placeholder until the kernel lands).
+// gemm_tc.cu -- K3': the batched tensor formulation on 5th-generation tensor cores.
+//
+// PAPER.md L302-L304 (Sec. 3.1): batch the query vectors AND the data vectors
+// and compute their similarity as one matrix product ("Tensor formulation,
+// based on BLAS"); L305 cosine as a dot product with normalised operands;
+// L319 late materialization (filter first, then batch).  Here the product
+// S = Q . X_sel^T is never materialised: it lives in TMEM one 128 x 256 tile
+// at a time and is consumed by a fused top-k epilogue.
+//
+// Per CTA: one work item = (query tile of 128, contiguous split of the row
+// tiles).  Warp roles (256 threads, 1 CTA / SM):
+//   warp 0  TMA producer: query block [128 x 32 fp32] + row block [256 x 32]
+//           per stage, 128-byte swizzle, 4-stage mbarrier ring
+//   warp 1  TMEM allocator + tcgen05.mma issuer (kind::tf32, M=128, N=256,
+//           K=8 per instruction), fp32 accumulators double-buffered in TMEM
+//           (2 x 256 columns)
+//   warp 2  per-row epilogue terms: ranking-key scale/bias of each of the 256
+//           rows of a tile (norm terms, bitmap mask) and row ids, 2-stage ring
+//   warps 4-7 epilogue: tcgen05.ld 32 columns at a time, key = fma(dot, a, b),
+//           compare with the query's running threshold, rare append to a
+//           per-(work item, query) candidate buffer, warp-cooperative radix
+//           compaction to the best KP when a buffer fills.
+// Precision: TF32 products, fp32 accumulation -> selection only; the k' = k+16
+// best per query are re-scored exactly in finalize.cu.
+//
+// Roofline: tensor (2*q*N_rows*d TF32 flops) for large q, HBM (4*d bytes per
+// row) for small q.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include "vrs_kernels.cuh"
 
 namespace vrs {
-GemmPlan gemm_plan(int64_t, int32_t, int64_t, int32_t, int) { return GemmPlan{0, 0, 0}; }
-size_t gemm_scratch_bytes(const GemmPlan &, int64_t, int32_t) { return 0; }
-cudaError_t launch_gemm(const GemmArgs &, const GemmPlan &, void *, cudaStream_t, int *) {
-  return cudaErrorNotSupported;
+
+namespace tc {
+constexpr int BM = 128;         // queries per tile (TMEM lanes)
+constexpr int BN = 256;         // rows per tile (TMEM columns, MMA N)
+constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+constexpr int B_BYTES = BN * BK * 4;   // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ACC_STAGES = 2;
+constexpr int TMEM_COLS = 512;
+constexpr int THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (item, query)
+// dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [2][BN] + epilogue histograms
+constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + ACC_STAGES * BN * 12 + 4 * 256 * 4 + 256;
+}  // namespace tc
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::tf32, both operands K-major.
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major operand in the canonical
+// 128-byte-swizzle layout written by TMA (8-row groups of 1024 bytes).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                   // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D fp32, A/B tf32, both K-major, N = BN, M = BM.
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+#define TMEM_LD_32x32b_X32(taddr, r)                                                                              \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                                  \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),  \
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),      \
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),     \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                  \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------- kernel
+struct TcParams {
+  int64_t n_rows;          // row space: n (identity / masked)
+  int32_t d;
+  int32_t nk;              // K blocks = ceil(d / 32)
+  int64_t q;
+  int32_t qtiles;
+  int32_t P;               // splits
+  int64_t row_tiles;       // ceil(n_rows / BN)
+  const uint32_t *bitmap;  // nullptr => every row qualifies
+  const float *nx2;
+  const float *inv_nx;
+  int32_t metric;
+  int32_t kp;              // retained entries per (item, query) (pow2 >= k')
+  int32_t cap;             // buffer capacity per (item, query)
+  float *cand_key;         // [P][q][cap]
+  int32_t *cand_id;
+};
+
+// Warp-cooperative compaction of one lane's candidate buffer to its best KP
+// entries (key desc, then buffer order = ascending row id).  Returns the new
+// threshold key (the KP-th best).  All 32 lanes call it with the same `owner`.
+__device__ float compact_lane(float *key, int32_t *id, int cnt, int kp, uint32_t *hist) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0, mask = 0;
+  int rem = kp;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+      const uint32_t ok = ordered_u32(key[i]);
+      if ((ok & mask) == prefix) atomicAdd(&hist[(ok >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { v[t] = hist[255 - 8 * lane - t]; s += v[t]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t before = incl - s;
+    int bin = -1, above = 0;
+    if (before < (uint32_t)rem && (uint32_t)rem <= incl) {
+      uint32_t run = before;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (bin < 0 && (uint32_t)rem <= run + v[t]) { bin = 255 - 8 * lane - t; above = (int)run; }
+        if (bin < 0) run += v[t];
+      }
+    }
+    const uint32_t who = __ballot_sync(0xffffffffu, bin >= 0);
+    const int src = __ffs(who) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    prefix |= (uint32_t)bin << shift;
+    mask |= 255u << shift;
+    rem -= above;
+    __syncwarp();
+  }
+  // stable in-place compaction: keys strictly above the threshold, plus the
+  // first `rem` ties in buffer order
+  int out = 0, ties = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int i = base + lane;
+    float kv = -INFINITY;
+    int32_t iv = -1;
+    uint32_t ok = 0;
+    if (i < cnt) { kv = key[i]; iv = id[i]; ok = ordered_u32(kv); }
+    const bool tie = (i < cnt) && ok == prefix;
+    const uint32_t tmask = __ballot_sync(0xffffffffu, tie);
+    const int my_tie_rank = ties + __popc(tmask & lanemask_lt());
+    ties += __popc(tmask);
+    const bool keep = (i < cnt) && (ok > prefix || (tie && my_tie_rank < rem));
+    const uint32_t kmask = __ballot_sync(0xffffffffu, keep);
+    const int pos = out + __popc(kmask & lanemask_lt());
+    __syncwarp();
+    if (keep) { key[pos] = kv; id[pos] = iv; }
+    out += __popc(kmask);
+    __syncwarp();
+  }
+  const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7fffffffu) : ~prefix;
+  return __uint_as_float(u);
+}
+
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
+                   TcParams p) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *stage_base = smem;
+  float *bias_a = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES);   // [2][BN]
+  float *bias_b = bias_a + ACC_STAGES * BN;                                   // [2][BN]
+  int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + ACC_STAGES * BN);    // [2][BN]
+  uint32_t *hist = reinterpret_cast<uint32_t *>(row_id + ACC_STAGES * BN);    // [4][256]
+
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
+  __shared__ __align__(8) uint64_t bfull_bar[ACC_STAGES], bempty_bar[ACC_STAGES];
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qtile = blockIdx.x % p.qtiles;
+  const int split = blockIdx.x / p.qtiles;
+  const int64_t t_begin = (p.row_tiles * split) / p.P;
+  const int64_t t_end = (p.row_tiles * (split + 1)) / p.P;
+  const int ntiles = (int)(t_end - t_begin);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < ACC_STAGES; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+      mbar_init(&bfull_bar[s], 32);
+      mbar_init(&bempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int row0 = (int)((t_begin + t) * BN);
+        for (int kb = 0; kb < p.nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t *sa = stage_base + stage * STAGE_BYTES;
+          uint8_t *sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          tma_load_2d(sa, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
+          tma_load_2d(sb, &tmap_x, &full_bar[stage], kb * BK, row0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = tf32_idesc(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      const uint32_t acc_phase = (t >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.nk; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
+            tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty_bar[stage]);                 // frees the smem slot when these MMAs finish
+          if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);  // accumulator ready
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ per-row epilogue terms
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t & 1;
+      mbar_wait(&bempty_bar[s], ((t >> 1) & 1) ^ 1);
+      const int64_t row0 = (t_begin + t) * BN;
+      for (int c = lane; c < BN; c += 32) {
+        const int64_t row = row0 + c;
+        bool valid = row < p.n_rows;
+        if (valid && p.bitmap) valid = (__ldg(p.bitmap + (row >> 5)) >> (row & 31)) & 1u;
+        float a = 1.f, b = valid ? 0.f : -INFINITY;
+        if (p.metric == VRS_L2) {
+          a = 2.f;
+          if (valid) b = -__ldg(p.nx2 + row);
+        } else if (p.metric == VRS_COSINE) {
+          a = valid ? __ldg(p.inv_nx + row) : 0.f;
+        }
+        bias_a[s * BN + c] = a;
+        bias_b[s * BN + c] = b;
+        row_id[s * BN + c] = (int32_t)row;
+      }
+      mbar_arrive(&bfull_bar[s]);
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------ epilogue: fused top-k
+    const int ew = warp - EPI_WARP0;               // == warp % 4: TMEM lane quadrant
+    const int m = ew * 32 + lane;                  // query row within the tile
+    const int64_t qg = (int64_t)qtile * BM + m;    // global query index
+    const bool active = qg < p.q;
+    const int64_t cbase = ((int64_t)split * p.q + (active ? qg : 0)) * p.cap;
+    float *ckey = p.cand_key + cbase;
+    int32_t *cid = p.cand_id + cbase;
+    uint32_t *whist = hist + ew * 256;
+    float tau = -INFINITY;
+    int cnt = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      const uint32_t ph = (t >> 1) & 1;
+      mbar_wait(&bfull_bar[acc], ph);
+      mbar_wait(&tfull_bar[acc], ph);
+      tc_fence_after();
+      const float *ba = bias_a + acc * BN;
+      const float *bb = bias_b + acc * BN;
+      const int32_t *rid = row_id + acc * BN;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c0);
+        TMEM_LD_32x32b_X32(taddr, r);
+        tmem_ld_wait();
+        if (active) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(ba + c0 + i);
+            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c0 + i);
+            const float kk[4] = {fmaf(__uint_as_float(r[i]), a4.x, b4.x), fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y),
+                                 fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z),
+                                 fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w)};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (kk[u] > tau) {
+                ckey[cnt] = kk[u];
+                cid[cnt] = rid[c0 + i + u];
+                ++cnt;
+              }
+            }
+          }
+        }
+        // a buffer that could overflow on the next 32 columns is compacted (warp-cooperative)
+        uint32_t need = __ballot_sync(0xffffffffu, cnt > p.cap - 32);
+        while (need) {
+          const int owner = __ffs(need) - 1;
+          need &= need - 1;
+          const int oc = __shfl_sync(0xffffffffu, cnt, owner);
+          const int64_t ob = ((int64_t)split * p.q + (int64_t)qtile * BM + ew * 32 + owner) * p.cap;
+          const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
+          if (lane == owner) { tau = nt; cnt = p.kp; }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) { mbar_arrive(&tempty_bar[acc]); mbar_arrive(&bempty_bar[acc]); }
+    }
+    // final: keep the best KP, pad the rest of the KP window
+    uint32_t need = __ballot_sync(0xffffffffu, cnt > p.kp);
+    while (need) {
+      const int owner = __ffs(need) - 1;
+      need &= need - 1;
+      const int oc = __shfl_sync(0xffffffffu, cnt, owner);
+      const int64_t ob = ((int64_t)split * p.q + (int64_t)qtile * BM + ew * 32 + owner) * p.cap;
+      compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
+      if (lane == owner) cnt = p.kp;
+    }
+    if (active)
+      for (int i = cnt; i < p.kp; ++i) { ckey[i] = -INFINITY; cid[i] = -1; }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void *f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap *m, const float *base, int64_t rows, int32_t d, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int kp_of(int32_t kprime) {
+  int kp = 32;
+  while (kp < kprime) kp <<= 1;
+  return kp;
+}
+
+GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms) {
+  GemmPlan g{0, 0, 0};
+  if (d % 4 != 0 || d < 4 || q < 1 || n_upper < 1 || kprime > 256) return g;
+  if (!encode_fn()) return g;
+  const int64_t qtiles = (q + tc::BM - 1) / tc::BM;
+  const int64_t row_tiles = (n_upper + tc::BN - 1) / tc::BN;
+  int64_t P = std::max<int64_t>(1, num_sms / qtiles);
+  // more splits when one wave leaves SMs idle
+  if (P * qtiles < num_sms) P = std::max<int64_t>(P, (num_sms + qtiles - 1) / qtiles);
+  P = std::min<int64_t>(P, row_tiles);
+  g.P = (int32_t)P;
+  g.qtiles = (int32_t)qtiles;
+  g.ok = 1;
+  return g;
+}
+
+size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
+  const int kp = kp_of(kprime);
+  return (size_t)plan.P * q * kp * tc::CAP_FACTOR * 8 + 512;
+}
+
+cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
+  if (a.ids != nullptr && !a.masked) return cudaErrorNotSupported;  // gather mode: not in this kernel yet
+  CUtensorMap mq, mx;
+  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN)) return cudaErrorInvalidValue;
+  TcParams p;
+  p.n_rows = a.n;
+  p.d = a.d;
+  p.nk = (a.d + tc::BK - 1) / tc::BK;
+  p.q = a.q;
+  p.qtiles = plan.qtiles;
+  p.P = plan.P;
+  p.row_tiles = (a.n + tc::BN - 1) / tc::BN;
+  p.bitmap = a.bitmap;
+  p.nx2 = a.nx2;
+  p.inv_nx = a.inv_nx;
+  p.metric = a.metric;
+  p.kp = kp_of(a.kprime);
+  p.cap = p.kp * tc::CAP_FACTOR;
+  p.cand_key = static_cast<float *>(scratch);
+  p.cand_id = reinterpret_cast<int32_t *>(p.cand_key + (size_t)plan.P * a.q * p.cap);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, p);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+// Where the finalize pass reads the GEMM candidate lists.
+void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
+                int32_t *stride, int32_t *kread) {
+  const int kp = kp_of(a.kprime);
+  const int cap = kp * tc::CAP_FACTOR;
+  *key = static_cast<const float *>(scratch);
+  *id = reinterpret_cast<const int32_t *>(static_cast<const float *>(scratch) + (size_t)plan.P * a.q * cap);
+  *stride = cap;
+  *kread = kp;
+}
+
 }  // namespace vrs

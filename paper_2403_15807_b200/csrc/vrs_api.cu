@@ -291,6 +291,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   if (path != VRS_PATH_SCAN) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
   if (path == VRS_PATH_AUTO) path = (q >= 8 && gp.ok) ? VRS_PATH_GEMM : VRS_PATH_SCAN;
   if (path == VRS_PATH_GEMM && !gp.ok) return fail(VRS_EUNSUPPORTED, "tensor-core path does not support this shape");
+  if (path == VRS_PATH_GEMM && rows_req == VRS_ROWS_GATHER)
+    return fail(VRS_EUNSUPPORTED, "tensor-core path: gathered rows are not implemented yet (use masked)");
 
   int qg = 0, P = 0;
   if (path == VRS_PATH_SCAN) {
@@ -303,7 +305,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     P = gp.P;
   }
   const size_t nwords = (size_t)((n + 31) / 32);
-  const size_t part_entries = (size_t)P * q * kprime;
+  const size_t part_entries = path == VRS_PATH_SCAN ? (size_t)P * q * kprime : 0;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
@@ -320,18 +322,23 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
 
   int launches = 0;
-  if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
-
+  const float *lk = part_key;
+  const int32_t *li = part_id;
+  int32_t stride = kprime, kread = kprime;
   if (path == VRS_PATH_SCAN) {
+    if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
     ScanArgs a{ix->X, n, d, sel_ids, count, queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime,
                part_key, part_id, P};
     CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
   } else {
-    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_req == VRS_ROWS_MASKED ? 1 : 0,
+    // tensor-core path streams full row tiles masked by the selection bitmap
+    if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, nullptr, count, sel_scratch, stream, &launches));
+    GemmArgs a{ix->X, n, d, nullptr, count, identity ? nullptr : bitmap, 1,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
     CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
+    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread);
   }
-  FinalizeArgs f{part_key, part_id, P, kprime, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
+  FinalizeArgs f{lk, li, P, kprime, stride, kread, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   CUDA_TRY(launch_finalize(f, stream, &launches));
   g_last_path = path;
   g_last_launches = launches;

@@ -65,13 +65,17 @@ struct GemmArgs {
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
+void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
+                int32_t *stride, int32_t *kread);
 
 // finalize.cu -- K7'/K12' merge + exact re-score; K10' shard merge
 struct FinalizeArgs {
   const float *part_key;   // [P][q][kprime]
   const int32_t *part_id;
   int32_t P;
-  int32_t kprime;
+  int32_t kprime;          // entries selected for the exact re-score
+  int32_t stride;          // list stride in entries
+  int32_t kread;           // entries read per list (<= stride)
   int64_t q;
   const float *X;
   int32_t d;
