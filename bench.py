@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py -- filtered exact top-k queries/sec on B200 (BASELINE.json metric).
+
+One STEP = one pass of the whole hot path over every (selectivity, Q) cell of
+the workload (default configs[1] = "c2": N=1M fp32 d=128 L2-normalised, IP,
+s in {0.1,1,10,100} %, Q in {1,16,256,4096}, k=10): per cell one
+vrs_search (predicate -> selection -> distances -> fused top-k -> exact
+re-score), plus, on N > 1 GPUs, an NCCL all-gather of the per-shard [Q x k]
+candidates and vrs_merge.  value = queries answered per second by the whole
+job (all cells, all ranks' shards merged).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+Multi-GPU: launched by torchrun, one process per GPU; the corpus rows are
+sharded contiguously over the ranks (strong scaling of the workload's N).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "filtered exact top-k queries/sec and % of HBM/tensor roofline at 1/2/4/8 B200"
+UNIT = "queries/s"
+NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense tf32 / bf16
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.lines, self.proc = dev, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(datagen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def cells_of(cfg):
+    return [(s, q) for s in cfg.sels for q in cfg.qs]
+
+
+def workload_desc(cfg, world):
+    return {"workload": f"{cfg.name} (BASELINE.json configs[{list(datagen.CONFIGS).index(cfg.name)}])",
+            "n": cfg.n, "d": cfg.d, "metric": ["l2", "ip", "cos"][cfg.metric], "k": cfg.k,
+            "selectivities": list(cfg.sels), "queries_per_cell": list(cfg.qs), "cells": len(cells_of(cfg)),
+            "data": "synthetic, seeded (datagen)", "l2_flush": "inputs > L2 (corpus %.0f MB)" % (cfg.n * cfg.d * 4 / 1e6),
+            "parallelism": f"rows sharded over {world} GPU(s), NCCL all-gather + merge" if world > 1 else "1 GPU"}
+
+
+# --------------------------------------------------------------------------- oracle legs
+def oracle_sample(cfg, X_h, attrs_h, Q_h, per_sel_queries: int, threads: int):
+    """Time the CPU oracle on `per_sel_queries` queries per selectivity over the full
+    (local) corpus; extrapolate to the step's query mix.  Returns (qps, seconds, desc)."""
+    import oracle
+    tq = {}
+    t_all = 0.0
+    for s in cfg.sels:
+        pred = datagen.predicate(cfg, s)
+        t0 = time.perf_counter()
+        oracle.search(X_h, attrs_h, pred, Q_h[:per_sel_queries], cfg.k, cfg.metric, 0, threads)
+        dt = time.perf_counter() - t0
+        t_all += dt
+        tq[s] = dt / per_sel_queries
+    total_q = sum(q for _, q in cells_of(cfg))
+    total_t = sum(q * tq[s] for s, q in cells_of(cfg))
+    desc = (f"{per_sel_queries} queries x {len(cfg.sels)} selectivities over the full {X_h.shape[0]}-row corpus "
+            f"(oracle: fp64 brute force + sort), per-query time extrapolated to the step's {total_q} queries")
+    return total_q / total_t, t_all, desc, total_t
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))) if torch.cuda.is_available() else "cpu"
+    X, attrs = datagen.corpus(cfg, 0, cfg.n, dev)
+    Q = datagen.queries(cfg, 64, dev)
+    X_h, attrs_h, Q_h = X.cpu().numpy(), [a.cpu().numpy() for a in attrs], Q.cpu().numpy()
+    del X
+    threads = len(os.sched_getaffinity(0))
+    per = 1
+    for _ in range(args.warmup):
+        oracle_sample(cfg, X_h, attrs_h, Q_h, per, threads)
+    times, qps = [], []
+    for _ in range(args.steps):
+        v, t, desc, _ = oracle_sample(cfg, X_h, attrs_h, Q_h, per, threads)
+        times.append(t)
+        qps.append(v)
+    value = statistics.median(qps)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_desc(cfg, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our path
+def main():
+    args = parse()
+    cfg = datagen.CONFIGS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import paper_2403_15807_b200 as vrs
+    vrs.library()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    r0, r1 = cfg.n * rank // world, cfg.n * (rank + 1) // world
+    X, attrs = datagen.corpus(cfg, r0, r1, dev)
+    qmax = max(cfg.qs)
+    Qall = datagen.queries(cfg, qmax, dev)
+    ix = vrs.Index(X, attrs, row_offset=r0)
+    cells = cells_of(cfg)
+    preds = {s: datagen.predicate(cfg, s) for s in cfg.sels}
+    k, metric = cfg.k, cfg.metric
+    bufs = {c: (torch.empty(c[1], k, dtype=torch.int64, device=dev), torch.empty(c[1], k, dtype=torch.float32, device=dev))
+            for c in cells}
+    if world > 1:
+        import torch.distributed as dist
+        gath = {c: (torch.empty(world, c[1], k, dtype=torch.int64, device=dev),
+                    torch.empty(world, c[1], k, dtype=torch.float32, device=dev)) for c in cells}
+    launches = [0]
+
+    def run_cell(c):
+        s, q = c
+        ids, dists = ix.search(Qall[:q], preds[s], k=k, metric=metric, out=bufs[c])
+        launches[0] += vrs.last_launches()
+        if world > 1:
+            gi, gd = gath[c]
+            dist.all_gather_into_tensor(gi, ids)
+            dist.all_gather_into_tensor(gd, dists)
+            out = vrs.merge(gi, gd, k, metric)
+            launches[0] += 1
+            return out
+        return ids, dists
+
+    def step():
+        for c in cells:
+            run_cell(c)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # selection sizes (outside timing) for the algorithmic byte / flop counts
+    nsel = {}
+    for s in cfg.sels:
+        _, cnt, _ = ix.select(preds[s])
+        nsel[s] = int(cnt.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------- timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    gpu_launches = launches[0]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    q_per_step = sum(q for _, q in cells)
+    value = args.steps * q_per_step / (ms / 1e3)
+
+    # ---------------- per-kernel CUDA-event pass (same steps) -> roofline of the dominant kernel
+    vrs.profile(True)
+    vrs.profile_reset()
+    for _ in range(min(args.steps, 5)):
+        step()
+    torch.cuda.synchronize()
+    prof = vrs.profile_read()
+    vrs.profile(False)
+    nprof = min(args.steps, 5)
+    pk = peaks()
+    tf32_peak_sus = pk["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    tf32_peak_burst = pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16
+    d = cfg.d
+    # algorithmic work per step, by kernel
+    flops_gemm = bytes_scan = 0.0
+    n_loc = r1 - r0
+    for s, q in cells:
+        ns = nsel[s]
+        # which path does this cell take?  (AUTO: tensor cores for q >= 8)
+        if q >= 8:
+            flops_gemm += 2.0 * q * ns * d
+        else:
+            bytes_scan += ns * (4.0 * d + 12) + q * 4.0 * d
+    dominant = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    roof = None
+    if dominant == "gemm":
+        t_s = prof["gemm"][0] / 1e3 / nprof
+        ach = flops_gemm / t_s / 1e12
+        roof = {"kernel": "gemm (tcgen05 TF32 + fused top-k)", "bound": "tensor", "achieved": ach,
+                "peak": tf32_peak_sus, "unit": "TFLOP/s", "frac": ach / tf32_peak_sus, "traffic": None,
+                "peak_note": "TF32 = measured bf16 sustained x nominal tf32/bf16 (1.1/2.25)",
+                "frac_vs_burst_peak": ach / tf32_peak_burst,
+                "algorithmic": "2*Q*N_sel*d per cell, summed over the step's tensor-core cells"}
+    elif dominant is not None:
+        t_s = prof[dominant][0] / 1e3 / nprof
+        ach = bytes_scan / t_s / 1e9
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "traffic": None,
+                "algorithmic": "N_sel*(4d+12) + 4*Q*d bytes per scan cell"}
+    if roof is not None:
+        roof["peak_source"] = pk["source"]
+        roof["kernel_share_of_step"] = {kname: v[0] / nprof / (ms / args.steps) for kname, v in prof.items()}
+
+    # ---------------- per-cell timings (events around each cell)
+    cell_out = []
+    for c in cells:
+        s, q = c
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        run_cell(c)
+        torch.cuda.synchronize()
+        reps = 5
+        a.record(stream)
+        for _ in range(reps):
+            run_cell(c)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / reps / 1e3
+        ns = nsel[s]
+        fl = 2.0 * q * ns * d
+        by = n_loc * sum(1 if cfg.attrs[i][0] == "u8" else 4 for i in range(len(cfg.attrs))) + ns * 4.0 * d + q * 4.0 * d + q * k * 12
+        cell_out.append({"sel": s, "q": q, "n_sel": ns, "ms": t * 1e3, "qps": q / t,
+                         "path": "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan",
+                         "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac": fl / t / 1e12 / tf32_peak_sus})
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    h2d = sum(q * d * 4 for _, q in cells)
+    d2h = sum(q * k * 12 for _, q in cells)
+    Qh = Qall.cpu().pin_memory()
+    if world == 1:
+        hbufs = {c: (torch.empty(c[1], k, dtype=torch.int64, pin_memory=True),
+                     torch.empty(c[1], k, dtype=torch.float32, pin_memory=True)) for c in cells}
+        qh = {q: Qh[:q].clone().pin_memory() for q in cfg.qs}
+
+        def e2e_step():
+            for c in cells:
+                s, q = c
+                ix.search_host(qh[q], preds[s], k=k, metric=metric, out=hbufs[c])
+    else:
+        hbufs = {c: (torch.empty(c[1], k, dtype=torch.int64, pin_memory=True),
+                     torch.empty(c[1], k, dtype=torch.float32, pin_memory=True)) for c in cells}
+        qh = {q: Qh[:q].clone().pin_memory() for q in cfg.qs}
+        qd = {q: torch.empty(q, d, device=dev) for q in cfg.qs}
+
+        def e2e_step():
+            for c in cells:
+                s, q = c
+                qd[q].copy_(qh[q], non_blocking=True)
+                ids, dists = ix.search(qd[q], preds[s], k=k, metric=metric, out=bufs[c])
+                gi, gd = gath[c]
+                dist.all_gather_into_tensor(gi, ids)
+                dist.all_gather_into_tensor(gd, dists)
+                mi, md = vrs.merge(gi, gd, k, metric)
+                hbufs[c][0].copy_(mi, non_blocking=True)
+                hbufs[c][1].copy_(md, non_blocking=True)
+            torch.cuda.synchronize()
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ems = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ems], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": args.steps * q_per_step / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h}
+
+    # ---------------- sampled parity + CPU baseline (rank 0, N = 1)
+    parity = None
+    cpu = None
+    if rank == 0 and world == 1 and not (args.no_parity and args.no_cpu_baseline):
+        import oracle
+        oracle.build()
+        X_h, attrs_h = X.cpu().numpy(), [a.cpu().numpy() for a in attrs]
+        Q_h = Qall[:64].cpu().numpy()
+        if not args.no_parity:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from parity import check_topk
+            checked = 0
+            for s, q in [(cfg.sels[1], cfg.qs[1]), (cfg.sels[-1], cfg.qs[-1])]:
+                ids, dists = run_cell((s, q))
+                torch.cuda.synchronize()
+                nq = 3
+                check_topk(ids[:nq].cpu().numpy(), dists[:nq].cpu().numpy(), X_h, attrs_h, preds[s], Q_h[:nq], k,
+                           metric)
+                checked += nq
+            parity = {"checked_queries": checked, "cells": [[cfg.sels[1], cfg.qs[1]], [cfg.sels[-1], cfg.qs[-1]]],
+                      "rule": "SURVEY 8(c) c.5 (1e-3 rel dists, id sets within the k-th band)", "ok": True}
+        if not args.no_cpu_baseline:
+            threads = len(os.sched_getaffinity(0))
+            v, t_all, desc, _ = oracle_sample(cfg, X_h, attrs_h, Q_h, 4, threads)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+                   "sample_seconds": t_all}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "tf32",
+                "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
+                "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+                "parity": parity, "cells": cell_out,
+                "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

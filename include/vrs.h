@@ -200,6 +200,17 @@ VRS_API const char *vrs_last_error(void);
 VRS_API int32_t vrs_last_path(void);
 VRS_API int32_t vrs_last_launches(void);
 
+/*
+ * Kernel timing for the bench (bench.py "roofline"): while enabled, every
+ * kernel libvrs enqueues is bracketed by CUDA events recorded on its launch
+ * stream; vrs_profile_read(i, ...) resolves them (synchronising those events)
+ * and reports per-kernel totals since the last reset.  Returns the number of
+ * kernel names (i past the end leaves the outputs untouched).
+ */
+VRS_API void vrs_profile_enable(int32_t on);
+VRS_API int32_t vrs_profile_read(int32_t i, const char **name, double *total_ms, int64_t *launches);
+VRS_API void vrs_profile_reset(void);
+
 /* Loaded index properties. */
 VRS_API int64_t vrs_index_rows(const vrs_index *ix);
 VRS_API int32_t vrs_index_dim(const vrs_index *ix);

@@ -57,6 +57,27 @@ def last_launches() -> int:
     return int(library().vrs_last_launches())
 
 
+def profile(on: bool = True):
+    """Enable / disable per-kernel CUDA-event timing inside libvrs."""
+    library().vrs_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    library().vrs_profile_reset()
+
+
+def profile_read() -> dict:
+    """{kernel: (total_ms, launches)} since the last reset (synchronises the recorded events)."""
+    lib = library()
+    out = {}
+    n = lib.vrs_profile_read(-1, None, None, None)
+    for i in range(n):
+        name, ms, cnt = ctypes.c_char_p(), ctypes.c_double(), ctypes.c_int64()
+        lib.vrs_profile_read(i, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(cnt))
+        out[name.value.decode()] = (ms.value, cnt.value)
+    return out
+
+
 class Index:
     """vrs_load over one (shard of a) relation: fp32 vectors [n, d] and
     int32 / uint8 attribute columns, all CUDA tensors (borrowed, kept alive here)."""

@@ -24,7 +24,8 @@ MAX_CLAUSES = 8
 
 # every symbol include/vrs.h declares (tests check the library exports them)
 EXPORTS = ("vrs_load", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
-           "vrs_last_error", "vrs_last_path", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim")
+           "vrs_last_error", "vrs_last_path", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
+           "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset")
 
 
 class VrsError(RuntimeError):
@@ -83,6 +84,12 @@ def load_library():
     lib.vrs_index_rows.restype = i64
     lib.vrs_index_dim.argtypes = [p]
     lib.vrs_index_dim.restype = i32
+    lib.vrs_profile_enable.argtypes = [i32]
+    lib.vrs_profile_enable.restype = None
+    lib.vrs_profile_reset.restype = None
+    lib.vrs_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(i64)]
+    lib.vrs_profile_read.restype = i32
     _lib = lib
     return lib
 

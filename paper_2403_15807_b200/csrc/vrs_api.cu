@@ -10,6 +10,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "vrs_kernels.cuh"
 
@@ -31,6 +34,72 @@ struct vrs_index {
   int32_t device;
   int32_t num_sms;
 };
+
+// ---- kernel profiler (CUDA events on the launch stream) --------------------------
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+struct ProfTotal {
+  std::string name;
+  double ms = 0;
+  int64_t n = 0;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_pending;
+std::vector<ProfTotal> g_prof_totals;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  const char *name;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char *n, cudaStream_t st) : name(n), s(st) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_prof_on) return;
+    a = prof_event();
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, s);
+    g_prof_pending.push_back({name, a, b});
+  }
+};
+
+void prof_resolve() {
+  for (auto &r : g_prof_pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto it = std::find_if(g_prof_totals.begin(), g_prof_totals.end(), [&](const ProfTotal &t) { return t.name == r.name; });
+    if (it == g_prof_totals.end()) {
+      g_prof_totals.push_back({r.name, 0, 0});
+      it = g_prof_totals.end() - 1;
+    }
+    it->ms += ms;
+    it->n += 1;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_pending.clear();
+}
+}  // namespace
 
 static thread_local char g_err[512];
 static thread_local int32_t g_last_path = 0;
@@ -167,6 +236,28 @@ static vrs_status make_pred(const vrs_index *ix, const vrs_predicate *pred, Pred
 extern "C" {
 
 const char *vrs_last_error(void) { return g_err; }
+
+void vrs_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+void vrs_profile_reset(void) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  prof_resolve();
+  g_prof_totals.clear();
+}
+
+int32_t vrs_profile_read(int32_t i, const char **name, double *total_ms, int64_t *launches) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  prof_resolve();
+  if (i >= 0 && i < (int32_t)g_prof_totals.size()) {
+    if (name) *name = g_prof_totals[i].name.c_str();
+    if (total_ms) *total_ms = g_prof_totals[i].ms;
+    if (launches) *launches = g_prof_totals[i].n;
+  }
+  return (int32_t)g_prof_totals.size();
+}
 int32_t vrs_last_path(void) { return g_last_path; }
 int32_t vrs_last_launches(void) { return g_last_launches; }
 int64_t vrs_index_rows(const vrs_index *ix) { return ix ? ix->n : -1; }
@@ -326,20 +417,33 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const int32_t *li = part_id;
   int32_t stride = kprime, kread = kprime;
   if (path == VRS_PATH_SCAN) {
-    if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
+    if (!identity) {
+      ProfScope ps("select", stream);
+      CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
+    }
     ScanArgs a{ix->X, n, d, sel_ids, count, queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime,
                part_key, part_id, P};
+    ProfScope ps("scan", stream);
     CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
   } else {
     // tensor-core path streams full row tiles masked by the selection bitmap
-    if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, nullptr, count, sel_scratch, stream, &launches));
+    if (!identity) {
+      ProfScope ps("select", stream);
+      CUDA_TRY(launch_select(pd, n, bitmap, nullptr, count, sel_scratch, stream, &launches));
+    }
     GemmArgs a{ix->X, n, d, nullptr, count, identity ? nullptr : bitmap, 1,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
-    CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
+    {
+      ProfScope ps("gemm", stream);
+      CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
+    }
     gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread);
   }
   FinalizeArgs f{lk, li, P, kprime, stride, kread, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
-  CUDA_TRY(launch_finalize(f, stream, &launches));
+  {
+    ProfScope ps("finalize", stream);
+    CUDA_TRY(launch_finalize(f, stream, &launches));
+  }
   g_last_path = path;
   g_last_launches = launches;
   return VRS_OK;
@@ -410,7 +514,10 @@ vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n
   if (st != VRS_OK) return st;
   int launches = 0;
   MergeArgs a{cand_ids, cand_dists, n_parts, q, k, (int32_t)metric, ids, dists};
-  CUDA_TRY(launch_merge(a, (cudaStream_t)cuda_stream, &launches));
+  {
+    ProfScope ps("merge", (cudaStream_t)cuda_stream);
+    CUDA_TRY(launch_merge(a, (cudaStream_t)cuda_stream, &launches));
+  }
   g_last_launches = launches;
   return VRS_OK;
 }
