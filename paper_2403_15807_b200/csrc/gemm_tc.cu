@@ -44,11 +44,17 @@ constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;
-constexpr int THREADS = 256;
 constexpr int EPI_WARP0 = 4;
-constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (item, query)
-// dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [2][BN] + epilogue histograms
-constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + ACC_STAGES * BN * 12 + 4 * 256 * 4 + 256;
+constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
+constexpr int EPI_COLS = BN / 2;
+constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (item, query, half)
+constexpr int BIAS_STAGES = 4;
+constexpr int STAGE_COLS = 16;  // per-warp key staging: [32 queries][16 columns] fp32, 16-byte-chunk swizzled
+// dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [BIAS_STAGES][BN] + per-warp key staging
+// (the staging area doubles as the compaction histogram)
+constexpr size_t SMEM_BYTES =
+    1024 + (size_t)STAGES * STAGE_BYTES + BIAS_STAGES * BN * 12 + EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
 }  // namespace tc
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -153,8 +159,9 @@ struct TcParams {
   int32_t metric;
   int32_t kp;              // retained entries per (item, query) (pow2 >= k')
   int32_t cap;             // buffer capacity per (item, query)
-  float *cand_key;         // [P][q][cap]
+  float *cand_key;         // [2P][q][cap]
   int32_t *cand_id;
+  uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none yet)
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -232,14 +239,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stage_base = smem;
-  float *bias_a = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES);   // [2][BN]
-  float *bias_b = bias_a + ACC_STAGES * BN;                                   // [2][BN]
-  int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + ACC_STAGES * BN);    // [2][BN]
-  uint32_t *hist = reinterpret_cast<uint32_t *>(row_id + ACC_STAGES * BN);    // [4][256]
+  float *bias_a = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES);     // [BIAS_STAGES][BN]
+  float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
+  int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
+  float *kstage = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [EPI_WARPS][32][STAGE_COLS]
 
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
-  __shared__ __align__(8) uint64_t bfull_bar[ACC_STAGES], bempty_bar[ACC_STAGES];
+  __shared__ __align__(8) uint64_t bfull_bar[BIAS_STAGES], bempty_bar[BIAS_STAGES];
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -251,12 +258,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int s = 0; s < ACC_STAGES; ++s) {
-      mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);
-      mbar_init(&bfull_bar[s], 32);
-      mbar_init(&bempty_bar[s], 4);
-    }
+    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
+    for (int s = 0; s < BIAS_STAGES; ++s) { mbar_init(&bfull_bar[s], 32); mbar_init(&bempty_bar[s], EPI_WARPS); }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); }
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           for (int k = 0; k < BK / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
             tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
           }
-          tc_commit(&empty_bar[stage]);                 // frees the smem slot when these MMAs finish
+          tc_commit(&empty_bar[stage]);                    // frees the smem slot when these MMAs finish
           if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);  // accumulator ready
         }
         __syncwarp();
@@ -318,97 +321,172 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
     }
   } else if (warp == 2) {
-    // ------------------------------------------------ per-row epilogue terms
+    // ------------------------------------------------ per-row epilogue terms (runs BIAS_STAGES tiles ahead)
     for (int t = 0; t < ntiles; ++t) {
-      const int s = t & 1;
-      mbar_wait(&bempty_bar[s], ((t >> 1) & 1) ^ 1);
-      const int64_t row0 = (t_begin + t) * BN;
-      for (int c = lane; c < BN; c += 32) {
-        const int64_t row = row0 + c;
-        bool valid = row < p.n_rows;
-        if (valid && p.bitmap) valid = (__ldg(p.bitmap + (row >> 5)) >> (row & 31)) & 1u;
+      const int s = t % BIAS_STAGES;
+      mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
+      const int64_t row0 = (t_begin + t) * BN + lane * 8;   // this lane: 8 consecutive rows
+      // all loads first (one memory latency per tile)
+      uint32_t word = 0xffffffffu;
+      if (p.bitmap && row0 < p.n_rows) word = __ldg(p.bitmap + (row0 >> 5));
+      float nv[8];
+      const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
+      if (row0 + 8 <= p.n_rows) {
+        const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + row0));
+        const float4 v1 = __ldg(reinterpret_cast<const float4 *>(src + row0) + 1);
+        nv[0] = v0.x; nv[1] = v0.y; nv[2] = v0.z; nv[3] = v0.w; nv[4] = v1.x; nv[5] = v1.y; nv[6] = v1.z; nv[7] = v1.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nv[u] = row0 + u < p.n_rows ? __ldg(src + row0 + u) : 0.f;
+      }
+      float av[8], bv[8];
+      int32_t iv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t row = row0 + u;
+        const bool valid = row < p.n_rows && ((word >> (row & 31)) & 1u);
         float a = 1.f, b = valid ? 0.f : -INFINITY;
         if (p.metric == VRS_L2) {
           a = 2.f;
-          if (valid) b = -__ldg(p.nx2 + row);
+          if (valid) b = -nv[u];
         } else if (p.metric == VRS_COSINE) {
-          a = valid ? __ldg(p.inv_nx + row) : 0.f;
+          a = valid ? nv[u] : 0.f;
         }
-        bias_a[s * BN + c] = a;
-        bias_b[s * BN + c] = b;
-        row_id[s * BN + c] = (int32_t)row;
+        av[u] = a; bv[u] = b; iv[u] = (int32_t)row;
       }
+      float *ba = bias_a + s * BN + lane * 8;
+      float *bb = bias_b + s * BN + lane * 8;
+      int32_t *bi = row_id + s * BN + lane * 8;
+      reinterpret_cast<float4 *>(ba)[0] = make_float4(av[0], av[1], av[2], av[3]);
+      reinterpret_cast<float4 *>(ba)[1] = make_float4(av[4], av[5], av[6], av[7]);
+      reinterpret_cast<float4 *>(bb)[0] = make_float4(bv[0], bv[1], bv[2], bv[3]);
+      reinterpret_cast<float4 *>(bb)[1] = make_float4(bv[4], bv[5], bv[6], bv[7]);
+      reinterpret_cast<int4 *>(bi)[0] = make_int4(iv[0], iv[1], iv[2], iv[3]);
+      reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[4], iv[5], iv[6], iv[7]);
       mbar_arrive(&bfull_bar[s]);
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------ epilogue: fused top-k
-    const int ew = warp - EPI_WARP0;               // == warp % 4: TMEM lane quadrant
-    const int m = ew * 32 + lane;                  // query row within the tile
+    const int ew = warp - EPI_WARP0;
+    const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;                      // which 128 of the tile's 256 columns
+    const int m = quad * 32 + lane;                // query row within the tile
     const int64_t qg = (int64_t)qtile * BM + m;    // global query index
     const bool active = qg < p.q;
-    const int64_t cbase = ((int64_t)split * p.q + (active ? qg : 0)) * p.cap;
+    const int list = split * 2 + half;             // candidate list index
+    const int64_t cbase = ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
     float *ckey = p.cand_key + cbase;
     int32_t *cid = p.cand_id + cbase;
-    uint32_t *whist = hist + ew * 256;
-    float tau = -INFINITY;
+    float *wst = kstage + ew * 32 * STAGE_COLS;
+    uint32_t *whist = reinterpret_cast<uint32_t *>(wst);   // compaction histogram aliases the staging area
+    float tau = active ? -INFINITY : INFINITY;     // inactive lanes never accept
     int cnt = 0;
+
+    // Thresholds: `tau` (own list, strict: later rows have larger ids) and the
+    // query's shared threshold gtau (max over every list's KP-th best key --
+    // any list's KP-th best bounds the global KP-th best from below).  A key is
+    // a candidate iff key > tau and key >= gtau; both fold into `thr`.
+    uint32_t *gtau_q = p.gtau + (active ? qg : 0);
+    auto shared_bound = [](uint32_t o) -> float {   // largest float strictly below the shared key
+      if (o == 0) return -INFINITY;
+      const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+      return nextafterf(__uint_as_float(u), -INFINITY);
+    };
+    float thr = tau;
+    auto compact_needed = [&](int threshold) {
+      uint32_t need = __ballot_sync(0xffffffffu, cnt > threshold);
+      while (need) {
+        const int owner = __ffs(need) - 1;
+        need &= need - 1;
+        const int oc = __shfl_sync(0xffffffffu, cnt, owner);
+        const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
+        const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
+        if (lane == owner) {
+          tau = nt;
+          cnt = p.kp;
+          thr = fmaxf(thr, tau);
+          atomicMax(gtau_q, ordered_u32(tau));
+        }
+      }
+    };
+
+    uint32_t g_next = active ? __ldcg(gtau_q) : 0u;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
-      const uint32_t ph = (t >> 1) & 1;
-      mbar_wait(&bfull_bar[acc], ph);
-      mbar_wait(&tfull_bar[acc], ph);
+      const int bs = t % BIAS_STAGES;
+      if (active) thr = fmaxf(thr, shared_bound(g_next));
+      if (active) g_next = __ldcg(gtau_q);   // consumed at the next tile (latency hidden)
+      mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
+      mbar_wait(&tfull_bar[acc], (t >> 1) & 1);
       tc_fence_after();
-      const float *ba = bias_a + acc * BN;
-      const float *bb = bias_b + acc * BN;
-      const int32_t *rid = row_id + acc * BN;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c0);
-        TMEM_LD_32x32b_X32(taddr, r);
-        tmem_ld_wait();
-        if (active) {
+      const float *ba = bias_a + bs * BN + half * EPI_COLS;
+      const float *bb = bias_b + bs * BN + half * EPI_COLS;
+      const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
+      uint32_t r[2][32];
+      TMEM_LD_32x32b_X32(tbase, r[0]);
+      tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 a4 = *reinterpret_cast<const float4 *>(ba + c0 + i);
-            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c0 + i);
-            const float kk[4] = {fmaf(__uint_as_float(r[i]), a4.x, b4.x), fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y),
-                                 fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z),
-                                 fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w)};
+      for (int c = 0; c < EPI_COLS / 32; ++c) {
+        uint32_t(&cur)[32] = r[c & 1];
+        if (c + 1 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, r[(c + 1) & 1]);
+        float key[32];
+        float kmax0 = -INFINITY, kmax1 = -INFINITY;   // columns 0-15 / 16-31 of the chunk
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (kk[u] > tau) {
-                ckey[cnt] = kk[u];
-                cid[cnt] = rid[c0 + i + u];
-                ++cnt;
+        for (int i = 0; i < 32; i += 4) {
+          const float4 a4 = *reinterpret_cast<const float4 *>(ba + c * 32 + i);
+          const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
+          key[i] = fmaf(__uint_as_float(cur[i]), a4.x, b4.x);
+          key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), a4.y, b4.y);
+          key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), a4.z, b4.z);
+          key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), a4.w, b4.w);
+          const float m4 = fmaxf(fmaxf(key[i], key[i + 1]), fmaxf(key[i + 2], key[i + 3]));
+          if (i < 16) kmax0 = fmaxf(kmax0, m4);
+          else kmax1 = fmaxf(kmax1, m4);
+        }
+        if (__any_sync(0xffffffffu, fmaxf(kmax0, kmax1) > thr)) {
+          // queries (lanes) with a candidate in these 32 columns: make room first (<= 32
+          // appends follow; compaction uses the staging area), then, 16 columns at a
+          // time, stage the keys so the warp processes each flagged query at once
+          compact_needed(p.cap - 32);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t fmask = __ballot_sync(0xffffffffu, (h ? kmax1 : kmax0) > thr);
+            if (!fmask) continue;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)   // row `lane`, 16-byte chunk (i/4) ^ ((lane >> 1) & 3)
+              *reinterpret_cast<float4 *>(wst + lane * STAGE_COLS + (((i >> 2) ^ ((lane >> 1) & 3)) << 2)) =
+                  make_float4(key[h * 16 + i], key[h * 16 + i + 1], key[h * 16 + i + 2], key[h * 16 + i + 3]);
+            __syncwarp();
+            const int col = lane & 15;
+            const int32_t my_row = rid[c * 32 + h * 16 + col];
+            while (fmask) {
+              const int j = __ffs(fmask) - 1;
+              fmask &= fmask - 1;
+              const float tj = __shfl_sync(0xffffffffu, thr, j);
+              const int cj = __shfl_sync(0xffffffffu, cnt, j);
+              const float v = wst[j * STAGE_COLS + (((col >> 2) ^ ((j >> 1) & 3)) << 2) + (col & 3)];
+              const bool take = lane < 16 && v > tj;
+              const uint32_t m = __ballot_sync(0xffffffffu, take);
+              if (take) {
+                const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + j) * p.cap;
+                const int pos = cj + __popc(m & lanemask_lt());
+                p.cand_key[ob + pos] = v;
+                p.cand_id[ob + pos] = my_row;
               }
+              if (lane == j) cnt += __popc(m);
             }
+            __syncwarp();
           }
         }
-        // a buffer that could overflow on the next 32 columns is compacted (warp-cooperative)
-        uint32_t need = __ballot_sync(0xffffffffu, cnt > p.cap - 32);
-        while (need) {
-          const int owner = __ffs(need) - 1;
-          need &= need - 1;
-          const int oc = __shfl_sync(0xffffffffu, cnt, owner);
-          const int64_t ob = ((int64_t)split * p.q + (int64_t)qtile * BM + ew * 32 + owner) * p.cap;
-          const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
-          if (lane == owner) { tau = nt; cnt = p.kp; }
-        }
+        tmem_ld_wait();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) { mbar_arrive(&tempty_bar[acc]); mbar_arrive(&bempty_bar[acc]); }
+      if (lane == 0) { mbar_arrive(&tempty_bar[acc]); mbar_arrive(&bempty_bar[bs]); }
     }
     // final: keep the best KP, pad the rest of the KP window
-    uint32_t need = __ballot_sync(0xffffffffu, cnt > p.kp);
-    while (need) {
-      const int owner = __ffs(need) - 1;
-      need &= need - 1;
-      const int oc = __shfl_sync(0xffffffffu, cnt, owner);
-      const int64_t ob = ((int64_t)split * p.q + (int64_t)qtile * BM + ew * 32 + owner) * p.cap;
-      compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
-      if (lane == owner) cnt = p.kp;
-    }
+    compact_needed(p.kp);
     if (active)
       for (int i = cnt; i < p.kp; ++i) { ckey[i] = -INFINITY; cid[i] = -1; }
   }
@@ -459,9 +537,10 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
   if (!encode_fn()) return g;
   const int64_t qtiles = (q + tc::BM - 1) / tc::BM;
   const int64_t row_tiles = (n_upper + tc::BN - 1) / tc::BN;
-  int64_t P = std::max<int64_t>(1, num_sms / qtiles);
-  // more splits when one wave leaves SMs idle
-  if (P * qtiles < num_sms) P = std::max<int64_t>(P, (num_sms + qtiles - 1) / qtiles);
+  // one CTA per SM; aim for up to 4 waves of (query tile, row split) items while keeping
+  // items >= ~128 row tiles (the fused top-k warms up once per item)
+  int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, row_tiles * qtiles / ((int64_t)num_sms * 128)));
+  int64_t P = std::max<int64_t>(1, (int64_t)num_sms * waves / qtiles);
   P = std::min<int64_t>(P, row_tiles);
   g.P = (int32_t)P;
   g.qtiles = (int32_t)qtiles;
@@ -471,7 +550,7 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
 
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
   const int kp = kp_of(kprime);
-  return (size_t)plan.P * q * kp * tc::CAP_FACTOR * 8 + 512;
+  return (size_t)plan.P * 2 * q * kp * tc::CAP_FACTOR * 8 + (size_t)q * 4 + 1024;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
@@ -493,7 +572,12 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.kp = kp_of(a.kprime);
   p.cap = p.kp * tc::CAP_FACTOR;
   p.cand_key = static_cast<float *>(scratch);
-  p.cand_id = reinterpret_cast<int32_t *>(p.cand_key + (size_t)plan.P * a.q * p.cap);
+  p.cand_id = reinterpret_cast<int32_t *>(p.cand_key + (size_t)plan.P * 2 * a.q * p.cap);
+  p.gtau = reinterpret_cast<uint32_t *>(p.cand_id + (size_t)plan.P * 2 * a.q * p.cap);
+  {
+    cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
@@ -507,11 +591,12 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
 
 // Where the finalize pass reads the GEMM candidate lists.
 void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread) {
+                int32_t *stride, int32_t *kread, int32_t *nlists) {
+  *nlists = plan.P * 2;
   const int kp = kp_of(a.kprime);
   const int cap = kp * tc::CAP_FACTOR;
   *key = static_cast<const float *>(scratch);
-  *id = reinterpret_cast<const int32_t *>(static_cast<const float *>(scratch) + (size_t)plan.P * a.q * cap);
+  *id = reinterpret_cast<const int32_t *>(static_cast<const float *>(scratch) + (size_t)plan.P * 2 * a.q * cap);
   *stride = cap;
   *kread = kp;
 }

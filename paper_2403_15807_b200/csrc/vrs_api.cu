@@ -415,7 +415,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   int launches = 0;
   const float *lk = part_key;
   const int32_t *li = part_id;
-  int32_t stride = kprime, kread = kprime;
+  int32_t stride = kprime, kread = kprime, nlists = P;
   if (path == VRS_PATH_SCAN) {
     if (!identity) {
       ProfScope ps("select", stream);
@@ -437,9 +437,9 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
     }
-    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread);
+    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread, &nlists);
   }
-  FinalizeArgs f{lk, li, P, kprime, stride, kread, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
+  FinalizeArgs f{lk, li, nlists, kprime, stride, kread, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   {
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));

@@ -66,7 +66,7 @@ struct GemmArgs {
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
 void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread);
+                int32_t *stride, int32_t *kread, int32_t *nlists);
 
 // finalize.cu -- K7'/K12' merge + exact re-score; K10' shard merge
 struct FinalizeArgs {

@@ -1,0 +1,36 @@
+"""Run one bench cell a few times (for ncu captures): python tools/run_cell.py --workload c2 --sel 1.0 --q 4096 --reps 2"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_2403_15807_b200 as vrs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2")
+ap.add_argument("--sel", type=float, default=1.0)
+ap.add_argument("--q", type=int, default=4096)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--path", type=int, default=0)
+ap.add_argument("--n", type=int, default=0)
+a = ap.parse_args()
+cfg = datagen.CONFIGS[a.workload]
+n = a.n or cfg.n
+X, attrs = datagen.corpus(cfg, 0, n, "cuda", n=n)
+Q = datagen.queries(cfg, a.q, "cuda")
+ix = vrs.Index(X, attrs)
+pred = datagen.predicate(cfg, a.sel)
+for _ in range(a.reps):
+    ids, d = ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(3):
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+e.record()
+torch.cuda.synchronize()
+print(f"cell {a.workload} sel={a.sel} q={a.q}: {s.elapsed_time(e)/3:.3f} ms/search, path={vrs.last_path()}")
