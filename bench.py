@@ -195,7 +195,8 @@ def main():
     vrs.library()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    r0, r1 = cfg.n * rank // world, cfg.n * (rank + 1) // world
+    from paper_2403_15807_b200.dist import shard_range
+    r0, r1 = shard_range(cfg.n, world, rank)
     X, attrs = datagen.corpus(cfg, r0, r1, dev)
     qmax = max(cfg.qs)
     Qall = datagen.queries(cfg, qmax, dev)
@@ -207,8 +208,7 @@ def main():
             for c in cells}
     if world > 1:
         import torch.distributed as dist
-        gath = {c: (torch.empty(world, c[1], k, dtype=torch.int64, device=dev),
-                    torch.empty(world, c[1], k, dtype=torch.float32, device=dev)) for c in cells}
+        from paper_2403_15807_b200.dist import gather_merge
     launches = [0]
 
     def run_cell(c):
@@ -216,10 +216,7 @@ def main():
         ids, dists = ix.search(Qall[:q], preds[s], k=k, metric=metric, out=bufs[c])
         launches[0] += vrs.last_launches()
         if world > 1:
-            gi, gd = gath[c]
-            dist.all_gather_into_tensor(gi, ids)
-            dist.all_gather_into_tensor(gd, dists)
-            out = vrs.merge(gi, gd, k, metric)
+            out = gather_merge(ids, dists, k, metric)   # NCCL all-gather + vrs_merge
             launches[0] += 1
             return out
         return ids, dists
@@ -357,10 +354,7 @@ def main():
                 s, q = c
                 qd[q].copy_(qh[q], non_blocking=True)
                 ids, dists = ix.search(qd[q], preds[s], k=k, metric=metric, out=bufs[c])
-                gi, gd = gath[c]
-                dist.all_gather_into_tensor(gi, ids)
-                dist.all_gather_into_tensor(gd, dists)
-                mi, md = vrs.merge(gi, gd, k, metric)
+                mi, md = gather_merge(ids, dists, k, metric)
                 hbufs[c][0].copy_(mi, non_blocking=True)
                 hbufs[c][1].copy_(md, non_blocking=True)
             torch.cuda.synchronize()

@@ -146,13 +146,16 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 // ---------------------------------------------------------------- kernel
 struct TcParams {
-  int64_t n_rows;          // row space: n (identity / masked)
+  int64_t n_rows;          // rows of the index (identity / masked row space)
+  const int32_t *ids;      // compacted ascending selection (nullptr: no predicate)
+  const int64_t *count;    // device count of ids
+  int32_t allow_gather;    // gathered-row mode allowed (selectivity switch decides on device)
   int32_t d;
   int32_t nk;              // K blocks = ceil(d / 32)
   int64_t q;
   int32_t qtiles;
   int32_t P;               // splits
-  int64_t row_tiles;       // ceil(n_rows / BN)
+  int64_t row_tiles_max;   // ceil(n_rows / BN)
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
   const float *inv_nx;
@@ -161,6 +164,7 @@ struct TcParams {
   int32_t cap;             // buffer capacity per (item, query)
   float *cand_key;         // [2P][q][cap]
   int32_t *cand_id;
+  const float *X;          // corpus base (gathered-row producer)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none yet)
 };
 
@@ -252,14 +256,25 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qtile = blockIdx.x % p.qtiles;
   const int split = blockIdx.x / p.qtiles;
-  const int64_t t_begin = (p.row_tiles * split) / p.P;
-  const int64_t t_end = (p.row_tiles * (split + 1)) / p.P;
+  // Selectivity-driven row delivery (decided on the device, no host sync):
+  //  gather: the compacted selection is the row space; rows land in SMEM by id
+  //          (cp.async into the 128B-swizzle layout) -- late materialization
+  //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
+  const int64_t n_sel = p.ids ? *p.count : p.n_rows;
+  const bool gather = p.ids != nullptr && (p.allow_gather == 2 || (p.allow_gather == 1 && n_sel * 2 <= p.n_rows));
+  const int64_t n_space = gather ? n_sel : p.n_rows;
+  const int64_t row_tiles = (n_space + BN - 1) / BN;
+  const int64_t t_begin = (row_tiles * split) / p.P;
+  const int64_t t_end = (row_tiles * (split + 1)) / p.P;
   const int ntiles = (int)(t_end - t_begin);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], gather ? 33 : 1); mbar_init(&empty_bar[s], 1); }
     for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
-    for (int s = 0; s < BIAS_STAGES; ++s) { mbar_init(&bfull_bar[s], 32); mbar_init(&bempty_bar[s], EPI_WARPS); }
+    for (int s = 0; s < BIAS_STAGES; ++s) {
+      mbar_init(&bfull_bar[s], 32);
+      mbar_init(&bempty_bar[s], EPI_WARPS + (gather ? 1 : 0));
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); }
@@ -285,9 +300,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *sa = stage_base + stage * STAGE_BYTES;
           uint8_t *sb = sa + A_BYTES;
-          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          mbar_expect_tx(&full_bar[stage], gather ? A_BYTES : STAGE_BYTES);
           tma_load_2d(sa, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          tma_load_2d(sb, &tmap_x, &full_bar[stage], kb * BK, row0);
+          if (!gather) tma_load_2d(sb, &tmap_x, &full_bar[stage], kb * BK, row0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -325,26 +340,47 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % BIAS_STAGES;
       mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
-      const int64_t row0 = (t_begin + t) * BN + lane * 8;   // this lane: 8 consecutive rows
-      // all loads first (one memory latency per tile)
-      uint32_t word = 0xffffffffu;
-      if (p.bitmap && row0 < p.n_rows) word = __ldg(p.bitmap + (row0 >> 5));
-      float nv[8];
+      const int64_t pos0 = (t_begin + t) * BN + lane * 8;   // this lane: 8 consecutive row-space slots
       const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
-      if (row0 + 8 <= p.n_rows) {
-        const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + row0));
-        const float4 v1 = __ldg(reinterpret_cast<const float4 *>(src + row0) + 1);
-        nv[0] = v0.x; nv[1] = v0.y; nv[2] = v0.z; nv[3] = v0.w; nv[4] = v1.x; nv[5] = v1.y; nv[6] = v1.z; nv[7] = v1.w;
-      } else {
+      float nv[8];
+      int32_t iv[8];
+      bool vv[8];
+      if (gather) {
+        if (pos0 + 8 <= n_sel) {
+          const int4 i0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0));
+          const int4 i1 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + 1);
+          iv[0] = i0.x; iv[1] = i0.y; iv[2] = i0.z; iv[3] = i0.w; iv[4] = i1.x; iv[5] = i1.y; iv[6] = i1.z; iv[7] = i1.w;
+        } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) nv[u] = row0 + u < p.n_rows ? __ldg(src + row0 + u) : 0.f;
+          for (int u = 0; u < 8; ++u) iv[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          vv[u] = iv[u] >= 0;
+          nv[u] = vv[u] ? __ldg(src + iv[u]) : 0.f;
+        }
+      } else {
+        uint32_t word = 0xffffffffu;
+        if (p.bitmap && pos0 < p.n_rows) word = __ldg(p.bitmap + (pos0 >> 5));
+        if (pos0 + 8 <= p.n_rows) {
+          const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0));
+          const float4 v1 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + 1);
+          nv[0] = v0.x; nv[1] = v0.y; nv[2] = v0.z; nv[3] = v0.w; nv[4] = v1.x; nv[5] = v1.y; nv[6] = v1.z; nv[7] = v1.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) nv[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t row = pos0 + u;
+          vv[u] = row < p.n_rows && ((word >> (row & 31)) & 1u);
+          iv[u] = (int32_t)row;
+        }
       }
       float av[8], bv[8];
-      int32_t iv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t row = row0 + u;
-        const bool valid = row < p.n_rows && ((word >> (row & 31)) & 1u);
+        const bool valid = vv[u];
         float a = 1.f, b = valid ? 0.f : -INFINITY;
         if (p.metric == VRS_L2) {
           a = 2.f;
@@ -352,7 +388,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         } else if (p.metric == VRS_COSINE) {
           a = valid ? nv[u] : 0.f;
         }
-        av[u] = a; bv[u] = b; iv[u] = (int32_t)row;
+        av[u] = a; bv[u] = b;
       }
       float *ba = bias_a + s * BN + lane * 8;
       float *bb = bias_b + s * BN + lane * 8;
@@ -364,6 +400,53 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       reinterpret_cast<int4 *>(bi)[0] = make_int4(iv[0], iv[1], iv[2], iv[3]);
       reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[4], iv[5], iv[6], iv[7]);
       mbar_arrive(&bfull_bar[s]);
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------ gathered rows (late materialization)
+    // Row r of a tile is X[ids[pos0 + r]]; lane handles 16-byte chunk (lane & 7) of
+    // rows (lane >> 3) + 4i, written at r*128 + ((chunk ^ (r & 7)) << 4): the same
+    // 128B-swizzle K-major layout TMA writes.  cp.async groups complete LAG stages
+    // behind issue; then fence.proxy.async and arrive on the stage's full barrier.
+    if (gather) {
+      constexpr int LAG = 2;
+      int stage = 0, pend_head = 0, npend = 0;
+      uint32_t phase = 0;
+      int pend[LAG + 1] = {0, 0, 0};
+      const int chunk = lane & 7;
+      auto retire_one = [&](bool all) {
+        if (all) cp_async_wait<0>();
+        else cp_async_wait<LAG>();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full_bar[pend[pend_head]]);
+        pend_head = (pend_head + 1) % (LAG + 1);
+        --npend;
+      };
+      for (int t = 0; t < ntiles; ++t) {
+        const int bs = t % BIAS_STAGES;
+        mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
+        const int32_t *rid = row_id + bs * BN;
+        for (int kb = 0; kb < p.nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t *sb = stage_base + stage * STAGE_BYTES + A_BYTES;
+          const int col = kb * BK + chunk * 4;
+#pragma unroll 8
+          for (int i = 0; i < BN / 4; ++i) {
+            const int r = (lane >> 3) + 4 * i;
+            const int32_t id = rid[r];
+            const bool ok = (r + (t_begin + t) * BN < n_sel) && col < p.d;
+            cp_async16(sb + r * 128 + ((chunk ^ (r & 7)) << 4),
+                       ok ? (const void *)(p.X + (int64_t)id * p.d + col) : p.X, ok);
+          }
+          cp_async_commit();
+          pend[(pend_head + npend) % (LAG + 1)] = stage;
+          ++npend;
+          if (npend > LAG) retire_one(false);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bempty_bar[bs]);
+      }
+      while (npend > 0) retire_one(true);
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------ epilogue: fused top-k
@@ -554,7 +637,6 @@ size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
-  if (a.ids != nullptr && !a.masked) return cudaErrorNotSupported;  // gather mode: not in this kernel yet
   CUtensorMap mq, mx;
   if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN)) return cudaErrorInvalidValue;
   TcParams p;
@@ -564,7 +646,11 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.q = a.q;
   p.qtiles = plan.qtiles;
   p.P = plan.P;
-  p.row_tiles = (a.n + tc::BN - 1) / tc::BN;
+  p.row_tiles_max = (a.n + tc::BN - 1) / tc::BN;
+  p.ids = a.ids;
+  p.count = a.count;
+  p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
+  p.X = a.X;
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
   p.inv_nx = a.inv_nx;

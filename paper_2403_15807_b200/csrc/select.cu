@@ -74,25 +74,37 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(PredDev pred, int64
     }
     s_wexcl[lane] = incl - c;
     const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 0) {
-      uint64_t excl = 0;
-      if (tile == 0) {
-        st_volatile_u64(tile_state + tile, kFlagIncl | total);
-      } else {
-        st_volatile_u64(tile_state + tile, kFlagAgg | total);
-        int64_t look = (int64_t)tile - 1;
-        while (look >= 0) {
-          uint64_t s;
+    // warp-parallel decoupled look-back: lane i inspects tile (look - i); the
+    // nearest inclusive prefix ends the walk, aggregates before it are summed
+    uint64_t excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile_u64(tile_state, kFlagIncl | total);
+    } else {
+      if (lane == 0) st_volatile_u64(tile_state + tile, kFlagAgg | total);
+      int64_t look = (int64_t)tile - 1;
+      while (true) {
+        const int64_t i = look - lane;
+        uint64_t st = kFlagIncl;  // before tile 0: inclusive prefix 0
+        if (i >= 0) {
           do {
-            s = ld_volatile_u64(tile_state + look);
-          } while ((s >> 62) == 0);
-          excl += s & kValMask;
-          if ((s >> 62) == 2) break;
-          --look;
+            st = ld_volatile_u64(tile_state + i);
+          } while ((st >> 62) == 0);
         }
+        const uint32_t incl_mask = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int first = incl_mask ? __ffs(incl_mask) - 1 : 32;
+        uint64_t v = (lane <= first) ? (st & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (incl_mask) break;
+        look -= 32;
+      }
+      if (lane == 0) {
         __threadfence();
         st_volatile_u64(tile_state + tile, kFlagIncl | (excl + total));
       }
+    }
+    if (lane == 0) {
       s_prefix = excl;
       if (tile == ntiles - 1) *count = (int64_t)(excl + total);
     }

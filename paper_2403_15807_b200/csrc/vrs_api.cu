@@ -382,8 +382,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   if (path != VRS_PATH_SCAN) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
   if (path == VRS_PATH_AUTO) path = (q >= 8 && gp.ok) ? VRS_PATH_GEMM : VRS_PATH_SCAN;
   if (path == VRS_PATH_GEMM && !gp.ok) return fail(VRS_EUNSUPPORTED, "tensor-core path does not support this shape");
-  if (path == VRS_PATH_GEMM && rows_req == VRS_ROWS_GATHER)
-    return fail(VRS_EUNSUPPORTED, "tensor-core path: gathered rows are not implemented yet (use masked)");
+
 
   int qg = 0, P = 0;
   if (path == VRS_PATH_SCAN) {
@@ -426,12 +425,13 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     ProfScope ps("scan", stream);
     CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
   } else {
-    // tensor-core path streams full row tiles masked by the selection bitmap
+    // tensor-core path: gathered selection or bitmap-masked full tiles, chosen on the device
     if (!identity) {
       ProfScope ps("select", stream);
-      CUDA_TRY(launch_select(pd, n, bitmap, nullptr, count, sel_scratch, stream, &launches));
+      CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
     }
-    GemmArgs a{ix->X, n, d, nullptr, count, identity ? nullptr : bitmap, 1,
+    const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
+    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
     {
       ProfScope ps("gemm", stream);

@@ -52,7 +52,7 @@ struct GemmArgs {
   const int32_t *ids;       // compacted ids (gather) or nullptr (identity)
   const int64_t *count;
   const uint32_t *bitmap;   // selection bitmap (masked mode) or nullptr
-  int32_t masked;           // 1 => stream full tiles, mask by bitmap
+  int32_t masked;           // 0 auto (device-side selectivity switch), 1 force masked, 2 force gathered
   const float *Q;
   int64_t q;
   const float *nx2;

@@ -1,0 +1,57 @@
+"""Row-sharded multi-GPU search (north_star (4)).
+
+One process per GPU (torchrun), NCCL process group.  Rank r owns the
+contiguous rows [r*N/G, (r+1)*N/G) of the corpus (global id = row_offset +
+local id); the queries and the predicate are replicated.  Each rank runs the
+whole single-GPU path on its shard (vrs_search -> exact [Q x k] dists and
+global ids); one all-gather of each output array over NCCL (NVLink 5 /
+NVSwitch) and vrs_merge on every rank give the identical global top-k
+(top-k is decomposable under the (dist, id) total order).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Contiguous row range [r0, r1) of `rank` (sizes differ by at most one row)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world / rank")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def all_gather_rows(t: torch.Tensor, group=None) -> torch.Tensor:
+    """[q, k] on every rank -> [world, q, k] (rank-major), same on every rank."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    try:
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    except (RuntimeError, NotImplementedError, AttributeError):
+        parts = list(out.unbind(0))
+        dist.all_gather(parts, t.contiguous(), group=group)
+    return out
+
+
+def gather_merge(ids: torch.Tensor, dists: torch.Tensor, k: int, metric, group=None, merge_fn=None):
+    """All-gather every rank's exact local top-k and merge (vrs_merge by default)."""
+    if merge_fn is None:
+        from . import merge as merge_fn
+    gi = all_gather_rows(ids, group)
+    gd = all_gather_rows(dists, group)
+    return merge_fn(gi, gd, k, metric)
+
+
+class ShardedIndex:
+    """The calling rank's shard of a row-sharded corpus."""
+
+    def __init__(self, vectors: torch.Tensor, attrs, row_offset: int, group=None):
+        from . import Index
+        self.group = group
+        self.local = Index(vectors, attrs, row_offset=row_offset)
+
+    def search(self, queries, pred=None, k: int = 10, metric="l2", path=None, rows=None):
+        ids, dists = self.local.search(queries, pred, k=k, metric=metric, path=path, rows=rows)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            return gather_merge(ids, dists, k, metric, self.group)
+        return ids, dists

@@ -19,9 +19,10 @@ def vrs():
     return m
 
 
-def _run(vrs, X, attrs, pred, Q, k, metric, off=0):
+def _run(vrs, X, attrs, pred, Q, k, metric, off=0, rows=None):
     ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off)
-    ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=vrs.PATH_GEMM)
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=vrs.PATH_GEMM,
+                           rows=rows)
     torch.cuda.synchronize()
     assert vrs.last_path() == vrs.PATH_GEMM
     return ids.cpu().numpy(), dists.cpu().numpy()
@@ -42,13 +43,14 @@ GEMM_CASES = [
 
 
 @pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: f"n{c[0]}-d{c[1]}-q{c[2]}-k{c[3]}-m{c[4]}")
-def test_gemm_parity(vrs, case):
+@pytest.mark.parametrize("rows", [0, 1, 2], ids=["auto", "gather", "masked"])
+def test_gemm_parity(vrs, case, rows):
     n, d, q, k, metric, pred = case
     rng = np.random.default_rng(n * 7 + d)
     X = rng.standard_normal((n, d)).astype(np.float32)
     attrs = [rng.integers(0, 1000, n).astype(np.int32)]
     Q = rng.standard_normal((q, d)).astype(np.float32)
-    gi, gd = _run(vrs, X, attrs, pred, Q, k, metric)
+    gi, gd = _run(vrs, X, attrs, pred, Q, k, metric, rows=rows)
     check_topk(gi, gd, X, attrs, pred, Q, k, metric)
 
 

@@ -1,0 +1,50 @@
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel:
+python tools/summarize_launches.py launches.csv [--skip-prefix at::] > profiles/..."""
+import collections
+import csv
+import re
+import sys
+
+
+VRS = ("select_kernel", "scan_topk_kernel", "tc_topk_kernel", "finalize_kernel", "merge_kernel", "norms_kernel")
+
+
+def short(name):
+    for v in VRS:
+        if v in name:
+            return v
+    name = re.sub(r"\(.*", "", name)
+    name = re.sub(r"<.*", "", name)
+    return name.split("::")[-1].strip()
+
+
+def main(path):
+    lines = open(path).read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(lines[start:]))
+    agg = collections.OrderedDict()
+    seq = []
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        k = short(r["Kernel Name"])
+        ns = float(r["Metric Value"].replace(",", ""))
+        a = agg.setdefault(k, [0, 0.0])
+        a[0] += 1
+        a[1] += ns
+        seq.append((k, ns, r.get("Grid Size", ""), r.get("Block Size", "")))
+    ours = {k: v for k, v in agg.items() if k in VRS}
+    tot = sum(v[1] for v in ours.values())
+    print(f"# ncu launch list summary ({path}); cold-cache, serialised launches: compare SHARES")
+    print("| kernel | launches | total ms | mean us | share of libvrs time |")
+    print("|---|---|---|---|---|")
+    for k, (n, ns) in sorted(ours.items(), key=lambda kv: -kv[1][1]):
+        print(f"| {k} | {n} | {ns / 1e6:.3f} | {ns / n / 1e3:.1f} | {ns / tot:.3f} |")
+    other = {k: v for k, v in agg.items() if k not in ours}
+    if other:
+        print(f"\nother (torch data generation / copies): {sum(v[0] for v in other.values())} launches, "
+              f"{sum(v[1] for v in other.values()) / 1e6:.3f} ms")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
