@@ -169,24 +169,85 @@ __device__ void warp_sort_desc_d(double *key, int64_t *id, int n) {
 }
 
 
+constexpr int kFinMaxStage = 3072;   // candidates staged in shared memory after pruning
+
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs a) {
   __shared__ int32_t s_id[kFinMaxSel];
   __shared__ float s_key[kFinMaxSel];
   __shared__ double s_score[kFinMaxSel];
   __shared__ int64_t s_sid[kFinMaxSel];
   __shared__ double s_nq;
+  __shared__ float s_ck[kFinMaxStage];
+  __shared__ int32_t s_ci[kFinMaxStage];
+  __shared__ float s_red[kFinThreads / 32];
+  __shared__ int s_nc;
   const int64_t j = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float *q = a.Q + j * a.d;
 
-  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    const int64_t p = c / a.kread, r = c - p * a.kread;
-    const int64_t o = (p * a.q + j) * a.stride + r;
-    id = a.part_id[o];
-    key = a.part_key[o];
-    return id >= 0;
-  };
-  const int m = block_select_top<int32_t>(get, (int64_t)a.P * a.kread, a.kprime, s_id, s_key);
+  // 1. a provable lower bound T0 of the k'-th best key: every list holding >= k'
+  //    entries at or above its own k'-th (scan: sorted lists) / KP-th (tensor
+  //    path: list_tau) best key bounds the union's k'-th best from below
+  float t0 = -INFINITY;
+  for (int l = tid; l < a.P; l += kFinThreads) {
+    if (a.list_tau) {
+      t0 = fmaxf(t0, a.list_tau[(int64_t)l * a.q + j]);
+    } else if (a.sorted) {
+      const int64_t o = ((int64_t)l * a.q + j) * a.stride + (a.kprime - 1);
+      if (a.part_id[o] >= 0) t0 = fmaxf(t0, a.part_key[o]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+  if (lane == 0) s_red[warp] = t0;
+  if (tid == 0) s_nc = 0;
+  __syncthreads();
+  t0 = s_red[0];
+#pragma unroll
+  for (int w = 1; w < kFinThreads / 32; ++w) t0 = fmaxf(t0, s_red[w]);
+
+  // 2. stage the candidates >= T0 in shared memory (one pass over the lists)
+  const int64_t C = (int64_t)a.P * a.kread;
+  for (int64_t c0 = 0; c0 < C; c0 += kFinThreads) {
+    const int64_t c = c0 + tid;
+    float key = -INFINITY;
+    int32_t id = -1;
+    if (c < C) {
+      const int64_t p = c / a.kread, r = c - p * a.kread;
+      const int64_t o = (p * a.q + j) * a.stride + r;
+      id = a.part_id[o];
+      key = a.part_key[o];
+    }
+    const bool keep = id >= 0 && key >= t0;
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(&s_nc, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const int pos = base + __popc(m & lanemask_lt());
+      if (pos < kFinMaxStage) { s_ck[pos] = key; s_ci[pos] = id; }
+    }
+  }
+  __syncthreads();
+  const int nc = s_nc;
+  int m;
+  if (nc <= kFinMaxStage) {
+    auto get_s = [&](int64_t c, float &key, int32_t &id) -> bool {
+      key = s_ck[c];
+      id = s_ci[c];
+      return true;
+    };
+    m = block_select_top<int32_t>(get_s, nc, a.kprime, s_id, s_key);
+  } else {
+    auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
+      const int64_t p = c / a.kread, r = c - p * a.kread;
+      const int64_t o = (p * a.q + j) * a.stride + r;
+      id = a.part_id[o];
+      key = a.part_key[o];
+      return id >= 0 && key >= t0;
+    };
+    m = block_select_top<int32_t>(get, C, a.kprime, s_id, s_key);
+  }
 
   // |q|^2 in fp64 (COSINE only)
   if (warp == 0) {
@@ -245,6 +306,75 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs a) {
       a.dists[o] = pad;
     }
   }
+}
+
+// ---------------------------------------------------------- probe threshold
+// Per query: the kp-th best key among the probe pass's lists (a subset of the
+// rows) -- a provable lower bound of the kp-th best over all rows -- raises the
+// query's shared threshold for the main pass (gemm_tc.cu).
+__global__ void __launch_bounds__(kFinThreads) probe_threshold_kernel(ProbeArgs a) {
+  __shared__ int32_t s_id[kFinMaxSel];
+  __shared__ float s_key[kFinMaxSel];
+  __shared__ float s_red[kFinThreads / 32];
+  const int64_t j = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
+    const int64_t p = c / a.kread, r = c - p * a.kread;
+    const int64_t o = (p * a.q + j) * a.stride + r;
+    id = a.id[o];
+    key = a.key[o];
+    return id >= 0;
+  };
+  const int m = block_select_top<int32_t>(get, (int64_t)a.lists * a.kread, a.kp, s_id, s_key);
+  if (m < a.kp) return;   // fewer than kp candidates sampled: no bound
+  float mn = INFINITY;
+  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) s_red[warp] = mn;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
+    mn = fminf(mn, s_red[0]);
+    atomicMax(a.gtau + j, ordered_u32(mn));
+  }
+}
+
+// Per query: the kp-th best raw key of the sample pass (-inf / NaN = no row).
+__global__ void __launch_bounds__(kFinThreads) sample_threshold_kernel(SampleArgs a) {
+  __shared__ int32_t s_id[kFinMaxSel];
+  __shared__ float s_key[kFinMaxSel];
+  __shared__ float s_red[kFinThreads / 32];
+  const int64_t j = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float *row = a.dense + j * a.ldd;
+  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
+    key = row[c];
+    id = (int32_t)c;
+    return key > -INFINITY;   // false for -inf padding and NaN fill
+  };
+  const int m = block_select_top<int32_t>(get, a.ldd, a.kp, s_id, s_key);
+  if (m < a.kp) return;
+  float mn = INFINITY;
+  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) s_red[warp] = mn;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 0; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
+    atomicMax(a.gtau + j, ordered_u32(mn));
+  }
+}
+
+cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s) {
+  sample_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_threshold(const ProbeArgs &a, cudaStream_t s) {
+  probe_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {

@@ -28,6 +28,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "vrs_kernels.cuh"
@@ -50,7 +53,7 @@ constexpr int EPI_COLS = BN / 2;
 constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (item, query, half)
 constexpr int BIAS_STAGES = 4;
-constexpr int STAGE_COLS = 16;  // per-warp key staging: [32 queries][16 columns] fp32, 16-byte-chunk swizzled
+constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
 // dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [BIAS_STAGES][BN] + per-warp key staging
 // (the staging area doubles as the compaction histogram)
 constexpr size_t SMEM_BYTES =
@@ -155,6 +158,10 @@ struct TcParams {
   int64_t q;
   int32_t qtiles;
   int32_t P;               // splits
+  int32_t tile_step;       // 1: every tile; > 1: probe pass over every tile_step-th tile
+  float *dense;            // sample pass: raw keys [q][ldd] of the first dense_tiles row tiles (no top-k)
+  int32_t ldd;
+  int32_t dense_tiles;
   int64_t row_tiles_max;   // ceil(n_rows / BN)
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
@@ -164,8 +171,12 @@ struct TcParams {
   int32_t cap;             // buffer capacity per (item, query)
   float *cand_key;         // [2P][q][cap]
   int32_t *cand_id;
-  const float *X;          // corpus base (gathered-row producer)
+  const float *X;          // corpus base
+  int64_t xsel_cap;        // rows of the materialised-selection buffer
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none yet)
+  float *list_tau;         // [2P][q] final KP-th best key per list (-inf: list never filled)
+  unsigned long long *stats;  // optional counters: chunks, slow chunks, flagged queries, compactions
+  float *dense_buf;        // host-provided scratch for the sample pass [q][SAMPLE_TILES * BN]
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -236,9 +247,35 @@ __device__ float compact_lane(float *key, int32_t *id, int cnt, int kp, uint32_t
   return __uint_as_float(u);
 }
 
+// Gathered rows iff a selection exists, it is at most half the rows (or forced)
+// and it fits the materialisation buffer.
+__device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t n, int64_t cap) {
+  if (ids == nullptr || allow == 0 || n_sel > cap) return false;
+  return allow == 2 || n_sel * 2 <= n;
+}
+
+// Late materialization ("(re-)materialized into dense
+// vectors"): X_sel[r] = X[ids[r]], one warp per row, 16-byte vector copies.
+// HBM-bound: 2 * 4d bytes per selected row.
+__global__ void __launch_bounds__(256) gather_copy_kernel(const float *__restrict__ X, int32_t d,
+                                                          const int32_t *__restrict__ ids,
+                                                          const int64_t *__restrict__ count, int64_t n, int allow,
+                                                          int64_t cap, float *__restrict__ xsel) {
+  const int64_t n_sel = *count;
+  if (!gather_mode(ids, allow, n_sel, n, cap)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int d4 = d >> 2;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_sel; r += warps) {
+    const float4 *src = reinterpret_cast<const float4 *>(X + (int64_t)__ldg(ids + r) * d);
+    float4 *dst = reinterpret_cast<float4 *>(xsel + r * d);
+    for (int i = lane; i < d4; i += 32) dst[i] = __ldg(src + i);
+  }
+}
+
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
-                   TcParams p) {
+                   const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -257,27 +294,40 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int qtile = blockIdx.x % p.qtiles;
   const int split = blockIdx.x / p.qtiles;
   // Selectivity-driven row delivery (decided on the device, no host sync):
-  //  gather: the compacted selection is the row space; rows land in SMEM by id
-  //          (cp.async into the 128B-swizzle layout) -- late materialization
+  //  gather: the selection was materialised densely (gather_copy_kernel, late
+  //          materialization) and streams by TMA from X_sel; ids map rows back
   //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
   const int64_t n_sel = p.ids ? *p.count : p.n_rows;
-  const bool gather = p.ids != nullptr && (p.allow_gather == 2 || (p.allow_gather == 1 && n_sel * 2 <= p.n_rows));
+  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.n_rows, p.xsel_cap);
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;
-  const int64_t t_begin = (row_tiles * split) / p.P;
-  const int64_t t_end = (row_tiles * (split + 1)) / p.P;
-  const int ntiles = (int)(t_end - t_begin);
+  // splits actually used: >= 16 row tiles per item when the (device-side) row
+  // space allows -- the fused top-k warms up once per item; CTAs of unused
+  // splits only publish empty candidate lists
+  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
+  const int64_t t_end = split < p_eff ? (p.dense ? std::min<int64_t>(row_tiles, p.dense_tiles)
+                                                 : (row_tiles * (split + 1)) / p_eff)
+                                      : 0;
+  // probe pass (tile_step > 1): every tile_step-th tile of the item, and only when
+  // the item is long enough for a threshold to pay off
+  const int64_t span = t_end - t_begin;
+  // probe: ~1/tile_step of the item's tiles (at least 4 of them, at most every 2nd)
+  const int step = p.tile_step == 1 ? 1 : (int)std::max<int64_t>(2, std::min<int64_t>(p.tile_step, span / 4));
+  // (the probe only pays off for masked full tiles: the gathered selection is short)
+  const int ntiles = p.tile_step == 1 ? (int)span : (span >= 8 && !gather ? (int)((span + step - 1) / step) : 0);
+  auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], gather ? 33 : 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
-      mbar_init(&bempty_bar[s], EPI_WARPS + (gather ? 1 : 0));
+      mbar_init(&bempty_bar[s], EPI_WARPS);
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); prefetch_tmap(&tmap_g); }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
                  "n"(TMEM_COLS)
@@ -295,14 +345,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = (int)((t_begin + t) * BN);
+        const int row0 = (int)(tile_of(t) * BN);
         for (int kb = 0; kb < p.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *sa = stage_base + stage * STAGE_BYTES;
           uint8_t *sb = sa + A_BYTES;
-          mbar_expect_tx(&full_bar[stage], gather ? A_BYTES : STAGE_BYTES);
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
           tma_load_2d(sa, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          if (!gather) tma_load_2d(sb, &tmap_x, &full_bar[stage], kb * BK, row0);
+          tma_load_2d(sb, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -340,7 +390,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % BIAS_STAGES;
       mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
-      const int64_t pos0 = (t_begin + t) * BN + lane * 8;   // this lane: 8 consecutive row-space slots
+      const int64_t pos0 = tile_of(t) * BN + lane * 8;   // this lane: 8 consecutive row-space slots
       const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
       float nv[8];
       int32_t iv[8];
@@ -401,53 +451,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[4], iv[5], iv[6], iv[7]);
       mbar_arrive(&bfull_bar[s]);
     }
-  } else if (warp == 3) {
-    // ------------------------------------------------ gathered rows (late materialization)
-    // Row r of a tile is X[ids[pos0 + r]]; lane handles 16-byte chunk (lane & 7) of
-    // rows (lane >> 3) + 4i, written at r*128 + ((chunk ^ (r & 7)) << 4): the same
-    // 128B-swizzle K-major layout TMA writes.  cp.async groups complete LAG stages
-    // behind issue; then fence.proxy.async and arrive on the stage's full barrier.
-    if (gather) {
-      constexpr int LAG = 2;
-      int stage = 0, pend_head = 0, npend = 0;
-      uint32_t phase = 0;
-      int pend[LAG + 1] = {0, 0, 0};
-      const int chunk = lane & 7;
-      auto retire_one = [&](bool all) {
-        if (all) cp_async_wait<0>();
-        else cp_async_wait<LAG>();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&full_bar[pend[pend_head]]);
-        pend_head = (pend_head + 1) % (LAG + 1);
-        --npend;
-      };
-      for (int t = 0; t < ntiles; ++t) {
-        const int bs = t % BIAS_STAGES;
-        mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
-        const int32_t *rid = row_id + bs * BN;
-        for (int kb = 0; kb < p.nk; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t *sb = stage_base + stage * STAGE_BYTES + A_BYTES;
-          const int col = kb * BK + chunk * 4;
-#pragma unroll 8
-          for (int i = 0; i < BN / 4; ++i) {
-            const int r = (lane >> 3) + 4 * i;
-            const int32_t id = rid[r];
-            const bool ok = (r + (t_begin + t) * BN < n_sel) && col < p.d;
-            cp_async16(sb + r * 128 + ((chunk ^ (r & 7)) << 4),
-                       ok ? (const void *)(p.X + (int64_t)id * p.d + col) : p.X, ok);
-          }
-          cp_async_commit();
-          pend[(pend_head + npend) % (LAG + 1)] = stage;
-          ++npend;
-          if (npend > LAG) retire_one(false);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bempty_bar[bs]);
-      }
-      while (npend > 0) retire_one(true);
-    }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------ epilogue: fused top-k
     const int ew = warp - EPI_WARP0;
@@ -476,6 +479,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       return nextafterf(__uint_as_float(u), -INFINITY);
     };
     float thr = tau;
+    uint32_t st_chunks = 0, st_slow = 0, st_flag = 0, st_comp = 0;
     auto compact_needed = [&](int threshold) {
       uint32_t need = __ballot_sync(0xffffffffu, cnt > threshold);
       while (need) {
@@ -484,6 +488,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int oc = __shfl_sync(0xffffffffu, cnt, owner);
         const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
         const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
+        ++st_comp;
         if (lane == owner) {
           tau = nt;
           cnt = p.kp;
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         uint32_t(&cur)[32] = r[c & 1];
         if (c + 1 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, r[(c + 1) & 1]);
         float key[32];
-        float kmax0 = -INFINITY, kmax1 = -INFINITY;   // columns 0-15 / 16-31 of the chunk
+        uint32_t amask = 0;   // bit i: column i of this chunk beats the query's threshold
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 a4 = *reinterpret_cast<const float4 *>(ba + c * 32 + i);
@@ -523,44 +528,53 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), a4.y, b4.y);
           key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), a4.z, b4.z);
           key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), a4.w, b4.w);
-          const float m4 = fmaxf(fmaxf(key[i], key[i + 1]), fmaxf(key[i + 2], key[i + 3]));
-          if (i < 16) kmax0 = fmaxf(kmax0, m4);
-          else kmax1 = fmaxf(kmax1, m4);
         }
-        if (__any_sync(0xffffffffu, fmaxf(kmax0, kmax1) > thr)) {
-          // queries (lanes) with a candidate in these 32 columns: make room first (<= 32
-          // appends follow; compaction uses the staging area), then, 16 columns at a
-          // time, stage the keys so the warp processes each flagged query at once
-          compact_needed(p.cap - 32);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
+        ++st_chunks;
+        if (p.dense) {   // sample pass: raw keys out, no selection
+          if (active) {
+            float *dst = p.dense + qg * p.ldd + tile_of(t) * BN + half * EPI_COLS + c * 32;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4 *>(dst + i) = make_float4(key[i], key[i + 1], key[i + 2], key[i + 3]);
+          }
+          tmem_ld_wait();
+          continue;
+        }
+        if (__any_sync(0xffffffffu, amask != 0)) {
+          ++st_slow;
+          // rare once a threshold exists: make room (<= 32 appends follow; the
+          // compaction histogram aliases the staging rows), re-test against the
+          // possibly raised threshold, then each lane appends its own columns in
+          // row order from its private staging row (16 columns at a time)
+          if (__any_sync(0xffffffffu, cnt + __popc(amask) > p.cap)) {
+            compact_needed(p.cap - 32);
+            amask = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
+          }
+          float *myrow = wst + lane * STAGE_COLS;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            uint32_t fmask = __ballot_sync(0xffffffffu, (h ? kmax1 : kmax0) > thr);
-            if (!fmask) continue;
+            uint32_t m = (amask >> (16 * h)) & 0xffffu;
+            if (m) {
+              st_flag += __popc(m);
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)   // row `lane`, 16-byte chunk (i/4) ^ ((lane >> 1) & 3)
-              *reinterpret_cast<float4 *>(wst + lane * STAGE_COLS + (((i >> 2) ^ ((lane >> 1) & 3)) << 2)) =
-                  make_float4(key[h * 16 + i], key[h * 16 + i + 1], key[h * 16 + i + 2], key[h * 16 + i + 3]);
-            __syncwarp();
-            const int col = lane & 15;
-            const int32_t my_row = rid[c * 32 + h * 16 + col];
-            while (fmask) {
-              const int j = __ffs(fmask) - 1;
-              fmask &= fmask - 1;
-              const float tj = __shfl_sync(0xffffffffu, thr, j);
-              const int cj = __shfl_sync(0xffffffffu, cnt, j);
-              const float v = wst[j * STAGE_COLS + (((col >> 2) ^ ((j >> 1) & 3)) << 2) + (col & 3)];
-              const bool take = lane < 16 && v > tj;
-              const uint32_t m = __ballot_sync(0xffffffffu, take);
-              if (take) {
-                const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + j) * p.cap;
-                const int pos = cj + __popc(m & lanemask_lt());
-                p.cand_key[ob + pos] = v;
-                p.cand_id[ob + pos] = my_row;
+              for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4 *>(myrow + i) =
+                    make_float4(key[h * 16 + i], key[h * 16 + i + 1], key[h * 16 + i + 2], key[h * 16 + i + 3]);
+              const int32_t *rrow = rid + c * 32 + h * 16;
+              while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1;
+                ckey[cnt] = myrow[i];
+                cid[cnt] = rrow[i];
+                ++cnt;
               }
-              if (lane == j) cnt += __popc(m);
             }
-            __syncwarp();
           }
+          __syncwarp();
         }
         tmem_ld_wait();
       }
@@ -569,9 +583,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       if (lane == 0) { mbar_arrive(&tempty_bar[acc]); mbar_arrive(&bempty_bar[bs]); }
     }
     // final: keep the best KP, pad the rest of the KP window
-    compact_needed(p.kp);
-    if (active)
+    if (!p.dense) compact_needed(p.kp);
+    if (p.stats && lane == 0) {
+      atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
+      atomicAdd(p.stats + 1, (unsigned long long)st_slow);
+      atomicAdd(p.stats + 2, (unsigned long long)st_flag);
+      atomicAdd(p.stats + 3, (unsigned long long)st_comp);
+    }
+    if (active && !p.dense) {
       for (int i = cnt; i < p.kp; ++i) { ckey[i] = -INFINITY; cid[i] = -1; }
+      p.list_tau[(int64_t)list * p.q + qg] = tau;
+    }
   }
 
   tc_fence_before();
@@ -595,12 +617,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static bool make_map(CUtensorMap *m, const float *base, int64_t rows, int32_t d, int box_rows) {
+static bool make_map(CUtensorMap *m, const float *base, int64_t rows, int32_t d, int box_rows, int box_cols = tc::BK) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -633,12 +655,16 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
 
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
   const int kp = kp_of(kprime);
-  return (size_t)plan.P * 2 * q * kp * tc::CAP_FACTOR * 8 + (size_t)q * 4 + 1024;
+  return (size_t)plan.P * 2 * q * kp * tc::CAP_FACTOR * 8 + (size_t)q * 4 + (size_t)plan.P * 2 * q * 4 +
+         (size_t)q * 16 * tc::BN * 4 + 4096;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
-  CUtensorMap mq, mx;
-  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN)) return cudaErrorInvalidValue;
+  const int64_t xcap = a.ids ? a.xsel_cap : 0;
+  CUtensorMap mq, mx, mg;
+  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN) ||
+      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, tc::BN))
+    return cudaErrorInvalidValue;
   TcParams p;
   p.n_rows = a.n;
   p.d = a.d;
@@ -651,6 +677,7 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.count = a.count;
   p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
   p.X = a.X;
+  p.xsel_cap = xcap;
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
   p.inv_nx = a.inv_nx;
@@ -660,6 +687,8 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.cand_key = static_cast<float *>(scratch);
   p.cand_id = reinterpret_cast<int32_t *>(p.cand_key + (size_t)plan.P * 2 * a.q * p.cap);
   p.gtau = reinterpret_cast<uint32_t *>(p.cand_id + (size_t)plan.P * 2 * a.q * p.cap);
+  p.list_tau = reinterpret_cast<float *>(p.gtau + ((a.q + 63) / 64) * 64);
+  p.dense_buf = p.list_tau + (((size_t)plan.P * 2 * a.q + 63) / 64) * 64;
   {
     cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
     if (e != cudaSuccess) return e;
@@ -670,14 +699,73 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, p);
+  if (xcap > 0 && p.allow_gather) {
+    gather_copy_kernel<<<4 * 148, 256, 0, s>>>(a.X, a.d, a.ids, a.count, a.n, p.allow_gather, xcap, a.xsel);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+  }
+  static unsigned long long *stats = nullptr;
+  static const bool want_stats = getenv("VRS_STATS") != nullptr;
+  if (want_stats && !stats) cudaMalloc(&stats, 64);
+  p.stats = want_stats ? stats : nullptr;
+  if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
+  // sample pass: raw keys of the first SAMPLE_TILES row tiles for every query ->
+  // per-query kp-th best -> initial shared threshold (no per-item warm-up)
+  constexpr int SAMPLE_TILES = 16;
+  p.dense = nullptr;
+  p.ldd = 0;
+  p.dense_tiles = 0;
+  p.tile_step = 1;
+  static const bool no_sample = getenv("VRS_NO_SAMPLE") != nullptr;
+  static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
+  if (p.row_tiles_max >= 8 && !no_sample) {
+    TcParams ps = p;
+    ps.P = 1;
+    ps.dense = p.dense_buf;
+    ps.ldd = SAMPLE_TILES * tc::BN;
+    ps.dense_tiles = SAMPLE_TILES;
+    cudaError_t e = cudaMemsetAsync(ps.dense, 0xff, (size_t)a.q * ps.ldd * 4, s);   // NaN fill = no row
+    if (e != cudaSuccess) return e;
+    tc_topk_kernel<<<plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
+    SampleArgs sa{ps.dense, ps.ldd, a.q, p.kp, p.gtau};
+    e = launch_sample_threshold(sa, s);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 2;
+  }
+  // probe pass over every PROBE_STEP-th row tile -> per-query threshold -> main pass
+  constexpr int PROBE_STEP = 16;
+  const bool probe = p.row_tiles_max / plan.P >= 8 && !no_probe;   // the kernel re-checks on the selected rows
+  if (probe) {
+    // each probe list keeps only its best kp/4 (>= 8): the union over all lists
+    // still holds >= kp entries, so its kp-th best remains a valid lower bound
+    TcParams pp = p;
+    pp.tile_step = PROBE_STEP;
+    pp.kp = std::max(8, p.kp / 4);
+    pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
+    tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pp);
+    ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
+    cudaError_t e = launch_probe_threshold(pa, s);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 2;
+  }
+  p.tile_step = 1;
+  tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, p);
+  if (want_stats) {
+    unsigned long long h[4];
+    cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[vrs stats] grid=%d P=%d qtiles=%d chunks=%llu slow=%llu (%.3f) flagged=%llu (%.2f/slow) compactions=%llu\n",
+            plan.P * plan.qtiles, plan.P, plan.qtiles, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2],
+            h[1] ? (double)h[2] / h[1] : 0.0, h[3]);
+  }
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
 
 // Where the finalize pass reads the GEMM candidate lists.
 void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread, int32_t *nlists) {
+                int32_t *stride, int32_t *kread, int32_t *nlists, const float **list_tau) {
   *nlists = plan.P * 2;
   const int kp = kp_of(a.kprime);
   const int cap = kp * tc::CAP_FACTOR;
@@ -685,6 +773,8 @@ void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const fl
   *id = reinterpret_cast<const int32_t *>(static_cast<const float *>(scratch) + (size_t)plan.P * 2 * a.q * cap);
   *stride = cap;
   *kread = kp;
+  const uint32_t *gt = reinterpret_cast<const uint32_t *>(*id + (size_t)plan.P * 2 * a.q * cap);
+  *list_tau = reinterpret_cast<const float *>(gt + ((a.q + 63) / 64) * 64);
 }
 
 }  // namespace vrs

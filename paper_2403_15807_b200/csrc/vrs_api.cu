@@ -397,9 +397,16 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const size_t nwords = (size_t)((n + 31) / 32);
   const size_t part_entries = path == VRS_PATH_SCAN ? (size_t)P * q * kprime : 0;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  // gathered tensor-core mode materialises the selection: up to half the rows,
+  // at most ~4 GiB (larger selections stream masked full tiles instead)
+  const int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
+                               ? std::min<int64_t>(rows_req == VRS_ROWS_GATHER ? n : (n + 1) / 2,
+                                                   std::max<int64_t>(1, (int64_t(4) << 30) / ((int64_t)d * 4)))
+                               : 0;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
-                                   path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0});
+                                   path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
+                                   (size_t)xsel_cap * d * 4});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -410,11 +417,13 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *part_key = cv.take<float>(part_entries);
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
+  float *xsel = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap * d) : nullptr;
 
   int launches = 0;
   const float *lk = part_key;
   const int32_t *li = part_id;
-  int32_t stride = kprime, kread = kprime, nlists = P;
+  int32_t stride = kprime, kread = kprime, nlists = P, sorted = 1;
+  const float *list_tau = nullptr;
   if (path == VRS_PATH_SCAN) {
     if (!identity) {
       ProfScope ps("select", stream);
@@ -431,15 +440,16 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
       CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
     }
     const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
-    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode,
+    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
     {
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
     }
-    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread, &nlists);
+    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread, &nlists, &list_tau);
+    sorted = 0;
   }
-  FinalizeArgs f{lk, li, nlists, kprime, stride, kread, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
+  FinalizeArgs f{lk, li, nlists, kprime, stride, kread, sorted, list_tau, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   {
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));

@@ -53,6 +53,8 @@ struct GemmArgs {
   const int64_t *count;
   const uint32_t *bitmap;   // selection bitmap (masked mode) or nullptr
   int32_t masked;           // 0 auto (device-side selectivity switch), 1 force masked, 2 force gathered
+  float *xsel;              // materialised-selection buffer [xsel_cap x d] (gathered mode)
+  int64_t xsel_cap;
   const float *Q;
   int64_t q;
   const float *nx2;
@@ -66,7 +68,7 @@ struct GemmArgs {
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
 void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread, int32_t *nlists);
+                int32_t *stride, int32_t *kread, int32_t *nlists, const float **list_tau);
 
 // finalize.cu -- K7'/K12' merge + exact re-score; K10' shard merge
 struct FinalizeArgs {
@@ -76,6 +78,8 @@ struct FinalizeArgs {
   int32_t kprime;          // entries selected for the exact re-score
   int32_t stride;          // list stride in entries
   int32_t kread;           // entries read per list (<= stride)
+  int32_t sorted;          // lists sorted best-first with >= kprime entries (scan path)
+  const float *list_tau;   // [P][q] per-list KP-th best key (-inf if unknown), or nullptr
   int64_t q;
   const float *X;
   int32_t d;
@@ -87,6 +91,27 @@ struct FinalizeArgs {
   float *dists;            // [q][k]
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches);
+
+struct ProbeArgs {
+  const float *key;        // probe pass lists [lists][q][stride]
+  const int32_t *id;
+  int32_t lists;
+  int32_t stride;
+  int32_t kread;
+  int64_t q;
+  int32_t kp;
+  uint32_t *gtau;          // [q] ordered-u32 shared thresholds (raised with atomicMax)
+};
+cudaError_t launch_probe_threshold(const ProbeArgs &a, cudaStream_t s);
+
+struct SampleArgs {
+  const float *dense;      // [q][ldd] raw keys of the sample pass (NaN / -inf = no row)
+  int32_t ldd;
+  int64_t q;
+  int32_t kp;
+  uint32_t *gtau;
+};
+cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s);
 
 struct MergeArgs {
   const int64_t *cand_ids;

@@ -17,6 +17,7 @@ ap.add_argument("--q", type=int, default=4096)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--graph", type=int, default=1)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.workload]
 n = a.n or cfg.n
@@ -33,4 +34,33 @@ for _ in range(3):
     ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
 e.record()
 torch.cuda.synchronize()
-print(f"cell {a.workload} sel={a.sel} q={a.q}: {s.elapsed_time(e)/3:.3f} ms/search, path={vrs.last_path()}")
+gms = float("nan")
+if a.graph:
+    out = (torch.empty(a.q, cfg.k, dtype=torch.int64, device="cuda"), torch.empty(a.q, cfg.k, device="cuda"))
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, out=out)
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(10):
+        g.replay()
+    e2.record()
+    torch.cuda.synchronize()
+    gms = s2.elapsed_time(e2) / 10
+vrs.profile(True)
+vrs.profile_reset()
+for _ in range(3):
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+torch.cuda.synchronize()
+prof = vrs.profile_read()
+vrs.profile(False)
+ks = " ".join(f"{k}={v[0]/v[1]*1e3:.0f}us" for k, v in prof.items())
+print(f"cell {a.workload} sel={a.sel} q={a.q}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, path={vrs.last_path()} | {ks}")
