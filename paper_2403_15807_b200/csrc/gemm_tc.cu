@@ -273,13 +273,20 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const float *__restric
   }
 }
 
+template <bool AR>   // AR: the query tile stays resident in shared memory (d <= 128)
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pipeline region (STAGES * STAGE_BYTES): AR ? [A: nk x 16 KB][B stages of 32 KB]
+  //                                              : [stages of (A 16 KB | B 32 KB)]
   uint8_t *stage_base = smem;
+  constexpr int SSTRIDE = AR ? B_BYTES : STAGE_BYTES;   // bytes per pipeline stage
+  constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
+  uint8_t *a_res = smem;                                 // AR: resident query tile
+  uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
   float *bias_a = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES);     // [BIAS_STAGES][BN]
   float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
@@ -288,6 +295,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
   __shared__ __align__(8) uint64_t bfull_bar[BIAS_STAGES], bempty_bar[BIAS_STAGES];
+  __shared__ __align__(8) uint64_t afull_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&afull_bar, 1);
     for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
@@ -344,15 +353,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      if (AR && ntiles > 0) {
+        mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
+      }
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)(tile_of(t) * BN);
         for (int kb = 0; kb < p.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t *sa = stage_base + stage * STAGE_BYTES;
-          uint8_t *sb = sa + A_BYTES;
-          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
-          tma_load_2d(sa, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          tma_load_2d(sb, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
+          uint8_t *st = b_base + stage * SSTRIDE;
+          if (AR) {
+            mbar_expect_tx(&full_bar[stage], B_BYTES);
+          } else {
+            mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+            tma_load_2d(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
+          }
+          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -362,6 +378,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     constexpr uint32_t idesc = tf32_idesc(BM, BN);
     int stage = 0;
     uint32_t phase = 0;
+    if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
@@ -372,8 +389,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
+          const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
             tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
@@ -695,10 +712,16 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(tc_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tc::SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tc_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
+  const bool ar = p.nk <= 4 && !no_ar;
+  auto kern = ar ? tc_topk_kernel<true> : tc_topk_kernel<false>;
   if (xcap > 0 && p.allow_gather) {
     gather_copy_kernel<<<4 * 148, 256, 0, s>>>(a.X, a.d, a.ids, a.count, a.n, p.allow_gather, xcap, a.xsel);
     cudaError_t e = cudaGetLastError();
@@ -727,7 +750,7 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     ps.dense_tiles = SAMPLE_TILES;
     cudaError_t e = cudaMemsetAsync(ps.dense, 0xff, (size_t)a.q * ps.ldd * 4, s);   // NaN fill = no row
     if (e != cudaSuccess) return e;
-    tc_topk_kernel<<<plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
+    kern<<<plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
     SampleArgs sa{ps.dense, ps.ldd, a.q, p.kp, p.gtau};
     e = launch_sample_threshold(sa, s);
     if (e != cudaSuccess) return e;
@@ -743,14 +766,14 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     pp.tile_step = PROBE_STEP;
     pp.kp = std::max(8, p.kp / 4);
     pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
-    tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pp);
+    kern<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pp);
     ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
     cudaError_t e = launch_probe_threshold(pa, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
   }
   p.tile_step = 1;
-  tc_topk_kernel<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, p);
+  kern<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, p);
   if (want_stats) {
     unsigned long long h[4];
     cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);

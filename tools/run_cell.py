@@ -18,6 +18,7 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--rows", type=int, default=0)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.workload]
 n = a.n or cfg.n
@@ -26,12 +27,12 @@ Q = datagen.queries(cfg, a.q, "cuda")
 ix = vrs.Index(X, attrs)
 pred = datagen.predicate(cfg, a.sel)
 for _ in range(a.reps):
-    ids, d = ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+    ids, d = ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
 for _ in range(3):
-    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
 e.record()
 torch.cuda.synchronize()
 gms = float("nan")
@@ -40,12 +41,12 @@ if a.graph:
     st = torch.cuda.Stream()
     st.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(st):
-        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, out=out)
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, out=out)
     torch.cuda.current_stream().wait_stream(st)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, out=out)
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, out=out)
     g.replay()
     torch.cuda.synchronize()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -58,7 +59,7 @@ if a.graph:
 vrs.profile(True)
 vrs.profile_reset()
 for _ in range(3):
-    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None)
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
 torch.cuda.synchronize()
 prof = vrs.profile_read()
 vrs.profile(False)
