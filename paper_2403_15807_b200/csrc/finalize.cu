@@ -340,6 +340,8 @@ __global__ void __launch_bounds__(kFinThreads) probe_threshold_kernel(ProbeArgs 
   }
 }
 
+constexpr int kSampleMax = 4096;   // sample keys per query (SAMPLE_TILES x 256 in gemm_tc.cu)
+
 // Per query: the kp-th best raw key of the sample pass (-inf / NaN = no row).
 __global__ void __launch_bounds__(kFinThreads) sample_threshold_kernel(SampleArgs a) {
   __shared__ int32_t s_id[kFinMaxSel];
@@ -347,9 +349,12 @@ __global__ void __launch_bounds__(kFinThreads) sample_threshold_kernel(SampleArg
   __shared__ float s_red[kFinThreads / 32];
   const int64_t j = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float s_row[kSampleMax];
   const float *row = a.dense + j * a.ldd;
+  for (int c = tid; c < a.ldd; c += kFinThreads) s_row[c] = row[c];   // one coalesced pass
+  __syncthreads();
   auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    key = row[c];
+    key = s_row[c];
     id = (int32_t)c;
     return key > -INFINITY;   // false for -inf padding and NaN fill
   };

@@ -278,8 +278,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
   using namespace tc;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
+  // array itself, so the compiler keeps the shared address space (LDS, not LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // pipeline region (STAGES * STAGE_BYTES): AR ? [A: nk x 16 KB][B stages of 32 KB]
   //                                              : [stages of (A 16 KB | B 32 KB)]
   uint8_t *stage_base = smem;
@@ -312,11 +314,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // splits actually used: >= 16 row tiles per item when the (device-side) row
   // space allows -- the fused top-k warms up once per item; CTAs of unused
   // splits only publish empty candidate lists
-  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
-  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
-  const int64_t t_end = split < p_eff ? (p.dense ? std::min<int64_t>(row_tiles, p.dense_tiles)
-                                                 : (row_tiles * (split + 1)) / p_eff)
-                                      : 0;
+  // (sample pass: the first dense_tiles row tiles, split over all P splits)
+  const int64_t t_space = p.dense ? std::min<int64_t>(row_tiles, p.dense_tiles) : row_tiles;
+  const int64_t p_eff = p.dense ? p.P : std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t t_begin = split < p_eff ? (t_space * split) / p_eff : 0;
+  const int64_t t_end = split < p_eff ? (t_space * (split + 1)) / p_eff : 0;
   // probe pass (tile_step > 1): every tile_step-th tile of the item, and only when
   // the item is long enough for a threshold to pay off
   const int64_t span = t_end - t_begin;
@@ -536,18 +538,30 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         uint32_t(&cur)[32] = r[c & 1];
         if (c + 1 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, r[(c + 1) & 1]);
         float key[32];
-        uint32_t amask = 0;   // bit i: column i of this chunk beats the query's threshold
+        float kmax = -INFINITY;
+        if (p.metric == VRS_COSINE) {   // per-row scale 1/|x|
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 a4 = *reinterpret_cast<const float4 *>(ba + c * 32 + i);
-          const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
-          key[i] = fmaf(__uint_as_float(cur[i]), a4.x, b4.x);
-          key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), a4.y, b4.y);
-          key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), a4.z, b4.z);
-          key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), a4.w, b4.w);
+          for (int i = 0; i < 32; i += 4) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(ba + c * 32 + i);
+            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
+            key[i] = fmaf(__uint_as_float(cur[i]), a4.x, b4.x);
+            key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), a4.y, b4.y);
+            key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), a4.z, b4.z);
+            key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), a4.w, b4.w);
+          }
+        } else {                        // constant scale (L2: 2, IP: 1), per-row bias
+          const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
+            key[i] = fmaf(__uint_as_float(cur[i]), sc, b4.x);
+            key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), sc, b4.y);
+            key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), sc, b4.z);
+            key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), sc, b4.w);
+          }
         }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
+        for (int i = 0; i < 32; i += 2) kmax = fmaxf(kmax, fmaxf(key[i], key[i + 1]));
         ++st_chunks;
         if (p.dense) {   // sample pass: raw keys out, no selection
           if (active) {
@@ -559,8 +573,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           tmem_ld_wait();
           continue;
         }
-        if (__any_sync(0xffffffffu, amask != 0)) {
+        if (__any_sync(0xffffffffu, kmax > thr)) {
           ++st_slow;
+          uint32_t amask = 0;   // bit i: column i beats the query's threshold
+#pragma unroll
+          for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
           // rare once a threshold exists: make room (<= 32 appends follow; the
           // compaction histogram aliases the staging rows), re-test against the
           // possibly raised threshold, then each lane appends its own columns in
@@ -744,13 +761,13 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
   if (p.row_tiles_max >= 8 && !no_sample) {
     TcParams ps = p;
-    ps.P = 1;
+    ps.P = std::max(1, std::min(SAMPLE_TILES, 148 / plan.qtiles));
     ps.dense = p.dense_buf;
     ps.ldd = SAMPLE_TILES * tc::BN;
     ps.dense_tiles = SAMPLE_TILES;
     cudaError_t e = cudaMemsetAsync(ps.dense, 0xff, (size_t)a.q * ps.ldd * 4, s);   // NaN fill = no row
     if (e != cudaSuccess) return e;
-    kern<<<plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
+    kern<<<ps.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
     SampleArgs sa{ps.dense, ps.ldd, a.q, p.kp, p.gtau};
     e = launch_sample_threshold(sa, s);
     if (e != cudaSuccess) return e;

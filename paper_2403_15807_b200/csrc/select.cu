@@ -34,12 +34,40 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
   __shared__ uint32_t s_cnt[kSelWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kSelRows + (int64_t)warp * kSelWordsPerWarp * 32;
+  // lane l owns row base + 32w + l for w = 0..31: per clause, all 32 column loads
+  // are issued before any is used (one memory latency per clause, not 32)
+  uint32_t selbits = 0xffffffffu;   // bit w: row base + 32w + lane qualifies
+#pragma unroll
+  for (int w = 0; w < kSelWordsPerWarp; ++w)
+    if (base + (int64_t)w * 32 + lane >= n) selbits &= ~(1u << w);
+  if (pred.empty) selbits = 0;
+#pragma unroll 1
+  for (int c = 0; c < pred.n; ++c) {
+    const ClauseDev cl = pred.c[c];
+    int32_t v[kSelWordsPerWarp];
+    if (cl.type == VRS_ATTR_I32) {
+      const int32_t *col = static_cast<const int32_t *>(cl.col);
+#pragma unroll
+      for (int w = 0; w < kSelWordsPerWarp; ++w) {
+        const int64_t row = base + (int64_t)w * 32 + lane;
+        v[w] = row < n ? __ldg(col + row) : 0;
+      }
+    } else {
+      const uint8_t *col = static_cast<const uint8_t *>(cl.col);
+#pragma unroll
+      for (int w = 0; w < kSelWordsPerWarp; ++w) {
+        const int64_t row = base + (int64_t)w * 32 + lane;
+        v[w] = row < n ? (int32_t)__ldg(col + row) : 0;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < kSelWordsPerWarp; ++w)
+      if (!(cl.lo <= v[w] && v[w] <= cl.hi)) selbits &= ~(1u << w);
+  }
   uint32_t my_word = 0;
-#pragma unroll 8
+#pragma unroll
   for (int w = 0; w < kSelWordsPerWarp; ++w) {
-    const int64_t row = base + (int64_t)w * 32 + lane;
-    const bool sel = (row < n) && eval_pred(pred, row);
-    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    const uint32_t word = __ballot_sync(0xffffffffu, (selbits >> w) & 1u);
     if (lane == w) my_word = word;
   }
   const int64_t wrow = base + (int64_t)lane * 32;
