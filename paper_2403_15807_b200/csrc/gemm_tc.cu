@@ -41,7 +41,8 @@ namespace tc {
 constexpr int BM = 128;         // queries per tile (TMEM lanes)
 constexpr int BN = 256;         // rows per tile (TMEM columns, MMA N)
 constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span
-constexpr int STAGES = 4;
+constexpr int STAGES = 4;          // (48 KB stages) -- the pipeline region holds STAGES * STAGE_BYTES
+constexpr int MAX_STAGES = 8;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -102,6 +103,49 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// ---- CTA-pair (cta_group::2) helpers: the even CTA of a 2-CTA cluster issues the
+// MMA for both; barrier addresses with bit 24 cleared name the even CTA's copy.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
+}
+// TMA executed by both CTAs of the pair; the transaction bytes land on the even CTA's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// MMA completion -> arrive on the barrier at this offset in both CTAs of the pair.
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
                : "memory");
 }
 
@@ -177,6 +221,7 @@ struct TcParams {
   float *list_tau;         // [2P][q] final KP-th best key per list (-inf: list never filled)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, flagged queries, compactions
   float *dense_buf;        // host-provided scratch for the sample pass [q][SAMPLE_TILES * BN]
+  int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -273,7 +318,11 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const float *__restric
   }
 }
 
-template <bool AR>   // AR: the query tile stays resident in shared memory (d <= 128)
+// AR: the query tile stays resident in shared memory (d <= 128).
+// CG: 1 = one CTA per 128-query tile; 2 = CTA pair (cluster of 2) sharing every row
+//     tile: M = 256 queries per MMA, each CTA stages half of the rows (cta_group::2),
+//     halving the L2 -> SM traffic per query.
+template <bool AR, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
@@ -285,7 +334,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // pipeline region (STAGES * STAGE_BYTES): AR ? [A: nk x 16 KB][B stages of 32 KB]
   //                                              : [stages of (A 16 KB | B 32 KB)]
   uint8_t *stage_base = smem;
-  constexpr int SSTRIDE = AR ? B_BYTES : STAGE_BYTES;   // bytes per pipeline stage
+  constexpr int B_LOCAL = B_BYTES / CG;                  // this CTA's share of a row tile
+  constexpr int SSTRIDE = AR ? B_LOCAL : A_BYTES + B_LOCAL;   // bytes per pipeline stage
+  // as many stages as the 192 KB pipeline region holds (TMA latency needs depth)
+  constexpr int NST = ((STAGES * STAGE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
+                          ? ((STAGES * STAGE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
+                          : MAX_STAGES;
   constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
   uint8_t *a_res = smem;                                 // AR: resident query tile
   uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
@@ -294,15 +348,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
   float *kstage = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [EPI_WARPS][32][STAGE_COLS]
 
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t full_bar[MAX_STAGES], empty_bar[MAX_STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
   __shared__ __align__(8) uint64_t bfull_bar[BIAS_STAGES], bempty_bar[BIAS_STAGES];
   __shared__ __align__(8) uint64_t afull_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qtile = blockIdx.x % p.qtiles;
-  const int split = blockIdx.x / p.qtiles;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int qgroups = (p.qtiles + CG - 1) / CG;
+  const int item = blockIdx.x / CG;
+  const int qtile = (item % qgroups) * CG + rank;
+  const int split = item / qgroups;
   // Selectivity-driven row delivery (decided on the device, no host sync):
   //  gather: the selection was materialised densely (gather_copy_kernel, late
   //          materialization) and streams by TMA from X_sel; ids map rows back
@@ -329,9 +386,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&afull_bar, 1);
-    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
+    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS * CG); }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
       mbar_init(&bempty_bar[s], EPI_WARPS);
@@ -340,13 +397,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   }
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); prefetch_tmap(&tmap_g); }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
 
@@ -355,29 +420,32 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // (pair: both CTAs load their own A and their half of B; the even CTA
+      //  accounts for the pair's bytes on its barriers)
+      auto load = [&](void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+        if (CG == 2) tma_load_2d_pair(dst, map, bar, c0, c1);
+        else tma_load_2d(dst, map, bar, c0, c1);
+      };
       if (AR && ntiles > 0) {
-        mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
-        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
+        if (rank == 0) mbar_expect_tx(&afull_bar, CG * p.nk * A_BYTES);
+        for (int kb = 0; kb < p.nk; ++kb) load(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
       }
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = (int)(tile_of(t) * BN);
+        const int row0 = (int)(tile_of(t) * BN) + rank * (BN / CG);
         for (int kb = 0; kb < p.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *st = b_base + stage * SSTRIDE;
-          if (AR) {
-            mbar_expect_tx(&full_bar[stage], B_BYTES);
-          } else {
-            mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
-            tma_load_2d(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          }
-          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * (AR ? B_LOCAL : A_BYTES + B_LOCAL));
+          if (!AR) load(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
+          load(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = tf32_idesc(BM, BN);
+    // ------------------------------------------------ MMA issuer (even CTA of a pair)
+    constexpr uint32_t idesc = tf32_idesc(BM * CG, BN);
+    if (CG == 1 || rank == 0) {
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
@@ -395,80 +463,97 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
-            tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            if (CG == 2) tc_mma_tf32_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
           }
-          tc_commit(&empty_bar[stage]);                    // frees the smem slot when these MMAs finish
-          if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);  // accumulator ready
+          // frees the smem slot(s) when these MMAs finish; accumulator ready after the last K block
+          if (CG == 2) {
+            tc_commit_pair(&empty_bar[stage]);
+            if (kb == p.nk - 1) tc_commit_pair(&tfull_bar[acc]);
+          } else {
+            tc_commit(&empty_bar[stage]);
+            if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
+          }
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == NST) { stage = 0; phase ^= 1; }
       }
     }
+    }
   } else if (warp == 2) {
-    // ------------------------------------------------ per-row epilogue terms (runs BIAS_STAGES tiles ahead)
-    for (int t = 0; t < ntiles; ++t) {
-      const int s = t % BIAS_STAGES;
-      mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
+    // ------------------------------------------------ per-row epilogue terms
+    // Loads for tile t + PF are issued before tile t is written out: the warp is
+    // memory-latency bound otherwise (one ~us round trip per tile).
+    constexpr int PF = 4;
+    const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
+    float nv[PF][8];
+    int32_t iv[PF][8];
+    uint32_t wv[PF];
+    auto fetch = [&](int t, float (&n8)[8], int32_t (&i8)[8], uint32_t &w) {
+      if (t >= ntiles) return;
       const int64_t pos0 = tile_of(t) * BN + lane * 8;   // this lane: 8 consecutive row-space slots
-      const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
-      float nv[8];
-      int32_t iv[8];
-      bool vv[8];
       if (gather) {
         if (pos0 + 8 <= n_sel) {
           const int4 i0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0));
           const int4 i1 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + 1);
-          iv[0] = i0.x; iv[1] = i0.y; iv[2] = i0.z; iv[3] = i0.w; iv[4] = i1.x; iv[5] = i1.y; iv[6] = i1.z; iv[7] = i1.w;
+          i8[0] = i0.x; i8[1] = i0.y; i8[2] = i0.z; i8[3] = i0.w; i8[4] = i1.x; i8[5] = i1.y; i8[6] = i1.z; i8[7] = i1.w;
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) iv[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
+          for (int u = 0; u < 8; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          vv[u] = iv[u] >= 0;
-          nv[u] = vv[u] ? __ldg(src + iv[u]) : 0.f;
-        }
+        for (int u = 0; u < 8; ++u) n8[u] = i8[u] >= 0 ? __ldg(src + i8[u]) : 0.f;
+        w = 0xffffffffu;
       } else {
-        uint32_t word = 0xffffffffu;
-        if (p.bitmap && pos0 < p.n_rows) word = __ldg(p.bitmap + (pos0 >> 5));
+        w = 0xffffffffu;
+        if (p.bitmap && pos0 < p.n_rows) w = __ldg(p.bitmap + (pos0 >> 5));
         if (pos0 + 8 <= p.n_rows) {
           const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0));
           const float4 v1 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + 1);
-          nv[0] = v0.x; nv[1] = v0.y; nv[2] = v0.z; nv[3] = v0.w; nv[4] = v1.x; nv[5] = v1.y; nv[6] = v1.z; nv[7] = v1.w;
+          n8[0] = v0.x; n8[1] = v0.y; n8[2] = v0.z; n8[3] = v0.w; n8[4] = v1.x; n8[5] = v1.y; n8[6] = v1.z; n8[7] = v1.w;
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) nv[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
+          for (int u = 0; u < 8; ++u) n8[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t row = pos0 + u;
-          vv[u] = row < p.n_rows && ((word >> (row & 31)) & 1u);
-          iv[u] = (int32_t)row;
-        }
+        for (int u = 0; u < 8; ++u) i8[u] = pos0 + u < p.n_rows ? (int32_t)(pos0 + u) : -1;
       }
-      float av[8], bv[8];
+    };
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool valid = vv[u];
-        float a = 1.f, b = valid ? 0.f : -INFINITY;
-        if (p.metric == VRS_L2) {
-          a = 2.f;
-          if (valid) b = -nv[u];
-        } else if (p.metric == VRS_COSINE) {
-          a = valid ? nv[u] : 0.f;
+    for (int u = 0; u < PF; ++u) fetch(u, nv[u], iv[u], wv[u]);
+    for (int t0 = 0; t0 < ntiles; t0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int t = t0 + u;
+        if (t >= ntiles) break;
+        const int s = t % BIAS_STAGES;
+        mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
+        const int64_t pos0 = tile_of(t) * BN + lane * 8;
+        float av[8], bv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const bool valid = iv[u][k] >= 0 && (gather || ((wv[u] >> ((pos0 + k) & 31)) & 1u));
+          float a = 1.f, b = valid ? 0.f : -INFINITY;
+          if (p.metric == VRS_L2) {
+            a = 2.f;
+            if (valid) b = -nv[u][k];
+          } else if (p.metric == VRS_COSINE) {
+            a = valid ? nv[u][k] : 0.f;
+          }
+          av[k] = a; bv[k] = b;
         }
-        av[u] = a; bv[u] = b;
+        float *ba = bias_a + s * BN + lane * 8;
+        float *bb = bias_b + s * BN + lane * 8;
+        int32_t *bi = row_id + s * BN + lane * 8;
+        reinterpret_cast<float4 *>(ba)[0] = make_float4(av[0], av[1], av[2], av[3]);
+        reinterpret_cast<float4 *>(ba)[1] = make_float4(av[4], av[5], av[6], av[7]);
+        reinterpret_cast<float4 *>(bb)[0] = make_float4(bv[0], bv[1], bv[2], bv[3]);
+        reinterpret_cast<float4 *>(bb)[1] = make_float4(bv[4], bv[5], bv[6], bv[7]);
+        reinterpret_cast<int4 *>(bi)[0] = make_int4(iv[u][0], iv[u][1], iv[u][2], iv[u][3]);
+        reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[u][4], iv[u][5], iv[u][6], iv[u][7]);
+        mbar_arrive(&bfull_bar[s]);
+        fetch(t + PF, nv[u], iv[u], wv[u]);
       }
-      float *ba = bias_a + s * BN + lane * 8;
-      float *bb = bias_b + s * BN + lane * 8;
-      int32_t *bi = row_id + s * BN + lane * 8;
-      reinterpret_cast<float4 *>(ba)[0] = make_float4(av[0], av[1], av[2], av[3]);
-      reinterpret_cast<float4 *>(ba)[1] = make_float4(av[4], av[5], av[6], av[7]);
-      reinterpret_cast<float4 *>(bb)[0] = make_float4(bv[0], bv[1], bv[2], bv[3]);
-      reinterpret_cast<float4 *>(bb)[1] = make_float4(bv[4], bv[5], bv[6], bv[7]);
-      reinterpret_cast<int4 *>(bi)[0] = make_int4(iv[0], iv[1], iv[2], iv[3]);
-      reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[4], iv[5], iv[6], iv[7]);
-      mbar_arrive(&bfull_bar[s]);
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------ epilogue: fused top-k
@@ -530,6 +615,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
       const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
+      if (p.epi_skip) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
+          else mbar_arrive(&tempty_bar[acc]);
+          mbar_arrive(&bempty_bar[bs]);
+        }
+        continue;
+      }
       uint32_t r[2][32];
       TMEM_LD_32x32b_X32(tbase, r[0]);
       tmem_ld_wait();
@@ -614,7 +709,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) { mbar_arrive(&tempty_bar[acc]); mbar_arrive(&bempty_bar[bs]); }
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
+        else mbar_arrive(&tempty_bar[acc]);
+        mbar_arrive(&bempty_bar[bs]);
+      }
     }
     // final: keep the best KP, pad the rest of the KP window
     if (!p.dense) compact_needed(p.kp);
@@ -631,10 +730,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();   // the pair's MMAs and remote arrivals are done
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
   }
 }
 
@@ -695,9 +798,13 @@ size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
+  // CTA pairs (cta_group::2) halve the L2->SM row traffic per query but add pair
+  // synchronisation; measured slower while the single-CTA pass is MMA-bound, so opt-in
+  static const bool use_pair = getenv("VRS_PAIR") != nullptr;
+  const int bn_rows = (plan.qtiles >= 2 && use_pair) ? tc::BN / 2 : tc::BN;   // a pair stages half a row tile per CTA
   CUtensorMap mq, mx, mg;
-  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN) ||
-      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, tc::BN))
+  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, bn_rows) ||
+      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, bn_rows))
     return cudaErrorInvalidValue;
   TcParams p;
   p.n_rows = a.n;
@@ -729,16 +836,12 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tc::SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(tc_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {tc_topk_kernel<true, 1>, tc_topk_kernel<false, 1>, tc_topk_kernel<true, 2>, tc_topk_kernel<false, 2>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
-  const bool ar = p.nk <= 4 && !no_ar;
-  auto kern = ar ? tc_topk_kernel<true> : tc_topk_kernel<false>;
   if (xcap > 0 && p.allow_gather) {
     gather_copy_kernel<<<4 * 148, 256, 0, s>>>(a.X, a.d, a.ids, a.count, a.n, p.allow_gather, xcap, a.xsel);
     cudaError_t e = cudaGetLastError();
@@ -750,6 +853,30 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   if (want_stats && !stats) cudaMalloc(&stats, 64);
   p.stats = want_stats ? stats : nullptr;
   if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
+  static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
+  static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
+  p.epi_skip = epi_skip ? 1 : 0;
+  const bool ar = p.nk <= 4 && !no_ar;
+  const int cg = bn_rows == tc::BN / 2 ? 2 : 1;
+  auto kern = cg == 2 ? (ar ? tc_topk_kernel<true, 2> : tc_topk_kernel<false, 2>)
+                      : (ar ? tc_topk_kernel<true, 1> : tc_topk_kernel<false, 1>);
+  // grid: (splits x query groups) work items, CG CTAs each (cluster of 2 for pairs)
+  const int qgroups = (plan.qtiles + cg - 1) / cg;
+  auto launch = [&](int splits, const TcParams &pr) -> cudaError_t {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(splits * qgroups * cg));
+    cfg.blockDim = dim3(tc::THREADS);
+    cfg.dynamicSmemBytes = tc::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mq, mx, mg, pr);
+  };
   // sample pass: raw keys of the first SAMPLE_TILES row tiles for every query ->
   // per-query kp-th best -> initial shared threshold (no per-item warm-up)
   constexpr int SAMPLE_TILES = 16;
@@ -761,13 +888,14 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
   if (p.row_tiles_max >= 8 && !no_sample) {
     TcParams ps = p;
-    ps.P = std::max(1, std::min(SAMPLE_TILES, 148 / plan.qtiles));
+    ps.P = std::max(1, std::min(SAMPLE_TILES, 148 / (qgroups * cg)));
     ps.dense = p.dense_buf;
     ps.ldd = SAMPLE_TILES * tc::BN;
     ps.dense_tiles = SAMPLE_TILES;
     cudaError_t e = cudaMemsetAsync(ps.dense, 0xff, (size_t)a.q * ps.ldd * 4, s);   // NaN fill = no row
     if (e != cudaSuccess) return e;
-    kern<<<ps.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, ps);
+    e = launch(ps.P, ps);
+    if (e != cudaSuccess) return e;
     SampleArgs sa{ps.dense, ps.ldd, a.q, p.kp, p.gtau};
     e = launch_sample_threshold(sa, s);
     if (e != cudaSuccess) return e;
@@ -783,14 +911,20 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     pp.tile_step = PROBE_STEP;
     pp.kp = std::max(8, p.kp / 4);
     pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
-    kern<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pp);
+    {
+      cudaError_t el = launch(plan.P, pp);
+      if (el != cudaSuccess) return el;
+    }
     ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
     cudaError_t e = launch_probe_threshold(pa, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
   }
   p.tile_step = 1;
-  kern<<<plan.P * plan.qtiles, tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, p);
+  {
+    cudaError_t el = launch(plan.P, p);
+    if (el != cudaSuccess) return el;
+  }
   if (want_stats) {
     unsigned long long h[4];
     cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
