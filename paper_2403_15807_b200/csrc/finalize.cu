@@ -377,6 +377,41 @@ cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Per query: the kp-th best key over every list's entries so far (part 1 of the
+// main pass) -- a lower bound of the final kp-th best -- raises the shared threshold.
+__global__ void __launch_bounds__(kFinThreads) refine_threshold_kernel(RefineArgs a) {
+  __shared__ int32_t s_id[kFinMaxSel];
+  __shared__ float s_key[kFinMaxSel];
+  __shared__ float s_red[kFinThreads / 32];
+  const int64_t j = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
+    const int64_t l = c / a.cap, r = c - l * a.cap;
+    if (r >= a.cnt[l * a.q + j]) return false;
+    const int64_t o = (l * a.q + j) * a.cap + r;
+    id = a.id[o];
+    key = a.key[o];
+    return true;
+  };
+  const int m = block_select_top<int32_t>(get, (int64_t)a.lists * a.cap, a.kp, s_id, s_key);
+  if (m < a.kp) return;
+  float mn = INFINITY;
+  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) s_red[warp] = mn;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 0; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
+    atomicMax(a.gtau + j, ordered_u32(mn));
+  }
+}
+
+cudaError_t launch_refine_threshold(const RefineArgs &a, cudaStream_t s) {
+  refine_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_probe_threshold(const ProbeArgs &a, cudaStream_t s) {
   probe_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
   return cudaGetLastError();

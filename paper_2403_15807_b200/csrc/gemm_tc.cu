@@ -41,12 +41,12 @@ namespace tc {
 constexpr int BM = 128;         // queries per tile (TMEM lanes)
 constexpr int BN = 256;         // rows per tile (TMEM columns, MMA N)
 constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span
-constexpr int STAGES = 4;          // (48 KB stages) -- the pipeline region holds STAGES * STAGE_BYTES
+constexpr int PIPE_BYTES = 192 * 1024;   // shared-memory pipeline region (A resident and/or stages)
 constexpr int MAX_STAGES = 8;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int ACC_STAGES = 2;
+constexpr int ACC_STAGES = 2;   // accumulator tiles in TMEM (2 x 256 columns)
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
@@ -58,7 +58,7 @@ constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 f
 // dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [BIAS_STAGES][BN] + per-warp key staging
 // (the staging area doubles as the compaction histogram)
 constexpr size_t SMEM_BYTES =
-    1024 + (size_t)STAGES * STAGE_BYTES + BIAS_STAGES * BN * 12 + EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
+    1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
 }  // namespace tc
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -222,6 +222,9 @@ struct TcParams {
   unsigned long long *stats;  // optional counters: chunks, slow chunks, flagged queries, compactions
   float *dense_buf;        // host-provided scratch for the sample pass [q][SAMPLE_TILES * BN]
   int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
+  int32_t part;            // 0: whole item; 1: first 1/PART_DIV of its tiles; 2: the rest (resumes part 1)
+  int32_t *cnt_state;      // [2P][q] list fill carried from part 1 to part 2
+  float *tau_state;        // [2P][q] list threshold carried from part 1 to part 2
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -337,13 +340,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   constexpr int B_LOCAL = B_BYTES / CG;                  // this CTA's share of a row tile
   constexpr int SSTRIDE = AR ? B_LOCAL : A_BYTES + B_LOCAL;   // bytes per pipeline stage
   // as many stages as the 192 KB pipeline region holds (TMA latency needs depth)
-  constexpr int NST = ((STAGES * STAGE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
-                          ? ((STAGES * STAGE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
+  constexpr int NST = ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
+                          ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
                           : MAX_STAGES;
   constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
   uint8_t *a_res = smem;                                 // AR: resident query tile
   uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
-  float *bias_a = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES);     // [BIAS_STAGES][BN]
+  float *bias_a = reinterpret_cast<float *>(smem + PIPE_BYTES);               // [BIAS_STAGES][BN]
   float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
   float *kstage = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [EPI_WARPS][32][STAGE_COLS]
@@ -374,8 +377,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // (sample pass: the first dense_tiles row tiles, split over all P splits)
   const int64_t t_space = p.dense ? std::min<int64_t>(row_tiles, p.dense_tiles) : row_tiles;
   const int64_t p_eff = p.dense ? p.P : std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
-  const int64_t t_begin = split < p_eff ? (t_space * split) / p_eff : 0;
-  const int64_t t_end = split < p_eff ? (t_space * (split + 1)) / p_eff : 0;
+  const int64_t i_begin = split < p_eff ? (t_space * split) / p_eff : 0;
+  const int64_t i_end = split < p_eff ? (t_space * (split + 1)) / p_eff : 0;
+  // two-part main pass: part 1 covers the first 1/PART_DIV of the item's tiles,
+  // a per-query selection over every list then raises the shared threshold, and
+  // part 2 resumes the lists over the remaining tiles
+  constexpr int PART_DIV = 8;
+  const int64_t i_mid = i_begin + (i_end - i_begin + PART_DIV - 1) / PART_DIV;
+  const int64_t t_begin = p.part == 2 ? i_mid : i_begin;
+  const int64_t t_end = p.part == 1 ? i_mid : i_end;
   // probe pass (tile_step > 1): every tile_step-th tile of the item, and only when
   // the item is long enough for a threshold to pay off
   const int64_t span = t_end - t_begin;
@@ -450,8 +460,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t phase = 0;
     if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t & 1;
-      const uint32_t acc_phase = (t >> 1) & 1;
+      const int acc = t % ACC_STAGES;
+      const uint32_t acc_phase = (t / ACC_STAGES) & 1;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -486,37 +496,42 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // memory-latency bound otherwise (one ~us round trip per tile).
     constexpr int PF = 4;
     const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
-    float nv[PF][8];
-    int32_t iv[PF][8];
+    constexpr int RPL = BN / 32;   // rows per lane
+    float nv[PF][RPL];
+    int32_t iv[PF][RPL];
     uint32_t wv[PF];
-    auto fetch = [&](int t, float (&n8)[8], int32_t (&i8)[8], uint32_t &w) {
+    auto fetch = [&](int t, float (&n8)[RPL], int32_t (&i8)[RPL], uint32_t &w) {
       if (t >= ntiles) return;
-      const int64_t pos0 = tile_of(t) * BN + lane * 8;   // this lane: 8 consecutive row-space slots
+      const int64_t pos0 = tile_of(t) * BN + lane * RPL;   // this lane: RPL consecutive row-space slots
       if (gather) {
-        if (pos0 + 8 <= n_sel) {
-          const int4 i0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0));
-          const int4 i1 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + 1);
-          i8[0] = i0.x; i8[1] = i0.y; i8[2] = i0.z; i8[3] = i0.w; i8[4] = i1.x; i8[5] = i1.y; i8[6] = i1.z; i8[7] = i1.w;
+        if (pos0 + RPL <= n_sel) {
+#pragma unroll
+          for (int v = 0; v < RPL / 4; ++v) {
+            const int4 i0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + v);
+            i8[4 * v] = i0.x; i8[4 * v + 1] = i0.y; i8[4 * v + 2] = i0.z; i8[4 * v + 3] = i0.w;
+          }
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
+          for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) n8[u] = i8[u] >= 0 ? __ldg(src + i8[u]) : 0.f;
+        for (int u = 0; u < RPL; ++u) n8[u] = i8[u] >= 0 ? __ldg(src + i8[u]) : 0.f;
         w = 0xffffffffu;
       } else {
         w = 0xffffffffu;
         if (p.bitmap && pos0 < p.n_rows) w = __ldg(p.bitmap + (pos0 >> 5));
-        if (pos0 + 8 <= p.n_rows) {
-          const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0));
-          const float4 v1 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + 1);
-          n8[0] = v0.x; n8[1] = v0.y; n8[2] = v0.z; n8[3] = v0.w; n8[4] = v1.x; n8[5] = v1.y; n8[6] = v1.z; n8[7] = v1.w;
+        if (pos0 + RPL <= p.n_rows) {
+#pragma unroll
+          for (int v = 0; v < RPL / 4; ++v) {
+            const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + v);
+            n8[4 * v] = v0.x; n8[4 * v + 1] = v0.y; n8[4 * v + 2] = v0.z; n8[4 * v + 3] = v0.w;
+          }
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) n8[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
+          for (int u = 0; u < RPL; ++u) n8[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) i8[u] = pos0 + u < p.n_rows ? (int32_t)(pos0 + u) : -1;
+        for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < p.n_rows ? (int32_t)(pos0 + u) : -1;
       }
     };
 #pragma unroll
@@ -528,10 +543,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (t >= ntiles) break;
         const int s = t % BIAS_STAGES;
         mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
-        const int64_t pos0 = tile_of(t) * BN + lane * 8;
-        float av[8], bv[8];
+        const int64_t pos0 = tile_of(t) * BN + lane * RPL;
+        float av[RPL], bv[RPL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < RPL; ++k) {
           const bool valid = iv[u][k] >= 0 && (gather || ((wv[u] >> ((pos0 + k) & 31)) & 1u));
           float a = 1.f, b = valid ? 0.f : -INFINITY;
           if (p.metric == VRS_L2) {
@@ -542,15 +557,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
           av[k] = a; bv[k] = b;
         }
-        float *ba = bias_a + s * BN + lane * 8;
-        float *bb = bias_b + s * BN + lane * 8;
-        int32_t *bi = row_id + s * BN + lane * 8;
-        reinterpret_cast<float4 *>(ba)[0] = make_float4(av[0], av[1], av[2], av[3]);
-        reinterpret_cast<float4 *>(ba)[1] = make_float4(av[4], av[5], av[6], av[7]);
-        reinterpret_cast<float4 *>(bb)[0] = make_float4(bv[0], bv[1], bv[2], bv[3]);
-        reinterpret_cast<float4 *>(bb)[1] = make_float4(bv[4], bv[5], bv[6], bv[7]);
-        reinterpret_cast<int4 *>(bi)[0] = make_int4(iv[u][0], iv[u][1], iv[u][2], iv[u][3]);
-        reinterpret_cast<int4 *>(bi)[1] = make_int4(iv[u][4], iv[u][5], iv[u][6], iv[u][7]);
+#pragma unroll
+        for (int v = 0; v < RPL / 4; ++v) {
+          reinterpret_cast<float4 *>(bias_a + s * BN + lane * RPL)[v] =
+              make_float4(av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3]);
+          reinterpret_cast<float4 *>(bias_b + s * BN + lane * RPL)[v] =
+              make_float4(bv[4 * v], bv[4 * v + 1], bv[4 * v + 2], bv[4 * v + 3]);
+          reinterpret_cast<int4 *>(row_id + s * BN + lane * RPL)[v] =
+              make_int4(iv[u][4 * v], iv[u][4 * v + 1], iv[u][4 * v + 2], iv[u][4 * v + 3]);
+        }
         mbar_arrive(&bfull_bar[s]);
         fetch(t + PF, nv[u], iv[u], wv[u]);
       }
@@ -571,6 +586,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t *whist = reinterpret_cast<uint32_t *>(wst);   // compaction histogram aliases the staging area
     float tau = active ? -INFINITY : INFINITY;     // inactive lanes never accept
     int cnt = 0;
+    if (p.part == 2 && active) {   // resume the list built by part 1
+      cnt = p.cnt_state[(int64_t)list * p.q + qg];
+      tau = p.tau_state[(int64_t)list * p.q + qg];
+    }
 
     // Thresholds: `tau` (own list, strict: later rows have larger ids) and the
     // query's shared threshold gtau (max over every list's KP-th best key --
@@ -604,12 +623,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
     uint32_t g_next = active ? __ldcg(gtau_q) : 0u;
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t & 1;
+      const int acc = t % ACC_STAGES;
       const int bs = t % BIAS_STAGES;
       if (active) thr = fmaxf(thr, shared_bound(g_next));
       if (active) g_next = __ldcg(gtau_q);   // consumed at the next tile (latency hidden)
       mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
-      mbar_wait(&tfull_bar[acc], (t >> 1) & 1);
+      mbar_wait(&tfull_bar[acc], (t / ACC_STAGES) & 1);
       tc_fence_after();
       const float *ba = bias_a + bs * BN + half * EPI_COLS;
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
@@ -715,17 +734,24 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_arrive(&bempty_bar[bs]);
       }
     }
-    // final: keep the best KP, pad the rest of the KP window
-    if (!p.dense) compact_needed(p.kp);
     if (p.stats && lane == 0) {
       atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
       atomicAdd(p.stats + 1, (unsigned long long)st_slow);
       atomicAdd(p.stats + 2, (unsigned long long)st_flag);
       atomicAdd(p.stats + 3, (unsigned long long)st_comp);
     }
+    if (p.part == 1) {   // hand the list over to part 2
+      if (active) {
+        p.cnt_state[(int64_t)list * p.q + qg] = cnt;
+        p.tau_state[(int64_t)list * p.q + qg] = tau;
+      }
+    } else {
+    // final: keep the best KP, pad the rest of the KP window
+    if (!p.dense) compact_needed(p.kp);
     if (active && !p.dense) {
       for (int i = cnt; i < p.kp; ++i) { ckey[i] = -INFINITY; cid[i] = -1; }
       p.list_tau[(int64_t)list * p.q + qg] = tau;
+    }
     }
   }
 
@@ -793,7 +819,7 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
   const int kp = kp_of(kprime);
   return (size_t)plan.P * 2 * q * kp * tc::CAP_FACTOR * 8 + (size_t)q * 4 + (size_t)plan.P * 2 * q * 4 +
-         (size_t)q * 16 * tc::BN * 4 + 4096;
+         (size_t)q * 4096 * 4 + (size_t)plan.P * 2 * q * 8 + 8192;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
@@ -830,6 +856,9 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.gtau = reinterpret_cast<uint32_t *>(p.cand_id + (size_t)plan.P * 2 * a.q * p.cap);
   p.list_tau = reinterpret_cast<float *>(p.gtau + ((a.q + 63) / 64) * 64);
   p.dense_buf = p.list_tau + (((size_t)plan.P * 2 * a.q + 63) / 64) * 64;
+  p.cnt_state = reinterpret_cast<int32_t *>(p.dense_buf + (size_t)a.q * 4096);
+  p.tau_state = reinterpret_cast<float *>(p.cnt_state + (((size_t)plan.P * 2 * a.q + 63) / 64) * 64);
+  p.part = 0;
   {
     cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
     if (e != cudaSuccess) return e;
@@ -875,11 +904,20 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, mq, mx, mg, pr);
+    if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mx, mg, pr);
+    if (want_stats) {
+      unsigned long long h[4];
+      cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      fprintf(stderr, "[vrs stats] part=%d dense=%d grid=%d chunks=%llu slow=%llu (%.3f) lane0-accepts=%llu compactions=%llu\n",
+              pr.part, pr.dense ? 1 : 0, (int)cfg.gridDim.x, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2], h[3]);
+    }
+    return e;
   };
   // sample pass: raw keys of the first SAMPLE_TILES row tiles for every query ->
   // per-query kp-th best -> initial shared threshold (no per-item warm-up)
-  constexpr int SAMPLE_TILES = 16;
+  constexpr int SAMPLE_TILES = 4096 / tc::BN;   // 4096 sampled rows
   p.dense = nullptr;
   p.ldd = 0;
   p.dense_tiles = 0;
@@ -901,37 +939,25 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
   }
-  // probe pass over every PROBE_STEP-th row tile -> per-query threshold -> main pass
-  constexpr int PROBE_STEP = 16;
-  const bool probe = p.row_tiles_max / plan.P >= 8 && !no_probe;   // the kernel re-checks on the selected rows
-  if (probe) {
-    // each probe list keeps only its best kp/4 (>= 8): the union over all lists
-    // still holds >= kp entries, so its kp-th best remains a valid lower bound
-    TcParams pp = p;
-    pp.tile_step = PROBE_STEP;
-    pp.kp = std::max(8, p.kp / 4);
-    pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
-    {
-      cudaError_t el = launch(plan.P, pp);
-      if (el != cudaSuccess) return el;
-    }
-    ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
-    cudaError_t e = launch_probe_threshold(pa, s);
-    if (e != cudaSuccess) return e;
-    if (launches) *launches += 2;
-  }
+  // main pass in two parts with a threshold refinement in between (see kernel)
   p.tile_step = 1;
+  static const bool one_part = getenv("VRS_ONE_PART") != nullptr;
+  const bool two_part = p.row_tiles_max / plan.P >= 16 && !one_part;
+  if (two_part) {
+    p.part = 1;
+    cudaError_t e = launch(plan.P, p);
+    if (e != cudaSuccess) return e;
+    RefineArgs ra{p.cand_key, p.cand_id, p.cnt_state, plan.P * 2, p.cap, a.q, p.kp, p.gtau};
+    e = launch_refine_threshold(ra, s);
+    if (e != cudaSuccess) return e;
+    p.part = 2;
+    if (launches) *launches += 2;
+  } else {
+    p.part = 0;
+  }
   {
     cudaError_t el = launch(plan.P, p);
     if (el != cudaSuccess) return el;
-  }
-  if (want_stats) {
-    unsigned long long h[4];
-    cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "[vrs stats] grid=%d P=%d qtiles=%d chunks=%llu slow=%llu (%.3f) flagged=%llu (%.2f/slow) compactions=%llu\n",
-            plan.P * plan.qtiles, plan.P, plan.qtiles, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2],
-            h[1] ? (double)h[2] / h[1] : 0.0, h[3]);
   }
   if (launches) *launches += 1;
   return cudaGetLastError();

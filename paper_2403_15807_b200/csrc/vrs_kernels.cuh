@@ -113,6 +113,18 @@ struct SampleArgs {
 };
 cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s);
 
+struct RefineArgs {
+  const float *key;        // main-pass lists [lists][q][cap]
+  const int32_t *id;
+  const int32_t *cnt;      // [lists][q] entries so far
+  int32_t lists;
+  int32_t cap;
+  int64_t q;
+  int32_t kp;
+  uint32_t *gtau;
+};
+cudaError_t launch_refine_threshold(const RefineArgs &a, cudaStream_t s);
+
 struct MergeArgs {
   const int64_t *cand_ids;
   const float *cand_dists;
