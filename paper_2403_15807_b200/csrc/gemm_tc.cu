@@ -939,11 +939,15 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
   }
-  // main pass in two parts with a threshold refinement in between (see kernel)
+  // Threshold refinement before the main pass (masked full tiles only; the kernel
+  // switches the probe off on gathered selections):
+  //  default: probe pass over every PROBE_STEP-th row tile -> per-query kp-th best
+  //  VRS_TWO_PART=1: main pass split 1/8 + 7/8 with a refinement over every list in between
   p.tile_step = 1;
-  static const bool one_part = getenv("VRS_ONE_PART") != nullptr;
-  const bool two_part = p.row_tiles_max / plan.P >= 16 && !one_part;
-  if (two_part) {
+  p.part = 0;
+  static const bool two_part_env = getenv("VRS_TWO_PART") != nullptr;
+  constexpr int PROBE_STEP = 16;
+  if (two_part_env && p.row_tiles_max / plan.P >= 16) {
     p.part = 1;
     cudaError_t e = launch(plan.P, p);
     if (e != cudaSuccess) return e;
@@ -952,8 +956,19 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     if (e != cudaSuccess) return e;
     p.part = 2;
     if (launches) *launches += 2;
-  } else {
-    p.part = 0;
+  } else if (p.row_tiles_max / plan.P >= 8 && !no_probe) {
+    // each probe list keeps only its best kp/4 (>= 8): the union over all lists
+    // still holds >= kp entries, so its kp-th best remains a valid lower bound
+    TcParams pp = p;
+    pp.tile_step = PROBE_STEP;
+    pp.kp = std::max(8, p.kp / 4);
+    pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
+    cudaError_t e = launch(plan.P, pp);
+    if (e != cudaSuccess) return e;
+    ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
+    e = launch_probe_threshold(pa, s);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 2;
   }
   {
     cudaError_t el = launch(plan.P, p);
