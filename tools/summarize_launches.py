@@ -6,16 +6,13 @@ import re
 import sys
 
 
-VRS = ("select_kernel", "scan_topk_kernel", "tc_topk_kernel", "finalize_kernel", "merge_kernel", "norms_kernel")
-
-
 def short(name):
-    for v in VRS:
-        if v in name:
-            return v
+    """libvrs kernels live in namespace vrs:: -> 'vrs::<kernel>'; anything else is torch / generation."""
+    mine = "vrs::" in name
     name = re.sub(r"\(.*", "", name)
     name = re.sub(r"<.*", "", name)
-    return name.split("::")[-1].strip()
+    name = name.split("::")[-1].strip()
+    return ("vrs::" + name) if mine else name
 
 
 def main(path):
@@ -33,7 +30,7 @@ def main(path):
         a[0] += 1
         a[1] += ns
         seq.append((k, ns, r.get("Grid Size", ""), r.get("Block Size", "")))
-    ours = {k: v for k, v in agg.items() if k in VRS}
+    ours = {k: v for k, v in agg.items() if k.startswith("vrs::")}
     tot = sum(v[1] for v in ours.values())
     print(f"# ncu launch list summary ({path}); cold-cache, serialised launches: compare SHARES")
     print("| kernel | launches | total ms | mean us | share of libvrs time |")
