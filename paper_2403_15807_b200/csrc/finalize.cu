@@ -1,11 +1,14 @@
 // finalize.cu -- K7'/K12' cross-CTA merge + exact re-score, and K10' vrs_merge.
 //
-// finalize_kernel (one CTA per query): the per-(CTA, query) candidate lists
+// finalize_kernel (one warp per query): the per-(CTA, query) candidate lists
 // written by the distance kernels (scan.cu, gemm_tc.cu) are reduced to the
 // k' best by ranking key with a radix select (ties -> lower id), each of the
 // k' rows is re-scored exactly (fp64 accumulation of the fp32 inputs, rounded
 // once to fp32 -- DESIGN.md "Precision"), and the k best by exact score are
 // written best-first with padding (reading R3).
+//
+// threshold_kernel (one warp per query): the k'-th largest probe slot maximum
+// of the tensor-core path -> the shared threshold of the main pass.
 //
 // merge_kernel (one CTA per query): top-k of n_parts shard results by
 // (dist, global id), the final step of the row-sharded search (north_star (4)).
@@ -169,137 +172,265 @@ __device__ void warp_sort_desc_d(double *key, int64_t *id, int n) {
 }
 
 
-constexpr int kFinMaxStage = 3072;   // candidates staged in shared memory after pruning
+// ------------------------------------------------------ warp-level selection
+constexpr int kFinWarps = 4;     // queries per CTA (one warp each)
+constexpr int kBufCap = 512;     // per-warp candidate buffer (>= 2 k' for every k' <= 256)
 
-__global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs a) {
-  __shared__ int32_t s_id[kFinMaxSel];
-  __shared__ float s_key[kFinMaxSel];
-  __shared__ double s_score[kFinMaxSel];
-  __shared__ int64_t s_sid[kFinMaxSel];
-  __shared__ double s_nq;
-  __shared__ float s_ck[kFinMaxStage];
-  __shared__ int32_t s_ci[kFinMaxStage];
-  __shared__ float s_red[kFinThreads / 32];
-  __shared__ int s_nc;
-  const int64_t j = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// The K-th largest of the u32 values get(i, u) (i < n, only those for which get
+// returns true), by a warp-cooperative radix select (8 bits per pass, histogram
+// in shared memory).  *above = how many values are strictly larger; returns
+// false (and *above = the number of values) when there are fewer than K.
+template <typename Get>
+__device__ bool warp_kth_largest(Get get, int n, int K, uint32_t *hist, uint32_t *out, int *above_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0, mask = 0;
+  int rem = K, above_total = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+      uint32_t u;
+      if (get(i, u) && (u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    // lane l owns bins [255-8l-7, 255-8l] (descending); suffix sums from the top
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { v[t] = hist[255 - 8 * lane - t]; s += v[t]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total < (uint32_t)rem) {   // only on the first pass: fewer than K values
+      *above_out = (int)total;
+      return false;
+    }
+    const uint32_t before = incl - s;
+    int bin = -1, above = 0;
+    if (before < (uint32_t)rem && (uint32_t)rem <= incl) {
+      uint32_t run = before;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (bin < 0 && (uint32_t)rem <= run + v[t]) { bin = 255 - 8 * lane - t; above = (int)run; }
+        if (bin < 0) run += v[t];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, bin >= 0)) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    prefix |= (uint32_t)bin << shift;
+    mask |= 255u << shift;
+    rem -= above;
+    above_total += above;
+    __syncwarp();
+  }
+  *out = prefix;
+  *above_out = above_total;
+  return true;
+}
+
+// Keep exactly the K best of the warp's buffer (key desc, then id asc), in place
+// (requires n >= K).  Returns the ordered key of the K-th best.
+__device__ __noinline__ uint32_t warp_keep_best(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v = 0, idv = 0xffffffffu;
+  int above = 0;
+  warp_kth_largest([&](int i, uint32_t &u) { u = ordered_u32(bk[i]); return true; }, n, K, hist, &v, &above);
+  // ties at v: keep the (K - above) smallest ids (row ids are unique per query)
+  int ties = 0;
+  for (int i = lane; i < n; i += 32) ties += ordered_u32(bk[i]) == v ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+  if (ties > K - above) {
+    uint32_t x = 0;
+    int ab2 = 0;
+    warp_kth_largest([&](int i, uint32_t &u) { u = ~(uint32_t)bi[i]; return ordered_u32(bk[i]) == v; }, n, K - above,
+                     hist, &x, &ab2);
+    idv = ~x;
+  }
+  int out = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    float kv = 0.f;
+    int32_t iv = 0;
+    bool keep = false;
+    if (i < n) {
+      kv = bk[i];
+      iv = bi[i];
+      const uint32_t ok = ordered_u32(kv);
+      keep = ok > v || (ok == v && (uint32_t)iv <= idv);
+    }
+    const uint32_t km = __ballot_sync(0xffffffffu, keep);
+    const int pos = out + __popc(km & lanemask_lt());
+    __syncwarp();
+    if (keep) { bk[pos] = kv; bi[pos] = iv; }
+    out += __popc(km);
+    __syncwarp();
+  }
+  n = out;
+  return v;
+}
+
+// ------------------------------------------------------------------ finalize
+// One warp per query: (1) a provable lower bound of the k'-th best ranking key
+// (the shared probe threshold, or for sorted scan lists the best of their k'-th
+// entries); (2) stream every list entry at or above it into a shared-memory
+// buffer, compacting to the k' best by radix select whenever it fills; (3) keep
+// exactly the k' best (ties -> lower id); (4) re-score those rows exactly (fp64
+// accumulation of the fp32 inputs, one lane per row); (5) sort by exact score
+// (ties -> lower id) and write the k best with padding.
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a) {
+  __shared__ float s_key[kFinWarps][kBufCap];
+  __shared__ int32_t s_id[kFinWarps][kBufCap];
+  __shared__ uint32_t s_hist[kFinWarps][256];
+  __shared__ double s_sc[kFinWarps][kFinMaxSel];
+  __shared__ int64_t s_sid[kFinWarps][kFinMaxSel];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * kFinWarps + w;
+  if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
+  float *bk = s_key[w];
+  int32_t *bi = s_id[w];
+  uint32_t *hist = s_hist[w];
+  const int K = a.kprime;
+
+  // 1. lower bound (ordered key): entries below it cannot be among the k' best
+  uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
+  if (a.sorted && K <= a.kread) {
+    for (int l = lane; l < a.lists; l += 32) {
+      const int64_t o = ((int64_t)l * a.q + j) * a.stride + (K - 1);
+      if (__ldg(a.id + o) >= 0) thr = max(thr, ordered_u32(__ldg(a.key + o)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) thr = max(thr, __shfl_xor_sync(0xffffffffu, thr, o));
+  }
+
+  // 2. stream: lane l walks list l (8 entries per step, loads issued together)
+  int n = 0;
+  for (int l0 = 0; l0 < a.lists; l0 += 32) {
+    const int l = l0 + lane;
+    int c = 0;
+    if (l < a.lists) c = a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread;
+    const int64_t base = ((int64_t)(l < a.lists ? l : 0) * a.q + j) * a.stride;
+    for (int r0 = 0; __any_sync(0xffffffffu, r0 < c); r0 += 8) {
+      float kv[8];
+      int32_t iv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        kv[u] = -INFINITY;
+        iv[u] = -1;
+        if (r0 + u < c) { kv[u] = __ldg(a.key + base + r0 + u); iv[u] = __ldg(a.id + base + r0 + u); }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        bool keep = iv[u] >= 0 && ordered_u32(kv[u]) >= thr;
+        uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (m == 0) continue;
+        if (n + __popc(m) > kBufCap) {
+          thr = max(thr, warp_keep_best(bk, bi, n, K, hist));
+          keep = keep && ordered_u32(kv[u]) >= thr;
+          m = __ballot_sync(0xffffffffu, keep);
+        }
+        if (keep) {
+          const int pos = n + __popc(m & lanemask_lt());
+          bk[pos] = kv[u];
+          bi[pos] = iv[u];
+        }
+        n += __popc(m);
+      }
+      __syncwarp();
+      if (a.sorted && !__any_sync(0xffffffffu, r0 + 8 < c && ordered_u32(kv[7]) >= thr)) break;
+    }
+  }
+  __syncwarp();
+  // 3. exactly the k' best by ranking key
+  if (n > K) warp_keep_best(bk, bi, n, K, hist);
+  const int m = n;
+
+  // 4. exact re-score: the warp reads each candidate row coalesced, 8 rows in
+  //    flight, fp64 accumulation, one butterfly reduction per row
   const float *q = a.Q + j * a.d;
-
-  // 1. a provable lower bound T0 of the k'-th best key: every list holding >= k'
-  //    entries at or above its own k'-th (scan: sorted lists) / KP-th (tensor
-  //    path: list_tau) best key bounds the union's k'-th best from below
-  float t0 = -INFINITY;
-  for (int l = tid; l < a.P; l += kFinThreads) {
-    if (a.list_tau) {
-      t0 = fmaxf(t0, a.list_tau[(int64_t)l * a.q + j]);
-    } else if (a.sorted) {
-      const int64_t o = ((int64_t)l * a.q + j) * a.stride + (a.kprime - 1);
-      if (a.part_id[o] >= 0) t0 = fmaxf(t0, a.part_key[o]);
-    }
-  }
+  const bool vec = (a.d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Q)) & 15) == 0;
+  double qq = 0.0;
+  if (a.metric == VRS_COSINE) {
+    for (int t = lane; t < a.d; t += 32) qq += (double)q[t] * (double)q[t];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
-  if (lane == 0) s_red[warp] = t0;
-  if (tid == 0) s_nc = 0;
-  __syncthreads();
-  t0 = s_red[0];
+    for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+  }
+  constexpr int U = 8;
+  for (int c0 = 0; c0 < m; c0 += U) {
+    const float *xr[U];
 #pragma unroll
-  for (int w = 1; w < kFinThreads / 32; ++w) t0 = fmaxf(t0, s_red[w]);
-
-  // 2. stage the candidates >= T0 in shared memory (one pass over the lists)
-  const int64_t C = (int64_t)a.P * a.kread;
-  for (int64_t c0 = 0; c0 < C; c0 += kFinThreads) {
-    const int64_t c = c0 + tid;
-    float key = -INFINITY;
-    int32_t id = -1;
-    if (c < C) {
-      const int64_t p = c / a.kread, r = c - p * a.kread;
-      const int64_t o = (p * a.q + j) * a.stride + r;
-      id = a.part_id[o];
-      key = a.part_key[o];
-    }
-    const bool keep = id >= 0 && key >= t0;
-    const uint32_t m = __ballot_sync(0xffffffffu, keep);
-    int base = 0;
-    if (lane == 0 && m) base = atomicAdd(&s_nc, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) {
-      const int pos = base + __popc(m & lanemask_lt());
-      if (pos < kFinMaxStage) { s_ck[pos] = key; s_ci[pos] = id; }
-    }
-  }
-  __syncthreads();
-  const int nc = s_nc;
-  int m;
-  if (nc <= kFinMaxStage) {
-    auto get_s = [&](int64_t c, float &key, int32_t &id) -> bool {
-      key = s_ck[c];
-      id = s_ci[c];
-      return true;
-    };
-    m = block_select_top<int32_t>(get_s, nc, a.kprime, s_id, s_key);
-  } else {
-    auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-      const int64_t p = c / a.kread, r = c - p * a.kread;
-      const int64_t o = (p * a.q + j) * a.stride + r;
-      id = a.part_id[o];
-      key = a.part_key[o];
-      return id >= 0 && key >= t0;
-    };
-    m = block_select_top<int32_t>(get, C, a.kprime, s_id, s_key);
-  }
-
-  // |q|^2 in fp64 (COSINE only)
-  if (warp == 0) {
-    double s = 0.0;
-    if (a.metric == VRS_COSINE)
-      for (int t = lane; t < a.d; t += 32) s += (double)q[t] * (double)q[t];
+    for (int u = 0; u < U; ++u) xr[u] = a.X + (int64_t)bi[min(c0 + u, m - 1)] * a.d;
+    double sc[U], xx[U];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) s_nq = s;
-  }
-  __syncthreads();
-  const bool zero_cos = (a.metric == VRS_COSINE) && !(s_nq > 0.0);
-
-  // exact re-score, one warp per candidate
-  for (int c = warp; c < m; c += kFinThreads / 32) {
-    const float *x = a.X + (int64_t)s_id[c] * a.d;
-    double s = 0.0, xx = 0.0;
-    if (a.metric == VRS_L2) {
-      for (int t = lane; t < a.d; t += 32) { const double df = (double)q[t] - (double)x[t]; s += df * df; }
+    for (int u = 0; u < U; ++u) { sc[u] = 0.0; xx[u] = 0.0; }
+    if (vec) {
+      for (int t = lane * 4; t < a.d; t += 128) {
+        const float4 qv = __ldg(reinterpret_cast<const float4 *>(q + t));
+        float4 xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const float4 *>(xr[u] + t));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (a.metric == VRS_L2) {
+            const double d0 = (double)qv.x - xv[u].x, d1 = (double)qv.y - xv[u].y, d2 = (double)qv.z - xv[u].z,
+                         d3 = (double)qv.w - xv[u].w;
+            sc[u] += d0 * d0; sc[u] += d1 * d1; sc[u] += d2 * d2; sc[u] += d3 * d3;
+          } else {
+            sc[u] += (double)qv.x * xv[u].x; sc[u] += (double)qv.y * xv[u].y;
+            sc[u] += (double)qv.z * xv[u].z; sc[u] += (double)qv.w * xv[u].w;
+            xx[u] += (double)xv[u].x * xv[u].x; xx[u] += (double)xv[u].y * xv[u].y;
+            xx[u] += (double)xv[u].z * xv[u].z; xx[u] += (double)xv[u].w * xv[u].w;
+          }
+        }
+      }
     } else {
       for (int t = lane; t < a.d; t += 32) {
-        const double xv = (double)x[t];
-        s += (double)q[t] * xv;
-        xx += xv * xv;
+        const double qv = __ldg(q + t);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double xv = __ldg(xr[u] + t);
+          if (a.metric == VRS_L2) { const double df = qv - xv; sc[u] += df * df; }
+          else { sc[u] += qv * xv; xx[u] += xv * xv; }
+        }
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      xx += __shfl_xor_sync(0xffffffffu, xx, o);
-    }
-    if (lane == 0) {
-      double sc = s;
-      if (a.metric == VRS_COSINE) sc = s / (sqrt(s_nq) * sqrt(xx));
-      s_score[c] = (a.metric == VRS_L2) ? -sc : sc;  // sort key: larger is better
-      s_sid[c] = s_id[c];
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+        if (a.metric == VRS_COSINE) xx[u] += __shfl_xor_sync(0xffffffffu, xx[u], o);
+      }
+      const int c = c0 + u;
+      if (lane == u && c < m) {
+        double v = sc[u];
+        if (a.metric == VRS_L2) v = -v;   // sort key: larger is better
+        else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xx[u]));
+        s_sc[w][c] = v;
+        s_sid[w][c] = bi[c];
+      }
     }
   }
-  __syncthreads();
+  __syncwarp();
   int np = 1;
   while (np < m) np <<= 1;
-  for (int c = m + tid; c < np; c += kFinThreads) { s_score[c] = -INFINITY; s_sid[c] = INT64_MAX; }
-  __syncthreads();
-  if (warp == 0 && m > 1) warp_sort_desc_d(s_score, s_sid, np);
-  __syncthreads();
+  for (int c = m + lane; c < np; c += 32) { s_sc[w][c] = -INFINITY; s_sid[w][c] = INT64_MAX; }
+  __syncwarp();
+  // 5. order by exact score and write the k best
+  if (m > 1) warp_sort_desc_d(s_sc[w], s_sid[w], np);
+  const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
   const int mv = zero_cos ? 0 : min(m, a.k);
   const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
-  for (int r = tid; r < a.k; r += kFinThreads) {
+  for (int r = lane; r < a.k; r += 32) {
     const int64_t o = j * a.k + r;
     if (r < mv) {
-      a.ids[o] = a.row_offset + s_sid[r];
-      const double sc = s_score[r];
+      a.ids[o] = a.row_offset + s_sid[w][r];
+      const double sc = s_sc[w][r];
       a.dists[o] = (float)(a.metric == VRS_L2 ? -sc : sc);
     } else {
       a.ids[o] = -1;
@@ -308,118 +439,80 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs a) {
   }
 }
 
-// ---------------------------------------------------------- probe threshold
-// Per query: the kp-th best key among the probe pass's lists (a subset of the
-// rows) -- a provable lower bound of the kp-th best over all rows -- raises the
-// query's shared threshold for the main pass (gemm_tc.cu).
-__global__ void __launch_bounds__(kFinThreads) probe_threshold_kernel(ProbeArgs a) {
-  __shared__ int32_t s_id[kFinMaxSel];
-  __shared__ float s_key[kFinMaxSel];
-  __shared__ float s_red[kFinThreads / 32];
-  const int64_t j = blockIdx.x;
+// Per query (one CTA): the kth largest probe slot maximum (each the key of a
+// distinct row) -> gtau, a lower bound of the kth best key over all rows.  The
+// values are staged once in shared memory (ordered u32, 0 = no row) and a
+// block-wide radix select (8 bits per pass) finds the kth largest.
+constexpr int kThrThreads = 256;
+__global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a) {
+  extern __shared__ uint32_t s_val[];
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_bin, s_above, s_total;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    const int64_t p = c / a.kread, r = c - p * a.kread;
-    const int64_t o = (p * a.q + j) * a.stride + r;
-    id = a.id[o];
-    key = a.key[o];
-    return id >= 0;
-  };
-  const int m = block_select_top<int32_t>(get, (int64_t)a.lists * a.kread, a.kp, s_id, s_key);
-  if (m < a.kp) return;   // fewer than kp candidates sampled: no bound
-  float mn = INFINITY;
-  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if (lane == 0) s_red[warp] = mn;
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
-    mn = fminf(mn, s_red[0]);
-    atomicMax(a.gtau + j, ordered_u32(mn));
-  }
-}
-
-constexpr int kSampleMax = 4096;   // sample keys per query (SAMPLE_TILES x 256 in gemm_tc.cu)
-
-// Per query: the kp-th best raw key of the sample pass (-inf / NaN = no row).
-__global__ void __launch_bounds__(kFinThreads) sample_threshold_kernel(SampleArgs a) {
-  __shared__ int32_t s_id[kFinMaxSel];
-  __shared__ float s_key[kFinMaxSel];
-  __shared__ float s_red[kFinThreads / 32];
   const int64_t j = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ float s_row[kSampleMax];
-  const float *row = a.dense + j * a.ldd;
-  for (int c = tid; c < a.ldd; c += kFinThreads) s_row[c] = row[c];   // one coalesced pass
-  __syncthreads();
-  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    key = s_row[c];
-    id = (int32_t)c;
-    return key > -INFINITY;   // false for -inf padding and NaN fill
-  };
-  const int m = block_select_top<int32_t>(get, a.ldd, a.kp, s_id, s_key);
-  if (m < a.kp) return;
-  float mn = INFINITY;
-  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if (lane == 0) s_red[warp] = mn;
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 0; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
-    atomicMax(a.gtau + j, ordered_u32(mn));
+  const float *v = a.vals + j * a.nvals;
+  for (int i = tid; i < a.nvals; i += kThrThreads) {
+    const float f = __ldg(v + i);
+    s_val[i] = f > -INFINITY ? ordered_u32(f) : 0u;
   }
-}
-
-cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s) {
-  sample_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-// Per query: the kp-th best key over every list's entries so far (part 1 of the
-// main pass) -- a lower bound of the final kp-th best -- raises the shared threshold.
-__global__ void __launch_bounds__(kFinThreads) refine_threshold_kernel(RefineArgs a) {
-  __shared__ int32_t s_id[kFinMaxSel];
-  __shared__ float s_key[kFinMaxSel];
-  __shared__ float s_red[kFinThreads / 32];
-  const int64_t j = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto get = [&](int64_t c, float &key, int32_t &id) -> bool {
-    const int64_t l = c / a.cap, r = c - l * a.cap;
-    if (r >= a.cnt[l * a.q + j]) return false;
-    const int64_t o = (l * a.q + j) * a.cap + r;
-    id = a.id[o];
-    key = a.key[o];
-    return true;
-  };
-  const int m = block_select_top<int32_t>(get, (int64_t)a.lists * a.cap, a.kp, s_id, s_key);
-  if (m < a.kp) return;
-  float mn = INFINITY;
-  for (int i = tid; i < m; i += kFinThreads) mn = fminf(mn, s_key[i]);
+  uint32_t prefix = 0, mask = 0;
+  int rem = a.kth;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += kThrThreads) hist[b] = 0;
+    __syncthreads();
+    for (int i = tid; i < a.nvals; i += kThrThreads) {
+      const uint32_t u = s_val[i];
+      if (u != 0u && (u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c[8], sum = 0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if (lane == 0) s_red[warp] = mn;
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 0; w < kFinThreads / 32; ++w) mn = fminf(mn, s_red[w]);
-    atomicMax(a.gtau + j, ordered_u32(mn));
+      for (int t = 0; t < 8; ++t) { c[t] = hist[255 - 8 * lane - t]; sum += c[t]; }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_total = incl;
+      const uint32_t before = incl - sum;
+      if (before < (uint32_t)rem && (uint32_t)rem <= incl) {
+        uint32_t run = before;
+        for (int t = 0; t < 8; ++t) {
+          if ((uint32_t)rem <= run + c[t]) { s_bin = 255 - 8 * lane - t; s_above = run; break; }
+          run += c[t];
+        }
+      }
+    }
+    __syncthreads();
+    if (s_total < (uint32_t)rem) {   // first pass only: fewer than kth rows probed
+      if (tid == 0) a.gtau[j] = 0u;
+      return;
+    }
+    prefix |= s_bin << shift;
+    mask |= 255u << shift;
+    rem -= (int)s_above;
+    __syncthreads();
   }
+  if (tid == 0) a.gtau[j] = prefix;
 }
 
-cudaError_t launch_refine_threshold(const RefineArgs &a, cudaStream_t s) {
-  refine_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_probe_threshold(const ProbeArgs &a, cudaStream_t s) {
-  probe_threshold_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
+  const size_t smem = (size_t)a.nvals * 4;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(threshold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  threshold_kernel<<<(unsigned)a.q, kThrThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
-  finalize_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+  finalize_kernel<<<(unsigned)((a.q + kFinWarps - 1) / kFinWarps), kFinWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -8,18 +8,24 @@
 // at a time and is consumed by a fused top-k epilogue.
 //
 // Per CTA: one work item = (query tile of 128, contiguous split of the row
-// tiles).  Warp roles (256 threads, 1 CTA / SM):
-//   warp 0  TMA producer: query block [128 x 32 fp32] + row block [256 x 32]
-//           per stage, 128-byte swizzle, 4-stage mbarrier ring
-//   warp 1  TMEM allocator + tcgen05.mma issuer (kind::tf32, M=128, N=256,
-//           K=8 per instruction), fp32 accumulators double-buffered in TMEM
-//           (2 x 256 columns)
-//   warp 2  per-row epilogue terms: ranking-key scale/bias of each of the 256
-//           rows of a tile (norm terms, bitmap mask) and row ids, 2-stage ring
-//   warps 4-7 epilogue: tcgen05.ld 32 columns at a time, key = fma(dot, a, b),
-//           compare with the query's running threshold, rare append to a
-//           per-(work item, query) candidate buffer, warp-cooperative radix
-//           compaction to the best KP when a buffer fills.
+// tiles).  Warp roles (384 threads, 1 CTA / SM):
+//   warp 0    TMA producer: query block [128 x 32 fp32] (resident for d <= 128)
+//             + row block [256 x 32] per stage, 128-byte swizzle, mbarrier ring
+//   warp 1    TMEM allocator + tcgen05.mma issuer (kind::tf32, M=128, N=256,
+//             K=8 per instruction), fp32 accumulators double-buffered in TMEM
+//             (2 x 256 columns)
+//   warp 2    per-row epilogue terms: ranking-key scale/bias of each of the 256
+//             rows of a tile (norm terms, bitmap mask -> -inf) and row ids
+//   warps 4-11 epilogue, 2 per TMEM lane quadrant (one query per lane, 128 of
+//             the tile's 256 columns per warp): tcgen05.ld 32 columns at a time,
+//             key = fma(dot, a, b), then
+//     PROBE pass (every 16th row tile): per-lane running maxima of 32 disjoint
+//             row slots -> [q][list][32]; branch-free.  threshold_kernel takes
+//             the k'-th largest of a query's slot maxima: k' distinct rows reach
+//             it, so it is a lower bound of the k'-th best key over all rows
+//     MAIN pass: compare with the query's threshold (own list / shared bound
+//             from the probe), rare append of (key, row) to a per-(list, query)
+//             candidate buffer, warp-cooperative radix compaction on overflow.
 // Precision: TF32 products, fp32 accumulation -> selection only; the k' = k+16
 // best per query are re-scored exactly in finalize.cu.
 //
@@ -45,20 +51,22 @@ constexpr int PIPE_BYTES = 192 * 1024;   // shared-memory pipeline region (A res
 constexpr int MAX_STAGES = 8;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;   // accumulator tiles in TMEM (2 x 256 columns)
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int EPI_COLS = BN / 2;
 constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
-constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (item, query, half)
+constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (list, query)
 constexpr int BIAS_STAGES = 4;
 constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
-// dynamic smem: [stages][A|B] (1024-aligned) + bias a/b/id [BIAS_STAGES][BN] + per-warp key staging
-// (the staging area doubles as the compaction histogram)
-constexpr size_t SMEM_BYTES =
-    1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
+constexpr int SLOTS = 32;       // probe: row slots per lane (column index mod 32)
+constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile
+constexpr int CHUNKS = BN / 32; // 32-column epilogue chunks per tile
+// dynamic smem: [pipeline region] + bias a/b/id [BIAS_STAGES][BN] + chunk bounds
+// [BIAS_STAGES][CHUNKS][4] + per-warp key staging (doubles as the compaction histogram)
+constexpr size_t SMEM_BYTES = 1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + BIAS_STAGES * CHUNKS * 16 +
+                              EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
 }  // namespace tc
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -106,49 +114,6 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
                : "memory");
 }
 
-// ---- CTA-pair (cta_group::2) helpers: the even CTA of a 2-CTA cluster issues the
-// MMA for both; barrier addresses with bit 24 cleared name the even CTA's copy.
-constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
-}
-// TMA executed by both CTAs of the pair; the transaction bytes land on the even CTA's barrier.
-__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                                 uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// MMA completion -> arrive on the barrier at this offset in both CTAs of the pair.
-__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
-               : "memory");
-}
-
 // D[tmem] (+)= A[smem] . B[smem]^T, kind::tf32, both operands K-major.
 __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -189,48 +154,50 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                  \
       : "r"(taddr))
 
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Wait for this thread's outstanding tcgen05.ld; the registers are tied to the
+// wait so no use of them can be scheduled above it.
+#define TMEM_LD_WAIT(r)                                                                                           \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                   \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),   \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),            \
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),          \
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),          \
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])                                                             \
+               :                                                                                                  \
+               : "memory")
 
 // ---------------------------------------------------------------- kernel
 struct TcParams {
   int64_t n_rows;          // rows of the index (identity / masked row space)
   const int32_t *ids;      // compacted ascending selection (nullptr: no predicate)
   const int64_t *count;    // device count of ids
-  int32_t allow_gather;    // gathered-row mode allowed (selectivity switch decides on device)
+  int32_t allow_gather;    // 0 never, 1 selectivity switch on the device, 2 forced
   int32_t d;
   int32_t nk;              // K blocks = ceil(d / 32)
   int64_t q;
   int32_t qtiles;
   int32_t P;               // splits
-  int32_t tile_step;       // 1: every tile; > 1: probe pass over every tile_step-th tile
-  float *dense;            // sample pass: raw keys [q][ldd] of the first dense_tiles row tiles (no top-k)
-  int32_t ldd;
-  int32_t dense_tiles;
-  int64_t row_tiles_max;   // ceil(n_rows / BN)
+  int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
   const float *inv_nx;
   int32_t metric;
-  int32_t kp;              // retained entries per (item, query) (pow2 >= k')
-  int32_t cap;             // buffer capacity per (item, query)
+  int32_t kp;              // entries kept by a compaction (pow2 >= k')
+  int32_t cap;             // buffer capacity per (list, query)
   float *cand_key;         // [2P][q][cap]
   int32_t *cand_id;
-  const float *X;          // corpus base
+  int32_t *cand_cnt;       // [2P][q] entries per list
+  float *probe_max;        // [q][2P][SLOTS] probe slot maxima
   int64_t xsel_cap;        // rows of the materialised-selection buffer
-  uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none yet)
-  float *list_tau;         // [2P][q] final KP-th best key per list (-inf: list never filled)
-  unsigned long long *stats;  // optional counters: chunks, slow chunks, flagged queries, compactions
-  float *dense_buf;        // host-provided scratch for the sample pass [q][SAMPLE_TILES * BN]
+  uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
+  unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
   int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
-  int32_t part;            // 0: whole item; 1: first 1/PART_DIV of its tiles; 2: the rest (resumes part 1)
-  int32_t *cnt_state;      // [2P][q] list fill carried from part 1 to part 2
-  float *tau_state;        // [2P][q] list threshold carried from part 1 to part 2
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
 // entries (key desc, then buffer order = ascending row id).  Returns the new
 // threshold key (the KP-th best).  All 32 lanes call it with the same `owner`.
-__device__ float compact_lane(float *key, int32_t *id, int cnt, int kp, uint32_t *hist) {
+__device__ __noinline__ float compact_lane(float *key, int32_t *id, int cnt, int kp, uint32_t *hist) {
   const int lane = threadIdx.x & 31;
   uint32_t prefix = 0, mask = 0;
   int rem = kp;
@@ -321,11 +288,13 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const float *__restric
   }
 }
 
+constexpr int MODE_MAIN = 0;
+constexpr int MODE_PROBE = 1;
+
 // AR: the query tile stays resident in shared memory (d <= 128).
-// CG: 1 = one CTA per 128-query tile; 2 = CTA pair (cluster of 2) sharing every row
-//     tile: M = 256 queries per MMA, each CTA stages half of the rows (cta_group::2),
-//     halving the L2 -> SM traffic per query.
-template <bool AR, int CG>
+// MODE: MAIN (fused top-k candidates) or PROBE (slot maxima for the threshold).
+// ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
+template <bool AR, int MODE, bool ROWSCALE>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
@@ -334,12 +303,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
   // array itself, so the compiler keeps the shared address space (LDS, not LD)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  // pipeline region (STAGES * STAGE_BYTES): AR ? [A: nk x 16 KB][B stages of 32 KB]
-  //                                              : [stages of (A 16 KB | B 32 KB)]
-  uint8_t *stage_base = smem;
-  constexpr int B_LOCAL = B_BYTES / CG;                  // this CTA's share of a row tile
-  constexpr int SSTRIDE = AR ? B_LOCAL : A_BYTES + B_LOCAL;   // bytes per pipeline stage
-  // as many stages as the 192 KB pipeline region holds (TMA latency needs depth)
+  // pipeline region: AR ? [A: nk x 16 KB][B stages of 32 KB] : [stages of (A 16 KB | B 32 KB)]
+  constexpr int SSTRIDE = AR ? B_BYTES : A_BYTES + B_BYTES;   // bytes per pipeline stage
   constexpr int NST = ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
                           ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
                           : MAX_STAGES;
@@ -349,7 +314,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   float *bias_a = reinterpret_cast<float *>(smem + PIPE_BYTES);               // [BIAS_STAGES][BN]
   float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
-  float *kstage = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [EPI_WARPS][32][STAGE_COLS]
+  // per 32-column chunk: {max b, max a, min a, -} over its rows (key upper bound)
+  float4 *cmeta = reinterpret_cast<float4 *>(row_id + BIAS_STAGES * BN);       // [BIAS_STAGES][CHUNKS]
+  float *kstage = reinterpret_cast<float *>(cmeta + BIAS_STAGES * CHUNKS);     // [EPI_WARPS][32][STAGE_COLS]
 
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES], empty_bar[MAX_STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
@@ -358,11 +325,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
-  const int qgroups = (p.qtiles + CG - 1) / CG;
-  const int item = blockIdx.x / CG;
-  const int qtile = (item % qgroups) * CG + rank;
-  const int split = item / qgroups;
+  const int qtile = blockIdx.x % p.qtiles;
+  const int split = blockIdx.x / p.qtiles;
   // Selectivity-driven row delivery (decided on the device, no host sync):
   //  gather: the selection was materialised densely (gather_copy_kernel, late
   //          materialization) and streams by TMA from X_sel; ids map rows back
@@ -371,34 +335,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.n_rows, p.xsel_cap);
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;
-  // splits actually used: >= 16 row tiles per item when the (device-side) row
-  // space allows -- the fused top-k warms up once per item; CTAs of unused
-  // splits only publish empty candidate lists
-  // (sample pass: the first dense_tiles row tiles, split over all P splits)
-  const int64_t t_space = p.dense ? std::min<int64_t>(row_tiles, p.dense_tiles) : row_tiles;
-  const int64_t p_eff = p.dense ? p.P : std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
-  const int64_t i_begin = split < p_eff ? (t_space * split) / p_eff : 0;
-  const int64_t i_end = split < p_eff ? (t_space * (split + 1)) / p_eff : 0;
-  // two-part main pass: part 1 covers the first 1/PART_DIV of the item's tiles,
-  // a per-query selection over every list then raises the shared threshold, and
-  // part 2 resumes the lists over the remaining tiles
-  constexpr int PART_DIV = 8;
-  const int64_t i_mid = i_begin + (i_end - i_begin + PART_DIV - 1) / PART_DIV;
-  const int64_t t_begin = p.part == 2 ? i_mid : i_begin;
-  const int64_t t_end = p.part == 1 ? i_mid : i_end;
-  // probe pass (tile_step > 1): every tile_step-th tile of the item, and only when
-  // the item is long enough for a threshold to pay off
+  // splits actually used: >= 4 row tiles per item when the (device-side) row
+  // space allows; CTAs of unused splits publish empty lists
+  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
+  const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
   const int64_t span = t_end - t_begin;
-  // probe: ~1/tile_step of the item's tiles (at least 4 of them, at most every 2nd)
-  const int step = p.tile_step == 1 ? 1 : (int)std::max<int64_t>(2, std::min<int64_t>(p.tile_step, span / 4));
-  // (the probe only pays off for masked full tiles: the gathered selection is short)
-  const int ntiles = p.tile_step == 1 ? (int)span : (span >= 8 && !gather ? (int)((span + step - 1) / step) : 0);
+  // probe: every tile_step-th tile of the item (the first tile of a shorter item)
+  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(p.tile_step, std::max<int64_t>(1, span)) : 1;
+  const int ntiles = (int)((span + step - 1) / step);
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&afull_bar, 1);
-    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS * CG); }
+    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
       mbar_init(&bempty_bar[s], EPI_WARPS);
@@ -407,21 +358,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   }
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); prefetch_tmap(&tmap_g); }
   if (warp == 1) {
-    if (CG == 2) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                   "n"(TMEM_COLS)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                   "n"(TMEM_COLS)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  if (CG == 2) cluster_sync_all();
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
 
@@ -430,32 +373,25 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      // (pair: both CTAs load their own A and their half of B; the even CTA
-      //  accounts for the pair's bytes on its barriers)
-      auto load = [&](void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
-        if (CG == 2) tma_load_2d_pair(dst, map, bar, c0, c1);
-        else tma_load_2d(dst, map, bar, c0, c1);
-      };
       if (AR && ntiles > 0) {
-        if (rank == 0) mbar_expect_tx(&afull_bar, CG * p.nk * A_BYTES);
-        for (int kb = 0; kb < p.nk; ++kb) load(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
+        mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
       }
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = (int)(tile_of(t) * BN) + rank * (BN / CG);
+        const int row0 = (int)(tile_of(t) * BN);
         for (int kb = 0; kb < p.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *st = b_base + stage * SSTRIDE;
-          if (rank == 0) mbar_expect_tx(&full_bar[stage], CG * (AR ? B_LOCAL : A_BYTES + B_LOCAL));
-          if (!AR) load(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          load(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
+          mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
+          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
+          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (even CTA of a pair)
-    constexpr uint32_t idesc = tf32_idesc(BM * CG, BN);
-    if (CG == 1 || rank == 0) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = tf32_idesc(BM, BN);
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
@@ -472,23 +408,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
           const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
-            if (CG == 2) tc_mma_tf32_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
-            else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
-          }
-          // frees the smem slot(s) when these MMAs finish; accumulator ready after the last K block
-          if (CG == 2) {
-            tc_commit_pair(&empty_bar[stage]);
-            if (kb == p.nk - 1) tc_commit_pair(&tfull_bar[acc]);
-          } else {
-            tc_commit(&empty_bar[stage]);
-            if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
-          }
+          for (int k = 0; k < BK / 8; ++k)  // K = 8 tf32 = 32 bytes per instruction
+            tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+          // frees the smem slot when these MMAs finish; accumulator ready after the last K block
+          tc_commit(&empty_bar[stage]);
+          if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
         }
         __syncwarp();
         if (++stage == NST) { stage = 0; phase ^= 1; }
       }
-    }
     }
   } else if (warp == 2) {
     // ------------------------------------------------ per-row epilogue terms
@@ -559,19 +487,32 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
 #pragma unroll
         for (int v = 0; v < RPL / 4; ++v) {
-          reinterpret_cast<float4 *>(bias_a + s * BN + lane * RPL)[v] =
-              make_float4(av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3]);
+          if (ROWSCALE)
+            reinterpret_cast<float4 *>(bias_a + s * BN + lane * RPL)[v] =
+                make_float4(av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3]);
           reinterpret_cast<float4 *>(bias_b + s * BN + lane * RPL)[v] =
               make_float4(bv[4 * v], bv[4 * v + 1], bv[4 * v + 2], bv[4 * v + 3]);
-          reinterpret_cast<int4 *>(row_id + s * BN + lane * RPL)[v] =
-              make_int4(iv[u][4 * v], iv[u][4 * v + 1], iv[u][4 * v + 2], iv[u][4 * v + 3]);
+          if (MODE == MODE_MAIN)
+            reinterpret_cast<int4 *>(row_id + s * BN + lane * RPL)[v] =
+                make_int4(iv[u][4 * v], iv[u][4 * v + 1], iv[u][4 * v + 2], iv[u][4 * v + 3]);
         }
+        // chunk bounds: this lane's 8 rows, then the 4 lanes of each 32-row chunk
+        float bmx = bv[0], amx = av[0], amn = av[0];
+#pragma unroll
+        for (int k = 1; k < RPL; ++k) { bmx = fmaxf(bmx, bv[k]); amx = fmaxf(amx, av[k]); amn = fminf(amn, av[k]); }
+#pragma unroll
+        for (int o = 1; o < 32 / RPL; o <<= 1) {
+          bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+          amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+          amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
+        }
+        if ((lane & (32 / RPL - 1)) == 0) cmeta[s * CHUNKS + lane / (32 / RPL)] = make_float4(bmx, amx, amn, 0.f);
         mbar_arrive(&bfull_bar[s]);
         fetch(t + PF, nv[u], iv[u], wv[u]);
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ------------------------------------------------ epilogue: fused top-k
+    // ------------------------------------------------ epilogue
     const int ew = warp - EPI_WARP0;
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
     const int half = ew >> 2;                      // which 128 of the tile's 256 columns
@@ -579,30 +520,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int64_t qg = (int64_t)qtile * BM + m;    // global query index
     const bool active = qg < p.q;
     const int list = split * 2 + half;             // candidate list index
+    const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
     const int64_t cbase = ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
     float *ckey = p.cand_key + cbase;
     int32_t *cid = p.cand_id + cbase;
     float *wst = kstage + ew * 32 * STAGE_COLS;
     uint32_t *whist = reinterpret_cast<uint32_t *>(wst);   // compaction histogram aliases the staging area
-    float tau = active ? -INFINITY : INFINITY;     // inactive lanes never accept
+    float thr = active ? -INFINITY : INFINITY;     // accept iff key > thr (inactive lanes never accept)
     int cnt = 0;
-    if (p.part == 2 && active) {   // resume the list built by part 1
-      cnt = p.cnt_state[(int64_t)list * p.q + qg];
-      tau = p.tau_state[(int64_t)list * p.q + qg];
+    uint32_t st_chunks = 0, st_slow = 0, st_app = 0, st_comp = 0;
+    float smax[SLOTS];
+#pragma unroll
+    for (int i = 0; i < SLOTS; ++i) smax[i] = -INFINITY;
+    // Shared threshold (probe): the k'-th best key over all rows is >= gtau, so
+    // keys below it can never be in the result; keys equal to it are kept.
+    if (MODE == MODE_MAIN && active) {
+      const uint32_t o = __ldcg(p.gtau + qg);
+      if (o != 0) {
+        const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        thr = nextafterf(__uint_as_float(u), -INFINITY);
+      }
     }
-
-    // Thresholds: `tau` (own list, strict: later rows have larger ids) and the
-    // query's shared threshold gtau (max over every list's KP-th best key --
-    // any list's KP-th best bounds the global KP-th best from below).  A key is
-    // a candidate iff key > tau and key >= gtau; both fold into `thr`.
-    uint32_t *gtau_q = p.gtau + (active ? qg : 0);
-    auto shared_bound = [](uint32_t o) -> float {   // largest float strictly below the shared key
-      if (o == 0) return -INFINITY;
-      const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
-      return nextafterf(__uint_as_float(u), -INFINITY);
-    };
-    float thr = tau;
-    uint32_t st_chunks = 0, st_slow = 0, st_flag = 0, st_comp = 0;
+    // own list: after a compaction to the KP best, a later row (larger id) must
+    // beat the KP-th best strictly
     auto compact_needed = [&](int threshold) {
       uint32_t need = __ballot_sync(0xffffffffu, cnt > threshold);
       while (need) {
@@ -613,157 +553,131 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
         ++st_comp;
         if (lane == owner) {
-          tau = nt;
           cnt = p.kp;
-          thr = fmaxf(thr, tau);
-          atomicMax(gtau_q, ordered_u32(tau));
+          thr = fmaxf(thr, nt);
+        }
+      }
+    };
+    // one 32-column chunk: r holds the raw dot products (turned into keys in place)
+    auto chunk = [&](uint32_t (&r)[32], const float *ba, const float *bb, const int32_t *rid, float4 cm) {
+      if (MODE == MODE_MAIN) {
+        // fast path: an upper bound of the chunk's keys from the largest raw dot
+        // and the chunk's bias / scale range; fma is monotone in each argument
+        // (scale > 0), so no key of the chunk can exceed it
+        float dm = __uint_as_float(r[0]);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) dm = fmaxf(dm, __uint_as_float(r[i]));
+        const float kb = ROWSCALE ? fmaf(dm, dm >= 0.f ? cm.y : cm.z, cm.x) : fmaf(dm, sc, cm.x);
+        ++st_chunks;
+        if (!__any_sync(0xffffffffu, kb > thr)) return;
+      }
+      float kmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 b4 = *reinterpret_cast<const float4 *>(bb + i);
+        float4 a4 = make_float4(sc, sc, sc, sc);
+        if (ROWSCALE) a4 = *reinterpret_cast<const float4 *>(ba + i);
+        const float k0 = fmaf(__uint_as_float(r[i]), a4.x, b4.x);
+        const float k1 = fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y);
+        const float k2 = fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z);
+        const float k3 = fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w);
+        r[i] = __float_as_uint(k0); r[i + 1] = __float_as_uint(k1);
+        r[i + 2] = __float_as_uint(k2); r[i + 3] = __float_as_uint(k3);
+        if (MODE == MODE_PROBE) {
+          smax[i] = fmaxf(smax[i], k0); smax[i + 1] = fmaxf(smax[i + 1], k1);
+          smax[i + 2] = fmaxf(smax[i + 2], k2); smax[i + 3] = fmaxf(smax[i + 3], k3);
+        } else {
+          kmax = fmaxf(kmax, fmaxf(fmaxf(k0, k1), fmaxf(k2, k3)));
+        }
+      }
+      if (MODE == MODE_PROBE) return;
+      if (!__any_sync(0xffffffffu, kmax > thr)) return;
+      // rare once the threshold is in place: make room (<= 32 appends follow; the
+      // compaction histogram aliases the staging rows), then each lane appends its
+      // own accepted columns in row order from its private staging row
+      ++st_slow;
+      if (__any_sync(0xffffffffu, cnt + 32 > p.cap)) compact_needed(p.cap - 32);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {   // (unrolled: r must stay in registers)
+        uint32_t msk = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) msk |= (__uint_as_float(r[h * 16 + i]) > thr ? 1u : 0u) << i;
+        if (__any_sync(0xffffffffu, msk != 0)) {
+          float *myrow = wst + lane * STAGE_COLS;
+          if (msk) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4 *>(myrow + i) =
+                  make_float4(__uint_as_float(r[h * 16 + i]), __uint_as_float(r[h * 16 + i + 1]),
+                              __uint_as_float(r[h * 16 + i + 2]), __uint_as_float(r[h * 16 + i + 3]));
+            st_app += __popc(msk);
+            while (msk) {
+              const int i = __ffs(msk) - 1;
+              msk &= msk - 1;
+              ckey[cnt] = myrow[i];
+              cid[cnt] = rid[h * 16 + i];
+              ++cnt;
+            }
+          }
+          __syncwarp();
         }
       }
     };
 
-    uint32_t g_next = active ? __ldcg(gtau_q) : 0u;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % ACC_STAGES;
       const int bs = t % BIAS_STAGES;
-      if (active) thr = fmaxf(thr, shared_bound(g_next));
-      if (active) g_next = __ldcg(gtau_q);   // consumed at the next tile (latency hidden)
       mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
       mbar_wait(&tfull_bar[acc], (t / ACC_STAGES) & 1);
       tc_fence_after();
       const float *ba = bias_a + bs * BN + half * EPI_COLS;
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
       const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
+      const float4 *cmt = cmeta + bs * CHUNKS + half * (EPI_COLS / 32);
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
-      if (p.epi_skip) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
-          else mbar_arrive(&tempty_bar[acc]);
-          mbar_arrive(&bempty_bar[bs]);
+      if (!p.epi_skip) {
+        uint32_t ra[32], rb[32];
+        TMEM_LD_32x32b_X32(tbase, ra);
+        TMEM_LD_WAIT(ra);
+#pragma unroll 1
+        for (int c = 0; c < EPI_COLS / 32; c += 2) {
+          TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, rb);
+          chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, cmt[c]);
+          TMEM_LD_WAIT(rb);
+          if (c + 2 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 2) * 32, ra);
+          chunk(rb, ba + (c + 1) * 32, bb + (c + 1) * 32, rid + (c + 1) * 32, cmt[c + 1]);
+          if (c + 2 < EPI_COLS / 32) TMEM_LD_WAIT(ra);
         }
-        continue;
-      }
-      uint32_t r[2][32];
-      TMEM_LD_32x32b_X32(tbase, r[0]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 0; c < EPI_COLS / 32; ++c) {
-        uint32_t(&cur)[32] = r[c & 1];
-        if (c + 1 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, r[(c + 1) & 1]);
-        float key[32];
-        float kmax = -INFINITY;
-        if (p.metric == VRS_COSINE) {   // per-row scale 1/|x|
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 a4 = *reinterpret_cast<const float4 *>(ba + c * 32 + i);
-            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
-            key[i] = fmaf(__uint_as_float(cur[i]), a4.x, b4.x);
-            key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), a4.y, b4.y);
-            key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), a4.z, b4.z);
-            key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), a4.w, b4.w);
-          }
-        } else {                        // constant scale (L2: 2, IP: 1), per-row bias
-          const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b4 = *reinterpret_cast<const float4 *>(bb + c * 32 + i);
-            key[i] = fmaf(__uint_as_float(cur[i]), sc, b4.x);
-            key[i + 1] = fmaf(__uint_as_float(cur[i + 1]), sc, b4.y);
-            key[i + 2] = fmaf(__uint_as_float(cur[i + 2]), sc, b4.z);
-            key[i + 3] = fmaf(__uint_as_float(cur[i + 3]), sc, b4.w);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) kmax = fmaxf(kmax, fmaxf(key[i], key[i + 1]));
-        ++st_chunks;
-        if (p.dense) {   // sample pass: raw keys out, no selection
-          if (active) {
-            float *dst = p.dense + qg * p.ldd + tile_of(t) * BN + half * EPI_COLS + c * 32;
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4 *>(dst + i) = make_float4(key[i], key[i + 1], key[i + 2], key[i + 3]);
-          }
-          tmem_ld_wait();
-          continue;
-        }
-        if (__any_sync(0xffffffffu, kmax > thr)) {
-          ++st_slow;
-          uint32_t amask = 0;   // bit i: column i beats the query's threshold
-#pragma unroll
-          for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
-          // rare once a threshold exists: make room (<= 32 appends follow; the
-          // compaction histogram aliases the staging rows), re-test against the
-          // possibly raised threshold, then each lane appends its own columns in
-          // row order from its private staging row (16 columns at a time)
-          if (__any_sync(0xffffffffu, cnt + __popc(amask) > p.cap)) {
-            compact_needed(p.cap - 32);
-            amask = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) amask |= (key[i] > thr ? 1u : 0u) << i;
-          }
-          float *myrow = wst + lane * STAGE_COLS;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t m = (amask >> (16 * h)) & 0xffffu;
-            if (m) {
-              st_flag += __popc(m);
-#pragma unroll
-              for (int i = 0; i < 16; i += 4)
-                *reinterpret_cast<float4 *>(myrow + i) =
-                    make_float4(key[h * 16 + i], key[h * 16 + i + 1], key[h * 16 + i + 2], key[h * 16 + i + 3]);
-              const int32_t *rrow = rid + c * 32 + h * 16;
-              while (m) {
-                const int i = __ffs(m) - 1;
-                m &= m - 1;
-                ckey[cnt] = myrow[i];
-                cid[cnt] = rrow[i];
-                ++cnt;
-              }
-            }
-          }
-          __syncwarp();
-        }
-        tmem_ld_wait();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_leader(&tempty_bar[acc]);
-        else mbar_arrive(&tempty_bar[acc]);
+        mbar_arrive(&tempty_bar[acc]);
         mbar_arrive(&bempty_bar[bs]);
       }
     }
     if (p.stats && lane == 0) {
       atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
       atomicAdd(p.stats + 1, (unsigned long long)st_slow);
-      atomicAdd(p.stats + 2, (unsigned long long)st_flag);
+      atomicAdd(p.stats + 2, (unsigned long long)st_app);
       atomicAdd(p.stats + 3, (unsigned long long)st_comp);
     }
-    if (p.part == 1) {   // hand the list over to part 2
-      if (active) {
-        p.cnt_state[(int64_t)list * p.q + qg] = cnt;
-        p.tau_state[(int64_t)list * p.q + qg] = tau;
+    if (active) {
+      if (MODE == MODE_PROBE) {
+        float4 *dst = reinterpret_cast<float4 *>(p.probe_max + ((qg * (2 * p.P)) + list) * SLOTS);
+#pragma unroll
+        for (int i = 0; i < SLOTS; i += 4) dst[i / 4] = make_float4(smax[i], smax[i + 1], smax[i + 2], smax[i + 3]);
+      } else {
+        p.cand_cnt[(int64_t)list * p.q + qg] = cnt;
       }
-    } else {
-    // final: keep the best KP, pad the rest of the KP window
-    if (!p.dense) compact_needed(p.kp);
-    if (active && !p.dense) {
-      for (int i = cnt; i < p.kp; ++i) { ckey[i] = -INFINITY; cid[i] = -1; }
-      p.list_tau[(int64_t)list * p.q + qg] = tau;
-    }
     }
   }
 
   tc_fence_before();
-  if (CG == 2) cluster_sync_all();   // the pair's MMAs and remote arrivals are done
-  else __syncthreads();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    if (CG == 2)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
   }
 }
 
@@ -806,32 +720,59 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
   const int64_t qtiles = (q + tc::BM - 1) / tc::BM;
   const int64_t row_tiles = (n_upper + tc::BN - 1) / tc::BN;
   // one CTA per SM; aim for up to 4 waves of (query tile, row split) items while keeping
-  // items >= ~128 row tiles (the fused top-k warms up once per item)
+  // items >= ~128 row tiles
   int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, row_tiles * qtiles / ((int64_t)num_sms * 128)));
   int64_t P = std::max<int64_t>(1, (int64_t)num_sms * waves / qtiles);
-  P = std::min<int64_t>(P, row_tiles);
+  P = std::min<int64_t>(std::min<int64_t>(P, row_tiles), 2 * num_sms);
   g.P = (int32_t)P;
   g.qtiles = (int32_t)qtiles;
   g.ok = 1;
   return g;
 }
 
+// scratch: cand_key, cand_id [2P][q][cap] | cand_cnt [2P][q] | gtau [q] | probe_max [q][2P][32]
+namespace {
+struct GemmScratch {
+  float *cand_key;
+  int32_t *cand_id;
+  int32_t *cand_cnt;
+  uint32_t *gtau;
+  float *probe_max;
+  size_t bytes;
+};
+GemmScratch carve_gemm(void *base, const GemmPlan &plan, int64_t q, int32_t kprime) {
+  const size_t lists = (size_t)plan.P * 2;
+  const size_t cap = (size_t)kp_of(kprime) * tc::CAP_FACTOR;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  char *p = static_cast<char *>(base);
+  GemmScratch s;
+  size_t off = 0;
+  s.cand_key = reinterpret_cast<float *>(p + off); off += al(lists * q * cap * 4);
+  s.cand_id = reinterpret_cast<int32_t *>(p + off); off += al(lists * q * cap * 4);
+  s.cand_cnt = reinterpret_cast<int32_t *>(p + off); off += al(lists * q * 4);
+  s.gtau = reinterpret_cast<uint32_t *>(p + off); off += al((size_t)q * 4);
+  s.probe_max = reinterpret_cast<float *>(p + off); off += al(lists * q * tc::SLOTS * 4);
+  s.bytes = off;
+  return s;
+}
+}  // namespace
+
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
-  const int kp = kp_of(kprime);
-  return (size_t)plan.P * 2 * q * kp * tc::CAP_FACTOR * 8 + (size_t)q * 4 + (size_t)plan.P * 2 * q * 4 +
-         (size_t)q * 4096 * 4 + (size_t)plan.P * 2 * q * 8 + 8192;
+  return carve_gemm(nullptr, plan, q, kprime).bytes;
+}
+
+template <bool AR, int MODE>
+static auto pick_kernel(bool rowscale) {
+  return rowscale ? tc_topk_kernel<AR, MODE, true> : tc_topk_kernel<AR, MODE, false>;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
-  // CTA pairs (cta_group::2) halve the L2->SM row traffic per query but add pair
-  // synchronisation; measured slower while the single-CTA pass is MMA-bound, so opt-in
-  static const bool use_pair = getenv("VRS_PAIR") != nullptr;
-  const int bn_rows = (plan.qtiles >= 2 && use_pair) ? tc::BN / 2 : tc::BN;   // a pair stages half a row tile per CTA
   CUtensorMap mq, mx, mg;
-  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, bn_rows) ||
-      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, bn_rows))
+  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN) ||
+      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, tc::BN))
     return cudaErrorInvalidValue;
+  const GemmScratch gs = carve_gemm(scratch, plan, a.q, a.kprime);
   TcParams p;
   p.n_rows = a.n;
   p.d = a.d;
@@ -839,11 +780,9 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.q = a.q;
   p.qtiles = plan.qtiles;
   p.P = plan.P;
-  p.row_tiles_max = (a.n + tc::BN - 1) / tc::BN;
   p.ids = a.ids;
   p.count = a.count;
   p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
-  p.X = a.X;
   p.xsel_cap = xcap;
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
@@ -851,29 +790,29 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.metric = a.metric;
   p.kp = kp_of(a.kprime);
   p.cap = p.kp * tc::CAP_FACTOR;
-  p.cand_key = static_cast<float *>(scratch);
-  p.cand_id = reinterpret_cast<int32_t *>(p.cand_key + (size_t)plan.P * 2 * a.q * p.cap);
-  p.gtau = reinterpret_cast<uint32_t *>(p.cand_id + (size_t)plan.P * 2 * a.q * p.cap);
-  p.list_tau = reinterpret_cast<float *>(p.gtau + ((a.q + 63) / 64) * 64);
-  p.dense_buf = p.list_tau + (((size_t)plan.P * 2 * a.q + 63) / 64) * 64;
-  p.cnt_state = reinterpret_cast<int32_t *>(p.dense_buf + (size_t)a.q * 4096);
-  p.tau_state = reinterpret_cast<float *>(p.cnt_state + (((size_t)plan.P * 2 * a.q + 63) / 64) * 64);
-  p.part = 0;
-  {
-    cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
-    if (e != cudaSuccess) return e;
-  }
+  p.cand_key = gs.cand_key;
+  p.cand_id = gs.cand_id;
+  p.cand_cnt = gs.cand_cnt;
+  p.gtau = gs.gtau;
+  p.probe_max = gs.probe_max;
+  p.tile_step = 1;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaSuccess;
-    for (auto fn : {tc_topk_kernel<true, 1>, tc_topk_kernel<false, 1>, tc_topk_kernel<true, 2>, tc_topk_kernel<false, 2>})
+    for (auto fn : {tc_topk_kernel<true, MODE_MAIN, false>, tc_topk_kernel<true, MODE_MAIN, true>,
+                    tc_topk_kernel<false, MODE_MAIN, false>, tc_topk_kernel<false, MODE_MAIN, true>,
+                    tc_topk_kernel<true, MODE_PROBE, false>, tc_topk_kernel<true, MODE_PROBE, true>,
+                    tc_topk_kernel<false, MODE_PROBE, false>, tc_topk_kernel<false, MODE_PROBE, true>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
+  if (e != cudaSuccess) return e;
   if (xcap > 0 && p.allow_gather) {
+    ProfScope ps("gemm.gather", s);
     gather_copy_kernel<<<4 * 148, 256, 0, s>>>(a.X, a.d, a.ids, a.count, a.n, p.allow_gather, xcap, a.xsel);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
@@ -881,115 +820,61 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   static const bool want_stats = getenv("VRS_STATS") != nullptr;
   if (want_stats && !stats) cudaMalloc(&stats, 64);
   p.stats = want_stats ? stats : nullptr;
-  if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
   static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
+  static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
   p.epi_skip = epi_skip ? 1 : 0;
   const bool ar = p.nk <= 4 && !no_ar;
-  const int cg = bn_rows == tc::BN / 2 ? 2 : 1;
-  auto kern = cg == 2 ? (ar ? tc_topk_kernel<true, 2> : tc_topk_kernel<false, 2>)
-                      : (ar ? tc_topk_kernel<true, 1> : tc_topk_kernel<false, 1>);
-  // grid: (splits x query groups) work items, CG CTAs each (cluster of 2 for pairs)
-  const int qgroups = (plan.qtiles + cg - 1) / cg;
-  auto launch = [&](int splits, const TcParams &pr) -> cudaError_t {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(splits * qgroups * cg));
-    cfg.blockDim = dim3(tc::THREADS);
-    cfg.dynamicSmemBytes = tc::SMEM_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cg;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+  const bool rowscale = a.metric == VRS_COSINE;
+  auto launch = [&](int mode, const TcParams &pr) -> cudaError_t {
+    auto kern = mode == MODE_PROBE ? (ar ? pick_kernel<true, MODE_PROBE>(rowscale) : pick_kernel<false, MODE_PROBE>(rowscale))
+                                   : (ar ? pick_kernel<true, MODE_MAIN>(rowscale) : pick_kernel<false, MODE_MAIN>(rowscale));
     if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mx, mg, pr);
+    kern<<<(unsigned)(pr.P * pr.qtiles), tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pr);
+    cudaError_t el = cudaGetLastError();
     if (want_stats) {
       unsigned long long h[4];
       cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      fprintf(stderr, "[vrs stats] part=%d dense=%d grid=%d chunks=%llu slow=%llu (%.3f) lane0-accepts=%llu compactions=%llu\n",
-              pr.part, pr.dense ? 1 : 0, (int)cfg.gridDim.x, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2], h[3]);
+      fprintf(stderr, "[vrs stats] mode=%d grid=%d chunks=%llu slow=%llu (%.3f) appends=%llu compactions=%llu\n", mode,
+              pr.P * pr.qtiles, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2], h[3]);
     }
-    return e;
+    return el;
   };
-  // sample pass: raw keys of the first SAMPLE_TILES row tiles for every query ->
-  // per-query kp-th best -> initial shared threshold (no per-item warm-up)
-  constexpr int SAMPLE_TILES = 4096 / tc::BN;   // 4096 sampled rows
-  p.dense = nullptr;
-  p.ldd = 0;
-  p.dense_tiles = 0;
-  p.tile_step = 1;
-  static const bool no_sample = getenv("VRS_NO_SAMPLE") != nullptr;
-  static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
-  if (p.row_tiles_max >= 8 && !no_sample) {
-    TcParams ps = p;
-    ps.P = std::max(1, std::min(SAMPLE_TILES, 148 / (qgroups * cg)));
-    ps.dense = p.dense_buf;
-    ps.ldd = SAMPLE_TILES * tc::BN;
-    ps.dense_tiles = SAMPLE_TILES;
-    cudaError_t e = cudaMemsetAsync(ps.dense, 0xff, (size_t)a.q * ps.ldd * 4, s);   // NaN fill = no row
-    if (e != cudaSuccess) return e;
-    e = launch(ps.P, ps);
-    if (e != cudaSuccess) return e;
-    SampleArgs sa{ps.dense, ps.ldd, a.q, p.kp, p.gtau};
-    e = launch_sample_threshold(sa, s);
-    if (e != cudaSuccess) return e;
-    if (launches) *launches += 2;
-  }
-  // Threshold refinement before the main pass (masked full tiles only; the kernel
-  // switches the probe off on gathered selections):
-  //  default: probe pass over every PROBE_STEP-th row tile -> per-query kp-th best
-  //  VRS_TWO_PART=1: main pass split 1/8 + 7/8 with a refinement over every list in between
-  p.tile_step = 1;
-  p.part = 0;
-  static const bool two_part_env = getenv("VRS_TWO_PART") != nullptr;
-  constexpr int PROBE_STEP = 16;
-  if (two_part_env && p.row_tiles_max / plan.P >= 16) {
-    p.part = 1;
-    cudaError_t e = launch(plan.P, p);
-    if (e != cudaSuccess) return e;
-    RefineArgs ra{p.cand_key, p.cand_id, p.cnt_state, plan.P * 2, p.cap, a.q, p.kp, p.gtau};
-    e = launch_refine_threshold(ra, s);
-    if (e != cudaSuccess) return e;
-    p.part = 2;
-    if (launches) *launches += 2;
-  } else if (p.row_tiles_max / plan.P >= 8 && !no_probe) {
-    // each probe list keeps only its best kp/4 (>= 8): the union over all lists
-    // still holds >= kp entries, so its kp-th best remains a valid lower bound
+  // Threshold before the main pass: probe pass over every PROBE_STEP-th row tile
+  // (slot maxima) -> per query the k'-th largest slot maximum -> gtau.
+  if (!no_probe) {
+    ProfScope pf("gemm.probe", s);
     TcParams pp = p;
-    pp.tile_step = PROBE_STEP;
-    pp.kp = std::max(8, p.kp / 4);
-    pp.cap = std::max(pp.kp * tc::CAP_FACTOR, pp.kp + 96);   // room for >= 96 appends between compactions
-    cudaError_t e = launch(plan.P, pp);
+    pp.tile_step = tc::PROBE_STEP;
+    e = launch(MODE_PROBE, pp);
     if (e != cudaSuccess) return e;
-    ProbeArgs pa{pp.cand_key, pp.cand_id, plan.P * 2, pp.cap, pp.kp, a.q, p.kp, p.gtau};
-    e = launch_probe_threshold(pa, s);
+    ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau};
+    ProfScope pt("gemm.threshold", s);
+    e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
   }
   {
-    cudaError_t el = launch(plan.P, p);
-    if (el != cudaSuccess) return el;
+    ProfScope pf("gemm.main", s);
+    e = launch(MODE_MAIN, p);
+    if (e != cudaSuccess) return e;
   }
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
 
 // Where the finalize pass reads the GEMM candidate lists.
-void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread, int32_t *nlists, const float **list_tau) {
-  *nlists = plan.P * 2;
-  const int kp = kp_of(a.kprime);
-  const int cap = kp * tc::CAP_FACTOR;
-  *key = static_cast<const float *>(scratch);
-  *id = reinterpret_cast<const int32_t *>(static_cast<const float *>(scratch) + (size_t)plan.P * 2 * a.q * cap);
-  *stride = cap;
-  *kread = kp;
-  const uint32_t *gt = reinterpret_cast<const uint32_t *>(*id + (size_t)plan.P * 2 * a.q * cap);
-  *list_tau = reinterpret_cast<const float *>(gt + ((a.q + 63) / 64) * 64);
+GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
+  const GemmScratch gs = carve_gemm(scratch, plan, a.q, a.kprime);
+  GemmLists l;
+  l.key = gs.cand_key;
+  l.id = gs.cand_id;
+  l.cnt = gs.cand_cnt;
+  l.lists = plan.P * 2;
+  l.stride = kp_of(a.kprime) * tc::CAP_FACTOR;
+  l.gtau = gs.gtau;
+  return l;
 }
 
 }  // namespace vrs

@@ -63,25 +63,6 @@ cudaEvent_t prof_event() {
   return e;
 }
 
-struct ProfScope {
-  const char *name;
-  cudaStream_t s;
-  cudaEvent_t a = nullptr;
-  ProfScope(const char *n, cudaStream_t st) : name(n), s(st) {
-    std::lock_guard<std::mutex> g(g_prof_mu);
-    if (!g_prof_on) return;
-    a = prof_event();
-    cudaEventRecord(a, s);
-  }
-  ~ProfScope() {
-    if (!a) return;
-    std::lock_guard<std::mutex> g(g_prof_mu);
-    cudaEvent_t b = prof_event();
-    cudaEventRecord(b, s);
-    g_prof_pending.push_back({name, a, b});
-  }
-};
-
 void prof_resolve() {
   for (auto &r : g_prof_pending) {
     cudaEventSynchronize(r.b);
@@ -100,6 +81,22 @@ void prof_resolve() {
   g_prof_pending.clear();
 }
 }  // namespace
+
+namespace vrs {
+ProfScope::ProfScope(const char *n, cudaStream_t st) : name(n), s(st) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  a = prof_event();
+  cudaEventRecord(a, s);
+}
+ProfScope::~ProfScope() {
+  if (!a) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEvent_t b = prof_event();
+  cudaEventRecord(b, s);
+  g_prof_pending.push_back({name, a, b});
+}
+}  // namespace vrs
 
 static thread_local char g_err[512];
 static thread_local int32_t g_last_path = 0;
@@ -420,10 +417,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *xsel = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap * d) : nullptr;
 
   int launches = 0;
-  const float *lk = part_key;
-  const int32_t *li = part_id;
-  int32_t stride = kprime, kread = kprime, nlists = P, sorted = 1;
-  const float *list_tau = nullptr;
+  FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, kprime, q, ix->X, d, queries,
+                 (int32_t)metric, k, ix->row_offset, ids, dists};
   if (path == VRS_PATH_SCAN) {
     if (!identity) {
       ProfScope ps("select", stream);
@@ -446,10 +441,16 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
     }
-    gemm_lists(a, gp, gemm_scr, &lk, &li, &stride, &kread, &nlists, &list_tau);
-    sorted = 0;
+    const GemmLists gl = gemm_lists(a, gp, gemm_scr);
+    f.key = gl.key;
+    f.id = gl.id;
+    f.cnt = gl.cnt;
+    f.lists = gl.lists;
+    f.stride = gl.stride;
+    f.kread = 0;
+    f.sorted = 0;
+    f.gtau = gl.gtau;
   }
-  FinalizeArgs f{lk, li, nlists, kprime, stride, kread, sorted, list_tau, q, ix->X, d, queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   {
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));

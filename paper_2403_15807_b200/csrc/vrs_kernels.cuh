@@ -9,6 +9,18 @@
 
 namespace vrs {
 
+// Kernel timing scope (vrs_profile_enable): CUDA events recorded on the launch
+// stream around the enclosed launches, resolved by vrs_profile_read.
+struct ProfScope {
+  const char *name;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char *n, cudaStream_t st);
+  ~ProfScope();
+  ProfScope(const ProfScope &) = delete;
+  ProfScope &operator=(const ProfScope &) = delete;
+};
+
 // select.cu -- K4'/K5'
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
                           void *scratch, cudaStream_t stream, int *launches);
@@ -67,19 +79,28 @@ struct GemmArgs {
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
-void gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch, const float **key, const int32_t **id,
-                int32_t *stride, int32_t *kread, int32_t *nlists, const float **list_tau);
+// the tensor-core pass's candidate lists, as finalize reads them
+struct GemmLists {
+  const float *key;        // [lists][q][stride]
+  const int32_t *id;
+  const int32_t *cnt;      // [lists][q] entries per list
+  int32_t lists;
+  int32_t stride;
+  const uint32_t *gtau;    // [q] ordered-u32 lower bound of the k'-th best key (0 = none)
+};
+GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch);
 
-// finalize.cu -- K7'/K12' merge + exact re-score; K10' shard merge
+// finalize.cu -- K7'/K12' candidate selection + exact re-score; K10' shard merge
 struct FinalizeArgs {
-  const float *part_key;   // [P][q][kprime]
-  const int32_t *part_id;
-  int32_t P;
-  int32_t kprime;          // entries selected for the exact re-score
+  const float *key;        // candidate lists [lists][q][stride] (ranking keys, larger = better)
+  const int32_t *id;       // local row ids, -1 = padding
+  const int32_t *cnt;      // [lists][q] entries per list, or nullptr: kread entries per list
+  int32_t lists;
   int32_t stride;          // list stride in entries
-  int32_t kread;           // entries read per list (<= stride)
-  int32_t sorted;          // lists sorted best-first with >= kprime entries (scan path)
-  const float *list_tau;   // [P][q] per-list KP-th best key (-inf if unknown), or nullptr
+  int32_t kread;           // entries per list when cnt == nullptr
+  int32_t sorted;          // lists sorted best-first (scan path): their kprime-th entries bound the result
+  const uint32_t *gtau;    // optional [q] ordered-u32 lower bound of the kprime-th best key (0 = none)
+  int32_t kprime;          // candidates selected for the exact re-score
   int64_t q;
   const float *X;
   int32_t d;
@@ -92,38 +113,16 @@ struct FinalizeArgs {
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches);
 
-struct ProbeArgs {
-  const float *key;        // probe pass lists [lists][q][stride]
-  const int32_t *id;
-  int32_t lists;
-  int32_t stride;
-  int32_t kread;
+// probe slot maxima -> per-query threshold: the kth largest of a query's values
+// (each the key of a distinct row) bounds the kth best key over all rows from below
+struct ThresholdArgs {
+  const float *vals;       // [q][nvals]
+  int32_t nvals;
   int64_t q;
-  int32_t kp;
-  uint32_t *gtau;          // [q] ordered-u32 shared thresholds (raised with atomicMax)
+  int32_t kth;
+  uint32_t *gtau;          // [q] ordered-u32 out (0 = fewer than kth finite values)
 };
-cudaError_t launch_probe_threshold(const ProbeArgs &a, cudaStream_t s);
-
-struct SampleArgs {
-  const float *dense;      // [q][ldd] raw keys of the sample pass (NaN / -inf = no row)
-  int32_t ldd;
-  int64_t q;
-  int32_t kp;
-  uint32_t *gtau;
-};
-cudaError_t launch_sample_threshold(const SampleArgs &a, cudaStream_t s);
-
-struct RefineArgs {
-  const float *key;        // main-pass lists [lists][q][cap]
-  const int32_t *id;
-  const int32_t *cnt;      // [lists][q] entries so far
-  int32_t lists;
-  int32_t cap;
-  int64_t q;
-  int32_t kp;
-  uint32_t *gtau;
-};
-cudaError_t launch_refine_threshold(const RefineArgs &a, cudaStream_t s);
+cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s);
 
 struct MergeArgs {
   const int64_t *cand_ids;
