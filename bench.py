@@ -211,10 +211,13 @@ def main():
         from paper_2403_15807_b200.dist import gather_merge
     launches = [0]
 
+    cell_path = {}
+
     def run_cell(c):
         s, q = c
         ids, dists = ix.search(Qall[:q], preds[s], k=k, metric=metric, out=bufs[c])
         launches[0] += vrs.last_launches()
+        cell_path[c] = vrs.last_path()
         if world > 1:
             out = gather_merge(ids, dists, k, metric)   # NCCL all-gather + vrs_merge
             launches[0] += 1
@@ -283,8 +286,7 @@ def main():
     n_loc = r1 - r0
     for s, q in cells:
         ns = nsel[s]
-        # which path does this cell take?  (AUTO: tensor cores for q >= 8)
-        if q >= 8:
+        if cell_path[(s, q)] == vrs.PATH_GEMM:
             flops_gemm += 2.0 * q * ns * d
         else:
             bytes_scan += ns * (4.0 * d + 12) + q * 4.0 * d
@@ -296,11 +298,16 @@ def main():
     if dominant == "gemm.main":
         t_s = prof["gemm.main"][0] / 1e3 / nprof
         ach = flops_gemm / t_s / 1e12
-        roof = {"kernel": "tc_topk_kernel main pass (tcgen05 TF32 + fused top-k)", "bound": "tensor", "achieved": ach,
-                "peak": tf32_peak_sus, "unit": "TFLOP/s", "frac": ach / tf32_peak_sus, "traffic": None,
-                "peak_note": "TF32 = measured bf16 sustained x nominal tf32/bf16 (1.1/2.25)",
-                "frac_vs_burst_peak": ach / tf32_peak_burst,
-                "algorithmic": "2*Q*N_sel*d per cell, summed over the step's tensor-core cells"}
+        if ix.precision == vrs.PREC_BF16:   # kind::f16 on the bf16 shadow: the measured bf16 peak
+            peak, peak_b, note, kind = (pk["bf16_tflops_sustained"], pk["bf16_tflops"],
+                                        "measured bf16 (cuBLAS, MEASURED_PEAKS.json) sustained; burst beside", "bf16")
+        else:
+            peak, peak_b, note, kind = (tf32_peak_sus, tf32_peak_burst,
+                                        "TF32 = measured bf16 sustained x nominal tf32/bf16 (1.1/2.25)", "TF32")
+        roof = {"kernel": f"tc_topk_kernel main pass (tcgen05 {kind} + fused top-k)", "bound": "tensor",
+                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                "peak_note": note, "frac_vs_burst_peak": ach / peak_b,
+                "algorithmic": "2*Q*N_sel*d per cell, summed over the step's tensor-core cells, / main-pass time"}
     elif dominant is not None:
         t_s = prof[dominant][0] / 1e3 / nprof
         ach = bytes_scan / t_s / 1e9
@@ -408,7 +415,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "tf32",
+                "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
+                "dtype": "bf16" if ix.precision == vrs.PREC_BF16 else "tf32",
+                "dtype_note": "tensor-core selection operands (fp32 accumulate); returned dists re-scored in fp64 from fp32",
                 "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
                 "parity": parity, "cells": cell_out,

@@ -101,6 +101,20 @@ typedef struct {
 
 typedef struct vrs_index vrs_index;
 
+/* Operand precision of the tensor-core SELECTION pass.
+ * Returned distances are always re-scored exactly from the fp32 inputs; the
+ * precision only decides which rows reach the re-score (k + 16 per query). */
+typedef enum {
+  VRS_PREC_DEFAULT = 0,  /* load: bf16 shadow when d % 8 == 0; search: the index's own */
+  VRS_PREC_TF32 = 1,     /* tcgen05 kind::tf32 on the fp32 corpus (no extra memory) */
+  VRS_PREC_BF16 = 2      /* tcgen05 kind::f16 on a bf16 shadow copy built at load (+2 bytes / element) */
+} vrs_precision;
+
+typedef struct {
+  int32_t precision;     /* vrs_precision */
+  int32_t reserved[7];
+} vrs_load_options;
+
 /*
  * vrs_load -- build an index over one (shard of a) relation R (PAPER.md L269,
  * "column-store layout that stores both vector and relational data").
@@ -118,6 +132,17 @@ typedef struct vrs_index vrs_index;
  */
 VRS_API vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
                     int64_t row_offset, const vrs_allocator *alloc, void *cuda_stream, vrs_index **out);
+
+/*
+ * vrs_load_ex -- vrs_load with options (opts == NULL => defaults).  precision:
+ * DEFAULT builds the bf16 shadow when d % 8 == 0 and the base is 16-byte aligned;
+ * TF32 never builds it; BF16 requires it (else VRS_EUNSUPPORTED).  The shadow is
+ * index-owned memory (n * d * 2 bytes, through `alloc`), converted on `cuda_stream`
+ * with round-to-nearest-even.
+ */
+VRS_API vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
+                               int64_t row_offset, const vrs_allocator *alloc, const vrs_load_options *opts,
+                               void *cuda_stream, vrs_index **out);
 
 /*
  * vrs_search -- sigma_{eps,v,theta_R}(R) for a batch of q query vectors.
@@ -148,7 +173,8 @@ typedef enum {
 typedef struct {
   int32_t path;      /* vrs_path */
   int32_t rows;      /* vrs_rows */
-  int32_t reserved[6];
+  int32_t precision; /* vrs_precision of the tensor-core selection (DEFAULT: bf16 if the index has the shadow) */
+  int32_t reserved[5];
 } vrs_search_options;
 
 /* vrs_search with explicit options (opts == NULL => defaults). */
@@ -198,6 +224,10 @@ VRS_API const char *vrs_last_error(void);
 /* Introspection for tests / bench: which path the last vrs_search_ex on this
  * thread took (vrs_path value) and how many kernels it enqueued. */
 VRS_API int32_t vrs_last_path(void);
+/* vrs_precision of the last vrs_search_ex's tensor-core pass on this thread (DEFAULT when it took the scan path). */
+VRS_API int32_t vrs_last_precision(void);
+/* VRS_PREC_BF16 if the index holds the bf16 shadow, else VRS_PREC_TF32. */
+VRS_API int32_t vrs_index_precision(const vrs_index *ix);
 VRS_API int32_t vrs_last_launches(void);
 
 /*

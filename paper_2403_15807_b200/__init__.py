@@ -15,10 +15,11 @@ import torch
 
 from . import _lib
 from ._lib import (ATTR_I32, ATTR_U8, COSINE, EXPORTS, IP, K_MAX, L2, PATH_AUTO, PATH_GEMM, PATH_SCAN,
-                   ROWS_AUTO, ROWS_GATHER, ROWS_MASKED, VrsError)
+                   PREC_BF16, PREC_DEFAULT, PREC_TF32, ROWS_AUTO, ROWS_GATHER, ROWS_MASKED, VrsError)
 
 __all__ = ["Index", "merge", "VrsError", "L2", "IP", "COSINE", "PATH_AUTO", "PATH_SCAN", "PATH_GEMM",
-           "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "K_MAX", "last_path", "last_launches", "library"]
+           "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "PREC_DEFAULT", "PREC_TF32", "PREC_BF16", "K_MAX", "last_path",
+           "last_precision", "last_launches", "library"]
 
 METRICS = {"l2": L2, "ip": IP, "cos": COSINE, "cosine": COSINE}
 
@@ -40,17 +41,23 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _options(path, rows):
-    if path is None and rows is None:
+def _options(path, rows, precision=None):
+    if path is None and rows is None and precision is None:
         return None
     o = _lib.SearchOptions()
     o.path = PATH_AUTO if path is None else int(path)
     o.rows = ROWS_AUTO if rows is None else int(rows)
+    o.precision = PREC_DEFAULT if precision is None else int(precision)
     return ctypes.byref(o)
 
 
 def last_path() -> int:
     return int(library().vrs_last_path())
+
+
+def last_precision() -> int:
+    """Tensor-core selection precision of the last search on this thread (PREC_DEFAULT: scan path)."""
+    return int(library().vrs_last_precision())
 
 
 def last_launches() -> int:
@@ -82,7 +89,7 @@ class Index:
     """vrs_load over one (shard of a) relation: fp32 vectors [n, d] and
     int32 / uint8 attribute columns, all CUDA tensors (borrowed, kept alive here)."""
 
-    def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None):
+    def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None, precision=None):
         lib = library()
         if vectors.dtype != torch.float32 or vectors.dim() != 2 or not vectors.is_contiguous():
             raise ValueError("vectors must be a contiguous float32 [n, d] tensor")
@@ -99,9 +106,12 @@ class Index:
             carr[i].data = a.data_ptr()
         h = ctypes.c_void_p()
         n, d = vectors.shape
-        st = lib.vrs_load(_ptr(vectors), n, d, carr, len(self.attrs), int(row_offset), None, _stream(stream),
-                          ctypes.byref(h))
-        _lib.check(st, "vrs_load")
+        opts = _lib.LoadOptions()
+        opts.precision = PREC_DEFAULT if precision is None else int(precision)
+        st = lib.vrs_load_ex(_ptr(vectors), n, d, carr, len(self.attrs), int(row_offset), None, ctypes.byref(opts),
+                             _stream(stream), ctypes.byref(h))
+        _lib.check(st, "vrs_load_ex")
+        self.precision = int(lib.vrs_index_precision(h))
         self._h = h
         self.n, self.d, self.row_offset = int(n), int(d), int(row_offset)
 
@@ -117,7 +127,7 @@ class Index:
             pass
 
     def search(self, queries: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
-               out=None, stream=None):
+               out=None, stream=None, precision=None):
         """-> (ids int64 [q, k], dists float32 [q, k]) on the device (async on `stream`)."""
         lib = library()
         q = queries.shape[0]
@@ -131,12 +141,12 @@ class Index:
         pr, keep = _lib.make_predicate(pred)
         st = lib.vrs_search_ex(self._h, _ptr(queries) if q else None, q, d, ctypes.byref(pr), int(k),
                                _metric(metric), _ptr(ids) if q else None, _ptr(dists) if q else None,
-                               _options(path, rows), _stream(stream))
+                               _options(path, rows, precision), _stream(stream))
         _lib.check(st, "vrs_search")
         return ids, dists
 
     def search_host(self, queries_h: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
-                    out=None, stream=None):
+                    out=None, stream=None, precision=None):
         """End-to-end call on host buffers (H2D + search + D2H inside libvrs; synchronous)."""
         lib = library()
         q, d = queries_h.shape
@@ -147,7 +157,7 @@ class Index:
             ids, dists = out
         pr, keep = _lib.make_predicate(pred)
         st = lib.vrs_search_host(self._h, _ptr(queries_h), q, d, ctypes.byref(pr), int(k), _metric(metric),
-                                 _ptr(ids), _ptr(dists), _options(path, rows), _stream(stream))
+                                 _ptr(ids), _ptr(dists), _options(path, rows, precision), _stream(stream))
         _lib.check(st, "vrs_search_host")
         return ids, dists
 

@@ -11,6 +11,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvrs.so")
+if os.environ.get("VRS_LIB") == "exp":   # experiment build of the same sources (csrc/Makefile `exp`)
+    LIB_PATH = os.path.join(_HERE, "libvrs_exp.so")
 
 OK, EINVAL, ENOTFOUND, EDEGENERATE, ENOMEM, ECUDA, ECOMM, EUNSUPPORTED = range(8)
 STATUS_NAMES = ["VRS_OK", "VRS_EINVAL", "VRS_ENOTFOUND", "VRS_EDEGENERATE", "VRS_ENOMEM", "VRS_ECUDA",
@@ -19,12 +21,13 @@ L2, IP, COSINE = 0, 1, 2
 ATTR_I32, ATTR_U8 = 0, 1
 PATH_AUTO, PATH_SCAN, PATH_GEMM = 0, 1, 2
 ROWS_AUTO, ROWS_GATHER, ROWS_MASKED = 0, 1, 2
+PREC_DEFAULT, PREC_TF32, PREC_BF16 = 0, 1, 2
 K_MAX = 240
 MAX_CLAUSES = 8
 
 # every symbol include/vrs.h declares (tests check the library exports them)
-EXPORTS = ("vrs_load", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
-           "vrs_last_error", "vrs_last_path", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
+EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
+           "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
            "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset")
 
 
@@ -52,7 +55,12 @@ class Allocator(ctypes.Structure):
 
 
 class SearchOptions(ctypes.Structure):
-    _fields_ = [("path", ctypes.c_int32), ("rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("path", ctypes.c_int32), ("rows", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
+
+
+class LoadOptions(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
 
 
 _lib = None
@@ -69,16 +77,20 @@ def load_library():
     lib = ctypes.CDLL(LIB_PATH)
     p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.vrs_load.argtypes = [p, i64, i32, p, i32, i64, p, p, ctypes.POINTER(p)]
+    lib.vrs_load_ex.argtypes = [p, i64, i32, p, i32, i64, p, p, p, ctypes.POINTER(p)]
     lib.vrs_search.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p]
     lib.vrs_search_ex.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p, p]
     lib.vrs_search_host.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p, p]
     lib.vrs_select.argtypes = [p, p, p, p, p, p]
     lib.vrs_merge.argtypes = [p, p, i32, i64, i32, ctypes.c_int, p, p, p]
     lib.vrs_free.argtypes = [p]
-    for f in ("vrs_load", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free"):
+    for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free"):
         getattr(lib, f).restype = ctypes.c_int
     lib.vrs_last_error.restype = ctypes.c_char_p
     lib.vrs_last_path.restype = i32
+    lib.vrs_last_precision.restype = i32
+    lib.vrs_index_precision.argtypes = [p]
+    lib.vrs_index_precision.restype = i32
     lib.vrs_last_launches.restype = i32
     lib.vrs_index_rows.argtypes = [p]
     lib.vrs_index_rows.restype = i64

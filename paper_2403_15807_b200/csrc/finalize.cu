@@ -173,7 +173,6 @@ __device__ void warp_sort_desc_d(double *key, int64_t *id, int n) {
 
 
 // ------------------------------------------------------ warp-level selection
-constexpr int kFinWarps = 4;     // queries per CTA (one warp each)
 constexpr int kBufCap = 512;     // per-warp candidate buffer (>= 2 k' for every k' <= 256)
 
 // The K-th largest of the u32 values get(i, u) (i < n, only those for which get
@@ -276,28 +275,29 @@ __device__ __noinline__ uint32_t warp_keep_best(float *bk, int32_t *bi, int &n, 
 }
 
 // ------------------------------------------------------------------ finalize
-// One warp per query: (1) a provable lower bound of the k'-th best ranking key
-// (the shared probe threshold, or for sorted scan lists the best of their k'-th
+// Per query: (1) a provable lower bound of the k'-th best ranking key (the
+// shared probe threshold, or for sorted scan lists the best of their k'-th
 // entries); (2) stream every list entry at or above it into a shared-memory
 // buffer, compacting to the k' best by radix select whenever it fills; (3) keep
 // exactly the k' best (ties -> lower id); (4) re-score those rows exactly (fp64
-// accumulation of the fp32 inputs, one lane per row); (5) sort by exact score
-// (ties -> lower id) and write the k best with padding.
-__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a) {
-  __shared__ float s_key[kFinWarps][kBufCap];
-  __shared__ int32_t s_id[kFinWarps][kBufCap];
-  __shared__ uint32_t s_hist[kFinWarps][256];
-  __shared__ double s_sc[kFinWarps][kFinMaxSel];
-  __shared__ int64_t s_sid[kFinWarps][kFinMaxSel];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j = (int64_t)blockIdx.x * kFinWarps + w;
-  if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
-  float *bk = s_key[w];
-  int32_t *bi = s_id[w];
-  uint32_t *hist = s_hist[w];
-  const int K = a.kprime;
+// accumulation of the fp32 inputs); (5) sort by exact score (ties -> lower id)
+// and write the k best with padding.
+// W = 1: one warp per query (4 queries per CTA) for large batches; W = 8: the
+// 8 warps of a CTA share one query (lists and re-score split between them, the
+// per-warp survivors merged by warp 0) so small batches are not latency-bound.
+constexpr int kFinGroup = 4;   // queries per CTA when W == 1
 
-  // 1. lower bound (ordered key): entries below it cannot be among the k' best
+struct FinBufs {
+  float key[kBufCap];
+  int32_t id[kBufCap];
+  uint32_t hist[256];
+};
+
+// Steps 1-2 for one warp over lists l = first, first + step, ... (in groups of
+// 32): the warp's buffer ends with at most K entries (or all it saw).
+__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufs &B) {
+  const int lane = threadIdx.x & 31;
+  const int K = a.kprime;
   uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
   if (a.sorted && K <= a.kread) {
     for (int l = lane; l < a.lists; l += 32) {
@@ -307,10 +307,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) thr = max(thr, __shfl_xor_sync(0xffffffffu, thr, o));
   }
-
-  // 2. stream: lane l walks list l (8 entries per step, loads issued together)
   int n = 0;
-  for (int l0 = 0; l0 < a.lists; l0 += 32) {
+  for (int l0 = first_group * 32; l0 < a.lists; l0 += group_step * 32) {
     const int l = l0 + lane;
     int c = 0;
     if (l < a.lists) c = a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread;
@@ -330,14 +328,14 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (m == 0) continue;
         if (n + __popc(m) > kBufCap) {
-          thr = max(thr, warp_keep_best(bk, bi, n, K, hist));
+          thr = max(thr, warp_keep_best(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv[u]) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
         }
         if (keep) {
           const int pos = n + __popc(m & lanemask_lt());
-          bk[pos] = kv[u];
-          bi[pos] = iv[u];
+          B.key[pos] = kv[u];
+          B.id[pos] = iv[u];
         }
         n += __popc(m);
       }
@@ -346,25 +344,22 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a
     }
   }
   __syncwarp();
-  // 3. exactly the k' best by ranking key
-  if (n > K) warp_keep_best(bk, bi, n, K, hist);
-  const int m = n;
+  if (n > K) warp_keep_best(B.key, B.id, n, K, B.hist);
+  return n;
+}
 
-  // 4. exact re-score: the warp reads each candidate row coalesced, 8 rows in
-  //    flight, fp64 accumulation, one butterfly reduction per row
+// Step 4 for candidates c0, c0 + cstep*U ... of ids[0..m): the warp reads each
+// row coalesced, U rows in flight, fp64 accumulation, one butterfly per row.
+__device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids, int m, int cfirst, int cstep,
+                            double qq, double *sc_out, int64_t *sid_out) {
+  const int lane = threadIdx.x & 31;
   const float *q = a.Q + j * a.d;
   const bool vec = (a.d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Q)) & 15) == 0;
-  double qq = 0.0;
-  if (a.metric == VRS_COSINE) {
-    for (int t = lane; t < a.d; t += 32) qq += (double)q[t] * (double)q[t];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
-  }
   constexpr int U = 8;
-  for (int c0 = 0; c0 < m; c0 += U) {
+  for (int c0 = cfirst * U; c0 < m; c0 += cstep * U) {
     const float *xr[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) xr[u] = a.X + (int64_t)bi[min(c0 + u, m - 1)] * a.d;
+    for (int u = 0; u < U; ++u) xr[u] = a.X + (int64_t)ids[min(c0 + u, m - 1)] * a.d;
     double sc[U], xx[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) { sc[u] = 0.0; xx[u] = 0.0; }
@@ -411,32 +406,113 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(FinalizeArgs a
         double v = sc[u];
         if (a.metric == VRS_L2) v = -v;   // sort key: larger is better
         else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xx[u]));
-        s_sc[w][c] = v;
-        s_sid[w][c] = bi[c];
+        sc_out[c] = v;
+        sid_out[c] = ids[c];
       }
     }
   }
-  __syncwarp();
+}
+
+__device__ double fin_qq(const FinalizeArgs &a, int64_t j) {
+  const int lane = threadIdx.x & 31;
+  double qq = 0.0;
+  if (a.metric == VRS_COSINE) {
+    const float *q = a.Q + j * a.d;
+    for (int t = lane; t < a.d; t += 32) qq += (double)q[t] * (double)q[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+  }
+  return qq;
+}
+
+// Step 5 (one warp).
+__device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double qq, double *sc, int64_t *sid) {
+  const int lane = threadIdx.x & 31;
   int np = 1;
   while (np < m) np <<= 1;
-  for (int c = m + lane; c < np; c += 32) { s_sc[w][c] = -INFINITY; s_sid[w][c] = INT64_MAX; }
+  for (int c = m + lane; c < np; c += 32) { sc[c] = -INFINITY; sid[c] = INT64_MAX; }
   __syncwarp();
-  // 5. order by exact score and write the k best
-  if (m > 1) warp_sort_desc_d(s_sc[w], s_sid[w], np);
+  if (m > 1) warp_sort_desc_d(sc, sid, np);
   const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
   const int mv = zero_cos ? 0 : min(m, a.k);
   const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
   for (int r = lane; r < a.k; r += 32) {
     const int64_t o = j * a.k + r;
     if (r < mv) {
-      a.ids[o] = a.row_offset + s_sid[w][r];
-      const double sc = s_sc[w][r];
-      a.dists[o] = (float)(a.metric == VRS_L2 ? -sc : sc);
+      a.ids[o] = a.row_offset + sid[r];
+      const double v = sc[r];
+      a.dists[o] = (float)(a.metric == VRS_L2 ? -v : v);
     } else {
       a.ids[o] = -1;
       a.dists[o] = pad;
     }
   }
+}
+
+__global__ void __launch_bounds__(kFinGroup * 32) finalize_warp_kernel(FinalizeArgs a) {
+  __shared__ FinBufs s_buf[kFinGroup];
+  __shared__ double s_sc[kFinGroup][kFinMaxSel];
+  __shared__ int64_t s_sid[kFinGroup][kFinMaxSel];
+  const int w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
+  if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
+  const int m = fin_stream(a, j, 0, 1, s_buf[w]);
+  const double qq = fin_qq(a, j);
+  fin_rescore(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w]);
+  __syncwarp();
+  fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w]);
+}
+
+constexpr int kFinW = 8;   // warps per query in the small-batch variant
+__global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a) {
+  __shared__ FinBufs s_buf[kFinW];
+  __shared__ double s_sc[kFinMaxSel];
+  __shared__ int64_t s_sid[kFinMaxSel];
+  __shared__ int s_n[kFinW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x;
+  // each warp: its share of the lists -> at most k' survivors
+  const int nw = fin_stream(a, j, w, kFinW, s_buf[w]);
+  if (lane == 0) s_n[w] = nw;
+  __syncthreads();
+  // warp 0 merges the survivors of all warps into its own buffer
+  if (w == 0) {
+    const int K = a.kprime;
+    FinBufs &B = s_buf[0];
+    int n = nw;
+    uint32_t thr = 0u;
+    for (int v = 1; v < kFinW; ++v) {
+      const int nv = s_n[v];
+      for (int i0 = 0; i0 < nv; i0 += 32) {
+        const int i = i0 + lane;
+        float kv = -INFINITY;
+        int32_t iv = -1;
+        if (i < nv) { kv = s_buf[v].key[i]; iv = s_buf[v].id[i]; }
+        bool keep = i < nv && ordered_u32(kv) >= thr;
+        uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (n + __popc(m) > kBufCap) {
+          thr = max(thr, warp_keep_best(B.key, B.id, n, K, B.hist));
+          keep = keep && ordered_u32(kv) >= thr;
+          m = __ballot_sync(0xffffffffu, keep);
+        }
+        if (keep) {
+          const int pos = n + __popc(m & lanemask_lt());
+          B.key[pos] = kv;
+          B.id[pos] = iv;
+        }
+        n += __popc(m);
+        __syncwarp();
+      }
+    }
+    if (n > K) warp_keep_best(B.key, B.id, n, K, B.hist);
+    if (lane == 0) s_n[0] = n;
+  }
+  __syncthreads();
+  const int m = s_n[0];
+  const double qq = fin_qq(a, j);
+  fin_rescore(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid);
+  __syncthreads();
+  if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid);
 }
 
 // Per query (one CTA): the kth largest probe slot maximum (each the key of a
@@ -512,7 +588,9 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
-  finalize_kernel<<<(unsigned)((a.q + kFinWarps - 1) / kFinWarps), kFinWarps * 32, 0, s>>>(a);
+  // small batches: a CTA of 8 warps per query; large: a warp per query
+  if (a.q < 4 * kSmCountB200) finalize_cta_kernel<<<(unsigned)a.q, kFinW * 32, 0, s>>>(a);
+  else finalize_warp_kernel<<<(unsigned)((a.q + kFinGroup - 1) / kFinGroup), kFinGroup * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

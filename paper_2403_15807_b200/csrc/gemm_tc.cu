@@ -33,6 +33,7 @@
 // row) for small q.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include <stdio.h>
 #include <stdlib.h>
@@ -45,13 +46,16 @@ namespace vrs {
 
 namespace tc {
 constexpr int BM = 128;         // queries per tile (TMEM lanes)
-constexpr int BN = 256;         // rows per tile (TMEM columns, MMA N)
-constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span
+#ifndef VRS_BN
+#define VRS_BN 256
+#endif
+constexpr int BN = VRS_BN;      // rows per tile (TMEM columns, MMA N)
+constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span (bf16: 64)
 constexpr int PIPE_BYTES = 192 * 1024;   // shared-memory pipeline region (A resident and/or stages)
 constexpr int MAX_STAGES = 8;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
-constexpr int B_BYTES = BN * BK * 4;   // 32 KB
-constexpr int ACC_STAGES = 2;   // accumulator tiles in TMEM (2 x 256 columns)
+constexpr int B_BYTES = BN * BK * 4;   // 32 KB at BN = 256
+constexpr int ACC_STAGES = 512 / BN;   // accumulator tiles in TMEM (all 512 columns)
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
@@ -62,10 +66,11 @@ constexpr int BIAS_STAGES = 4;
 constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
 constexpr int SLOTS = 32;       // probe: row slots per lane (column index mod 32)
 constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile
-constexpr int CHUNKS = BN / 32; // 32-column epilogue chunks per tile
-// dynamic smem: [pipeline region] + bias a/b/id [BIAS_STAGES][BN] + chunk bounds
-// [BIAS_STAGES][CHUNKS][4] + per-warp key staging (doubles as the compaction histogram)
-constexpr size_t SMEM_BYTES = 1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + BIAS_STAGES * CHUNKS * 16 +
+constexpr int GROUPS = BN / 8;  // 8-column key-bound groups per tile
+// dynamic smem: [pipeline region] + bias a/b/id [BIAS_STAGES][BN] + group bounds
+// max b / max a / min a [3][BIAS_STAGES][GROUPS] + per-warp key staging (doubles as
+// the compaction histogram)
+constexpr size_t SMEM_BYTES = 1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + 3 * BIAS_STAGES * GROUPS * 4 +
                               EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
 }  // namespace tc
 
@@ -127,6 +132,19 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, ui
       : "memory");
 }
 
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), both K-major.
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Shared-memory matrix descriptor, K-major operand in the canonical
 // 128-byte-swizzle layout written by TMA (8-row groups of 1024 bytes).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -139,9 +157,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: D fp32, A/B tf32, both K-major, N = BN, M = BM.
-__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: D fp32, A/B tf32 (format 2) or bf16 (format 1), both
+// K-major, N = BN, M = BM.
+__host__ __device__ constexpr uint32_t mma_idesc(int M, int N, bool bf16) {
+  return (1u << 4) | ((bf16 ? 1u : 2u) << 7) | ((bf16 ? 1u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
 #define TMEM_LD_32x32b_X32(taddr, r)                                                                              \
@@ -270,22 +290,45 @@ __device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64
 }
 
 // Late materialization ("(re-)materialized into dense
-// vectors"): X_sel[r] = X[ids[r]], one warp per row, 16-byte vector copies.
-// HBM-bound: 2 * 4d bytes per selected row.
-__global__ void __launch_bounds__(256) gather_copy_kernel(const float *__restrict__ X, int32_t d,
+// vectors"): X_sel[r] = X[ids[r]] (rows of row_bytes, a multiple of 16: the fp32
+// corpus or its bf16 shadow), one warp per row, 16-byte vector copies.
+// HBM-bound: 2 * row_bytes per selected row.
+__global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict__ X, int32_t row_bytes,
                                                           const int32_t *__restrict__ ids,
                                                           const int64_t *__restrict__ count, int64_t n, int allow,
-                                                          int64_t cap, float *__restrict__ xsel) {
+                                                          int64_t cap, void *__restrict__ xsel) {
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, n, cap)) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int d4 = d >> 2;
+  const int v16 = row_bytes >> 4;
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_sel; r += warps) {
-    const float4 *src = reinterpret_cast<const float4 *>(X + (int64_t)__ldg(ids + r) * d);
-    float4 *dst = reinterpret_cast<float4 *>(xsel + r * d);
-    for (int i = lane; i < d4; i += 32) dst[i] = __ldg(src + i);
+    const int4 *src = reinterpret_cast<const int4 *>(static_cast<const char *>(X) + (int64_t)__ldg(ids + r) * row_bytes);
+    int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(xsel) + r * row_bytes);
+    for (int i = lane; i < v16; i += 32) dst[i] = __ldg(src + i);
   }
+}
+
+// fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per search.
+__global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (count >> 2); i += stride) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(in) + i);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t *>(&lo);
+    w.y = *reinterpret_cast<uint32_t *>(&hi);
+    reinterpret_cast<uint2 *>(out)[i] = w;
+  }
+  for (int64_t i = (count & ~int64_t(3)) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((count / 4 + 255) / 256 + 1, 148 * 16);
+  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, static_cast<__nv_bfloat16 *>(out), count);
+  return cudaGetLastError();
 }
 
 constexpr int MODE_MAIN = 0;
@@ -294,7 +337,8 @@ constexpr int MODE_PROBE = 1;
 // AR: the query tile stays resident in shared memory (d <= 128).
 // MODE: MAIN (fused top-k candidates) or PROBE (slot maxima for the threshold).
 // ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
-template <bool AR, int MODE, bool ROWSCALE>
+// BF: operands are bf16 (shadow corpus, kind::f16) instead of fp32 (kind::tf32).
+template <bool AR, int MODE, bool ROWSCALE, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
@@ -309,14 +353,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                           ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
                           : MAX_STAGES;
   constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
+  constexpr int KE = BF ? 2 * BK : BK;                   // elements per 128-byte K block
   uint8_t *a_res = smem;                                 // AR: resident query tile
   uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
   float *bias_a = reinterpret_cast<float *>(smem + PIPE_BYTES);               // [BIAS_STAGES][BN]
   float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
-  // per 32-column chunk: {max b, max a, min a, -} over its rows (key upper bound)
-  float4 *cmeta = reinterpret_cast<float4 *>(row_id + BIAS_STAGES * BN);       // [BIAS_STAGES][CHUNKS]
-  float *kstage = reinterpret_cast<float *>(cmeta + BIAS_STAGES * CHUNKS);     // [EPI_WARPS][32][STAGE_COLS]
+  // per 8-row group: max b, max a, min a over its rows (the group's key upper bound)
+  float *g_bmax = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [BIAS_STAGES][GROUPS]
+  float *g_amax = g_bmax + BIAS_STAGES * GROUPS;
+  float *g_amin = g_amax + BIAS_STAGES * GROUPS;
+  float *kstage = g_amin + BIAS_STAGES * GROUPS;                                // [EPI_WARPS][32][STAGE_COLS]
 
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES], empty_bar[MAX_STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
@@ -375,7 +422,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       uint32_t phase = 0;
       if (AR && ntiles > 0) {
         mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
-        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * BK, qtile * BM);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
       }
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)(tile_of(t) * BN);
@@ -383,15 +430,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *st = b_base + stage * SSTRIDE;
           mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
-          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * BK, qtile * BM);
-          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * BK, row0);
+          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
+          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * KE, row0);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = tf32_idesc(BM, BN);
+    constexpr uint32_t idesc = mma_idesc(BM, BN, BF);
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
@@ -408,8 +455,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
           const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k)  // K = 8 tf32 = 32 bytes per instruction
-            tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // K = 8 tf32 / 16 bf16 = 32 bytes per instruction
+            if (BF) tc_mma_bf16(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+          }
           // frees the smem slot when these MMAs finish; accumulator ready after the last K block
           tc_commit(&empty_bar[stage]);
           if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
@@ -422,7 +471,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // ------------------------------------------------ per-row epilogue terms
     // Loads for tile t + PF are issued before tile t is written out: the warp is
     // memory-latency bound otherwise (one ~us round trip per tile).
-    constexpr int PF = 4;
+    constexpr int PF = 2;
     const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
     constexpr int RPL = BN / 32;   // rows per lane
     float nv[PF][RPL];
@@ -496,17 +545,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             reinterpret_cast<int4 *>(row_id + s * BN + lane * RPL)[v] =
                 make_int4(iv[u][4 * v], iv[u][4 * v + 1], iv[u][4 * v + 2], iv[u][4 * v + 3]);
         }
-        // chunk bounds: this lane's 8 rows, then the 4 lanes of each 32-row chunk
+        // group bounds over 8-row groups (8 / RPL lanes each)
+        static_assert(RPL <= 8 && 8 % RPL == 0, "8-row groups of whole lanes");
         float bmx = bv[0], amx = av[0], amn = av[0];
 #pragma unroll
         for (int k = 1; k < RPL; ++k) { bmx = fmaxf(bmx, bv[k]); amx = fmaxf(amx, av[k]); amn = fminf(amn, av[k]); }
 #pragma unroll
-        for (int o = 1; o < 32 / RPL; o <<= 1) {
+        for (int o = 1; o < 8 / RPL; o <<= 1) {
           bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
           amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
           amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
         }
-        if ((lane & (32 / RPL - 1)) == 0) cmeta[s * CHUNKS + lane / (32 / RPL)] = make_float4(bmx, amx, amn, 0.f);
+        if ((lane & (8 / RPL - 1)) == 0) {
+          g_bmax[s * GROUPS + lane / (8 / RPL)] = bmx;
+          if (ROWSCALE) { g_amax[s * GROUPS + lane / (8 / RPL)] = amx; g_amin[s * GROUPS + lane / (8 / RPL)] = amn; }
+        }
         mbar_arrive(&bfull_bar[s]);
         fetch(t + PF, nv[u], iv[u], wv[u]);
       }
@@ -558,69 +611,79 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
       }
     };
-    // one 32-column chunk: r holds the raw dot products (turned into keys in place)
-    auto chunk = [&](uint32_t (&r)[32], const float *ba, const float *bb, const int32_t *rid, float4 cm) {
-      if (MODE == MODE_MAIN) {
-        // fast path: an upper bound of the chunk's keys from the largest raw dot
-        // and the chunk's bias / scale range; fma is monotone in each argument
-        // (scale > 0), so no key of the chunk can exceed it
-        float dm = __uint_as_float(r[0]);
+    auto f4 = [](const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; };
+    // one 32-column chunk: r holds the raw dot products; gb/ga/gn: the chunk's 4
+    // group bounds (max b, max a, min a)
+    auto chunk = [&](uint32_t (&r)[32], const float *ba, const float *bb, const int32_t *rid, const float *gb,
+                     const float *ga, const float *gn) {
+      if (MODE == MODE_PROBE) {   // exact keys -> running slot maxima
 #pragma unroll
-        for (int i = 1; i < 32; ++i) dm = fmaxf(dm, __uint_as_float(r[i]));
-        const float kb = ROWSCALE ? fmaf(dm, dm >= 0.f ? cm.y : cm.z, cm.x) : fmaf(dm, sc, cm.x);
-        ++st_chunks;
-        if (!__any_sync(0xffffffffu, kb > thr)) return;
-      }
-      float kmax = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 b4 = *reinterpret_cast<const float4 *>(bb + i);
-        float4 a4 = make_float4(sc, sc, sc, sc);
-        if (ROWSCALE) a4 = *reinterpret_cast<const float4 *>(ba + i);
-        const float k0 = fmaf(__uint_as_float(r[i]), a4.x, b4.x);
-        const float k1 = fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y);
-        const float k2 = fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z);
-        const float k3 = fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w);
-        r[i] = __float_as_uint(k0); r[i + 1] = __float_as_uint(k1);
-        r[i + 2] = __float_as_uint(k2); r[i + 3] = __float_as_uint(k3);
-        if (MODE == MODE_PROBE) {
-          smax[i] = fmaxf(smax[i], k0); smax[i + 1] = fmaxf(smax[i + 1], k1);
-          smax[i + 2] = fmaxf(smax[i + 2], k2); smax[i + 3] = fmaxf(smax[i + 3], k3);
-        } else {
-          kmax = fmaxf(kmax, fmaxf(fmaxf(k0, k1), fmaxf(k2, k3)));
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = *reinterpret_cast<const float4 *>(bb + i);
+          float4 a4 = make_float4(sc, sc, sc, sc);
+          if (ROWSCALE) a4 = *reinterpret_cast<const float4 *>(ba + i);
+          smax[i] = fmaxf(smax[i], fmaf(__uint_as_float(r[i]), a4.x, b4.x));
+          smax[i + 1] = fmaxf(smax[i + 1], fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y));
+          smax[i + 2] = fmaxf(smax[i + 2], fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z));
+          smax[i + 3] = fmaxf(smax[i + 3], fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w));
         }
+        return;
       }
-      if (MODE == MODE_PROBE) return;
-      if (!__any_sync(0xffffffffu, kmax > thr)) return;
-      // rare once the threshold is in place: make room (<= 32 appends follow; the
-      // compaction histogram aliases the staging rows), then each lane appends its
-      // own accepted columns in row order from its private staging row
+      // fast path: per 8-column group an upper bound of its keys from the group's
+      // largest raw dot and its bias / scale range -- fma is monotone in each
+      // argument (scale > 0), so no key of the group can exceed it
+      const float4 b4 = *reinterpret_cast<const float4 *>(gb);
+      float4 ax4 = b4, an4 = b4;
+      if (ROWSCALE) { ax4 = *reinterpret_cast<const float4 *>(ga); an4 = *reinterpret_cast<const float4 *>(gn); }
+      uint32_t pass = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float dm = __uint_as_float(r[g * 8]);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) dm = fmaxf(dm, __uint_as_float(r[g * 8 + i]));
+        const float kb = ROWSCALE ? fmaf(dm, dm >= 0.f ? f4(ax4, g) : f4(an4, g), f4(b4, g)) : fmaf(dm, sc, f4(b4, g));
+        pass |= (kb > thr ? 1u : 0u) << g;
+      }
+      ++st_chunks;
+      if (!__any_sync(0xffffffffu, pass != 0)) return;
+      // rare once the threshold is in place: exact keys of the flagged groups, make
+      // room (<= 8 appends follow; the compaction histogram aliases the staging
+      // rows), then each lane appends its accepted columns in row order from its
+      // private staging row
       ++st_slow;
       if (__any_sync(0xffffffffu, cnt + 32 > p.cap)) compact_needed(p.cap - 32);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {   // (unrolled: r must stay in registers)
+      for (int g = 0; g < 4; ++g) {   // (unrolled: r must stay in registers)
+        if (!__any_sync(0xffffffffu, (pass >> g) & 1u)) continue;
+        float kk[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 4) {
+          const float4 bq = *reinterpret_cast<const float4 *>(bb + g * 8 + i);
+          float4 aq = make_float4(sc, sc, sc, sc);
+          if (ROWSCALE) aq = *reinterpret_cast<const float4 *>(ba + g * 8 + i);
+          kk[i] = fmaf(__uint_as_float(r[g * 8 + i]), aq.x, bq.x);
+          kk[i + 1] = fmaf(__uint_as_float(r[g * 8 + i + 1]), aq.y, bq.y);
+          kk[i + 2] = fmaf(__uint_as_float(r[g * 8 + i + 2]), aq.z, bq.z);
+          kk[i + 3] = fmaf(__uint_as_float(r[g * 8 + i + 3]), aq.w, bq.w);
+        }
         uint32_t msk = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) msk |= (__uint_as_float(r[h * 16 + i]) > thr ? 1u : 0u) << i;
-        if (__any_sync(0xffffffffu, msk != 0)) {
-          float *myrow = wst + lane * STAGE_COLS;
-          if (msk) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4 *>(myrow + i) =
-                  make_float4(__uint_as_float(r[h * 16 + i]), __uint_as_float(r[h * 16 + i + 1]),
-                              __uint_as_float(r[h * 16 + i + 2]), __uint_as_float(r[h * 16 + i + 3]));
-            st_app += __popc(msk);
-            while (msk) {
-              const int i = __ffs(msk) - 1;
-              msk &= msk - 1;
-              ckey[cnt] = myrow[i];
-              cid[cnt] = rid[h * 16 + i];
-              ++cnt;
-            }
+        for (int i = 0; i < 8; ++i) msk |= (kk[i] > thr ? 1u : 0u) << i;
+        if (!__any_sync(0xffffffffu, msk != 0)) continue;
+        float *myrow = wst + lane * STAGE_COLS;
+        if (msk) {
+          *reinterpret_cast<float4 *>(myrow) = make_float4(kk[0], kk[1], kk[2], kk[3]);
+          *reinterpret_cast<float4 *>(myrow + 4) = make_float4(kk[4], kk[5], kk[6], kk[7]);
+          st_app += __popc(msk);
+          while (msk) {
+            const int i = __ffs(msk) - 1;
+            msk &= msk - 1;
+            ckey[cnt] = myrow[i];
+            cid[cnt] = rid[g * 8 + i];
+            ++cnt;
           }
-          __syncwarp();
         }
+        __syncwarp();
       }
     };
 
@@ -633,20 +696,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const float *ba = bias_a + bs * BN + half * EPI_COLS;
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
       const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
-      const float4 *cmt = cmeta + bs * CHUNKS + half * (EPI_COLS / 32);
+      const int g0 = bs * GROUPS + half * (EPI_COLS / 8);   // this warp's first group
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
-      if (!p.epi_skip) {
-        uint32_t ra[32], rb[32];
-        TMEM_LD_32x32b_X32(tbase, ra);
-        TMEM_LD_WAIT(ra);
+      if (!p.epi_skip) {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
+        uint32_t ra[32];
 #pragma unroll 1
-        for (int c = 0; c < EPI_COLS / 32; c += 2) {
-          TMEM_LD_32x32b_X32(tbase + (c + 1) * 32, rb);
-          chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, cmt[c]);
-          TMEM_LD_WAIT(rb);
-          if (c + 2 < EPI_COLS / 32) TMEM_LD_32x32b_X32(tbase + (c + 2) * 32, ra);
-          chunk(rb, ba + (c + 1) * 32, bb + (c + 1) * 32, rid + (c + 1) * 32, cmt[c + 1]);
-          if (c + 2 < EPI_COLS / 32) TMEM_LD_WAIT(ra);
+        for (int c = 0; c < EPI_COLS / 32; ++c) {
+          TMEM_LD_32x32b_X32(tbase + c * 32, ra);
+          TMEM_LD_WAIT(ra);
+          chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, g_bmax + g0 + c * 4, g_amax + g0 + c * 4, g_amin + g0 + c * 4);
         }
       }
       tc_fence_before();
@@ -694,14 +752,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static bool make_map(CUtensorMap *m, const float *base, int64_t rows, int32_t d, int box_rows, int box_cols = tc::BK) {
+// 2-D map over a row-major [rows x d] matrix of fp32 or bf16, boxes of one
+// 128-byte K block x box_rows rows, 128-byte swizzle.
+static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows, bool bf16) {
   auto fn = encode_fn();
   if (!fn) return false;
+  const int esz = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void *>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -761,22 +823,33 @@ size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
   return carve_gemm(nullptr, plan, q, kprime).bytes;
 }
 
-template <bool AR, int MODE>
-static auto pick_kernel(bool rowscale) {
-  return rowscale ? tc_topk_kernel<AR, MODE, true> : tc_topk_kernel<AR, MODE, false>;
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
+template <int MODE, bool BF>
+static TcKernel pick_kernel(bool ar, bool rowscale) {
+  return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF> : tc_topk_kernel<true, MODE, false, BF>)
+            : (rowscale ? tc_topk_kernel<false, MODE, true, BF> : tc_topk_kernel<false, MODE, false, BF>);
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches) {
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
+  const bool bf = a.bf16 != 0;
+  cudaError_t e = cudaSuccess;
+  if (bf) {   // queries -> bf16 (the corpus shadow was converted at load)
+    e = launch_to_bf16(a.Q, a.Qb, a.q * a.d, s);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+  }
+  const void *qsrc = bf ? a.Qb : (const void *)a.Q;
+  const void *xsrc = bf ? a.Xb : (const void *)a.X;
   CUtensorMap mq, mx, mg;
-  if (!make_map(&mq, a.Q, a.q, a.d, tc::BM) || !make_map(&mx, a.X, a.n, a.d, tc::BN) ||
-      !make_map(&mg, xcap > 0 ? a.xsel : a.X, xcap > 0 ? xcap : a.n, a.d, tc::BN))
+  if (!make_map(&mq, qsrc, a.q, a.d, tc::BM, bf) || !make_map(&mx, xsrc, a.n, a.d, tc::BN, bf) ||
+      !make_map(&mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf))
     return cudaErrorInvalidValue;
   const GemmScratch gs = carve_gemm(scratch, plan, a.q, a.kprime);
   TcParams p;
   p.n_rows = a.n;
   p.d = a.d;
-  p.nk = (a.d + tc::BK - 1) / tc::BK;
+  p.nk = (a.d + (bf ? 2 * tc::BK : tc::BK) - 1) / (bf ? 2 * tc::BK : tc::BK);
   p.q = a.q;
   p.qtiles = plan.qtiles;
   p.P = plan.P;
@@ -798,20 +871,21 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.tile_step = 1;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaSuccess;
-    for (auto fn : {tc_topk_kernel<true, MODE_MAIN, false>, tc_topk_kernel<true, MODE_MAIN, true>,
-                    tc_topk_kernel<false, MODE_MAIN, false>, tc_topk_kernel<false, MODE_MAIN, true>,
-                    tc_topk_kernel<true, MODE_PROBE, false>, tc_topk_kernel<true, MODE_PROBE, true>,
-                    tc_topk_kernel<false, MODE_PROBE, false>, tc_topk_kernel<false, MODE_PROBE, true>})
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+    for (bool ar_ : {false, true})
+      for (bool rs : {false, true})
+        for (TcKernel fn : {pick_kernel<MODE_MAIN, false>(ar_, rs), pick_kernel<MODE_PROBE, false>(ar_, rs),
+                            pick_kernel<MODE_MAIN, true>(ar_, rs), pick_kernel<MODE_PROBE, true>(ar_, rs)})
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  cudaError_t e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
+  e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
   if (e != cudaSuccess) return e;
   if (xcap > 0 && p.allow_gather) {
     ProfScope ps("gemm.gather", s);
-    gather_copy_kernel<<<4 * 148, 256, 0, s>>>(a.X, a.d, a.ids, a.count, a.n, p.allow_gather, xcap, a.xsel);
+    gather_copy_kernel<<<4 * 148, 256, 0, s>>>(xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n, p.allow_gather, xcap,
+                                               a.xsel);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
@@ -827,8 +901,9 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   const bool ar = p.nk <= 4 && !no_ar;
   const bool rowscale = a.metric == VRS_COSINE;
   auto launch = [&](int mode, const TcParams &pr) -> cudaError_t {
-    auto kern = mode == MODE_PROBE ? (ar ? pick_kernel<true, MODE_PROBE>(rowscale) : pick_kernel<false, MODE_PROBE>(rowscale))
-                                   : (ar ? pick_kernel<true, MODE_MAIN>(rowscale) : pick_kernel<false, MODE_MAIN>(rowscale));
+    const TcKernel kern = mode == MODE_PROBE
+                              ? (bf ? pick_kernel<MODE_PROBE, true>(ar, rowscale) : pick_kernel<MODE_PROBE, false>(ar, rowscale))
+                              : (bf ? pick_kernel<MODE_MAIN, true>(ar, rowscale) : pick_kernel<MODE_MAIN, false>(ar, rowscale));
     if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
     kern<<<(unsigned)(pr.P * pr.qtiles), tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pr);
     cudaError_t el = cudaGetLastError();

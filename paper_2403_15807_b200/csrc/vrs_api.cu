@@ -31,6 +31,7 @@ struct vrs_index {
   float *nx2;
   float *inv_nx;
   int32_t has_zero_row;
+  void *xb;                // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
   int32_t device;
   int32_t num_sms;
 };
@@ -101,6 +102,7 @@ ProfScope::~ProfScope() {
 static thread_local char g_err[512];
 static thread_local int32_t g_last_path = 0;
 static thread_local int32_t g_last_launches = 0;
+static thread_local int32_t g_last_prec = 0;
 
 static vrs_status fail(vrs_status st, const char *fmt, ...) {
   va_list ap;
@@ -256,12 +258,20 @@ int32_t vrs_profile_read(int32_t i, const char **name, double *total_ms, int64_t
   return (int32_t)g_prof_totals.size();
 }
 int32_t vrs_last_path(void) { return g_last_path; }
+int32_t vrs_last_precision(void) { return g_last_prec; }
+int32_t vrs_index_precision(const vrs_index *ix) { return ix ? (ix->xb ? VRS_PREC_BF16 : VRS_PREC_TF32) : -1; }
 int32_t vrs_last_launches(void) { return g_last_launches; }
 int64_t vrs_index_rows(const vrs_index *ix) { return ix ? ix->n : -1; }
 int32_t vrs_index_dim(const vrs_index *ix) { return ix ? ix->d : -1; }
 
 vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
                     int64_t row_offset, const vrs_allocator *alloc, void *cuda_stream, vrs_index **out) {
+  return vrs_load_ex(vectors, n, d, attrs, n_attrs, row_offset, alloc, nullptr, cuda_stream, out);
+}
+
+vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
+                       int64_t row_offset, const vrs_allocator *alloc, const vrs_load_options *opts,
+                       void *cuda_stream, vrs_index **out) {
   g_err[0] = 0;
   if (!out) return fail(VRS_EINVAL, "out is NULL");
   *out = nullptr;
@@ -271,6 +281,13 @@ vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *
   if (n_attrs > 0 && !attrs) return fail(VRS_EINVAL, "attrs is NULL with n_attrs > 0");
   if (row_offset < 0) return fail(VRS_EINVAL, "row_offset < 0");
   if (alloc && (!alloc->alloc || !alloc->free)) return fail(VRS_EINVAL, "allocator without alloc/free");
+  const int prec = opts ? opts->precision : VRS_PREC_DEFAULT;
+  if (prec < VRS_PREC_DEFAULT || prec > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision %d", prec);
+  // bf16 rows must be 16-byte aligned for TMA: d % 8 == 0 and a 16-byte aligned base
+  const bool shadow_ok = d % 8 == 0 && ((uintptr_t)vectors & 15) == 0;
+  if (prec == VRS_PREC_BF16 && !shadow_ok)
+    return fail(VRS_EUNSUPPORTED, "bf16 shadow needs d %% 8 == 0 and 16-byte aligned vectors (d = %d)", d);
+  const bool want_shadow = prec == VRS_PREC_BF16 || (prec == VRS_PREC_DEFAULT && shadow_ok);
   int dev = 0, sms = 0;
   vrs_status st = check_device(&dev, &sms);
   if (st != VRS_OK) return st;
@@ -292,7 +309,7 @@ vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *
   ix->device = dev;
   ix->num_sms = sms;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 4});
+  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 4, want_shadow ? (size_t)n * d * 2 : 0});
   void *mem = nullptr;
   if (alloc) {
     mem = alloc->alloc(bytes, cuda_stream, alloc->ctx);
@@ -309,9 +326,11 @@ vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vrs_attr *
   ix->nx2 = cv.take<float>(n);
   ix->inv_nx = cv.take<float>(n);
   int32_t *zf = cv.take<int32_t>(1);
+  ix->xb = want_shadow ? cv.take<char>((size_t)n * d * 2) : nullptr;
   int32_t zero = 0;
   cudaError_t e = cudaMemsetAsync(zf, 0, 4, stream);
   if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
+  if (e == cudaSuccess && ix->xb) e = launch_to_bf16(vectors, ix->xb, n * (int64_t)d, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&zero, zf, 4, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {
@@ -354,6 +373,10 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const int rows_req = opts ? opts->rows : VRS_ROWS_AUTO;
   if (path_req < VRS_PATH_AUTO || path_req > VRS_PATH_GEMM) return fail(VRS_EINVAL, "bad path option");
   if (rows_req < VRS_ROWS_AUTO || rows_req > VRS_ROWS_MASKED) return fail(VRS_EINVAL, "bad rows option");
+  const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
+  if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision option");
+  if (prec_req == VRS_PREC_BF16 && !ix->xb) return fail(VRS_EUNSUPPORTED, "the index has no bf16 shadow");
+  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;
   PredDev pd;
   vrs_status st = make_pred(ix, pred, &pd);
   if (st != VRS_OK) return st;
@@ -376,8 +399,12 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // path choice (A16: per-tuple for small batches, tensor formulation for large ones)
   int path = path_req;
   GemmPlan gp{0, 0, 0};
-  if (path != VRS_PATH_SCAN) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
-  if (path == VRS_PATH_AUTO) path = (q >= 8 && gp.ok) ? VRS_PATH_GEMM : VRS_PATH_SCAN;
+  // the TMA paths need 16-byte aligned rows and bases
+  const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
+  if (path != VRS_PATH_SCAN && tma_ok) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
+  // (measured on C2: the tensor-core pass over the bf16 shadow is HBM-bound and beats
+  // the fp32 FFMA scan already at q = 1 -- it reads half the bytes)
+  if (path == VRS_PATH_AUTO) path = gp.ok ? VRS_PATH_GEMM : VRS_PATH_SCAN;
   if (path == VRS_PATH_GEMM && !gp.ok) return fail(VRS_EUNSUPPORTED, "tensor-core path does not support this shape");
 
 
@@ -403,7 +430,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
-                                   (size_t)xsel_cap * d * 4});
+                                   (size_t)xsel_cap * d * 4, use_bf16 && path == VRS_PATH_GEMM ? (size_t)q * d * 2 : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -415,6 +442,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
   float *xsel = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap * d) : nullptr;
+  void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>((size_t)q * d * 2) : nullptr;
 
   int launches = 0;
   FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, kprime, q, ix->X, d, queries,
@@ -436,7 +464,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     }
     const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
     GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
-               queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P};
+               queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
+               use_bf16 ? 1 : 0, ix->xb, qb};
     {
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
@@ -456,6 +485,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     CUDA_TRY(launch_finalize(f, stream, &launches));
   }
   g_last_path = path;
+  g_last_prec = path == VRS_PATH_GEMM ? (use_bf16 ? VRS_PREC_BF16 : VRS_PREC_TF32) : VRS_PREC_DEFAULT;
   g_last_launches = launches;
   return VRS_OK;
 }

@@ -65,7 +65,7 @@ struct GemmArgs {
   const int64_t *count;
   const uint32_t *bitmap;   // selection bitmap (masked mode) or nullptr
   int32_t masked;           // 0 auto (device-side selectivity switch), 1 force masked, 2 force gathered
-  float *xsel;              // materialised-selection buffer [xsel_cap x d] (gathered mode)
+  void *xsel;               // materialised-selection buffer [xsel_cap x d] fp32 / bf16 (gathered mode)
   int64_t xsel_cap;
   const float *Q;
   int64_t q;
@@ -76,8 +76,12 @@ struct GemmArgs {
   float *part_key;          // [P][q][kprime]
   int32_t *part_id;
   int32_t P;
+  int32_t bf16;             // select on the bf16 shadow (kind::f16) instead of fp32 (kind::tf32)
+  const void *Xb;           // bf16 shadow corpus [n x d] (bf16 only)
+  void *Qb;                 // scratch [q x d] bf16 queries (bf16 only)
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
+cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
 // the tensor-core pass's candidate lists, as finalize reads them
 struct GemmLists {

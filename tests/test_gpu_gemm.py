@@ -19,12 +19,15 @@ def vrs():
     return m
 
 
-def _run(vrs, X, attrs, pred, Q, k, metric, off=0, rows=None):
-    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off)
+def _run(vrs, X, attrs, pred, Q, k, metric, off=0, rows=None, precision=None):
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off,
+                   precision=precision)
     ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=vrs.PATH_GEMM,
                            rows=rows)
     torch.cuda.synchronize()
     assert vrs.last_path() == vrs.PATH_GEMM
+    if precision is not None:
+        assert vrs.last_precision() == precision
     return ids.cpu().numpy(), dists.cpu().numpy()
 
 
@@ -44,13 +47,16 @@ GEMM_CASES = [
 
 @pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: f"n{c[0]}-d{c[1]}-q{c[2]}-k{c[3]}-m{c[4]}")
 @pytest.mark.parametrize("rows", [0, 1, 2], ids=["auto", "gather", "masked"])
-def test_gemm_parity(vrs, case, rows):
+@pytest.mark.parametrize("prec", [1, 2], ids=["tf32", "bf16"])
+def test_gemm_parity(vrs, case, rows, prec):
     n, d, q, k, metric, pred = case
+    if prec == 2 and d % 8:
+        pytest.skip("bf16 shadow needs d % 8 == 0")
     rng = np.random.default_rng(n * 7 + d)
     X = rng.standard_normal((n, d)).astype(np.float32)
     attrs = [rng.integers(0, 1000, n).astype(np.int32)]
     Q = rng.standard_normal((q, d)).astype(np.float32)
-    gi, gd = _run(vrs, X, attrs, pred, Q, k, metric, rows=rows)
+    gi, gd = _run(vrs, X, attrs, pred, Q, k, metric, rows=rows, precision=prec)
     check_topk(gi, gd, X, attrs, pred, Q, k, metric)
 
 

@@ -19,6 +19,7 @@ ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--rows", type=int, default=0)
+ap.add_argument("--prec", type=int, default=0, help="0 default (bf16 shadow), 1 tf32, 2 bf16")
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.workload]
 n = a.n or cfg.n
@@ -27,12 +28,12 @@ Q = datagen.queries(cfg, a.q, "cuda")
 ix = vrs.Index(X, attrs)
 pred = datagen.predicate(cfg, a.sel)
 for _ in range(a.reps):
-    ids, d = ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
+    ids, d = ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
 for _ in range(3):
-    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None)
 e.record()
 torch.cuda.synchronize()
 gms = float("nan")
@@ -41,12 +42,12 @@ if a.graph:
     st = torch.cuda.Stream()
     st.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(st):
-        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, out=out)
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None, out=out)
     torch.cuda.current_stream().wait_stream(st)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, out=out)
+        ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None, out=out)
     g.replay()
     torch.cuda.synchronize()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -59,9 +60,9 @@ if a.graph:
 vrs.profile(True)
 vrs.profile_reset()
 for _ in range(3):
-    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None)
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None)
 torch.cuda.synchronize()
 prof = vrs.profile_read()
 vrs.profile(False)
 ks = " ".join(f"{k}={v[0]/v[1]*1e3:.0f}us" for k, v in prof.items())
-print(f"cell {a.workload} sel={a.sel} q={a.q}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, path={vrs.last_path()} | {ks}")
+print(f"cell {a.workload} sel={a.sel} q={a.q} prec={vrs.last_precision()}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, path={vrs.last_path()} | {ks}")
