@@ -117,9 +117,10 @@ def cells_of(cfg):
 
 def workload_desc(cfg, world):
     return {"workload": f"{cfg.name} (BASELINE.json configs[{list(datagen.CONFIGS).index(cfg.name)}])",
-            "n": cfg.n, "d": cfg.d, "metric": ["l2", "ip", "cos"][cfg.metric], "k": cfg.k,
+            "n": datagen.rows_of(cfg, world, 0)[2], "d": cfg.d, "metric": ["l2", "ip", "cos"][cfg.metric],
+            "k": cfg.k, "rows_per_gpu": datagen.rows_of(cfg, world, 0)[1],
             "selectivities": list(cfg.sels), "queries_per_cell": list(cfg.qs), "cells": len(cells_of(cfg)),
-            "data": "synthetic, seeded (datagen)", "l2_flush": "inputs > L2 (corpus %.0f MB)" % (cfg.n * cfg.d * 4 / 1e6),
+            "data": "synthetic, seeded (datagen)", "l2_flush": "inputs > L2 (corpus %.0f MB per GPU)" % (datagen.rows_of(cfg, world, 0)[1] * cfg.d * 4 / 1e6),
             "parallelism": f"rows sharded over {world} GPU(s), NCCL all-gather + merge" if world > 1 else "1 GPU"}
 
 
@@ -150,7 +151,8 @@ def run_reference(args, cfg, world, rank):
     import oracle
     oracle.build()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))) if torch.cuda.is_available() else "cpu"
-    X, attrs = datagen.corpus(cfg, 0, cfg.n, dev)
+    r0, r1, _ = datagen.rows_of(cfg, 1, 0)
+    X, attrs = datagen.corpus(cfg, r0, r1, dev)
     Q = datagen.queries(cfg, 64, dev)
     X_h, attrs_h, Q_h = X.cpu().numpy(), [a.cpu().numpy() for a in attrs], Q.cpu().numpy()
     del X
@@ -166,7 +168,8 @@ def run_reference(args, cfg, world, rank):
     value = statistics.median(qps)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if cfg.shard_rows else "strong", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic", "config": workload_desc(cfg, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -195,8 +198,7 @@ def main():
     vrs.library()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    from paper_2403_15807_b200.dist import shard_range
-    r0, r1 = shard_range(cfg.n, world, rank)
+    r0, r1, n_total = datagen.rows_of(cfg, world, rank)
     X, attrs = datagen.corpus(cfg, r0, r1, dev)
     qmax = max(cfg.qs)
     Qall = datagen.queries(cfg, qmax, dev)
@@ -252,14 +254,17 @@ def main():
     barrier()
     torch.cuda.synchronize()
     launches[0] = 0
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
+        step_ev[i].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    step_ms = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
     gpu_launches = launches[0]
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -279,6 +284,7 @@ def main():
     nprof = min(args.steps, 5)
     pk = peaks()
     tf32_peak_sus = pk["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    tc_peak_sus = pk["bf16_tflops_sustained"] if ix.precision == vrs.PREC_BF16 else tf32_peak_sus
     tf32_peak_burst = pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16
     d = cfg.d
     # algorithmic work per step, by kernel
@@ -337,7 +343,7 @@ def main():
         by = n_loc * sum(1 if cfg.attrs[i][0] == "u8" else 4 for i in range(len(cfg.attrs))) + ns * 4.0 * d + q * 4.0 * d + q * k * 12
         cell_out.append({"sel": s, "q": q, "n_sel": ns, "ms": t * 1e3, "qps": q / t,
                          "path": "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan",
-                         "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac": fl / t / 1e12 / tf32_peak_sus})
+                         "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac": fl / t / 1e12 / tc_peak_sus})
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -397,14 +403,16 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from parity import check_topk
             checked = 0
-            for s, q in [(cfg.sels[1], cfg.qs[1]), (cfg.sels[-1], cfg.qs[-1])]:
+            pcells = sorted({(cfg.sels[min(1, len(cfg.sels) - 1)], cfg.qs[min(1, len(cfg.qs) - 1)]),
+                             (cfg.sels[-1], cfg.qs[-1])})
+            for s, q in pcells:
                 ids, dists = run_cell((s, q))
                 torch.cuda.synchronize()
                 nq = 3
                 check_topk(ids[:nq].cpu().numpy(), dists[:nq].cpu().numpy(), X_h, attrs_h, preds[s], Q_h[:nq], k,
                            metric)
                 checked += nq
-            parity = {"checked_queries": checked, "cells": [[cfg.sels[1], cfg.qs[1]], [cfg.sels[-1], cfg.qs[-1]]],
+            parity = {"checked_queries": checked, "cells": [list(c) for c in pcells],
                       "rule": "SURVEY 8(c) c.5 (1e-3 rel dists, id sets within the k-th band)", "ok": True}
         if not args.no_cpu_baseline:
             threads = len(os.sched_getaffinity(0))
@@ -415,12 +423,12 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
+                "scaling": "weak" if cfg.shard_rows else "strong", "vs_baseline": None,
                 "dtype": "bf16" if ix.precision == vrs.PREC_BF16 else "tf32",
                 "dtype_note": "tensor-core selection operands (fp32 accumulate); returned dists re-scored in fp64 from fp32",
                 "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
-                "parity": parity, "cells": cell_out,
+                "parity": parity, "cells": cell_out, "step_ms": [round(x, 4) for x in step_ms],
                 "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
         print(json.dumps(line), flush=True)
     if world > 1:

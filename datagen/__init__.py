@@ -43,6 +43,7 @@ class Config:
     kind: str            # "gauss" | "gauss_norm" | "mixture"
     attrs: tuple         # per attribute: ("i32", modulus) or ("u8", modulus)
     gpus: tuple = (1,)
+    shard_rows: int = 0  # > 0: weak scaling, each GPU holds this many rows (C4: 50M / 8; C5: 20M / 8)
 
 
 CONFIGS = {
@@ -53,9 +54,9 @@ CONFIGS = {
                  (0.0001, 0.001, 0.01, 0.015625, 0.10, 1.0), "gauss",
                  (("i32", 1 << 20), ("u8", 64)), (1, 2)),
     "c4": Config("c4", 4, 50_000_000, 1536, IP, 100, (1, 256, 8192), (0.001, 0.05, 0.50), "gauss",
-                 (("i32", 1_000_000),), (1, 2, 4, 8)),
+                 (("i32", 1_000_000),), (1, 2, 4, 8), 6_250_000),
     "c5": Config("c5", 5, 20_000_000, 256, COS, 50, (2048,), (0.001, 0.01, 0.10, 0.30), "mixture",
-                 (("i32", 1031),), (8,)),
+                 (("i32", 1031),), (8,), 2_500_000),
 }
 
 C5_CENTROIDS = 1024
@@ -97,6 +98,15 @@ def _randint(dev, m, dtype):
 def centroids(cfg: Config, device="cpu") -> torch.Tensor:
     g = _gen(device, cfg.seed, S_CENTROIDS, 0)
     return torch.randn(C5_CENTROIDS, cfg.d, generator=g, device=device, dtype=torch.float32)
+
+
+def rows_of(cfg: Config, world: int, rank: int):
+    """(r0, r1, n_total) of `rank`'s shard: weak scaling (shard_rows per GPU, the
+    first `world` shards of the global corpus) when the config has shard_rows,
+    else the contiguous 1/world of cfg.n (strong scaling)."""
+    if cfg.shard_rows:
+        return rank * cfg.shard_rows, (rank + 1) * cfg.shard_rows, cfg.shard_rows * world
+    return cfg.n * rank // world, cfg.n * (rank + 1) // world, cfg.n
 
 
 def corpus(cfg: Config, r0: int = 0, r1: int | None = None, device="cpu", n: int | None = None,

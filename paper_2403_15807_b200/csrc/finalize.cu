@@ -59,12 +59,15 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += kFinThreads) hist[b] = 0;
     __syncthreads();
-    for (int64_t c = tid; c < C; c += kFinThreads) {
+    for (int64_t c0 = 0; c0 < C; c0 += kFinThreads) {
+      const int64_t c = c0 + tid;
       float k; IdT i;
-      if (get(c, k, i)) {
+      uint32_t bin = 256u;
+      if (c < C && get(c, k, i)) {
         const uint32_t ok = ordered_u32(k);
-        if ((ok & mask) == prefix) atomicAdd(&hist[(ok >> shift) & 255u], 1u);
+        if ((ok & mask) == prefix) bin = (ok >> shift) & 255u;
       }
+      hist_add_warp(hist, bin);
     }
     __syncthreads();
     if (warp == 0) {
@@ -188,9 +191,11 @@ __device__ bool warp_kth_largest(Get get, int n, int K, uint32_t *hist, uint32_t
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
     __syncwarp();
 #pragma unroll 4
-    for (int i = lane; i < n; i += 32) {
-      uint32_t u;
-      if (get(i, u) && (u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t u, bin = 256u;
+      if (i < n && get(i, u) && (u & mask) == prefix) bin = (u >> shift) & 255u;
+      hist_add_warp(hist, bin);
     }
     __syncwarp();
     // lane l owns bins [255-8l-7, 255-8l] (descending); suffix sums from the top
@@ -536,9 +541,10 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += kThrThreads) hist[b] = 0;
     __syncthreads();
-    for (int i = tid; i < a.nvals; i += kThrThreads) {
-      const uint32_t u = s_val[i];
-      if (u != 0u && (u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    for (int i0 = 0; i0 < a.nvals; i0 += kThrThreads) {
+      const int i = i0 + tid;
+      const uint32_t u = i < a.nvals ? s_val[i] : 0u;
+      hist_add_warp(hist, (u != 0u && (u & mask) == prefix) ? (u >> shift) & 255u : 256u);
     }
     __syncthreads();
     if (warp == 0) {

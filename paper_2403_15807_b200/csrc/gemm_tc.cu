@@ -224,9 +224,10 @@ __device__ __noinline__ float compact_lane(float *key, int32_t *id, int cnt, int
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
     __syncwarp();
-    for (int i = lane; i < cnt; i += 32) {
-      const uint32_t ok = ordered_u32(key[i]);
-      if ((ok & mask) == prefix) atomicAdd(&hist[(ok >> shift) & 255u], 1u);
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      const uint32_t ok = i < cnt ? ordered_u32(key[i]) : 0u;
+      hist_add_warp(hist, (i < cnt && (ok & mask) == prefix) ? (ok >> shift) & 255u : 256u);
     }
     __syncwarp();
     uint32_t v[8], s = 0;
@@ -282,11 +283,10 @@ __device__ __noinline__ float compact_lane(float *key, int32_t *id, int cnt, int
   return __uint_as_float(u);
 }
 
-// Gathered rows iff a selection exists, it is at most half the rows (or forced)
-// and it fits the materialisation buffer.
+// Gathered rows iff a selection exists and fits the materialisation buffer,
+// whose capacity the host sized by the selectivity break-even (vrs_api.cu).
 __device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t n, int64_t cap) {
-  if (ids == nullptr || allow == 0 || n_sel > cap) return false;
-  return allow == 2 || n_sel * 2 <= n;
+  return ids != nullptr && allow != 0 && n_sel <= cap;
 }
 
 // Late materialization ("(re-)materialized into dense
@@ -299,13 +299,15 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
                                                           int64_t cap, void *__restrict__ xsel) {
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, n, cap)) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  // one 16-byte vector per thread, consecutive threads along a row (coalesced);
+  // the row's id is a broadcast load shared by the row's threads
   const int v16 = row_bytes >> 4;
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_sel; r += warps) {
+  const int64_t total = n_sel * v16, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t r = i / v16;
+    const int v = (int)(i - r * v16);
     const int4 *src = reinterpret_cast<const int4 *>(static_cast<const char *>(X) + (int64_t)__ldg(ids + r) * row_bytes);
-    int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(xsel) + r * row_bytes);
-    for (int i = lane; i < v16; i += 32) dst[i] = __ldg(src + i);
+    reinterpret_cast<int4 *>(static_cast<char *>(xsel) + r * row_bytes)[v] = __ldg(src + v);
   }
 }
 
@@ -880,11 +882,9 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
-  if (e != cudaSuccess) return e;
   if (xcap > 0 && p.allow_gather) {
     ProfScope ps("gemm.gather", s);
-    gather_copy_kernel<<<4 * 148, 256, 0, s>>>(xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n, p.allow_gather, xcap,
+    gather_copy_kernel<<<8 * 148, 256, 0, s>>>(xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n, p.allow_gather, xcap,
                                                a.xsel);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -897,6 +897,10 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
   static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
   static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
+  if (no_probe) {   // (otherwise threshold_kernel writes every query's gtau)
+    e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   p.epi_skip = epi_skip ? 1 : 0;
   const bool ar = p.nk <= 4 && !no_ar;
   const bool rowscale = a.metric == VRS_COSINE;

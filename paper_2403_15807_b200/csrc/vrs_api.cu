@@ -156,7 +156,16 @@ struct Scratch {
 };
 
 static vrs_status scratch_alloc(Scratch &s, size_t bytes) {
+  // size classes of 1/8 of a power of two: consecutive searches of different
+  // shapes then reuse the stream-ordered pool's blocks instead of mapping new
+  // memory (large gather buffers made that churn cost more than the search)
   bytes = std::max<size_t>(bytes, 256);
+  {
+    size_t p2 = 1;
+    while (p2 < bytes) p2 <<= 1;
+    const size_t step = std::max<size_t>(p2 / 8, 256);
+    bytes = (bytes + step - 1) / step * step;
+  }
   if (s.alloc) {
     s.ptr = s.alloc->alloc(bytes, s.stream, s.alloc->ctx);
     if (!s.ptr) return fail(VRS_ENOMEM, "allocator returned NULL for %zu bytes", bytes);
@@ -421,16 +430,27 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const size_t nwords = (size_t)((n + 31) / 32);
   const size_t part_entries = path == VRS_PATH_SCAN ? (size_t)P * q * kprime : 0;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
-  // gathered tensor-core mode materialises the selection: up to half the rows,
-  // at most ~4 GiB (larger selections stream masked full tiles instead)
+  // Selectivity-driven row delivery of the tensor-core pass (decided on the
+  // device from the selection count): the selection is materialised densely
+  // ("gathered", late materialization) iff N_sel <= xsel_cap, else full row
+  // tiles stream with unqualified rows masked.  Gathering costs a copy of the
+  // selected rows (2 x row bytes each); masking costs MMA / TMEM work and HBM
+  // reads on the unselected rows.  Break-even (C2/C3/C4 measurements, DESIGN.md
+  // Sec. 6): selectivity 1/3 while the pass is HBM-bound (q < 256), ~0.45 at
+  // q = 256, 0.9 once it is tensor / TMEM-bound (q >= 1024).  The buffer holds
+  // at most 16 GiB of rows.
+  const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
+  const int64_t gather_rows = rows_req == VRS_ROWS_GATHER ? n
+                              : q >= 1024                 ? n * 9 / 10
+                              : q >= 256                  ? n * 9 / 20
+                                                          : n / 3;
   const int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
-                               ? std::min<int64_t>(rows_req == VRS_ROWS_GATHER ? n : (n + 1) / 2,
-                                                   std::max<int64_t>(1, (int64_t(4) << 30) / ((int64_t)d * 4)))
+                               ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
                                : 0;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
-                                   (size_t)xsel_cap * d * 4, use_bf16 && path == VRS_PATH_GEMM ? (size_t)q * d * 2 : 0});
+                                   (size_t)(xsel_cap * row_bytes), use_bf16 && path == VRS_PATH_GEMM ? (size_t)q * d * 2 : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -441,7 +461,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *part_key = cv.take<float>(part_entries);
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
-  float *xsel = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap * d) : nullptr;
+  void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
   void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>((size_t)q * d * 2) : nullptr;
 
   int launches = 0;

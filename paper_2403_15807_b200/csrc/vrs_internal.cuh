@@ -46,6 +46,15 @@ __device__ __forceinline__ uint32_t ordered_u32(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Warp-aggregated histogram increment for radix selection: the lanes holding
+// the same bin add once (keys in one radix pass share their leading bits, so
+// plain shared atomics would serialise on one or two bins).  All 32 lanes of
+// the warp must call it; bin >= 256 means "no value".
+__device__ __forceinline__ void hist_add_warp(uint32_t *hist, uint32_t bin) {
+  const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+  if (bin < 256u && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

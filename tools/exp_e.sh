@@ -1,0 +1,10 @@
+#!/bin/bash
+# benches of the non-default workloads after the gather-rule change
+cd $GRAFT_REPO_ROOT
+O=gpurun_out; P=${PFX:-e}
+timeout 900 python -m pytest tests -m gpu -x -q > $O/${P}_pytest.log 2>&1; echo "PYTEST_EXIT $?" >> $O/${P}_pytest.log
+for w in c1 c5 c4; do
+  timeout 900 python bench.py --workload $w --steps 3 --warmup 3 > $O/${P}_bench_$w.json 2> $O/${P}_bench_$w.err
+done
+timeout 400 python bench.py > $O/${P}_bench_c2.json 2> $O/${P}_bench_c2.err
+echo done
