@@ -460,6 +460,8 @@ __global__ void __launch_bounds__(kFinGroup * 32) finalize_warp_kernel(FinalizeA
   __shared__ int64_t s_sid[kFinGroup][kFinMaxSel];
   const int w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
+  pdl_wait();
+  pdl_trigger();
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
   const int m = fin_stream(a, j, 0, 1, s_buf[w]);
   const double qq = fin_qq(a, j);
@@ -476,6 +478,8 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   __shared__ int s_n[kFinW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
   // each warp: its share of the lists -> at most k' survivors
   const int nw = fin_stream(a, j, w, kFinW, s_buf[w]);
   if (lane == 0) s_n[w] = nw;
@@ -532,6 +536,8 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t j = blockIdx.x;
   const float *v = a.vals + j * a.nvals;
+  pdl_wait();
+  pdl_trigger();
   for (int i = tid; i < a.nvals; i += kThrThreads) {
     const float f = __ldg(v + i);
     s_val[i] = f > -INFINITY ? ordered_u32(f) : 0u;
@@ -588,15 +594,16 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  threshold_kernel<<<(unsigned)a.q, kThrThreads, smem, s>>>(a);
+  return launch_k(threshold_kernel, dim3((unsigned)a.q), dim3(kThrThreads), smem, s, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
-  if (a.q < 4 * kSmCountB200) finalize_cta_kernel<<<(unsigned)a.q, kFinW * 32, 0, s>>>(a);
-  else finalize_warp_kernel<<<(unsigned)((a.q + kFinGroup - 1) / kFinGroup), kFinGroup * 32, 0, s>>>(a);
+  if (a.q < 4 * kSmCountB200) return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), 0, s, a);
+  return launch_k(finalize_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32), 0,
+                  s, a);
   return cudaGetLastError();
 }
 
@@ -608,6 +615,8 @@ __global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
   __shared__ double s_k2[kFinMaxSel];
   __shared__ int64_t s_i2[kFinMaxSel];
   const int64_t j = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5;
   auto get = [&](int64_t c, float &key, int64_t &id) -> bool {
     const int64_t p = c / a.k, r = c - p * a.k;
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
 
 cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
-  merge_kernel<<<(unsigned)a.q, kFinThreads, 0, s>>>(a);
+  return launch_k(merge_kernel, dim3((unsigned)a.q), dim3(kFinThreads), 0, s, a);
   return cudaGetLastError();
 }
 

@@ -297,6 +297,8 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
                                                           const int32_t *__restrict__ ids,
                                                           const int64_t *__restrict__ count, int64_t n, int allow,
                                                           int64_t cap, void *__restrict__ xsel) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, n, cap)) return;
   // one 16-byte vector per thread, consecutive threads along a row (coalesced);
@@ -313,6 +315,8 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
 
 // fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per search.
 __global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (count >> 2); i += stride) {
     const float4 v = __ldg(reinterpret_cast<const float4 *>(in) + i);
@@ -329,8 +333,8 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *
 cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>((count / 4 + 255) / 256 + 1, 148 * 16);
-  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, static_cast<__nv_bfloat16 *>(out), count);
-  return cudaGetLastError();
+  return launch_k(f32_to_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, in,
+                  static_cast<__nv_bfloat16 *>(out), count);
 }
 
 constexpr int MODE_MAIN = 0;
@@ -376,25 +380,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qtile = blockIdx.x % p.qtiles;
   const int split = blockIdx.x / p.qtiles;
-  // Selectivity-driven row delivery (decided on the device, no host sync):
-  //  gather: the selection was materialised densely (gather_copy_kernel, late
-  //          materialization) and streams by TMA from X_sel; ids map rows back
-  //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
-  const int64_t n_sel = p.ids ? *p.count : p.n_rows;
-  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.n_rows, p.xsel_cap);
-  const int64_t n_space = gather ? n_sel : p.n_rows;
-  const int64_t row_tiles = (n_space + BN - 1) / BN;
-  // splits actually used: >= 4 row tiles per item when the (device-side) row
-  // space allows; CTAs of unused splits publish empty lists
-  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
-  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
-  const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
-  const int64_t span = t_end - t_begin;
-  // probe: every tile_step-th tile of the item (the first tile of a shorter item)
-  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(p.tile_step, std::max<int64_t>(1, span)) : 1;
-  const int ntiles = (int)((span + step - 1) / step);
-  auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&afull_bar, 1);
@@ -416,6 +401,28 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  // (the prologue above overlaps the predecessor kernel's tail; global memory from here on)
+  pdl_wait();
+  pdl_trigger();
+  // Selectivity-driven row delivery (decided on the device, no host sync):
+  //  gather: the selection was materialised densely (gather_copy_kernel, late
+  //          materialization) and streams by TMA from X_sel; ids map rows back
+  //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
+  const int64_t n_sel = p.ids ? *p.count : p.n_rows;
+  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.n_rows, p.xsel_cap);
+  const int64_t n_space = gather ? n_sel : p.n_rows;
+  const int64_t row_tiles = (n_space + BN - 1) / BN;
+  // splits actually used: >= 4 row tiles per item when the (device-side) row
+  // space allows; CTAs of unused splits publish empty lists
+  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
+  const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
+  const int64_t span = t_end - t_begin;
+  // probe: every tile_step-th tile of the item (the first tile of a shorter item)
+  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(p.tile_step, std::max<int64_t>(1, span)) : 1;
+  const int ntiles = (int)((span + step - 1) / step);
+  auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
+
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -884,9 +891,8 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   }
   if (xcap > 0 && p.allow_gather) {
     ProfScope ps("gemm.gather", s);
-    gather_copy_kernel<<<8 * 148, 256, 0, s>>>(xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n, p.allow_gather, xcap,
-                                               a.xsel);
-    e = cudaGetLastError();
+    e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
+                 (int)p.allow_gather, xcap, a.xsel);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
@@ -909,8 +915,8 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
                               ? (bf ? pick_kernel<MODE_PROBE, true>(ar, rowscale) : pick_kernel<MODE_PROBE, false>(ar, rowscale))
                               : (bf ? pick_kernel<MODE_MAIN, true>(ar, rowscale) : pick_kernel<MODE_MAIN, false>(ar, rowscale));
     if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
-    kern<<<(unsigned)(pr.P * pr.qtiles), tc::THREADS, tc::SMEM_BYTES, s>>>(mq, mx, mg, pr);
-    cudaError_t el = cudaGetLastError();
+    cudaError_t el = launch_k(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, mq, mx,
+                              mg, pr);
     if (want_stats) {
       unsigned long long h[4];
       cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);

@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
 
   const int64_t q0 = (int64_t)blockIdx.y * QG;
   const int nq = (int)(a.q - q0 < QG ? a.q - q0 : QG);
+  pdl_wait();
+  pdl_trigger();
 
   for (int i = threadIdx.x; i < QG * dpad; i += kScThreads) {
     const int j = i / dpad, t = i - j * dpad;
@@ -239,8 +241,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a, int gy, cudaStream_t stream)
   auto fn = scan_topk_kernel<QG, KPE, VEC4>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<dim3(a.P, gy), kScThreads, smem, stream>>>(a);
-  return cudaGetLastError();
+  return launch_k(fn, dim3(a.P, gy), dim3(kScThreads), smem, stream, a);
 }
 
 template <int QG, int KPE>

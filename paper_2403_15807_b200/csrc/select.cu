@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
                                                                    uint32_t *__restrict__ bitmap,
                                                                    uint32_t *__restrict__ chunk_count) {
   __shared__ uint32_t s_cnt[kSelWarps];
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kSelRows + (int64_t)warp * kSelWordsPerWarp * 32;
   // lane l owns row base + 32w + l for w = 0..31: per clause, all 32 column loads
@@ -90,6 +92,8 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, 
                                                                      int32_t *__restrict__ ids,
                                                                      int64_t *__restrict__ count) {
   __shared__ uint64_t s_red[kSelWarps];
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_wsum[kSelWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // prefix over the chunks before this block
@@ -135,11 +139,14 @@ cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int3
                           void *scratch, cudaStream_t stream, int *launches) {
   const uint32_t nchunks = (uint32_t)((n + kSelRows - 1) / kSelRows);
   uint32_t *chunk_count = static_cast<uint32_t *>(scratch);
-  select_count_kernel<<<nchunks, kSelThreads, 0, stream>>>(pred, n, bitmap, chunk_count);
+  cudaError_t e0 = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap, chunk_count);
+  if (e0 != cudaSuccess) return e0;
   if (launches) *launches += 1;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  select_scatter_kernel<<<nchunks, kSelThreads, 0, stream>>>(n, bitmap, chunk_count, ids, count);
+  e = launch_k(select_scatter_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, n, (const uint32_t *)bitmap,
+               (const uint32_t *)chunk_count, ids, count);
+  if (e != cudaSuccess) return e;
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

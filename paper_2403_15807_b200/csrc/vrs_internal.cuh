@@ -8,9 +8,39 @@
 
 #include "vrs.h"
 
+#include <stdlib.h>
+
+#include <utility>
+
 namespace vrs {
 
 constexpr int kSmCountB200 = 148;
+
+// ---- programmatic dependent launch ---------------------------------------------
+// Every libvrs kernel is launched with programmatic stream serialization: it may
+// be scheduled while its stream predecessor drains, runs its prologue (barrier
+// init, TMEM allocation, tensor-map prefetch) and calls pdl_wait() -- which
+// returns once every predecessor grid has completed and its writes are visible
+// -- before it touches global memory.  pdl_trigger() lets the successor launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args &&...args) {
+  static const bool pdl = getenv("VRS_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // One clause of theta_R in device form: the [lo, hi] interval clamped to the
 // column type's range (empty => the whole predicate selects nothing).
