@@ -303,9 +303,10 @@ struct FinBufs {
 __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufs &B) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
+  const int lists = a.split.bn ? (int)min((int64_t)a.lists, 2 * splits_used(a.split)) : a.lists;
   uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
   if (a.sorted && K <= a.kread) {
-    for (int l = lane; l < a.lists; l += 32) {
+    for (int l = lane; l < lists; l += 32) {
       const int64_t o = ((int64_t)l * a.q + j) * a.stride + (K - 1);
       if (__ldg(a.id + o) >= 0) thr = max(thr, ordered_u32(__ldg(a.key + o)));
     }
@@ -313,11 +314,11 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
     for (int o = 16; o > 0; o >>= 1) thr = max(thr, __shfl_xor_sync(0xffffffffu, thr, o));
   }
   int n = 0;
-  for (int l0 = first_group * 32; l0 < a.lists; l0 += group_step * 32) {
+  for (int l0 = first_group * 32; l0 < lists; l0 += group_step * 32) {
     const int l = l0 + lane;
     int c = 0;
-    if (l < a.lists) c = a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread;
-    const int64_t base = ((int64_t)(l < a.lists ? l : 0) * a.q + j) * a.stride;
+    if (l < lists) c = a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread;
+    const int64_t base = ((int64_t)(l < lists ? l : 0) * a.q + j) * a.stride;
     for (int r0 = 0; __any_sync(0xffffffffu, r0 < c); r0 += 8) {
       float kv[8];
       int32_t iv[8];
@@ -538,7 +539,8 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   const float *v = a.vals + j * a.nvals;
   pdl_wait();
   pdl_trigger();
-  for (int i = tid; i < a.nvals; i += kThrThreads) {
+  const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);   // lists of used splits only
+  for (int i = tid; i < nvals; i += kThrThreads) {
     const float f = __ldg(v + i);
     s_val[i] = f > -INFINITY ? ordered_u32(f) : 0u;
   }
@@ -547,9 +549,9 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += kThrThreads) hist[b] = 0;
     __syncthreads();
-    for (int i0 = 0; i0 < a.nvals; i0 += kThrThreads) {
+    for (int i0 = 0; i0 < nvals; i0 += kThrThreads) {
       const int i = i0 + tid;
-      const uint32_t u = i < a.nvals ? s_val[i] : 0u;
+      const uint32_t u = i < nvals ? s_val[i] : 0u;
       hist_add_warp(hist, (u != 0u && (u & mask) == prefix) ? (u >> shift) & 255u : 256u);
     }
     __syncthreads();

@@ -283,11 +283,8 @@ __device__ __noinline__ float compact_lane(float *key, int32_t *id, int cnt, int
   return __uint_as_float(u);
 }
 
-// Gathered rows iff a selection exists and fits the materialisation buffer,
-// whose capacity the host sized by the selectivity break-even (vrs_api.cu).
-__device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t n, int64_t cap) {
-  return ids != nullptr && allow != 0 && n_sel <= cap;
-}
+// (gather_mode: gathered rows iff a selection exists and fits the materialisation
+// buffer, whose capacity the host sized by the selectivity break-even, vrs_api.cu)
 
 // Late materialization ("(re-)materialized into dense
 // vectors"): X_sel[r] = X[ids[r]] (rows of row_bytes, a multiple of 16: the fp32
@@ -300,7 +297,7 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
   pdl_wait();
   pdl_trigger();
   const int64_t n_sel = *count;
-  if (!gather_mode(ids, allow, n_sel, n, cap)) return;
+  if (!gather_mode(ids, allow, n_sel, cap)) return;
   // one 16-byte vector per thread, consecutive threads along a row (coalesced);
   // the row's id is a broadcast load shared by the row's threads
   const int v16 = row_bytes >> 4;
@@ -313,11 +310,16 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
   }
 }
 
-// fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per search.
-__global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count) {
+// fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per
+// search; elements [count, total) are zero (query tiles padded to whole 128-row
+// tiles, so the TMA loads of the query operand never fall out of bounds).
+__global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count,
+                                   int64_t total) {
   pdl_wait();
   pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = count + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    out[i] = __float2bfloat16_rn(0.f);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (count >> 2); i += stride) {
     const float4 v = __ldg(reinterpret_cast<const float4 *>(in) + i);
     __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
@@ -330,11 +332,11 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *
     out[i] = __float2bfloat16_rn(in[i]);
 }
 
-cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, cudaStream_t s) {
-  if (count <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>((count / 4 + 255) / 256 + 1, 148 * 16);
+cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 16);
   return launch_k(f32_to_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, in,
-                  static_cast<__nv_bfloat16 *>(out), count);
+                  static_cast<__nv_bfloat16 *>(out), count, total);
 }
 
 constexpr int MODE_MAIN = 0;
@@ -409,11 +411,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   //          materialization) and streams by TMA from X_sel; ids map rows back
   //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
   const int64_t n_sel = p.ids ? *p.count : p.n_rows;
-  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.n_rows, p.xsel_cap);
+  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.xsel_cap);
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;
-  // splits actually used: >= 4 row tiles per item when the (device-side) row
-  // space allows; CTAs of unused splits publish empty lists
+  // splits actually used (splits_used): >= 4 row tiles per item when the
+  // (device-side) row space allows; CTAs of unused splits publish empty lists
   const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
   const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
   const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
@@ -844,14 +846,14 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   const bool bf = a.bf16 != 0;
   cudaError_t e = cudaSuccess;
   if (bf) {   // queries -> bf16 (the corpus shadow was converted at load)
-    e = launch_to_bf16(a.Q, a.Qb, a.q * a.d, s);
+    e = launch_to_bf16(a.Q, a.Qb, a.q * a.d, (int64_t)plan.qtiles * tc::BM * a.d, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
   const void *qsrc = bf ? a.Qb : (const void *)a.Q;
   const void *xsrc = bf ? a.Xb : (const void *)a.X;
   CUtensorMap mq, mx, mg;
-  if (!make_map(&mq, qsrc, a.q, a.d, tc::BM, bf) || !make_map(&mx, xsrc, a.n, a.d, tc::BN, bf) ||
+  if (!make_map(&mq, qsrc, bf ? (int64_t)plan.qtiles * tc::BM : a.q, a.d, tc::BM, bf) || !make_map(&mx, xsrc, a.n, a.d, tc::BN, bf) ||
       !make_map(&mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf))
     return cudaErrorInvalidValue;
   const GemmScratch gs = carve_gemm(scratch, plan, a.q, a.kprime);
@@ -934,7 +936,8 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     pp.tile_step = tc::PROBE_STEP;
     e = launch(MODE_PROBE, pp);
     if (e != cudaSuccess) return e;
-    ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau};
+    ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
+                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, xcap, tc::BN}};
     ProfScope pt("gemm.threshold", s);
     e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;
@@ -959,6 +962,8 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
   l.lists = plan.P * 2;
   l.stride = kp_of(a.kprime) * tc::CAP_FACTOR;
   l.gtau = gs.gtau;
+  l.split = SplitInfo{a.ids, a.count, a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1), plan.P, a.n,
+                      a.ids ? a.xsel_cap : 0, tc::BN};
   return l;
 }
 

@@ -339,7 +339,7 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   int32_t zero = 0;
   cudaError_t e = cudaMemsetAsync(zf, 0, 4, stream);
   if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
-  if (e == cudaSuccess && ix->xb) e = launch_to_bf16(vectors, ix->xb, n * (int64_t)d, stream);
+  if (e == cudaSuccess && ix->xb) e = launch_to_bf16(vectors, ix->xb, n * (int64_t)d, n * (int64_t)d, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&zero, zf, 4, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {
@@ -440,6 +440,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // q = 256, 0.9 once it is tensor / TMEM-bound (q >= 1024).  The buffer holds
   // at most 16 GiB of rows.
   const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
+  const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;   // bf16 queries, whole 128-row tiles
   const int64_t gather_rows = rows_req == VRS_ROWS_GATHER ? n
                               : q >= 1024                 ? n * 9 / 10
                               : q >= 256                  ? n * 9 / 20
@@ -450,7 +451,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
-                                   (size_t)(xsel_cap * row_bytes), use_bf16 && path == VRS_PATH_GEMM ? (size_t)q * d * 2 : 0});
+                                   (size_t)(xsel_cap * row_bytes), use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -462,11 +463,11 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
   void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
-  void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>((size_t)q * d * 2) : nullptr;
+  void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
 
   int launches = 0;
-  FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, kprime, q, ix->X, d, queries,
-                 (int32_t)metric, k, ix->row_offset, ids, dists};
+  FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, SplitInfo{}, kprime, q, ix->X, d,
+                 queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   if (path == VRS_PATH_SCAN) {
     if (!identity) {
       ProfScope ps("select", stream);
@@ -499,6 +500,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     f.kread = 0;
     f.sorted = 0;
     f.gtau = gl.gtau;
+    f.split = gl.split;
   }
   {
     ProfScope ps("finalize", stream);

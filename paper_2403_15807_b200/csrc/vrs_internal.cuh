@@ -108,6 +108,32 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// How many of the tensor-core pass's P row splits carry work: the row space
+// (gathered selection or all rows) is decided on the device from the selection
+// count, and each used split spans >= 4 row tiles.  The probe / main kernels,
+// the threshold and the finalize kernels all derive it the same way, so the
+// latter two skip the lists of unused splits.  bn == 0: all P splits.
+struct SplitInfo {
+  const int32_t *ids;      // compacted selection (nullptr: no predicate)
+  const int64_t *count;
+  int32_t allow_gather;
+  int32_t P;
+  int64_t n_rows;
+  int64_t xsel_cap;
+  int32_t bn;              // rows per tile
+};
+__device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t cap) {
+  return ids != nullptr && allow != 0 && n_sel <= cap;
+}
+__device__ __forceinline__ int64_t splits_used(const SplitInfo &si) {
+  if (si.bn == 0) return si.P;
+  const int64_t n_sel = si.ids ? *si.count : si.n_rows;
+  const int64_t n_space = gather_mode(si.ids, si.allow_gather, n_sel, si.xsel_cap) ? n_sel : si.n_rows;
+  const int64_t row_tiles = (n_space + si.bn - 1) / si.bn;
+  const int64_t p = row_tiles / 4 < si.P ? row_tiles / 4 : si.P;
+  return p > 1 ? p : 1;
+}
+
 // Ranking key used by the selection passes, larger = better for every metric
 // (DESIGN.md "Selection key"):  L2: 2<q,x> - |x|^2  (= |q|^2 - L2, same order),
 // IP: <q,x>,  COS: <q,x>/|x|  (1/|q| > 0 does not change the order).

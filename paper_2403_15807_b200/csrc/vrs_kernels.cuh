@@ -81,7 +81,7 @@ struct GemmArgs {
   void *Qb;                 // scratch [q x d] bf16 queries (bf16 only)
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
-cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, cudaStream_t s);
+cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
 // the tensor-core pass's candidate lists, as finalize reads them
 struct GemmLists {
@@ -91,6 +91,7 @@ struct GemmLists {
   int32_t lists;
   int32_t stride;
   const uint32_t *gtau;    // [q] ordered-u32 lower bound of the k'-th best key (0 = none)
+  SplitInfo split;         // lists 2s, 2s+1 belong to split s; only splits_used() carry entries
 };
 GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch);
 
@@ -104,6 +105,7 @@ struct FinalizeArgs {
   int32_t kread;           // entries per list when cnt == nullptr
   int32_t sorted;          // lists sorted best-first (scan path): their kprime-th entries bound the result
   const uint32_t *gtau;    // optional [q] ordered-u32 lower bound of the kprime-th best key (0 = none)
+  SplitInfo split;         // tensor-core lists: 2 per split, only splits_used() carry entries (bn 0: all)
   int32_t kprime;          // candidates selected for the exact re-score
   int64_t q;
   const float *X;
@@ -125,6 +127,7 @@ struct ThresholdArgs {
   int64_t q;
   int32_t kth;
   uint32_t *gtau;          // [q] ordered-u32 out (0 = fewer than kth finite values)
+  SplitInfo split;         // values [list][32] per query: only lists < 2 * splits_used() are read
 };
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s);
 
