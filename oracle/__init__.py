@@ -22,6 +22,7 @@ _SRC = os.path.join(_HERE, "vrs_oracle.c")
 _LIB = os.path.join(_HERE, "libvrs_oracle.so")
 
 OK, EINVAL, ENOTFOUND, EDEGENERATE, ENOMEM = 0, 1, 2, 3, 4
+ERANGE = 8
 L2, IP, COS = 0, 1, 2
 I32, U8 = 0, 1
 
@@ -61,9 +62,12 @@ def _load():
                                    ctypes.c_int32, p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                    ctypes.c_int64, p, p, p, ctypes.c_int32]
         lib.orc_score.argtypes = [p, ctypes.c_int32, p, p, ctypes.c_int64, ctypes.c_int32, p]
+        lib.orc_range.argtypes = [p, ctypes.c_int64, ctypes.c_int32, p, p, ctypes.c_int32, p, ctypes.c_int32, p,
+                                  ctypes.c_int64, ctypes.c_double, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                  p, p, p, p, ctypes.c_int32]
         lib.orc_merge.argtypes = [p, p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                   p, p]
-        for f in ("orc_select", "orc_search", "orc_score", "orc_merge"):
+        for f in ("orc_select", "orc_search", "orc_score", "orc_range", "orc_merge"):
             getattr(lib, f).restype = ctypes.c_int
         lib.orc_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -163,6 +167,37 @@ def merge(cand_ids: np.ndarray, cand_dists: np.ndarray, k: int, metric: int):
     if st != OK:
         raise OracleError(st, "merge")
     return ids, dists
+
+
+def range_search(X: np.ndarray, attrs, pred, Q: np.ndarray, tau: float, metric: int, row_offset: int = 0,
+                 nthreads: int = 0):
+    """Threshold selection (orc_range): every qualifying row with score >= tau
+    (IP, COS) / squared distance <= tau (L2), ascending id.
+    -> (offsets int64[q+1], ids int64[total], dists float32[total], scores float64[total])."""
+    lib = _load()
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    Q = np.ascontiguousarray(Q, dtype=np.float32)
+    n, d = X.shape
+    q = Q.shape[0]
+    if q and Q.shape[1] != d:
+        raise OracleError(EINVAL, "range_search (dimension mismatch)")
+    cols, ptrs, tarr = _attrs(attrs)
+    carr, nc = _clauses(pred)
+    offsets = np.zeros(q + 1, dtype=np.int64)
+    cap = 0
+    for _ in range(2):   # count, then fill with the exact capacity
+        ids = np.zeros(max(cap, 1), dtype=np.int64)
+        dists = np.zeros(max(cap, 1), dtype=np.float32)
+        sc = np.zeros(max(cap, 1), dtype=np.float64)
+        st = lib.orc_range(_ptr(X), n, d, ptrs, _ptr(tarr), len(cols), carr, nc, _ptr(Q), q, float(tau), metric,
+                           row_offset, cap, _ptr(offsets), _ptr(ids), _ptr(dists), _ptr(sc), nthreads)
+        if st == OK:
+            t = int(offsets[q])
+            return offsets, ids[:t].copy(), dists[:t].copy(), sc[:t].copy()
+        if st != ERANGE:
+            raise OracleError(st, "range_search")
+        cap = int(offsets[q])
+    raise OracleError(ERANGE, "range_search")
 
 
 def num_threads() -> int:

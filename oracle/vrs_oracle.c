@@ -281,6 +281,92 @@ int orc_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n_parts,
   return ORC_OK;
 }
 
+/*
+ * Range (threshold) selection -- eps as "the score satisfies tau" instead of
+ * "the k best":
+ *   PAPER.md L354 (Sec. 5): "We use cosine similarity > 0.9 as a vector
+ *   distance metric"; L1436 (Sec. 6): "range instead of top-k search";
+ *   SPEC.md L129-L133 THRESHOLD mode, L144 "THRESHOLD mode: every returned score
+ *   satisfies the threshold; sorted by row_id ascending", L178 ">= tau".
+ * For each query every qualifying row with score >= tau (IP, COS) or squared
+ * distance <= tau (L2; reading R14), ascending global id, scores in fp64 as in
+ * orc_search.  A zero-norm COS query selects nothing (as its top-k row is padding).
+ * offsets [q + 1] are always written; ids / dists / scores64 (optional) only
+ * when capacity >= offsets[q], else ORC_ERANGE (call again with the total).
+ */
+enum { ORC_ERANGE = 8 };
+
+static int range_keep(double s, double tau, int32_t metric) { return metric == ORC_L2 ? (s <= tau) : (s >= tau); }
+
+int orc_range(const float *X, int64_t n, int32_t d, const void *const *attrs, const int32_t *attr_types,
+              int32_t n_attrs, const orc_clause *clauses, int32_t n_clauses, const float *Qv, int64_t q, double tau,
+              int32_t metric, int64_t row_offset, int64_t capacity, int64_t *offsets, int64_t *ids, float *dists,
+              double *scores64, int32_t nthreads) {
+  if (n < 1 || d < 1 || q < 0 || capacity < 0) return ORC_EINVAL;
+  if (metric < ORC_L2 || metric > ORC_COS) return ORC_EINVAL;
+  if (isnan(tau)) return ORC_EINVAL;
+  int st = check_pred(n_attrs, attr_types, clauses, n_clauses);
+  if (st != ORC_OK) return st;
+  if (!all_finite(X, n * (int64_t)d) || !all_finite(Qv, q * (int64_t)d)) return ORC_EINVAL;
+  if (metric == ORC_COS) {
+    for (int64_t i = 0; i < n; ++i)
+      if (dot64(X + i * (int64_t)d, X + i * (int64_t)d, d) == 0.0) return ORC_EDEGENERATE;
+  }
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  int64_t *sel = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  double *sc = (double *)malloc((size_t)n * sizeof(double));
+  if (!sel || !sc) {
+    free(sel);
+    free(sc);
+    return ORC_ENOMEM;
+  }
+  int64_t nsel = 0;
+  st = orc_select(attrs, attr_types, n_attrs, n, clauses, n_clauses, NULL, &nsel, sel);
+  if (st != ORC_OK) {
+    free(sel);
+    free(sc);
+    return st;
+  }
+  offsets[0] = 0;
+  /* pass 1: how many rows each query keeps */
+  for (int64_t j = 0; j < q; ++j) {
+    const float *qv = Qv + j * (int64_t)d;
+    int64_t m = 0;
+    if (!(metric == ORC_COS && dot64(qv, qv, d) == 0.0)) {
+#pragma omp parallel for schedule(static) reduction(+ : m)
+      for (int64_t r = 0; r < nsel; ++r) m += range_keep(score64(qv, X + sel[r] * (int64_t)d, d, metric), tau, metric);
+    }
+    offsets[j + 1] = offsets[j] + m;
+  }
+  if (offsets[q] > capacity) {
+    free(sel);
+    free(sc);
+    return ORC_ERANGE;
+  }
+  /* pass 2: the kept rows in ascending id (the selection is ascending) */
+  for (int64_t j = 0; j < q; ++j) {
+    const float *qv = Qv + j * (int64_t)d;
+    if (offsets[j + 1] == offsets[j]) continue;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < nsel; ++r) sc[r] = score64(qv, X + sel[r] * (int64_t)d, d, metric);
+    int64_t o = offsets[j];
+    for (int64_t r = 0; r < nsel; ++r) {
+      if (!range_keep(sc[r], tau, metric)) continue;
+      ids[o] = row_offset + sel[r];
+      dists[o] = (float)sc[r];
+      if (scores64) scores64[o] = sc[r];
+      ++o;
+    }
+  }
+  free(sel);
+  free(sc);
+  return ORC_OK;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

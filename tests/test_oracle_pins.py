@@ -353,3 +353,104 @@ def test_fp32_rounding_of_returned_dists():
     ids, d, s = _search(X, None, [], Q, 40, IP)
     assert (d == s.astype(np.float32)).all()
     assert np.all(np.diff(s, axis=1) <= 0)
+
+
+# ---------------------------------------------------------------- range (threshold) selection
+# orc_range: PAPER.md L354 ("cosine similarity > 0.9"), L1436 ("range instead of
+# top-k"); SPEC.md L129-L133, L144 (ascending row id), L178 (>= tau); reading R14.
+
+@pytest.mark.parametrize("ex", GOLD["range_search"], ids=lambda e: e["cite"][:24])
+def test_spec_range_examples(ex):
+    X = np.array(ex["rows"], dtype=np.float32)
+    attrs = [np.array(ex.get("attr", [0] * len(X)), dtype=np.int32)]
+    pred = [(0, ex["lo"], ex["hi"])] if "lo" in ex else []
+    off, ids, dists, sc = oracle.range_search(X, attrs, pred, np.array([ex["query"]], dtype=np.float32), ex["tau"],
+                                             COS)
+    assert off.tolist() == [0, len(ex["ids"])]
+    assert ids.tolist() == ex["ids"]
+    assert np.allclose(dists, ex["dists"], atol=1e-7)
+
+
+def _rand(n, d, seed, dup=False):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    if dup:
+        X[n // 2] = X[0]
+    attrs = [rng.integers(0, 10, n).astype(np.int32)]
+    return rng, X, attrs
+
+
+@pytest.mark.parametrize("metric", [L2, IP, COS])
+def test_range_extremes_and_ascending_ids(metric):
+    rng, X, attrs = _rand(300, 7, 11)
+    Q = rng.standard_normal((3, 7)).astype(np.float32)
+    pred = [(0, 2, 6)]
+    _, _, sel = oracle.select(attrs, len(X), pred)
+    everything = -np.inf if metric != L2 else np.inf
+    nothing = np.inf if metric != L2 else -1.0
+    off, ids, _, _ = oracle.range_search(X, attrs, pred, Q, everything, metric)
+    assert off.tolist() == [0, len(sel), 2 * len(sel), 3 * len(sel)]
+    for j in range(3):
+        assert ids[off[j]:off[j + 1]].tolist() == sel.tolist()      # every qualifying row, ascending
+    off, ids, _, _ = oracle.range_search(X, attrs, pred, Q, nothing, metric)
+    assert off.tolist() == [0, 0, 0, 0] and len(ids) == 0
+
+
+@pytest.mark.parametrize("metric", [L2, IP, COS])
+def test_range_equals_independent_numpy_filter(metric):
+    """Brute force with numpy fp64 (independent of the C oracle's loops)."""
+    rng, X, attrs = _rand(257, 13, 12)
+    Q = rng.standard_normal((4, 13)).astype(np.float32)
+    pred = [(0, 0, 4)]
+    keep_row = (attrs[0] >= 0) & (attrs[0] <= 4)
+    Xd, Qd = X.astype(np.float64), Q.astype(np.float64)
+    if metric == L2:
+        S = ((Qd[:, None, :] - Xd[None, :, :]) ** 2).sum(-1)
+    elif metric == IP:
+        S = Qd @ Xd.T
+    else:
+        S = (Qd @ Xd.T) / np.linalg.norm(Qd, axis=1)[:, None] / np.linalg.norm(Xd, axis=1)[None, :]
+    tau = float(np.median(S))
+    off, ids, _, sc = oracle.range_search(X, attrs, pred, Q, tau, metric)
+    for j in range(4):
+        want = np.nonzero(keep_row & ((S[j] <= tau) if metric == L2 else (S[j] >= tau)))[0]
+        assert ids[off[j]:off[j + 1]].tolist() == want.tolist()
+        assert np.allclose(sc[off[j]:off[j + 1]], S[j, want], rtol=1e-12)
+
+
+@pytest.mark.parametrize("metric", [L2, IP, COS])
+def test_range_containment_and_monotone_in_tau(metric):
+    rng, X, attrs = _rand(400, 9, 13)
+    Q = rng.standard_normal((2, 9)).astype(np.float32)
+    _, _, sc = oracle.search(X, attrs, [], Q, 50, metric)
+    lo_tau, hi_tau = float(np.median(sc[:, 20])), float(np.median(sc[:, 40]))   # two thresholds
+    a = oracle.range_search(X, attrs, [(0, 3, 8)], Q, lo_tau, metric)
+    b = oracle.range_search(X, attrs, [], Q, lo_tau, metric)
+    c = oracle.range_search(X, attrs, [], Q, hi_tau, metric)
+    _, _, sel = oracle.select(attrs, len(X), [(0, 3, 8)])
+    for j in range(2):
+        fa, fb, fc = (set(r[1][r[0][j]:r[0][j + 1]].tolist()) for r in (a, b, c))
+        assert fa == fb & set(sel.tolist())          # result(theta) = result(no theta) n sigma_theta
+        strict, loose = (fb, fc) if (metric == L2) == (lo_tau < hi_tau) else (fc, fb)
+        assert strict <= loose                       # monotone in tau
+
+
+@pytest.mark.parametrize("metric", [L2, IP, COS])
+def test_range_at_kth_score_equals_topk(metric):
+    """Tie-free data: the range result at tau = the k-th best score is the top-k set."""
+    rng, X, attrs = _rand(500, 16, 14)
+    Q = rng.standard_normal((3, 16)).astype(np.float32)
+    k = 17
+    tk_ids, _, tk_sc = oracle.search(X, attrs, [(0, 1, 9)], Q, k, metric)
+    for j in range(3):
+        off, ids, _, _ = oracle.range_search(X, attrs, [(0, 1, 9)], Q[j:j + 1], float(tk_sc[j, k - 1]), metric)
+        assert sorted(ids.tolist()) == sorted(tk_ids[j].tolist()) and len(ids) == k
+
+
+def test_range_l2_duplicate_row_at_zero_and_cos_zero_query():
+    rng, X, attrs = _rand(64, 5, 15, dup=True)
+    off, ids, dists, _ = oracle.range_search(X, attrs, [], X[:1], 0.0, L2)
+    assert ids.tolist() == [0, 32] and dists.tolist() == [0.0, 0.0]
+    Qz = np.zeros((1, 5), dtype=np.float32)
+    off, ids, _, _ = oracle.range_search(X, attrs, [], Qz, -1.0, COS)
+    assert off.tolist() == [0, 0]
