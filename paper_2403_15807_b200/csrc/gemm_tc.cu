@@ -65,7 +65,7 @@ constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries pe
 constexpr int BIAS_STAGES = 4;
 constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
 constexpr int SLOTS = 32;       // probe: row slots per lane (column index mod 32)
-constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile
+constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile (8 / 32 for large / small batches)
 constexpr int GROUPS = BN / 8;  // 8-column key-bound groups per tile
 // dynamic smem: [pipeline region] + bias a/b/id [BIAS_STAGES][BN] + group bounds
 // max b / max a / min a [3][BIAS_STAGES][GROUPS] + per-warp key staging (doubles as
@@ -933,7 +933,12 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   if (!no_probe) {
     ProfScope pf("gemm.probe", s);
     TcParams pp = p;
-    pp.tile_step = tc::PROBE_STEP;
+    // probe density: a denser probe gives a tighter threshold (fewer slow-path
+    // chunks in the main pass, which matters once the main pass is TMEM / MMA
+    // bound); small batches are HBM-bound and want the cheapest probe
+    // (C2 measurements: 1/8 best at Q = 4096, 1/16 at Q = 256, 1/32 at Q = 16)
+    static const int probe_env = getenv("VRS_PROBE_STEP") ? atoi(getenv("VRS_PROBE_STEP")) : 0;
+    pp.tile_step = probe_env > 0 ? probe_env : (a.q >= 1024 ? 8 : (a.q >= 64 ? tc::PROBE_STEP : 32));
     e = launch(MODE_PROBE, pp);
     if (e != cudaSuccess) return e;
     ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
