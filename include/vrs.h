@@ -63,7 +63,8 @@ typedef enum {
   VRS_ENOMEM = 4,        /* the allocator returned NULL */
   VRS_ECUDA = 5,         /* a CUDA runtime error (including asynchronous faults) */
   VRS_ECOMM = 6,         /* reserved for collective errors raised by callers of vrs_merge */
-  VRS_EUNSUPPORTED = 7   /* k > VRS_K_MAX, too many clauses, or a device that is not sm_100 */
+  VRS_EUNSUPPORTED = 7,  /* k > VRS_K_MAX, too many clauses, or a device that is not sm_100 */
+  VRS_ERANGE = 8         /* vrs_range_search: more results than `capacity` (*total = the size needed) */
 } vrs_status;
 
 typedef enum { VRS_L2 = 0, VRS_IP = 1, VRS_COSINE = 2 } vrs_metric;
@@ -191,6 +192,32 @@ VRS_API vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q,
 VRS_API vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,
                            const vrs_predicate *pred, int32_t k, vrs_metric metric, int64_t *h_ids,
                            float *h_dists, const vrs_search_options *opts, void *cuda_stream);
+
+/*
+ * vrs_range_search -- threshold selection instead of top-k: eps = "the score
+ * satisfies tau" (Sec. 5: "We use cosine similarity > 0.9";
+ * L1436, Sec. 6: "range instead of top-k search").
+ * For each query j, every qualifying row with score >= tau (VRS_IP, VRS_COSINE)
+ * or squared distance <= tau (VRS_L2), in ascending global row id, with its
+ * exact score (fp64 from the fp32 inputs, rounded once to fp32); the decision
+ * score-vs-tau is taken on that fp64 score.
+ *   offsets : device int64 [q + 1] (output): query j's results are
+ *             ids[offsets[j] .. offsets[j+1]), offsets[q] = total.
+ *   ids     : device int64 [capacity], dists: device fp32 [capacity] (outputs).
+ *   total   : HOST int64 (output): the number of results.
+ * The call SYNCHRONISES `cuda_stream` twice (once to size the candidate buffer,
+ * once to check `capacity`); the final writes stay enqueued.  If total >
+ * capacity it returns VRS_ERANGE with *total and the device offsets valid and
+ * ids / dists untouched: call again with capacity >= *total.
+ * Runs on the tensor-core path (d % 4 == 0, 16-byte aligned rows and queries);
+ * other shapes get VRS_EUNSUPPORTED.  opts: precision / rows as in vrs_search_ex
+ * (path is ignored).  Errors: as vrs_search, plus EINVAL for a NaN tau or a
+ * negative capacity, ERANGE.
+ */
+VRS_API vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int32_t d,
+                                    const vrs_predicate *pred, double tau, vrs_metric metric, int64_t capacity,
+                                    int64_t *offsets, int64_t *ids, float *dists, int64_t *total,
+                                    const vrs_search_options *opts, void *cuda_stream);
 
 /*
  * vrs_select -- the relational step alone, sigma_{theta_R}(R):

@@ -161,6 +161,34 @@ class Index:
         _lib.check(st, "vrs_search_host")
         return ids, dists
 
+    def range_search(self, queries: torch.Tensor, pred=None, tau: float = 0.9, metric="cos", capacity=None,
+                     rows=None, precision=None, stream=None):
+        """vrs_range_search: every qualifying row with score >= tau (ip / cos) or squared
+        distance <= tau (l2), ascending global id.  -> (offsets int64 [q+1], ids int64 [total],
+        dists float32 [total]) on the device.  Synchronises the stream (the result size is
+        data-dependent); grows the output and calls again if `capacity` is too small."""
+        lib = library()
+        q = queries.shape[0]
+        d = queries.shape[1] if queries.dim() == 2 else self.d
+        dev = self.vectors.device
+        offsets = torch.empty(q + 1, dtype=torch.int64, device=dev)
+        cap = int(capacity) if capacity is not None else max(1024, 64 * q)
+        pr, keep = _lib.make_predicate(pred)
+        for _ in range(2):
+            ids = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+            dists = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+            total = ctypes.c_int64(0)
+            st = lib.vrs_range_search(self._h, _ptr(queries) if q else None, q, d, ctypes.byref(pr), float(tau),
+                                      _metric(metric), cap, _ptr(offsets), _ptr(ids), _ptr(dists),
+                                      ctypes.byref(total), _options(None, rows, precision), _stream(stream))
+            if st == _lib.ERANGE:
+                cap = int(total.value)
+                continue
+            _lib.check(st, "vrs_range_search")
+            t = int(total.value)
+            return offsets, ids[:t], dists[:t]
+        _lib.check(st, "vrs_range_search")
+
     def select(self, pred=None, with_ids: bool = False, stream=None):
         """-> (bitmap uint32-as-int32 [ceil(n/32)], count int64 [1], ids int32 [n] or None); device tensors."""
         lib = library()

@@ -14,9 +14,9 @@ LIB_PATH = os.path.join(_HERE, "libvrs.so")
 if os.environ.get("VRS_LIB") == "exp":   # experiment build of the same sources (csrc/Makefile `exp`)
     LIB_PATH = os.path.join(_HERE, "libvrs_exp.so")
 
-OK, EINVAL, ENOTFOUND, EDEGENERATE, ENOMEM, ECUDA, ECOMM, EUNSUPPORTED = range(8)
+OK, EINVAL, ENOTFOUND, EDEGENERATE, ENOMEM, ECUDA, ECOMM, EUNSUPPORTED, ERANGE = range(9)
 STATUS_NAMES = ["VRS_OK", "VRS_EINVAL", "VRS_ENOTFOUND", "VRS_EDEGENERATE", "VRS_ENOMEM", "VRS_ECUDA",
-                "VRS_ECOMM", "VRS_EUNSUPPORTED"]
+                "VRS_ECOMM", "VRS_EUNSUPPORTED", "VRS_ERANGE"]
 L2, IP, COSINE = 0, 1, 2
 ATTR_I32, ATTR_U8 = 0, 1
 PATH_AUTO, PATH_SCAN, PATH_GEMM = 0, 1, 2
@@ -26,7 +26,7 @@ K_MAX = 240
 MAX_CLAUSES = 8
 
 # every symbol include/vrs.h declares (tests check the library exports them)
-EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
+EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
            "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
            "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset")
 
@@ -81,10 +81,12 @@ def load_library():
     lib.vrs_search.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p]
     lib.vrs_search_ex.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p, p]
     lib.vrs_search_host.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p, p]
+    lib.vrs_range_search.argtypes = [p, p, i64, i32, p, ctypes.c_double, ctypes.c_int, i64, p, p, p,
+                                     ctypes.POINTER(i64), p, p]
     lib.vrs_select.argtypes = [p, p, p, p, p, p]
     lib.vrs_merge.argtypes = [p, p, i32, i64, i32, ctypes.c_int, p, p, p]
     lib.vrs_free.argtypes = [p]
-    for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free"):
+    for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free"):
         getattr(lib, f).restype = ctypes.c_int
     lib.vrs_last_error.restype = ctypes.c_char_p
     lib.vrs_last_path.restype = i32

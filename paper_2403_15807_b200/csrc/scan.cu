@@ -24,20 +24,33 @@ namespace vrs {
 // ------------------------------------------------------------------ K6' norms
 // |x|^2 and 1/|x| per row (fp32), computed once at vrs_load (PAPER.md L305,
 // L790 "then normalized"); zero_flag records a zero-norm row (COSINE degenerate).
+// zero_flag[1] collects the largest |x|^2 as float bits (non-negative floats order
+// as integers) -- the range search's error bound uses max |x|.
 __global__ void norms_kernel(const float *__restrict__ X, int64_t n, int32_t d, float *__restrict__ nx2,
                              float *__restrict__ inv_nx, int32_t *__restrict__ zero_flag) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const float *x = X + row * d;
+  __shared__ float s_max[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
   float s = 0.f;
-  for (int t = lane; t < d; t += 32) s = fmaf(x[t], x[t], s);
+  if (row < n) {
+    const float *x = X + row * d;
+    for (int t = lane; t < d; t += 32) s = fmaf(x[t], x[t], s);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) {
-    nx2[row] = s;
-    inv_nx[row] = s > 0.f ? 1.0f / sqrtf(s) : 0.f;
-    if (!(s > 0.f)) atomicOr(zero_flag, 1);
+    if (row < n) {
+      nx2[row] = s;
+      inv_nx[row] = s > 0.f ? 1.0f / sqrtf(s) : 0.f;
+      if (!(s > 0.f)) atomicOr(zero_flag, 1);
+    }
+    s_max[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = s_max[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, s_max[i]);
+    atomicMax(zero_flag + 1, __float_as_int(m));
   }
 }
 

@@ -1,0 +1,767 @@
+// tc_kernel.cuh -- the tcgen05 tensor-core pass (kernel template shared by
+// gemm_tc.cu: top-k probe / main modes, and gemm_range.cu: range count / fill
+// modes).  See gemm_tc.cu for the design notes.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "vrs_kernels.cuh"
+
+namespace vrs {
+
+namespace tc {
+constexpr int BM = 128;         // queries per tile (TMEM lanes)
+#ifndef VRS_BN
+#define VRS_BN 256
+#endif
+constexpr int BN = VRS_BN;      // rows per tile (TMEM columns, MMA N)
+constexpr int BK = 32;          // fp32 per K block = 128 bytes = one swizzle span (bf16: 64)
+constexpr int PIPE_BYTES = 192 * 1024;   // shared-memory pipeline region (A resident and/or stages)
+constexpr int MAX_STAGES = 8;
+constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+constexpr int B_BYTES = BN * BK * 4;   // 32 KB at BN = 256
+constexpr int ACC_STAGES = 512 / BN;   // accumulator tiles in TMEM (all 512 columns)
+constexpr int TMEM_COLS = 512;
+constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
+constexpr int EPI_COLS = BN / 2;
+constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (list, query)
+constexpr int BIAS_STAGES = 4;
+constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
+constexpr int SLOTS = 32;       // probe: row slots per lane (column index mod 32)
+constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile (8 / 32 for large / small batches)
+constexpr int GROUPS = BN / 8;  // 8-column key-bound groups per tile
+// dynamic smem: [pipeline region] + bias a/b/id [BIAS_STAGES][BN] + group bounds
+// max b / max a / min a [3][BIAS_STAGES][GROUPS] + per-warp key staging (doubles as
+// the compaction histogram)
+constexpr size_t SMEM_BYTES = 1024 + (size_t)PIPE_BYTES + BIAS_STAGES * BN * 12 + 3 * BIAS_STAGES * GROUPS * 4 +
+                              EPI_WARPS * 32 * STAGE_COLS * 4 + 256;
+}  // namespace tc
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::tf32, both operands K-major.
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), both K-major.
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major operand in the canonical
+// 128-byte-swizzle layout written by TMA (8-row groups of 1024 bytes).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                   // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D fp32, A/B tf32 (format 2) or bf16 (format 1), both
+// K-major, N = BN, M = BM.
+__host__ __device__ constexpr uint32_t mma_idesc(int M, int N, bool bf16) {
+  return (1u << 4) | ((bf16 ? 1u : 2u) << 7) | ((bf16 ? 1u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+#define TMEM_LD_32x32b_X32(taddr, r)                                                                              \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                                  \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),  \
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),      \
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),     \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                  \
+      : "r"(taddr))
+
+// Wait for this thread's outstanding tcgen05.ld; the registers are tied to the
+// wait so no use of them can be scheduled above it.
+#define TMEM_LD_WAIT(r)                                                                                           \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                   \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),   \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),            \
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),          \
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),          \
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])                                                             \
+               :                                                                                                  \
+               : "memory")
+
+// ---------------------------------------------------------------- kernel
+struct TcParams {
+  int64_t n_rows;          // rows of the index (identity / masked row space)
+  const int32_t *ids;      // compacted ascending selection (nullptr: no predicate)
+  const int64_t *count;    // device count of ids
+  int32_t allow_gather;    // 0 never, 1 selectivity switch on the device, 2 forced
+  int32_t d;
+  int32_t nk;              // K blocks = ceil(d / 32)
+  int64_t q;
+  int32_t qtiles;
+  int32_t P;               // splits
+  int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
+  const uint32_t *bitmap;  // nullptr => every row qualifies
+  const float *nx2;
+  const float *inv_nx;
+  int32_t metric;
+  int32_t kp;              // entries kept by a compaction (pow2 >= k')
+  int32_t cap;             // buffer capacity per (list, query)
+  float *cand_key;         // [2P][q][cap]
+  int32_t *cand_id;
+  int32_t *cand_cnt;       // [2P][q] entries per list (MAIN, RCOUNT)
+  const int64_t *coff;     // RFILL: [q][2P] start of each (query, list) segment in cand_id
+  float *probe_max;        // [q][2P][SLOTS] probe slot maxima
+  int64_t xsel_cap;        // rows of the materialised-selection buffer
+  uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
+  unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
+  int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
+};
+
+// Warp-cooperative compaction of one lane's candidate buffer to its best KP
+// entries (key desc, then buffer order = ascending row id).  Returns the new
+// threshold key (the KP-th best).  All 32 lanes call it with the same `owner`.
+static __device__ __noinline__ float compact_lane(float *key, int32_t *id, int cnt, int kp, uint32_t *hist) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0, mask = 0;
+  int rem = kp;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      const uint32_t ok = i < cnt ? ordered_u32(key[i]) : 0u;
+      hist_add_warp(hist, (i < cnt && (ok & mask) == prefix) ? (ok >> shift) & 255u : 256u);
+    }
+    __syncwarp();
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { v[t] = hist[255 - 8 * lane - t]; s += v[t]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t before = incl - s;
+    int bin = -1, above = 0;
+    if (before < (uint32_t)rem && (uint32_t)rem <= incl) {
+      uint32_t run = before;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (bin < 0 && (uint32_t)rem <= run + v[t]) { bin = 255 - 8 * lane - t; above = (int)run; }
+        if (bin < 0) run += v[t];
+      }
+    }
+    const uint32_t who = __ballot_sync(0xffffffffu, bin >= 0);
+    const int src = __ffs(who) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    prefix |= (uint32_t)bin << shift;
+    mask |= 255u << shift;
+    rem -= above;
+    __syncwarp();
+  }
+  // stable in-place compaction: keys strictly above the threshold, plus the
+  // first `rem` ties in buffer order
+  int out = 0, ties = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int i = base + lane;
+    float kv = -INFINITY;
+    int32_t iv = -1;
+    uint32_t ok = 0;
+    if (i < cnt) { kv = key[i]; iv = id[i]; ok = ordered_u32(kv); }
+    const bool tie = (i < cnt) && ok == prefix;
+    const uint32_t tmask = __ballot_sync(0xffffffffu, tie);
+    const int my_tie_rank = ties + __popc(tmask & lanemask_lt());
+    ties += __popc(tmask);
+    const bool keep = (i < cnt) && (ok > prefix || (tie && my_tie_rank < rem));
+    const uint32_t kmask = __ballot_sync(0xffffffffu, keep);
+    const int pos = out + __popc(kmask & lanemask_lt());
+    __syncwarp();
+    if (keep) { key[pos] = kv; id[pos] = iv; }
+    out += __popc(kmask);
+    __syncwarp();
+  }
+  const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7fffffffu) : ~prefix;
+  return __uint_as_float(u);
+}
+
+constexpr int MODE_MAIN = 0;    // fused top-k candidates
+constexpr int MODE_PROBE = 1;   // slot maxima for the threshold
+constexpr int MODE_RCOUNT = 2;  // range search: count keys >= the query's threshold per list
+constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the list's segment
+
+// AR: the query tile stays resident in shared memory (d <= 128).
+// MODE: MAIN (fused top-k candidates) or PROBE (slot maxima for the threshold).
+// ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
+// BF: operands are bf16 (shadow corpus, kind::f16) instead of fp32 (kind::tf32).
+template <bool AR, int MODE, bool ROWSCALE, bool BF>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
+                   const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
+  // array itself, so the compiler keeps the shared address space (LDS, not LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // pipeline region: AR ? [A: nk x 16 KB][B stages of 32 KB] : [stages of (A 16 KB | B 32 KB)]
+  constexpr int SSTRIDE = AR ? B_BYTES : A_BYTES + B_BYTES;   // bytes per pipeline stage
+  constexpr int NST = ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
+                          ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
+                          : MAX_STAGES;
+  constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
+  constexpr int KE = BF ? 2 * BK : BK;                   // elements per 128-byte K block
+  uint8_t *a_res = smem;                                 // AR: resident query tile
+  uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
+  float *bias_a = reinterpret_cast<float *>(smem + PIPE_BYTES);               // [BIAS_STAGES][BN]
+  float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
+  int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
+  // per 8-row group: max b, max a, min a over its rows (the group's key upper bound)
+  float *g_bmax = reinterpret_cast<float *>(row_id + BIAS_STAGES * BN);        // [BIAS_STAGES][GROUPS]
+  float *g_amax = g_bmax + BIAS_STAGES * GROUPS;
+  float *g_amin = g_amax + BIAS_STAGES * GROUPS;
+  float *kstage = g_amin + BIAS_STAGES * GROUPS;                                // [EPI_WARPS][32][STAGE_COLS]
+
+  __shared__ __align__(8) uint64_t full_bar[MAX_STAGES], empty_bar[MAX_STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[ACC_STAGES], tempty_bar[ACC_STAGES];
+  __shared__ __align__(8) uint64_t bfull_bar[BIAS_STAGES], bempty_bar[BIAS_STAGES];
+  __shared__ __align__(8) uint64_t afull_bar;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qtile = blockIdx.x % p.qtiles;
+  const int split = blockIdx.x / p.qtiles;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&afull_bar, 1);
+    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
+    for (int s = 0; s < BIAS_STAGES; ++s) {
+      mbar_init(&bfull_bar[s], 32);
+      mbar_init(&bempty_bar[s], EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); prefetch_tmap(&tmap_g); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  // (the prologue above overlaps the predecessor kernel's tail; global memory from here on)
+  pdl_wait();
+  pdl_trigger();
+  // Selectivity-driven row delivery (decided on the device, no host sync):
+  //  gather: the selection was materialised densely (gather_copy_kernel, late
+  //          materialization) and streams by TMA from X_sel; ids map rows back
+  //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
+  const int64_t n_sel = p.ids ? *p.count : p.n_rows;
+  const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.xsel_cap);
+  const int64_t n_space = gather ? n_sel : p.n_rows;
+  const int64_t row_tiles = (n_space + BN - 1) / BN;
+  // splits actually used (splits_used): >= 4 row tiles per item when the
+  // (device-side) row space allows; CTAs of unused splits publish empty lists
+  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
+  const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
+  const int64_t span = t_end - t_begin;
+  // probe: every tile_step-th tile of the item (the first tile of a shorter item)
+  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(p.tile_step, std::max<int64_t>(1, span)) : 1;
+  const int ntiles = (int)((span + step - 1) / step);
+  auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
+
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      if (AR && ntiles > 0) {
+        mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+      }
+      for (int t = 0; t < ntiles; ++t) {
+        const int row0 = (int)(tile_of(t) * BN);
+        for (int kb = 0; kb < p.nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t *st = b_base + stage * SSTRIDE;
+          mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
+          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
+          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * KE, row0);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = mma_idesc(BM, BN, BF);
+    int stage = 0;
+    uint32_t phase = 0;
+    if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t % ACC_STAGES;
+      const uint32_t acc_phase = (t / ACC_STAGES) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.nk; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
+          const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // K = 8 tf32 / 16 bf16 = 32 bytes per instruction
+            if (BF) tc_mma_bf16(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+          }
+          // frees the smem slot when these MMAs finish; accumulator ready after the last K block
+          tc_commit(&empty_bar[stage]);
+          if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ per-row epilogue terms
+    // Loads for tile t + PF are issued before tile t is written out: the warp is
+    // memory-latency bound otherwise (one ~us round trip per tile).
+    constexpr int PF = 2;
+    const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
+    constexpr int RPL = BN / 32;   // rows per lane
+    float nv[PF][RPL];
+    int32_t iv[PF][RPL];
+    uint32_t wv[PF];
+    auto fetch = [&](int t, float (&n8)[RPL], int32_t (&i8)[RPL], uint32_t &w) {
+      if (t >= ntiles) return;
+      const int64_t pos0 = tile_of(t) * BN + lane * RPL;   // this lane: RPL consecutive row-space slots
+      if (gather) {
+        if (pos0 + RPL <= n_sel) {
+#pragma unroll
+          for (int v = 0; v < RPL / 4; ++v) {
+            const int4 i0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + v);
+            i8[4 * v] = i0.x; i8[4 * v + 1] = i0.y; i8[4 * v + 2] = i0.z; i8[4 * v + 3] = i0.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) n8[u] = i8[u] >= 0 ? __ldg(src + i8[u]) : 0.f;
+        w = 0xffffffffu;
+      } else {
+        w = 0xffffffffu;
+        if (p.bitmap && pos0 < p.n_rows) w = __ldg(p.bitmap + (pos0 >> 5));
+        if (pos0 + RPL <= p.n_rows) {
+#pragma unroll
+          for (int v = 0; v < RPL / 4; ++v) {
+            const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + v);
+            n8[4 * v] = v0.x; n8[4 * v + 1] = v0.y; n8[4 * v + 2] = v0.z; n8[4 * v + 3] = v0.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) n8[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < p.n_rows ? (int32_t)(pos0 + u) : -1;
+      }
+    };
+#pragma unroll
+    for (int u = 0; u < PF; ++u) fetch(u, nv[u], iv[u], wv[u]);
+    for (int t0 = 0; t0 < ntiles; t0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int t = t0 + u;
+        if (t >= ntiles) break;
+        const int s = t % BIAS_STAGES;
+        mbar_wait(&bempty_bar[s], ((t / BIAS_STAGES) & 1) ^ 1);
+        const int64_t pos0 = tile_of(t) * BN + lane * RPL;
+        float av[RPL], bv[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          const bool valid = iv[u][k] >= 0 && (gather || ((wv[u] >> ((pos0 + k) & 31)) & 1u));
+          float a = 1.f, b = valid ? 0.f : -INFINITY;
+          if (p.metric == VRS_L2) {
+            a = 2.f;
+            if (valid) b = -nv[u][k];
+          } else if (p.metric == VRS_COSINE) {
+            a = valid ? nv[u][k] : 0.f;
+          }
+          av[k] = a; bv[k] = b;
+        }
+#pragma unroll
+        for (int v = 0; v < RPL / 4; ++v) {
+          if (ROWSCALE)
+            reinterpret_cast<float4 *>(bias_a + s * BN + lane * RPL)[v] =
+                make_float4(av[4 * v], av[4 * v + 1], av[4 * v + 2], av[4 * v + 3]);
+          reinterpret_cast<float4 *>(bias_b + s * BN + lane * RPL)[v] =
+              make_float4(bv[4 * v], bv[4 * v + 1], bv[4 * v + 2], bv[4 * v + 3]);
+          if (MODE == MODE_MAIN || MODE == MODE_RFILL)
+            reinterpret_cast<int4 *>(row_id + s * BN + lane * RPL)[v] =
+                make_int4(iv[u][4 * v], iv[u][4 * v + 1], iv[u][4 * v + 2], iv[u][4 * v + 3]);
+        }
+        // group bounds over 8-row groups (8 / RPL lanes each)
+        static_assert(RPL <= 8 && 8 % RPL == 0, "8-row groups of whole lanes");
+        float bmx = bv[0], amx = av[0], amn = av[0];
+#pragma unroll
+        for (int k = 1; k < RPL; ++k) { bmx = fmaxf(bmx, bv[k]); amx = fmaxf(amx, av[k]); amn = fminf(amn, av[k]); }
+#pragma unroll
+        for (int o = 1; o < 8 / RPL; o <<= 1) {
+          bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+          amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+          amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, o));
+        }
+        if ((lane & (8 / RPL - 1)) == 0) {
+          g_bmax[s * GROUPS + lane / (8 / RPL)] = bmx;
+          if (ROWSCALE) { g_amax[s * GROUPS + lane / (8 / RPL)] = amx; g_amin[s * GROUPS + lane / (8 / RPL)] = amn; }
+        }
+        mbar_arrive(&bfull_bar[s]);
+        fetch(t + PF, nv[u], iv[u], wv[u]);
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------ epilogue
+    const int ew = warp - EPI_WARP0;
+    const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;                      // which 128 of the tile's 256 columns
+    const int m = quad * 32 + lane;                // query row within the tile
+    const int64_t qg = (int64_t)qtile * BM + m;    // global query index
+    const bool active = qg < p.q;
+    const int list = split * 2 + half;             // candidate list index
+    const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
+    const int64_t cbase = MODE == MODE_RFILL ? (active ? p.coff[qg * (2 * p.P) + list] : 0)
+                                             : ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
+    float *ckey = p.cand_key + (MODE == MODE_RFILL ? 0 : cbase);
+    int32_t *cid = p.cand_id + cbase;
+    float *wst = kstage + ew * 32 * STAGE_COLS;
+    uint32_t *whist = reinterpret_cast<uint32_t *>(wst);   // compaction histogram aliases the staging area
+    float thr = active ? -INFINITY : INFINITY;     // accept iff key > thr (inactive lanes never accept)
+    int cnt = 0;
+    uint32_t st_chunks = 0, st_slow = 0, st_app = 0, st_comp = 0;
+    float smax[SLOTS];
+#pragma unroll
+    for (int i = 0; i < SLOTS; ++i) smax[i] = -INFINITY;
+    // Shared threshold (probe): the k'-th best key over all rows is >= gtau, so
+    // keys below it can never be in the result; keys equal to it are kept.
+    // (range modes: gtau is the query's key threshold, margin included)
+    if (MODE != MODE_PROBE && active) {
+      const uint32_t o = __ldcg(p.gtau + qg);
+      if (o != 0) {
+        const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        thr = nextafterf(__uint_as_float(u), -INFINITY);
+      }
+    }
+    // own list: after a compaction to the KP best, a later row (larger id) must
+    // beat the KP-th best strictly
+    auto compact_needed = [&](int threshold) {
+      uint32_t need = __ballot_sync(0xffffffffu, cnt > threshold);
+      while (need) {
+        const int owner = __ffs(need) - 1;
+        need &= need - 1;
+        const int oc = __shfl_sync(0xffffffffu, cnt, owner);
+        const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
+        const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
+        ++st_comp;
+        if (lane == owner) {
+          cnt = p.kp;
+          thr = fmaxf(thr, nt);
+        }
+      }
+    };
+    auto f4 = [](const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; };
+    // one 32-column chunk: r holds the raw dot products; gb/ga/gn: the chunk's 4
+    // group bounds (max b, max a, min a)
+    auto chunk = [&](uint32_t (&r)[32], const float *ba, const float *bb, const int32_t *rid, const float *gb,
+                     const float *ga, const float *gn) {
+      if (MODE == MODE_PROBE) {   // exact keys -> running slot maxima
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = *reinterpret_cast<const float4 *>(bb + i);
+          float4 a4 = make_float4(sc, sc, sc, sc);
+          if (ROWSCALE) a4 = *reinterpret_cast<const float4 *>(ba + i);
+          smax[i] = fmaxf(smax[i], fmaf(__uint_as_float(r[i]), a4.x, b4.x));
+          smax[i + 1] = fmaxf(smax[i + 1], fmaf(__uint_as_float(r[i + 1]), a4.y, b4.y));
+          smax[i + 2] = fmaxf(smax[i + 2], fmaf(__uint_as_float(r[i + 2]), a4.z, b4.z));
+          smax[i + 3] = fmaxf(smax[i + 3], fmaf(__uint_as_float(r[i + 3]), a4.w, b4.w));
+        }
+        return;
+      }
+      // fast path: per 8-column group an upper bound of its keys from the group's
+      // largest raw dot and its bias / scale range -- fma is monotone in each
+      // argument (scale > 0), so no key of the group can exceed it
+      const float4 b4 = *reinterpret_cast<const float4 *>(gb);
+      float4 ax4 = b4, an4 = b4;
+      if (ROWSCALE) { ax4 = *reinterpret_cast<const float4 *>(ga); an4 = *reinterpret_cast<const float4 *>(gn); }
+      uint32_t pass = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float dm = __uint_as_float(r[g * 8]);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) dm = fmaxf(dm, __uint_as_float(r[g * 8 + i]));
+        const float kb = ROWSCALE ? fmaf(dm, dm >= 0.f ? f4(ax4, g) : f4(an4, g), f4(b4, g)) : fmaf(dm, sc, f4(b4, g));
+        pass |= (kb > thr ? 1u : 0u) << g;
+      }
+      ++st_chunks;
+      if (!__any_sync(0xffffffffu, pass != 0)) return;
+      // rare once the threshold is in place: exact keys of the flagged groups, make
+      // room (<= 8 appends follow; the compaction histogram aliases the staging
+      // rows), then each lane appends its accepted columns in row order from its
+      // private staging row
+      ++st_slow;
+      if (MODE == MODE_MAIN && __any_sync(0xffffffffu, cnt + 32 > p.cap)) compact_needed(p.cap - 32);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {   // (unrolled: r must stay in registers)
+        if (!__any_sync(0xffffffffu, (pass >> g) & 1u)) continue;
+        float kk[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 4) {
+          const float4 bq = *reinterpret_cast<const float4 *>(bb + g * 8 + i);
+          float4 aq = make_float4(sc, sc, sc, sc);
+          if (ROWSCALE) aq = *reinterpret_cast<const float4 *>(ba + g * 8 + i);
+          kk[i] = fmaf(__uint_as_float(r[g * 8 + i]), aq.x, bq.x);
+          kk[i + 1] = fmaf(__uint_as_float(r[g * 8 + i + 1]), aq.y, bq.y);
+          kk[i + 2] = fmaf(__uint_as_float(r[g * 8 + i + 2]), aq.z, bq.z);
+          kk[i + 3] = fmaf(__uint_as_float(r[g * 8 + i + 3]), aq.w, bq.w);
+        }
+        uint32_t msk = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) msk |= (kk[i] > thr ? 1u : 0u) << i;
+        if (MODE == MODE_RCOUNT) { cnt += __popc(msk); continue; }
+        if (MODE == MODE_RFILL) {   // the list's segment, rows in ascending order
+          while (msk) {
+            const int i = __ffs(msk) - 1;
+            msk &= msk - 1;
+            cid[cnt++] = rid[g * 8 + i];
+          }
+          continue;
+        }
+        if (!__any_sync(0xffffffffu, msk != 0)) continue;
+        float *myrow = wst + lane * STAGE_COLS;
+        if (msk) {
+          *reinterpret_cast<float4 *>(myrow) = make_float4(kk[0], kk[1], kk[2], kk[3]);
+          *reinterpret_cast<float4 *>(myrow + 4) = make_float4(kk[4], kk[5], kk[6], kk[7]);
+          st_app += __popc(msk);
+          while (msk) {
+            const int i = __ffs(msk) - 1;
+            msk &= msk - 1;
+            ckey[cnt] = myrow[i];
+            cid[cnt] = rid[g * 8 + i];
+            ++cnt;
+          }
+        }
+        __syncwarp();
+      }
+    };
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t % ACC_STAGES;
+      const int bs = t % BIAS_STAGES;
+      mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
+      mbar_wait(&tfull_bar[acc], (t / ACC_STAGES) & 1);
+      tc_fence_after();
+      const float *ba = bias_a + bs * BN + half * EPI_COLS;
+      const float *bb = bias_b + bs * BN + half * EPI_COLS;
+      const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
+      const int g0 = bs * GROUPS + half * (EPI_COLS / 8);   // this warp's first group
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
+      if (!p.epi_skip) {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
+        uint32_t ra[32];
+#pragma unroll 1
+        for (int c = 0; c < EPI_COLS / 32; ++c) {
+          TMEM_LD_32x32b_X32(tbase + c * 32, ra);
+          TMEM_LD_WAIT(ra);
+          chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, g_bmax + g0 + c * 4, g_amax + g0 + c * 4, g_amin + g0 + c * 4);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&tempty_bar[acc]);
+        mbar_arrive(&bempty_bar[bs]);
+      }
+    }
+    if (p.stats && lane == 0) {
+      atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
+      atomicAdd(p.stats + 1, (unsigned long long)st_slow);
+      atomicAdd(p.stats + 2, (unsigned long long)st_app);
+      atomicAdd(p.stats + 3, (unsigned long long)st_comp);
+    }
+    if (active) {
+      if (MODE == MODE_PROBE) {
+        float4 *dst = reinterpret_cast<float4 *>(p.probe_max + ((qg * (2 * p.P)) + list) * SLOTS);
+#pragma unroll
+        for (int i = 0; i < SLOTS; i += 4) dst[i / 4] = make_float4(smax[i], smax[i + 1], smax[i + 2], smax[i + 3]);
+      } else if (MODE != MODE_RFILL) {
+        p.cand_cnt[(int64_t)list * p.q + qg] = cnt;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- launch plumbing
+// Everything a tensor-core pass launch needs: the three tensor maps (queries,
+// rows, gathered rows), the mode-independent parameters and the variant flags.
+struct TcLaunch {
+  CUtensorMap mq, mx, mg;
+  TcParams p;
+  bool bf, ar, rowscale;
+};
+// Queries -> bf16 (padded tiles), tensor maps, parameters, and the gather copy
+// when the selection is materialised (gemm_tc.cu).
+cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L);
+
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
+template <bool AR, int MODE, bool ROWSCALE, bool BF>
+__global__ void tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
+                               const __grid_constant__ CUtensorMap tmap_g, TcParams p);
+template <int MODE, bool BF>
+static TcKernel pick_kernel(bool ar, bool rowscale) {
+  return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF> : tc_topk_kernel<true, MODE, false, BF>)
+            : (rowscale ? tc_topk_kernel<false, MODE, true, BF> : tc_topk_kernel<false, MODE, false, BF>);
+}
+
+// One launch of the pass in MODE (the kernels of a mode are instantiated in the
+// translation unit that calls this).  VRS_STATS=1 prints the epilogue counters.
+template <int MODE>
+static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStream_t s) {
+  static bool attr_set = false;
+  cudaError_t e = cudaSuccess;
+  if (!attr_set) {
+    for (bool ar_ : {false, true})
+      for (bool rs : {false, true})
+        for (TcKernel fn : {pick_kernel<MODE, false>(ar_, rs), pick_kernel<MODE, true>(ar_, rs)})
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale) : pick_kernel<MODE, false>(L.ar, L.rowscale);
+  static unsigned long long *stats = nullptr;
+  static const bool want_stats = getenv("VRS_STATS") != nullptr;
+  if (want_stats && !stats) cudaMalloc(&stats, 64);
+  TcParams p2 = pr;
+  p2.stats = want_stats ? stats : nullptr;
+  if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
+  e = launch_k(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, L.mq, L.mx, L.mg, p2);
+  if (want_stats) {
+    unsigned long long h[4];
+    cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[vrs stats] mode=%d grid=%d chunks=%llu slow=%llu (%.3f) appends=%llu compactions=%llu\n", MODE,
+            pr.P * pr.qtiles, h[0], h[1], h[0] ? (double)h[1] / h[0] : 0.0, h[2], h[3]);
+  }
+  return e;
+}
+
+// ---------------------------------------------------------------- tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void *f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major [rows x d] matrix of fp32 or bf16, boxes of one
+// 128-byte K block x box_rows rows, 128-byte swizzle.
+static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows, bool bf16) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int esz = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace vrs

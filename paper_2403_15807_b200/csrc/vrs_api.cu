@@ -31,6 +31,7 @@ struct vrs_index {
   float *nx2;
   float *inv_nx;
   int32_t has_zero_row;
+  float xmax;              // max row norm (range search error bound)
   void *xb;                // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
   int32_t device;
   int32_t num_sms;
@@ -318,7 +319,7 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   ix->device = dev;
   ix->num_sms = sms;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 4, want_shadow ? (size_t)n * d * 2 : 0});
+  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 8, want_shadow ? (size_t)n * d * 2 : 0});
   void *mem = nullptr;
   if (alloc) {
     mem = alloc->alloc(bytes, cuda_stream, alloc->ctx);
@@ -334,19 +335,24 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   Carve cv(mem);
   ix->nx2 = cv.take<float>(n);
   ix->inv_nx = cv.take<float>(n);
-  int32_t *zf = cv.take<int32_t>(1);
+  int32_t *zf = cv.take<int32_t>(2);   // [0] zero-norm row flag, [1] max |x|^2 (float bits)
   ix->xb = want_shadow ? cv.take<char>((size_t)n * d * 2) : nullptr;
-  int32_t zero = 0;
-  cudaError_t e = cudaMemsetAsync(zf, 0, 4, stream);
+  int32_t zero[2] = {0, 0};
+  cudaError_t e = cudaMemsetAsync(zf, 0, 8, stream);
   if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
   if (e == cudaSuccess && ix->xb) e = launch_to_bf16(vectors, ix->xb, n * (int64_t)d, n * (int64_t)d, stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&zero, zf, 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(zero, zf, 8, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) {
     vrs_free(ix);
     return fail(VRS_ECUDA, "vrs_load norms: %s", cudaGetErrorString(e));
   }
-  ix->has_zero_row = zero;
+  ix->has_zero_row = zero[0];
+  {
+    float m2;
+    memcpy(&m2, &zero[1], 4);
+    ix->xmax = sqrtf(m2) * (1.0f + 1e-6f);
+  }
   *out = ix;
   return VRS_OK;
 }
@@ -515,6 +521,125 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
 vrs_status vrs_search(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
                       int32_t k, vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream) {
   return vrs_search_ex(ix, queries, q, d, pred, k, metric, ids, dists, nullptr, cuda_stream);
+}
+
+vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
+                            double tau, vrs_metric metric, int64_t capacity, int64_t *offsets, int64_t *ids,
+                            float *dists, int64_t *total, const vrs_search_options *opts, void *cuda_stream) {
+  g_err[0] = 0;
+  g_last_launches = 0;
+  if (!ix) return fail(VRS_EINVAL, "index is NULL");
+  if (!total) return fail(VRS_EINVAL, "total is NULL");
+  if (q < 0) return fail(VRS_EINVAL, "q < 0");
+  if (d != ix->d) return fail(VRS_EINVAL, "d = %d differs from the loaded d = %d", d, ix->d);
+  if (metric != VRS_L2 && metric != VRS_IP && metric != VRS_COSINE)
+    return fail(VRS_EINVAL, "bad metric %d", (int)metric);
+  if (tau != tau) return fail(VRS_EINVAL, "tau is NaN");
+  if (capacity < 0) return fail(VRS_EINVAL, "capacity < 0");
+  const int rows_req = opts ? opts->rows : VRS_ROWS_AUTO;
+  if (rows_req < VRS_ROWS_AUTO || rows_req > VRS_ROWS_MASKED) return fail(VRS_EINVAL, "bad rows option");
+  const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
+  if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision option");
+  if (prec_req == VRS_PREC_BF16 && !ix->xb) return fail(VRS_EUNSUPPORTED, "the index has no bf16 shadow");
+  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;
+  PredDev pd;
+  vrs_status st = make_pred(ix, pred, &pd);
+  if (st != VRS_OK) return st;
+  if (metric == VRS_COSINE && ix->has_zero_row)
+    return fail(VRS_EDEGENERATE, "COSINE over a corpus with a zero-norm row");
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  if (!is_device_ptr(offsets)) return fail(VRS_EINVAL, "offsets must be a device pointer");
+  if (q == 0) {
+    *total = 0;
+    CUDA_TRY(cudaMemsetAsync(offsets, 0, 8, stream));
+    return VRS_OK;
+  }
+  if (!is_device_ptr(queries)) return fail(VRS_EINVAL, "queries must be a device pointer");
+  if (capacity > 0 && (!is_device_ptr(ids) || !is_device_ptr(dists)))
+    return fail(VRS_EINVAL, "ids / dists must be device pointers");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != ix->device) return fail(VRS_EINVAL, "current device %d differs from the index device %d", dev, ix->device);
+  const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
+  const int64_t n = ix->n;
+  GemmPlan gp{0, 0, 0};
+  if (tma_ok) gp = gemm_plan(q, d, n, 32, ix->num_sms);
+  if (!gp.ok)
+    return fail(VRS_EUNSUPPORTED, "range search runs on the tensor-core path: d %% 4 == 0 and 16-byte aligned rows");
+  const bool identity = (pd.n == 0);
+  const size_t nwords = (size_t)((n + 31) / 32);
+  const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
+  const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;
+  const int64_t gather_rows = rows_req == VRS_ROWS_GATHER ? n
+                              : q >= 1024                 ? n * 9 / 10
+                              : q >= 256                  ? n * 9 / 20
+                                                          : n / 3;
+  const int64_t xsel_cap = (!identity && rows_req != VRS_ROWS_MASKED)
+                               ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                               : 0;
+  const int L = 2 * gp.P;
+  Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
+                                      (size_t)(xsel_cap * row_bytes), use_bf16 ? qpad_bytes : 0, (size_t)q * 4,
+                                      (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4}));
+  if (st != VRS_OK) return st;
+  Carve cv(scr.ptr);
+  uint32_t *bitmap = cv.take<uint32_t>(nwords);
+  int32_t *sel_ids = identity ? nullptr : cv.take<int32_t>((size_t)n);
+  int64_t *count = cv.take<int64_t>(1);
+  void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
+  void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
+  void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
+  RangeState r;
+  r.gtau = cv.take<uint32_t>((size_t)q);
+  r.cand_cnt = cv.take<int32_t>((size_t)L * q);
+  r.coff = cv.take<int64_t>((size_t)L * q + 1);
+  r.kept = cv.take<int32_t>((size_t)q);
+  r.tau = tau;
+  r.xmax = ix->xmax;
+  // |<q,x>~ - <q,x>| <= gamma |q| |x|: operand rounding (bf16 RN 2^-9 each, TF32
+  // <= 2^-10 each) plus fp32 accumulation (d 2^-24), doubled for safety
+  r.gamma = use_bf16 ? 2.0 * (0x1p-8 + 0x1p-18 + d * 0x1p-23) : 2.0 * (0x1p-9 + 0x1p-20 + d * 0x1p-23);
+  r.offsets = offsets;
+  r.ids = ids;
+  r.dists = dists;
+  r.row_offset = ix->row_offset;
+  struct TcGuard {
+    TcLaunch *t;
+    ~TcGuard() { range_tc_free(t); }
+  } guard{range_tc_alloc()};
+  r.tc = guard.t;
+  int launches = 0;
+  if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
+  const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
+  GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
+             queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
+             use_bf16 ? 1 : 0, ix->xb, qb};
+  CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));
+  int64_t C = 0;
+  CUDA_TRY(cudaMemcpyAsync(&C, r.coff + (size_t)L * q, 8, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  Scratch scr2{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  st = scratch_alloc(scr2, carve_size({(size_t)C * 4, (size_t)C * 8, (size_t)C}));
+  if (st != VRS_OK) return st;
+  Carve cv2(scr2.ptr);
+  r.cand = cv2.take<int32_t>((size_t)C);
+  r.score = cv2.take<double>((size_t)C);
+  r.keep = cv2.take<uint8_t>((size_t)C);
+  CUDA_TRY(launch_range_fill(a, gp, r, stream, &launches));
+  int64_t R = 0;
+  CUDA_TRY(cudaMemcpyAsync(&R, offsets + q, 8, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  *total = R;
+  g_last_path = VRS_PATH_GEMM;
+  g_last_prec = use_bf16 ? VRS_PREC_BF16 : VRS_PREC_TF32;
+  if (R > capacity) {
+    g_last_launches = launches;
+    return fail(VRS_ERANGE, "%lld results > capacity %lld", (long long)R, (long long)capacity);
+  }
+  CUDA_TRY(launch_range_write(a, gp, r, stream, &launches));
+  g_last_launches = launches;
+  return VRS_OK;
 }
 
 vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,

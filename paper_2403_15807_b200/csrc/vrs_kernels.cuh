@@ -131,6 +131,31 @@ struct ThresholdArgs {
 };
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s);
 
+// gemm_range.cu -- range (threshold) selection on the tensor-core pass
+struct TcLaunch;   // tc_kernel.cuh
+struct RangeState {
+  TcLaunch *tc;            // from range_tc_alloc (tensor maps + parameters shared by the passes)
+  double tau;              // the caller's threshold (score >= tau; squared L2 <= tau)
+  double xmax;             // max row norm of the index
+  double gamma;            // tensor-core product error bound / (|q| |x|)
+  uint32_t *gtau;          // [q] key thresholds (ordered u32)
+  int32_t *cand_cnt;       // [2P][q] candidate counts
+  int64_t *coff;           // [q * 2P + 1] candidate segment offsets, query-major; coff[q*2P] = C
+  int32_t *cand;           // [C] candidate local row ids
+  double *score;           // [C] exact scores
+  uint8_t *keep;           // [C] 1 iff the exact score satisfies tau
+  int32_t *kept;           // [q]
+  int64_t *offsets;        // [q + 1] (the caller's) result offsets; offsets[q] = R
+  int64_t *ids;            // [capacity] (the caller's)
+  float *dists;
+  int64_t row_offset;
+};
+TcLaunch *range_tc_alloc();
+void range_tc_free(TcLaunch *t);
+cudaError_t launch_range_count(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
+cudaError_t launch_range_fill(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
+cudaError_t launch_range_write(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
+
 struct MergeArgs {
   const int64_t *cand_ids;
   const float *cand_dists;
