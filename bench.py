@@ -359,6 +359,28 @@ def main():
                          "path": "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan",
                          "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac": fl / t / 1e12 / tc_peak_sus})
 
+    # ---------------- range (threshold) mode, SURVEY 8(f) NEXT #1 (not part of the step)
+    range_out = []
+    if world == 1 and cfg.metric != datagen.L2:
+        s_all = cfg.sels[-1]
+        q_r = min(256, max(cfg.qs))
+        # the paper's threshold (cosine > 0.9) selects ~nothing on random
+        # data; a second tau keeps tens of rows per query (C2 unit vectors: 0.35 ~ 4 sigma)
+        for tau in (0.9, 0.35 if cfg.kind == "gauss_norm" else 0.9):
+            ix.range_search(Qall[:q_r], preds[s_all], tau=tau, metric=metric)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps = 5
+            for _ in range(reps):
+                off, rid, rdist = ix.range_search(Qall[:q_r], preds[s_all], tau=tau, metric=metric)
+            torch.cuda.synchronize()
+            t = (time.perf_counter() - t0) / reps
+            range_out.append({"tau": tau, "sel": s_all, "q": q_r, "ms": t * 1e3, "qps": q_r / t,
+                              "results_per_query": rid.numel() / q_r,
+                              "timing": "host wall clock (the call synchronises twice to size its output)"})
+            if cfg.kind != "gauss_norm":
+                break
+
     # ---------------- e2e through the public API with host buffers
     e2e = None
     h2d = sum(q * d * 4 for _, q in cells)
@@ -442,7 +464,7 @@ def main():
                 "dtype_note": "tensor-core selection operands (fp32 accumulate); returned dists re-scored in fp64 from fp32",
                 "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
-                "parity": parity, "cells": cell_out, "step_ms": [round(x, 4) for x in step_ms],
+                "parity": parity, "cells": cell_out, "range_search": range_out, "step_ms": [round(x, 4) for x in step_ms],
                 "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
         print(json.dumps(line), flush=True)
     if world > 1:
