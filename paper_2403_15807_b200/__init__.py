@@ -32,7 +32,12 @@ def _metric(m):
     return METRICS[m.lower()] if isinstance(m, str) else int(m)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream=None):
+    if stream is None and _raw_stream is not None:   # (no Stream object per call)
+        return ctypes.c_void_p(_raw_stream(torch.cuda.current_device()))
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
@@ -41,14 +46,21 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+_opt_cache = {}
+
+
 def _options(path, rows, precision=None):
     if path is None and rows is None and precision is None:
         return None
+    key = (path, rows, precision)
+    if key in _opt_cache:
+        return _opt_cache[key][1]
     o = _lib.SearchOptions()
     o.path = PATH_AUTO if path is None else int(path)
     o.rows = ROWS_AUTO if rows is None else int(rows)
     o.precision = PREC_DEFAULT if precision is None else int(precision)
-    return ctypes.byref(o)
+    _opt_cache[key] = (o, ctypes.byref(o))   # the struct stays alive with its reference
+    return _opt_cache[key][1]
 
 
 def last_path() -> int:

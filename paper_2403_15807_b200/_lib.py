@@ -114,11 +114,22 @@ def check(status: int, call: str):
         raise VrsError(status, call, msg)
 
 
+_pred_cache = {}
+
+
 def make_predicate(clauses):
-    """[(attr, lo, hi), ...] -> (Predicate, keepalive)."""
+    """[(attr, lo, hi), ...] -> (Predicate, keepalive); cached per clause tuple."""
+    try:
+        key = tuple((int(a), int(lo), int(hi)) for a, lo, hi in (clauses or []))
+    except (TypeError, ValueError):
+        key = None
+    if key is not None and key in _pred_cache:
+        return _pred_cache[key]
     clauses = list(clauses or [])
     arr = (Clause * max(len(clauses), 1))()
     for i, (a, lo, hi) in enumerate(clauses):
         arr[i].attr, arr[i].lo, arr[i].hi = int(a), int(lo), int(hi)
     pred = Predicate(len(clauses), ctypes.cast(arr, ctypes.POINTER(Clause)))
+    if key is not None and len(_pred_cache) < 1024:
+        _pred_cache[key] = (pred, arr)
     return pred, arr

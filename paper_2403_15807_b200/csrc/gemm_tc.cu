@@ -153,7 +153,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
   const bool bf = a.bf16 != 0;
   cudaError_t e = cudaSuccess;
-  if (bf) {   // queries -> bf16 (the corpus shadow was converted at load)
+  if (bf && !a.prepped) {   // queries -> bf16 (the corpus shadow was converted at load)
     e = launch_to_bf16(a.Q, a.Qb, a.q * a.d, (int64_t)plan.qtiles * tc::BM * a.d, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;

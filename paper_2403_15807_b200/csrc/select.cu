@@ -18,6 +18,8 @@
 //
 // Algorithmic bytes per row: sum of attribute widths read + 1/8 (bitmap) +
 // 4 * selectivity (ids).  HBM-bound.
+#include <cuda_bf16.h>
+
 #include "vrs_kernels.cuh"
 
 namespace vrs {
@@ -30,10 +32,18 @@ constexpr int kSelRows = kSelWords * 32;                 // 8192 rows per block
 
 __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred, int64_t n,
                                                                    uint32_t *__restrict__ bitmap,
-                                                                   uint32_t *__restrict__ chunk_count) {
+                                                                   uint32_t *__restrict__ chunk_count,
+                                                                   SelectFuse fz) {
   __shared__ uint32_t s_cnt[kSelWarps];
   pdl_wait();
   pdl_trigger();
+  if (fz.q_out) {   // folded in: this block's slice of the fp32 -> bf16 query conversion (zero padding)
+    const int64_t per = ((fz.q_total + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
+    const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(fz.q_total, e0 + per);
+    __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(fz.q_out);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += kSelThreads)
+      out[e] = __float2bfloat16_rn(e < fz.q_count ? fz.q_in[e] : 0.f);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kSelRows + (int64_t)warp * kSelWordsPerWarp * 32;
   // lane l owns row base + 32w + l for w = 0..31: per clause, all 32 column loads
@@ -136,10 +146,11 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, 
 // Host launcher.  Scratch: chunk counts uint32[nchunks].  ids may be nullptr
 // (bitmap + count only).
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
-                          void *scratch, cudaStream_t stream, int *launches) {
+                          void *scratch, cudaStream_t stream, int *launches, const SelectFuse *fuse) {
+  const SelectFuse fz = fuse ? *fuse : SelectFuse{};
   const uint32_t nchunks = (uint32_t)((n + kSelRows - 1) / kSelRows);
   uint32_t *chunk_count = static_cast<uint32_t *>(scratch);
-  cudaError_t e0 = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap, chunk_count);
+  cudaError_t e0 = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap, chunk_count, fz);
   if (e0 != cudaSuccess) return e0;
   if (launches) *launches += 1;
   cudaError_t e = cudaGetLastError();

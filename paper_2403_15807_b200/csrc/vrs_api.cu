@@ -241,6 +241,20 @@ static vrs_status make_pred(const vrs_index *ix, const vrs_predicate *pred, Pred
   return VRS_OK;
 }
 
+// The work the select kernels do for the tensor-core pass: bf16 query conversion
+// (zero-padded to whole 128-row tiles).
+static SelectFuse select_fuse(const vrs_index *ix, const float *queries, int64_t q, const GemmPlan &gp, bool bf16,
+                              void *qb) {
+  SelectFuse f{};
+  if (bf16) {
+    f.q_in = queries;
+    f.q_out = qb;
+    f.q_count = q * ix->d;
+    f.q_total = (int64_t)gp.qtiles * 128 * ix->d;
+  }
+  return f;
+}
+
 // ---- ABI ----------------------------------------------------------------------------
 extern "C" {
 
@@ -485,14 +499,15 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
   } else {
     // tensor-core path: gathered selection or bitmap-masked full tiles, chosen on the device
-    if (!identity) {
-      ProfScope ps("select", stream);
-      CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
-    }
     const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
+    if (!identity) {   // (the bf16 query conversion rides along)
+      ProfScope ps("select", stream);
+      const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
+      CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
+    }
     GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
-               use_bf16 ? 1 : 0, ix->xb, qb};
+               use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
     {
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
@@ -610,11 +625,14 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   } guard{range_tc_alloc()};
   r.tc = guard.t;
   int launches = 0;
-  if (!identity) CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches));
   const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
+  if (!identity) {
+    const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
+    CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
+  }
   GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
              queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
-             use_bf16 ? 1 : 0, ix->xb, qb};
+             use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));
   int64_t C = 0;
   CUDA_TRY(cudaMemcpyAsync(&C, r.coff + (size_t)L * q, 8, cudaMemcpyDeviceToHost, stream));

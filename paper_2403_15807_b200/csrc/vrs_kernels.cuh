@@ -21,9 +21,17 @@ struct ProfScope {
   ProfScope &operator=(const ProfScope &) = delete;
 };
 
-// select.cu -- K4'/K5'
+// select.cu -- K4'/K5'.  Optional work folded into the count kernel (saves a
+// launch on the tensor-core path): the bf16 conversion of the queries.  (Folding
+// the row gather into the 1-CTA-per-8192-rows scatter kernel was measured slower
+// than the separate gather_copy_kernel.)
+struct SelectFuse {
+  const float *q_in;       // fp32 queries (nullptr: no conversion)
+  void *q_out;             // bf16 [q_total]: q_count converted values, zero padding after
+  int64_t q_count, q_total;
+};
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
-                          void *scratch, cudaStream_t stream, int *launches);
+                          void *scratch, cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
 size_t select_scratch_bytes(int64_t n);
 
 // scan.cu -- K6' norms, K2' scan + fused top-k
@@ -79,6 +87,7 @@ struct GemmArgs {
   int32_t bf16;             // select on the bf16 shadow (kind::f16) instead of fp32 (kind::tf32)
   const void *Xb;           // bf16 shadow corpus [n x d] (bf16 only)
   void *Qb;                 // scratch [q x d] bf16 queries (bf16 only)
+  int32_t prepped;          // 1: the select kernels already converted the queries
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s);

@@ -57,6 +57,14 @@ if a.graph:
     e2.record()
     torch.cuda.synchronize()
     gms = s2.elapsed_time(e2) / 10
+# host-side cost of one search call (no sync: 40 calls stay within the launch queue)
+torch.cuda.synchronize()
+import time as _time
+t0 = _time.perf_counter()
+for _ in range(40):
+    ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None)
+host_us = (_time.perf_counter() - t0) / 40 * 1e6
+torch.cuda.synchronize()
 vrs.profile(True)
 vrs.profile_reset()
 for _ in range(3):
@@ -65,4 +73,4 @@ torch.cuda.synchronize()
 prof = vrs.profile_read()
 vrs.profile(False)
 ks = " ".join(f"{k}={v[0]/v[1]*1e3:.0f}us" for k, v in prof.items())
-print(f"cell {a.workload} sel={a.sel} q={a.q} prec={vrs.last_precision()}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, path={vrs.last_path()} | {ks}")
+print(f"cell {a.workload} sel={a.sel} q={a.q} prec={vrs.last_precision()}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, host {host_us:.1f} us/call, path={vrs.last_path()} | {ks}")
