@@ -476,9 +476,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
         // group bounds over 8-row groups (8 / RPL lanes each)
         static_assert(RPL <= 8 && 8 % RPL == 0, "8-row groups of whole lanes");
-        float bmx = bv[0], amx = av[0], amn = av[0];
+        // (without a per-row scale the third slot holds min b instead of min a: the
+        // probe's raw-dot fast path needs to know that a group's bias is uniformly 0)
+        float bmx = bv[0], amx = av[0], amn = ROWSCALE ? av[0] : bv[0];
 #pragma unroll
-        for (int k = 1; k < RPL; ++k) { bmx = fmaxf(bmx, bv[k]); amx = fmaxf(amx, av[k]); amn = fminf(amn, av[k]); }
+        for (int k = 1; k < RPL; ++k) {
+          bmx = fmaxf(bmx, bv[k]);
+          amx = fmaxf(amx, av[k]);
+          amn = fminf(amn, ROWSCALE ? av[k] : bv[k]);
+        }
 #pragma unroll
         for (int o = 1; o < 8 / RPL; o <<= 1) {
           bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
@@ -487,7 +493,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
         if ((lane & (8 / RPL - 1)) == 0) {
           g_bmax[s * GROUPS + lane / (8 / RPL)] = bmx;
-          if (ROWSCALE) { g_amax[s * GROUPS + lane / (8 / RPL)] = amx; g_amin[s * GROUPS + lane / (8 / RPL)] = amn; }
+          g_amin[s * GROUPS + lane / (8 / RPL)] = amn;
+          if (ROWSCALE) g_amax[s * GROUPS + lane / (8 / RPL)] = amx;
         }
         mbar_arrive(&bfull_bar[s]);
         fetch(t + PF, nv[u], iv[u], wv[u]);
@@ -548,6 +555,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     auto chunk = [&](uint32_t (&r)[32], const float *ba, const float *bb, const int32_t *rid, const float *gb,
                      const float *ga, const float *gn) {
       if (MODE == MODE_PROBE) {   // exact keys -> running slot maxima
+        if (!ROWSCALE && p.metric == VRS_IP) {
+          // inner product with every row of the chunk selected: key = dot exactly
+          const float4 bx = *reinterpret_cast<const float4 *>(gb), bn = *reinterpret_cast<const float4 *>(gn);
+          if (bx.x == 0.f && bx.y == 0.f && bx.z == 0.f && bx.w == 0.f && bn.x == 0.f && bn.y == 0.f && bn.z == 0.f &&
+              bn.w == 0.f) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) smax[i] = fmaxf(smax[i], __uint_as_float(r[i]));
+            return;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 b4 = *reinterpret_cast<const float4 *>(bb + i);
