@@ -432,13 +432,40 @@ __device__ double fin_qq(const FinalizeArgs &a, int64_t j) {
 }
 
 // Step 5 (one warp).
+// Bitonic sort of <= 32 (score, id) pairs held one per lane: best first (score
+// descending, then id ascending -- ids are unique, so the order is strict).
+__device__ __forceinline__ void warp_reg_sort_desc(double &key, int64_t &id) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      const double pk = __shfl_xor_sync(0xffffffffu, key, jj);
+      const int64_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
+      const bool partner_first = pk > key || (pk == key && pid < id);
+      const bool keep_first = ((lane & k) == 0) == ((lane & jj) == 0);   // this slot holds the better of the pair
+      if (keep_first == partner_first) { key = pk; id = pid; }
+    }
+  }
+}
+
 __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double qq, double *sc, int64_t *sid) {
   const int lane = threadIdx.x & 31;
-  int np = 1;
-  while (np < m) np <<= 1;
-  for (int c = m + lane; c < np; c += 32) { sc[c] = -INFINITY; sid[c] = INT64_MAX; }
-  __syncwarp();
-  if (m > 1) warp_sort_desc_d(sc, sid, np);
+  if (m <= 32) {   // registers: one candidate per lane
+    double key = lane < m ? sc[lane] : -INFINITY;
+    int64_t id = lane < m ? sid[lane] : INT64_MAX;
+    warp_reg_sort_desc(key, id);
+    __syncwarp();
+    sc[lane] = key;
+    sid[lane] = id;
+    __syncwarp();
+  } else {
+    int np = 1;
+    while (np < m) np <<= 1;
+    for (int c = m + lane; c < np; c += 32) { sc[c] = -INFINITY; sid[c] = INT64_MAX; }
+    __syncwarp();
+    warp_sort_desc_d(sc, sid, np);
+  }
   const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
   const int mv = zero_cos ? 0 : min(m, a.k);
   const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
@@ -529,7 +556,9 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
 // distinct row) -> gtau, a lower bound of the kth best key over all rows.  The
 // values are staged once in shared memory (ordered u32, 0 = no row) and a
 // block-wide radix select (8 bits per pass) finds the kth largest.
-constexpr int kThrThreads = 256;
+// (block size: 256 threads for large batches, 1024 for small ones -- few queries,
+// long value lists, so more threads per query)
+template <int kThrThreads>
 __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a) {
   extern __shared__ uint32_t s_val[];
   __shared__ uint32_t hist[256];
@@ -620,12 +649,14 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(threshold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(threshold_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(threshold_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  return launch_k(threshold_kernel, dim3((unsigned)a.q), dim3(kThrThreads), smem, s, a);
-  return cudaGetLastError();
+  if (a.q < kSmCountB200) return launch_k(threshold_kernel<1024>, dim3((unsigned)a.q), dim3(1024), smem, s, a);
+  return launch_k(threshold_kernel<256>, dim3((unsigned)a.q), dim3(256), smem, s, a);
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
