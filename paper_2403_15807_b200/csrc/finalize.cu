@@ -384,8 +384,10 @@ __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids
           } else {
             sc[u] += (double)qv.x * xv[u].x; sc[u] += (double)qv.y * xv[u].y;
             sc[u] += (double)qv.z * xv[u].z; sc[u] += (double)qv.w * xv[u].w;
-            xx[u] += (double)xv[u].x * xv[u].x; xx[u] += (double)xv[u].y * xv[u].y;
-            xx[u] += (double)xv[u].z * xv[u].z; xx[u] += (double)xv[u].w * xv[u].w;
+            if (a.metric == VRS_COSINE) {   // |x|^2 only for the cosine
+              xx[u] += (double)xv[u].x * xv[u].x; xx[u] += (double)xv[u].y * xv[u].y;
+              xx[u] += (double)xv[u].z * xv[u].z; xx[u] += (double)xv[u].w * xv[u].w;
+            }
           }
         }
       }
@@ -396,7 +398,7 @@ __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids
         for (int u = 0; u < U; ++u) {
           const double xv = __ldg(xr[u] + t);
           if (a.metric == VRS_L2) { const double df = qv - xv; sc[u] += df * df; }
-          else { sc[u] += qv * xv; xx[u] += xv * xv; }
+          else { sc[u] += qv * xv; if (a.metric == VRS_COSINE) xx[u] += xv * xv; }
         }
       }
     }
@@ -617,9 +619,11 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   if (tid == 0) a.gtau[j] = prefix;
 }
 
-// Large batches: one warp per query (values read straight from L2 / L1 in each
-// radix pass -- the block version's barriers dominated at 1152 values / query).
+// Large batches: one warp per query, the query's values staged once in the
+// warp's slice of shared memory (ordered u32, 0 = no row), radix passes without
+// block barriers (the block version's barriers dominate at ~1k values / query).
 __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(ThresholdArgs a) {
+  extern __shared__ uint32_t s_vals[];
   __shared__ uint32_t s_hist[kFinGroup][256];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
@@ -628,24 +632,37 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
   const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
+  uint32_t *mine = s_vals + (size_t)w * a.nvals;
+  for (int i = lane; i < nvals; i += 32) {
+    const float f = __ldg(v + i);
+    mine[i] = f > -INFINITY ? ordered_u32(f) : 0u;
+  }
+  __syncwarp();
   uint32_t x = 0;
   int above = 0;
   const bool ok = warp_kth_largest(
       [&](int i, uint32_t &u) {
-        const float f = __ldg(v + i);
-        u = ordered_u32(f);
-        return f > -INFINITY;
+        u = mine[i];
+        return u != 0u;
       },
       nvals, a.kth, s_hist[w], &x, &above);
   if (lane == 0) a.gtau[j] = ok ? x : 0u;
 }
 
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
-  // (a warp-per-query variant, threshold_warp_kernel, measured slower at Q = 4096: 68 vs 53 us)
-  static const bool warp_thr = getenv("VRS_WARP_THRESHOLD") != nullptr;
-  if (warp_thr)
+  // large batches with short value lists: a warp per query (A/B: VRS_BLOCK_THRESHOLD forces the block kernel)
+  static const bool block_thr = getenv("VRS_BLOCK_THRESHOLD") != nullptr;
+  const size_t wsmem = (size_t)kFinGroup * a.nvals * 4;
+  if (!block_thr && a.q >= 4 * kSmCountB200 && wsmem <= 96 * 1024) {
+    static size_t wattr = 0;
+    if (wsmem > 48 * 1024 && wsmem > wattr) {
+      cudaError_t e = cudaFuncSetAttribute(threshold_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+      if (e != cudaSuccess) return e;
+      wattr = wsmem;
+    }
     return launch_k(threshold_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32),
-                    0, s, a);
+                    wsmem, s, a);
+  }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
