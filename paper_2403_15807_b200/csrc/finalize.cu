@@ -279,6 +279,120 @@ __device__ __noinline__ uint32_t warp_keep_best(float *bk, int32_t *bi, int &n, 
   return v;
 }
 
+// Bitonic sort of 64 (key, id) pairs, two per lane (element lane and lane + 32):
+// best first (key descending, then id ascending).
+__device__ __forceinline__ bool pair_first(float ka, int32_t ia, float kb, int32_t ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+__device__ __forceinline__ void warp_reg_sort64(float &ka, int32_t &ia, float &kb, int32_t &ib) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj == 32) {   // partners are the lane's two elements; k == 64: one ascending block
+        if (pair_first(kb, ib, ka, ia)) {
+          const float tk = ka; ka = kb; kb = tk;
+          const int32_t ti = ia; ia = ib; ib = ti;
+        }
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float &key = h ? kb : ka;
+        int32_t &id = h ? ib : ia;
+        const int i = lane + 32 * h;
+        const float pk = __shfl_xor_sync(0xffffffffu, key, jj);
+        const int32_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
+        const bool partner_first = pair_first(pk, pid, key, id);
+        const bool keep_first = ((i & k) == 0) == ((i & jj) == 0);
+        if (keep_first == partner_first) { key = pk; id = pid; }
+      }
+    }
+  }
+}
+
+// Keep exactly the K best of the warp's buffer (K <= 64), usually in one
+// histogram pass: keys bucketed linearly over [min, max] (a monotone map), the
+// bucket holding the K-th best found from the top, every entry from that bucket
+// up collected (<= 64 of them in the common case) and sorted in registers.
+// Falls back to the radix select when the collected set is larger (ties, spikes).
+__device__ __noinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
+  const int lane = threadIdx.x & 31;
+  if (K > 64) return warp_keep_best(bk, bi, n, K, hist);
+  float lo = INFINITY, hi = -INFINITY;
+  for (int i = lane; i < n; i += 32) { lo = fminf(lo, bk[i]); hi = fmaxf(hi, bk[i]); }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const float range = hi - lo;
+  if (!(range > 0.f) || !(range < INFINITY)) return warp_keep_best(bk, bi, n, K, hist);
+  const float scale = 255.5f / range;
+  auto bucket = [&](float key) { return (uint32_t)min(255, (int)((key - lo) * scale)); };
+  for (int b = lane; b < 256; b += 32) hist[b] = 0;
+  __syncwarp();
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    hist_add_warp(hist, i < n ? bucket(bk[i]) : 256u);
+  }
+  __syncwarp();
+  // lane l owns buckets [255-8l-7, 255-8l]; find the bucket where the count from the top reaches K
+  uint32_t v[8], sum = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) { v[t] = hist[255 - 8 * lane - t]; sum += v[t]; }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int bstar = -1, upto = 0;   // upto: entries in buckets >= bstar
+  const uint32_t before = incl - sum;
+  if (before < (uint32_t)K && (uint32_t)K <= incl) {
+    uint32_t run = before;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (bstar < 0 && (uint32_t)K <= run + v[t]) { bstar = 255 - 8 * lane - t; upto = (int)(run + v[t]); }
+      if (bstar < 0) run += v[t];
+    }
+  }
+  const int src = __ffs(__ballot_sync(0xffffffffu, bstar >= 0)) - 1;
+  bstar = __shfl_sync(0xffffffffu, bstar, src);
+  upto = __shfl_sync(0xffffffffu, upto, src);
+  if (upto > 64) return warp_keep_best(bk, bi, n, K, hist);
+  // collect the candidates from bucket bstar up into the (no longer needed)
+  // histogram space, then two per lane into registers
+  float *ck = reinterpret_cast<float *>(hist);
+  int32_t *ci = reinterpret_cast<int32_t *>(hist + 64);
+  __syncwarp();
+  int got = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const bool take = i < n && (int)bucket(bk[i]) >= bstar;
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const int pos = got + __popc(m & lanemask_lt());
+      ck[pos] = bk[i];
+      ci[pos] = bi[i];
+    }
+    got += __popc(m);
+  }
+  __syncwarp();
+  float ka = lane < got ? ck[lane] : -INFINITY, kb2 = lane + 32 < got ? ck[lane + 32] : -INFINITY;
+  int32_t ia = lane < got ? ci[lane] : INT32_MAX, ib = lane + 32 < got ? ci[lane + 32] : INT32_MAX;
+  warp_reg_sort64(ka, ia, kb2, ib);
+  // the K best: elements 0..K-1 (element e sits in lane e & 31, slot e >> 5)
+  __syncwarp();
+  if (lane < K) { bk[lane] = ka; bi[lane] = ia; }
+  if (lane + 32 < K) { bk[lane + 32] = kb2; bi[lane + 32] = ib; }
+  __syncwarp();
+  n = K;
+  const float kth = __shfl_sync(0xffffffffu, K - 1 < 32 ? ka : kb2, (K - 1) & 31);
+  return ordered_u32(kth);
+}
+
 // ------------------------------------------------------------------ finalize
 // Per query: (1) a provable lower bound of the k'-th best ranking key (the
 // shared probe threshold, or for sorted scan lists the best of their k'-th
@@ -334,7 +448,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (m == 0) continue;
         if (n + __popc(m) > kBufCap) {
-          thr = max(thr, warp_keep_best(B.key, B.id, n, K, B.hist));
+          thr = max(thr, warp_keep_best_fast(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv[u]) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
         }
@@ -350,7 +464,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
     }
   }
   __syncwarp();
-  if (n > K) warp_keep_best(B.key, B.id, n, K, B.hist);
+  if (n > K) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
   return n;
 }
 
@@ -530,7 +644,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
         bool keep = i < nv && ordered_u32(kv) >= thr;
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (n + __popc(m) > kBufCap) {
-          thr = max(thr, warp_keep_best(B.key, B.id, n, K, B.hist));
+          thr = max(thr, warp_keep_best_fast(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
         }
@@ -543,7 +657,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
         __syncwarp();
       }
     }
-    if (n > K) warp_keep_best(B.key, B.id, n, K, B.hist);
+    if (n > K) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
     if (lane == 0) s_n[0] = n;
   }
   __syncthreads();

@@ -6,9 +6,23 @@ import re
 import sys
 
 
+OURS = ("select_count_kernel", "select_scatter_kernel", "gather_copy_kernel", "f32_to_bf16_kernel", "tc_topk_kernel",
+        "threshold_kernel", "threshold_warp_kernel", "finalize_warp_kernel", "finalize_cta_kernel", "scan_topk_kernel",
+        "merge_kernel", "norms_kernel", "range_threshold_kernel", "range_prefix_kernel", "range_verify_kernel",
+        "range_write_kernel")
+
+
 def short(name):
-    """libvrs kernels live in namespace vrs:: -> 'vrs::<kernel>'; anything else is torch / generation."""
-    mine = "vrs::" in name
+    """libvrs kernels (namespace vrs::, or their base names when ncu drops the namespace)
+    -> 'vrs::<kernel>[<template args>]'; anything else is torch / generation."""
+    base = re.sub(r"\(.*", "", name).replace("void ", "").strip()
+    mine = "vrs::" in name or any(base.split("<")[0].split("::")[-1] == k for k in OURS)
+    if mine and "tc_topk_kernel" in base:
+        # template args <AR, MODE, ROWSCALE, BF>: name the mode
+        m = re.search(r"<(\d+), (\d+), (\d+), (\d+)>", base)
+        if m:
+            mode = {"0": "main", "1": "probe", "2": "range-count", "3": "range-fill"}[m.group(2)]
+            return f"vrs::tc_topk_kernel[{mode}]"
     name = re.sub(r"\(.*", "", name)
     name = re.sub(r"<.*", "", name)
     name = name.split("::")[-1].strip()
