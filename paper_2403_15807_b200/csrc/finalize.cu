@@ -393,6 +393,87 @@ __device__ __noinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int
   return ordered_u32(kth);
 }
 
+// The K-th largest (K <= 64) of the nonzero ordered-u32 values v[0..n) (0 = no
+// value), warp-cooperative, usually in one histogram pass: values bucketed
+// linearly over [min, max] (monotone), the bucket holding the K-th largest found
+// from the top, everything from it up (<= 64) sorted in registers.  Falls back
+// to the radix select.  Returns false when fewer than K values exist.
+__device__ bool warp_kth_value_fast(const uint32_t *v, int n, int K, uint32_t *hist, uint32_t *out) {
+  const int lane = threadIdx.x & 31;
+  auto radix = [&]() {
+    int above = 0;
+    return warp_kth_largest([&](int i, uint32_t &u) { u = v[i]; return u != 0u; }, n, K, hist, out, &above);
+  };
+  if (K > 64) return radix();
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  int cnt = 0;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t u = v[i];
+    if (u) { lo = min(lo, u); hi = max(hi, u); ++cnt; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (cnt < K) return false;
+  if (hi == lo) { *out = hi; return true; }
+  const float scale = 255.5f / (float)(hi - lo);
+  auto bucket = [&](uint32_t u) { return (uint32_t)min(255, (int)((float)(u - lo) * scale)); };
+  for (int b = lane; b < 256; b += 32) hist[b] = 0;
+  __syncwarp();
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t u = i < n ? v[i] : 0u;
+    hist_add_warp(hist, u ? bucket(u) : 256u);
+  }
+  __syncwarp();
+  uint32_t c[8], sum = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) { c[t] = hist[255 - 8 * lane - t]; sum += c[t]; }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int bstar = -1, upto = 0;
+  const uint32_t before = incl - sum;
+  if (before < (uint32_t)K && (uint32_t)K <= incl) {
+    uint32_t run = before;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (bstar < 0 && (uint32_t)K <= run + c[t]) { bstar = 255 - 8 * lane - t; upto = (int)(run + c[t]); }
+      if (bstar < 0) run += c[t];
+    }
+  }
+  const int src = __ffs(__ballot_sync(0xffffffffu, bstar >= 0)) - 1;
+  bstar = __shfl_sync(0xffffffffu, bstar, src);
+  upto = __shfl_sync(0xffffffffu, upto, src);
+  if (upto > 64) return radix();
+  __syncwarp();
+  uint32_t *cv = hist;   // reuse: the collected values
+  int got = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t u = i < n ? v[i] : 0u;
+    const bool take = u != 0u && (int)bucket(u) >= bstar;
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    if (take) cv[got + __popc(m & lanemask_lt())] = u;
+    got += __popc(m);
+  }
+  __syncwarp();
+  // ordered u32 -> float keys for the shared register sort (ids: position, irrelevant)
+  auto to_f = [](uint32_t o) { return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o); };
+  float ka = lane < got ? to_f(cv[lane]) : -INFINITY, kb = lane + 32 < got ? to_f(cv[lane + 32]) : -INFINITY;
+  int32_t ia = lane, ib = lane + 32;
+  warp_reg_sort64(ka, ia, kb, ib);
+  const float kth = __shfl_sync(0xffffffffu, K - 1 < 32 ? ka : kb, (K - 1) & 31);
+  *out = ordered_u32(kth);
+  return true;
+}
+
 // ------------------------------------------------------------------ finalize
 // Per query: (1) a provable lower bound of the k'-th best ranking key (the
 // shared probe threshold, or for sorted scan lists the best of their k'-th
@@ -685,10 +766,83 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   pdl_wait();
   pdl_trigger();
   const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);   // lists of used splits only
+  __shared__ uint32_t s_lo[32], s_hi[32], s_cnt[32], s_cv[64];
+  __shared__ int s_bstar, s_upto, s_got;
+  // fast path: min / max, one histogram over value buckets, the <= 64 values
+  // from the K-th largest's bucket up sorted by warp 0 (else the radix passes)
+  uint32_t lo = 0xffffffffu, hi = 0u, cnt = 0;
   for (int i = tid; i < nvals; i += kThrThreads) {
     const float f = __ldg(v + i);
-    s_val[i] = f > -INFINITY ? ordered_u32(f) : 0u;
+    const uint32_t u = f > -INFINITY ? ordered_u32(f) : 0u;
+    s_val[i] = u;
+    if (u) { lo = min(lo, u); hi = max(hi, u); ++cnt; }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; s_cnt[warp] = cnt; }
+  for (int b = tid; b < 256; b += kThrThreads) hist[b] = 0;
+  if (tid == 0) s_got = 0;
+  __syncthreads();
+  lo = 0xffffffffu; hi = 0u; cnt = 0;
+  for (int w = 0; w < kThrThreads / 32; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); cnt += s_cnt[w]; }
+  if (cnt < (uint32_t)a.kth) {   // fewer than kth rows probed: no bound
+    if (tid == 0) a.gtau[j] = 0u;
+    return;
+  }
+  if (hi == lo || a.kth > 64) goto radix;
+  {
+    const float scale = 255.5f / (float)(hi - lo);
+    auto bucket = [&](uint32_t u) { return (uint32_t)min(255, (int)((float)(u - lo) * scale)); };
+    for (int i0 = 0; i0 < nvals; i0 += kThrThreads) {
+      const int i = i0 + tid;
+      const uint32_t u = i < nvals ? s_val[i] : 0u;
+      hist_add_warp(hist, u ? bucket(u) : 256u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c[8], sum = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { c[t] = hist[255 - 8 * lane - t]; sum += c[t]; }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t before = incl - sum;
+      if (before < (uint32_t)a.kth && (uint32_t)a.kth <= incl) {
+        uint32_t run = before;
+        for (int t = 0; t < 8; ++t) {
+          if ((uint32_t)a.kth <= run + c[t]) { s_bstar = 255 - 8 * lane - t; s_upto = (int)(run + c[t]); break; }
+          run += c[t];
+        }
+      }
+    }
+    __syncthreads();
+    const int bstar = s_bstar, upto = s_upto;
+    if (upto <= 64) {
+      for (int i = tid; i < nvals; i += kThrThreads) {
+        const uint32_t u = s_val[i];
+        if (u && (int)bucket(u) >= bstar) s_cv[atomicAdd(&s_got, 1)] = u;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int got = s_got;
+        auto to_f = [](uint32_t o) { return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o); };
+        float ka = lane < got ? to_f(s_cv[lane]) : -INFINITY, kb = lane + 32 < got ? to_f(s_cv[lane + 32]) : -INFINITY;
+        int32_t ia = lane, ib = lane + 32;
+        warp_reg_sort64(ka, ia, kb, ib);
+        const float kth = __shfl_sync(0xffffffffu, a.kth - 1 < 32 ? ka : kb, (a.kth - 1) & 31);
+        if (lane == 0) a.gtau[j] = ordered_u32(kth);
+      }
+      return;
+    }
+  }
+radix:
   uint32_t prefix = 0, mask = 0;
   int rem = a.kth;
   for (int shift = 24; shift >= 0; shift -= 8) {
@@ -753,13 +907,7 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   }
   __syncwarp();
   uint32_t x = 0;
-  int above = 0;
-  const bool ok = warp_kth_largest(
-      [&](int i, uint32_t &u) {
-        u = mine[i];
-        return u != 0u;
-      },
-      nvals, a.kth, s_hist[w], &x, &above);
+  const bool ok = warp_kth_value_fast(mine, nvals, a.kth, s_hist[w], &x);
   if (lane == 0) a.gtau[j] = ok ? x : 0u;
 }
 

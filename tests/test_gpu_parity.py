@@ -188,3 +188,24 @@ def test_search_host_end_to_end(vrs):
     ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
     ids, dists = ix.search_host(torch.from_numpy(Q).pin_memory(), [(0, 0, 499)], k=7, metric="ip")
     check_topk(ids.numpy(), dists.numpy(), X, attrs, [(0, 0, 499)], Q, 7, oracle.IP)
+
+
+@pytest.mark.parametrize("dups", [3, 200], ids=["few-dups", "many-dups"])
+@pytest.mark.parametrize("k", [10, 100], ids=["k10", "k100"])
+def test_exact_ties_go_to_lower_ids(vrs, dups, k):
+    """Duplicated rows score identically: the returned ids must be the oracle's
+    (lowest ids among the tied rows), through every selection stage (probe
+    threshold, list buffers, finalize's bucket / radix selection)."""
+    rng = np.random.default_rng(dups + k)
+    n, d = 30000, 128
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    src = rng.integers(0, n, 40)
+    for s in src:   # `dups` copies of 40 rows scattered over the corpus
+        X[rng.integers(0, n, dups)] = X[s]
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    Q = X[src[:6]] + 1e-3 * rng.standard_normal((6, d)).astype(np.float32)
+    for metric in (oracle.L2, oracle.IP):
+        gi, gd = _run(vrs, X, attrs, [(0, 0, 899)], Q, k, metric)
+        ri, rd, _ = oracle.search(X, attrs, [(0, 0, 899)], Q, k, metric)
+        assert (gi == ri).all()
+        assert np.allclose(gd, rd, rtol=1e-6)
