@@ -392,9 +392,12 @@ def main():
         qh = {q: Qh[:q].clone().pin_memory() for q in cfg.qs}
 
         def e2e_step():
+            # every cell's queries H2D, search, ids / dists D2H, all enqueued through the
+            # public host-buffer call (pinned buffers, host_async); one sync per step
             for c in cells:
                 s, q = c
-                ix.search_host(qh[q], preds[s], k=k, metric=metric, out=hbufs[c])
+                ix.search_host(qh[q], preds[s], k=k, metric=metric, out=hbufs[c], host_async=True)
+            torch.cuda.synchronize()
     else:
         hbufs = {c: (torch.empty(c[1], k, dtype=torch.int64, pin_memory=True),
                      torch.empty(c[1], k, dtype=torch.float32, pin_memory=True)) for c in cells}

@@ -175,7 +175,9 @@ typedef struct {
   int32_t path;      /* vrs_path */
   int32_t rows;      /* vrs_rows */
   int32_t precision; /* vrs_precision of the tensor-core selection (DEFAULT: bf16 if the index has the shadow) */
-  int32_t reserved[5];
+  int32_t host_async; /* vrs_search_host only: 1 = do not synchronise; the caller synchronises cuda_stream
+                         before reading h_ids / h_dists, and the host buffers must be pinned */
+  int32_t reserved[4];
 } vrs_search_options;
 
 /* vrs_search with explicit options (opts == NULL => defaults). */
@@ -186,8 +188,9 @@ VRS_API vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q,
 /*
  * vrs_search_host -- end-to-end call on HOST buffers: copies the queries
  * host->device, runs vrs_search_ex, copies ids/dists device->host, and
- * synchronises `cuda_stream` before returning.  h_queries / h_ids / h_dists
- * are host memory (pinned memory makes the copies asynchronous DMA).
+ * synchronises `cuda_stream` before returning (unless opts->host_async, then
+ * the caller synchronises).  h_queries / h_ids / h_dists are host memory
+ * (pinned memory makes the copies asynchronous DMA; required with host_async).
  */
 VRS_API vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,
                            const vrs_predicate *pred, int32_t k, vrs_metric metric, int64_t *h_ids,

@@ -49,16 +49,17 @@ def _ptr(t: torch.Tensor | None):
 _opt_cache = {}
 
 
-def _options(path, rows, precision=None):
-    if path is None and rows is None and precision is None:
+def _options(path, rows, precision=None, host_async=False):
+    if path is None and rows is None and precision is None and not host_async:
         return None
-    key = (path, rows, precision)
+    key = (path, rows, precision, bool(host_async))
     if key in _opt_cache:
         return _opt_cache[key][1]
     o = _lib.SearchOptions()
     o.path = PATH_AUTO if path is None else int(path)
     o.rows = ROWS_AUTO if rows is None else int(rows)
     o.precision = PREC_DEFAULT if precision is None else int(precision)
+    o.host_async = 1 if host_async else 0
     _opt_cache[key] = (o, ctypes.byref(o))   # the struct stays alive with its reference
     return _opt_cache[key][1]
 
@@ -158,8 +159,9 @@ class Index:
         return ids, dists
 
     def search_host(self, queries_h: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
-                    out=None, stream=None, precision=None):
-        """End-to-end call on host buffers (H2D + search + D2H inside libvrs; synchronous)."""
+                    out=None, stream=None, precision=None, host_async=False):
+        """End-to-end call on host buffers (H2D + search + D2H inside libvrs).  Synchronous,
+        unless host_async: then the caller synchronises the stream (pinned buffers)."""
         lib = library()
         q, d = queries_h.shape
         if out is None:
@@ -169,7 +171,8 @@ class Index:
             ids, dists = out
         pr, keep = _lib.make_predicate(pred)
         st = lib.vrs_search_host(self._h, _ptr(queries_h), q, d, ctypes.byref(pr), int(k), _metric(metric),
-                                 _ptr(ids), _ptr(dists), _options(path, rows, precision), _stream(stream))
+                                 _ptr(ids), _ptr(dists), _options(path, rows, precision, host_async),
+                                 _stream(stream))
         _lib.check(st, "vrs_search_host")
         return ids, dists
 

@@ -56,7 +56,7 @@ class Allocator(ctypes.Structure):
 
 class SearchOptions(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("rows", ctypes.c_int32), ("precision", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("host_async", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 class LoadOptions(ctypes.Structure):

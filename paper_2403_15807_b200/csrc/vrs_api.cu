@@ -683,7 +683,7 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
   if (st != VRS_OK) return st;
   CUDA_TRY(cudaMemcpyAsync(h_ids, di, ib, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaMemcpyAsync(h_dists, dd, db, cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (!(opts && opts->host_async)) CUDA_TRY(cudaStreamSynchronize(stream));
   return VRS_OK;
 }
 

@@ -188,6 +188,14 @@ def test_search_host_end_to_end(vrs):
     ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
     ids, dists = ix.search_host(torch.from_numpy(Q).pin_memory(), [(0, 0, 499)], k=7, metric="ip")
     check_topk(ids.numpy(), dists.numpy(), X, attrs, [(0, 0, 499)], Q, 7, oracle.IP)
+    # host_async: several calls enqueued back to back, one synchronisation
+    outs = []
+    for lo in (0, 100, 200):
+        outs.append(ix.search_host(torch.from_numpy(Q).pin_memory(), [(0, lo, lo + 399)], k=7, metric="ip",
+                                   host_async=True))
+    torch.cuda.synchronize()
+    for lo, (i2, d2) in zip((0, 100, 200), outs):
+        check_topk(i2.numpy(), d2.numpy(), X, attrs, [(0, lo, lo + 399)], Q, 7, oracle.IP)
 
 
 @pytest.mark.parametrize("dups", [3, 200], ids=["few-dups", "many-dups"])
