@@ -32,7 +32,16 @@ struct vrs_index {
   float *inv_nx;
   int32_t has_zero_row;
   float xmax;              // max row norm (range search error bound)
-  void *xb;                // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
+  void *xb;
+  // vrs_search_host staging: two device slots (queries in, ids / dists out) so
+  // that the upload of one call overlaps the compute of the previous one; the
+  // copies run on their own streams, ordered by events.
+  std::mutex host_mu;
+  cudaStream_t up_stream = nullptr, down_stream = nullptr;
+  void *slot_buf[2] = {nullptr, nullptr};
+  size_t slot_cap[2] = {0, 0};
+  cudaEvent_t slot_free[2] = {nullptr, nullptr}, up_done[2] = {nullptr, nullptr}, comp_done[2] = {nullptr, nullptr};
+  int slot_next = 0;                // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
   int32_t device;
   int32_t num_sms;
 };
@@ -373,6 +382,18 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
 
 vrs_status vrs_free(vrs_index *ix) {
   if (!ix) return VRS_OK;
+  if (ix->up_stream) {
+    cudaStreamSynchronize(ix->up_stream);
+    cudaStreamSynchronize(ix->down_stream);
+    for (int i = 0; i < 2; ++i) {
+      if (ix->slot_buf[i]) cudaFree(ix->slot_buf[i]);
+      cudaEventDestroy(ix->slot_free[i]);
+      cudaEventDestroy(ix->up_done[i]);
+      cudaEventDestroy(ix->comp_done[i]);
+    }
+    cudaStreamDestroy(ix->up_stream);
+    cudaStreamDestroy(ix->down_stream);
+  }
   if (ix->nx2) {
     if (ix->has_alloc) ix->alloc.free(ix->nx2, nullptr, ix->alloc.ctx);
     else cudaFree(ix->nx2);
@@ -670,19 +691,51 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
   if (!h_queries || !h_ids || !h_dists) return fail(VRS_EINVAL, "NULL host buffer");
   if (d != ix->d) return fail(VRS_EINVAL, "d = %d differs from the loaded d = %d", d, ix->d);
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  Scratch io{ix->has_alloc ? &ix->alloc : nullptr, stream};
+  std::lock_guard<std::mutex> guard(ix->host_mu);
+  if (!ix->up_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ix->up_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ix->down_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(cudaEventCreateWithFlags(&ix->slot_free[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&ix->up_done[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&ix->comp_done[i], cudaEventDisableTiming));
+    }
+  }
+  const int slot = ix->slot_next;
+  ix->slot_next ^= 1;
   const size_t qb = (size_t)q * d * 4, ib = (size_t)q * k * 8, db = (size_t)q * k * 4;
-  vrs_status st = scratch_alloc(io, carve_size({qb, ib, db}));
-  if (st != VRS_OK) return st;
-  Carve cv(io.ptr);
+  const size_t need = carve_size({qb, ib, db});
+  if (ix->slot_cap[slot] < need) {   // grow (rare): wait for the slot's last use, then reallocate
+    CUDA_TRY(cudaEventSynchronize(ix->slot_free[slot]));
+    if (ix->slot_buf[slot]) cudaFree(ix->slot_buf[slot]);
+    ix->slot_buf[slot] = nullptr;
+    ix->slot_cap[slot] = 0;
+    if (cudaMalloc(&ix->slot_buf[slot], need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(VRS_ENOMEM, "cudaMalloc(%zu) for the host-call staging failed", need);
+    }
+    ix->slot_cap[slot] = need;
+  }
+  Carve cv(ix->slot_buf[slot]);
   float *dq = cv.take<float>((size_t)q * d);
   int64_t *di = cv.take<int64_t>((size_t)q * k);
   float *dd = cv.take<float>((size_t)q * k);
-  CUDA_TRY(cudaMemcpyAsync(dq, h_queries, qb, cudaMemcpyHostToDevice, stream));
-  st = vrs_search_ex(ix, dq, q, d, pred, k, metric, di, dd, opts, cuda_stream);
+  // upload (its own stream, once the slot's previous results are downloaded)
+  CUDA_TRY(cudaStreamWaitEvent(ix->up_stream, ix->slot_free[slot], 0));
+  CUDA_TRY(cudaMemcpyAsync(dq, h_queries, qb, cudaMemcpyHostToDevice, ix->up_stream));
+  CUDA_TRY(cudaEventRecord(ix->up_done[slot], ix->up_stream));
+  // search on the caller's stream
+  CUDA_TRY(cudaStreamWaitEvent(stream, ix->up_done[slot], 0));
+  vrs_status st = vrs_search_ex(ix, dq, q, d, pred, k, metric, di, dd, opts, cuda_stream);
   if (st != VRS_OK) return st;
-  CUDA_TRY(cudaMemcpyAsync(h_ids, di, ib, cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaMemcpyAsync(h_dists, dd, db, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaEventRecord(ix->comp_done[slot], stream));
+  // download (its own stream), then the caller's stream waits for it so that
+  // synchronising the caller's stream covers the host results
+  CUDA_TRY(cudaStreamWaitEvent(ix->down_stream, ix->comp_done[slot], 0));
+  CUDA_TRY(cudaMemcpyAsync(h_ids, di, ib, cudaMemcpyDeviceToHost, ix->down_stream));
+  CUDA_TRY(cudaMemcpyAsync(h_dists, dd, db, cudaMemcpyDeviceToHost, ix->down_stream));
+  CUDA_TRY(cudaEventRecord(ix->slot_free[slot], ix->down_stream));
+  CUDA_TRY(cudaStreamWaitEvent(stream, ix->slot_free[slot], 0));
   if (!(opts && opts->host_async)) CUDA_TRY(cudaStreamSynchronize(stream));
   return VRS_OK;
 }

@@ -65,6 +65,19 @@ for _ in range(40):
     ix.search(Q, pred, k=cfg.k, metric=cfg.metric, path=a.path or None, rows=a.rows or None, precision=a.prec or None)
 host_us = (_time.perf_counter() - t0) / 40 * 1e6
 torch.cuda.synchronize()
+# e2e on host buffers (public call, host_async, pinned): per-call device time incl. H2D / D2H
+Qh = Q.cpu().pin_memory()
+hid = torch.empty(a.q, cfg.k, dtype=torch.int64, pin_memory=True)
+hdi = torch.empty(a.q, cfg.k, dtype=torch.float32, pin_memory=True)
+ix.search_host(Qh, pred, k=cfg.k, metric=cfg.metric, out=(hid, hdi), host_async=True)
+torch.cuda.synchronize()
+s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s3.record()
+for _ in range(10):
+    ix.search_host(Qh, pred, k=cfg.k, metric=cfg.metric, out=(hid, hdi), host_async=True)
+e3.record()
+torch.cuda.synchronize()
+e2e_ms = s3.elapsed_time(e3) / 10
 vrs.profile(True)
 vrs.profile_reset()
 for _ in range(3):
@@ -73,4 +86,4 @@ torch.cuda.synchronize()
 prof = vrs.profile_read()
 vrs.profile(False)
 ks = " ".join(f"{k}={v[0]/v[1]*1e3:.0f}us" for k, v in prof.items())
-print(f"cell {a.workload} sel={a.sel} q={a.q} prec={vrs.last_precision()}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, host {host_us:.1f} us/call, path={vrs.last_path()} | {ks}")
+print(f"cell {a.workload} sel={a.sel} q={a.q} prec={vrs.last_precision()}: {s.elapsed_time(e)/3:.3f} ms/search, graph {gms:.3f} ms, host {host_us:.1f} us/call, e2e {e2e_ms:.3f} ms, path={vrs.last_path()} | {ks}")
