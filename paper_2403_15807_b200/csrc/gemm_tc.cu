@@ -183,6 +183,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.kp = kp_of(a.kprime);
   p.cap = p.kp * tc::CAP_FACTOR;
   p.tile_step = 1;
+  p.min_span = tc_min_span();
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
   static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
   p.epi_skip = epi_skip ? 1 : 0;
@@ -229,7 +230,7 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     e = tc_launch_mode<MODE_PROBE>(L, pp, s);
     if (e != cudaSuccess) return e;
     ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
-                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, p.xsel_cap, tc::BN}};
+                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, p.xsel_cap, tc::BN, p.min_span}};
     ProfScope pt("gemm.threshold", s);
     e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;
@@ -255,7 +256,7 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
   l.stride = kp_of(a.kprime) * tc::CAP_FACTOR;
   l.gtau = gs.gtau;
   l.split = SplitInfo{a.ids, a.count, a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1), plan.P, a.n,
-                      a.ids ? a.xsel_cap : 0, tc::BN};
+                      a.ids ? a.xsel_cap : 0, tc::BN, tc_min_span()};
   return l;
 }
 

@@ -169,6 +169,7 @@ struct TcParams {
   int32_t qtiles;
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
+  int32_t min_span;        // used splits span >= this many row tiles (splits_used)
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
   const float *inv_nx;
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int64_t row_tiles = (n_space + BN - 1) / BN;
   // splits actually used (splits_used): >= 4 row tiles per item when the
   // (device-side) row space allows; CTAs of unused splits publish empty lists
-  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / 4));
+  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / p.min_span));
   const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
   const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
   const int64_t span = t_end - t_begin;
@@ -694,6 +695,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
   }
+}
+
+// Minimum row tiles per used split (VRS_MIN_SPAN overrides; default 4).
+static int tc_min_span() {
+  static const int v = getenv("VRS_MIN_SPAN") ? std::max(1, atoi(getenv("VRS_MIN_SPAN"))) : 4;
+  return v;
 }
 
 // ---------------------------------------------------------------- launch plumbing

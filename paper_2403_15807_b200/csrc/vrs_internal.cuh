@@ -121,6 +121,7 @@ struct SplitInfo {
   int64_t n_rows;
   int64_t xsel_cap;
   int32_t bn;              // rows per tile
+  int32_t min_span;        // >= this many row tiles per used split
 };
 __device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t cap) {
   return ids != nullptr && allow != 0 && n_sel <= cap;
@@ -130,7 +131,7 @@ __device__ __forceinline__ int64_t splits_used(const SplitInfo &si) {
   const int64_t n_sel = si.ids ? *si.count : si.n_rows;
   const int64_t n_space = gather_mode(si.ids, si.allow_gather, n_sel, si.xsel_cap) ? n_sel : si.n_rows;
   const int64_t row_tiles = (n_space + si.bn - 1) / si.bn;
-  const int64_t p = row_tiles / 4 < si.P ? row_tiles / 4 : si.P;
+  const int64_t p = row_tiles / si.min_span < si.P ? row_tiles / si.min_span : si.P;
   return p > 1 ? p : 1;
 }
 
