@@ -487,15 +487,18 @@ __device__ bool warp_kth_value_fast(const uint32_t *v, int n, int K, uint32_t *h
 // per-warp survivors merged by warp 0) so small batches are not latency-bound.
 constexpr int kFinGroup = 4;   // queries per CTA when W == 1
 
-struct FinBufs {
-  float key[kBufCap];
-  int32_t id[kBufCap];
+template <int CAP>
+struct FinBufsT {
+  float key[CAP];
+  int32_t id[CAP];
   uint32_t hist[256];
 };
+using FinBufs = FinBufsT<kBufCap>;
 
 // Steps 1-2 for one warp over lists l = first, first + step, ... (in groups of
 // 32): the warp's buffer ends with at most K entries (or all it saw).
-__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufs &B) {
+template <int CAP>
+__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP> &B) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
   const int lists = a.split.bn ? (int)min((int64_t)a.lists, 2 * splits_used(a.split)) : a.lists;
@@ -528,7 +531,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
         bool keep = iv[u] >= 0 && ordered_u32(kv[u]) >= thr;
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (m == 0) continue;
-        if (n + __popc(m) > kBufCap) {
+        if (n + __popc(m) > CAP) {
           thr = max(thr, warp_keep_best_fast(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv[u]) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
@@ -679,10 +682,14 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
   }
 }
 
+// (CAP: candidate buffer per warp, >= 2 k'; SEL: re-scored rows per warp, >= k'.
+// The k' <= 64 variant needs 4 KB of shared memory per warp instead of 9 KB, so
+// a 4096-query batch runs in one wave.)
+template <int CAP, int SEL>
 __global__ void __launch_bounds__(kFinGroup * 32) finalize_warp_kernel(FinalizeArgs a) {
-  __shared__ FinBufs s_buf[kFinGroup];
-  __shared__ double s_sc[kFinGroup][kFinMaxSel];
-  __shared__ int64_t s_sid[kFinGroup][kFinMaxSel];
+  __shared__ FinBufsT<CAP> s_buf[kFinGroup];
+  __shared__ double s_sc[kFinGroup][SEL];
+  __shared__ int64_t s_sid[kFinGroup][SEL];
   const int w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
   pdl_wait();
@@ -887,9 +894,13 @@ radix:
   if (tid == 0) a.gtau[j] = prefix;
 }
 
-// Large batches: one warp per query, the query's values staged once in the
-// warp's slice of shared memory (ordered u32, 0 = no row), radix passes without
-// block barriers (the block version's barriers dominate at ~1k values / query).
+// Large batches: one warp per query, registers only.  Each lane keeps the two
+// largest of its values (slot `lane` of every list); the K-th largest of that
+// union of 64 values is <= the K-th largest of all values (a subset's K-th
+// largest never exceeds the whole set's), so it is still a valid lower bound of
+// the K-th best key -- a slightly looser one when a lane holds more than two of
+// the top K.  Exact when every lane holds <= 2 values.
+// K > 64 stages the values in shared memory for the radix select.
 __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(ThresholdArgs a) {
   extern __shared__ uint32_t s_vals[];
   __shared__ uint32_t s_hist[kFinGroup][256];
@@ -900,21 +911,43 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
   const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
-  uint32_t *mine = s_vals + (size_t)w * a.nvals;
-  for (int i = lane; i < nvals; i += 32) {
-    const float f = __ldg(v + i);
-    mine[i] = f > -INFINITY ? ordered_u32(f) : 0u;
+  if (a.kth > 64) {
+    uint32_t *mine = s_vals + (size_t)w * a.nvals;
+    for (int i = lane; i < nvals; i += 32) {
+      const float f = __ldg(v + i);
+      mine[i] = f > -INFINITY ? ordered_u32(f) : 0u;
+    }
+    __syncwarp();
+    uint32_t x = 0;
+    const bool ok = warp_kth_value_fast(mine, nvals, a.kth, s_hist[w], &x);
+    if (lane == 0) a.gtau[j] = ok ? x : 0u;
+    return;
   }
-  __syncwarp();
-  uint32_t x = 0;
-  const bool ok = warp_kth_value_fast(mine, nvals, a.kth, s_hist[w], &x);
-  if (lane == 0) a.gtau[j] = ok ? x : 0u;
+  float t0 = -INFINITY, t1 = -INFINITY;   // this lane's two largest (t0 >= t1)
+  int i = lane;
+  for (; i + 96 < nvals; i += 128) {
+    float f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) f[u] = __ldg(v + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { t1 = fmaxf(t1, fminf(t0, f[u])); t0 = fmaxf(t0, f[u]); }
+  }
+  for (; i < nvals; i += 32) {
+    const float f = __ldg(v + i);
+    t1 = fmaxf(t1, fminf(t0, f));
+    t0 = fmaxf(t0, f);
+  }
+  const int have = __popc(__ballot_sync(0xffffffffu, t0 > -INFINITY)) + __popc(__ballot_sync(0xffffffffu, t1 > -INFINITY));
+  int32_t ia = lane, ib = lane + 32;
+  warp_reg_sort64(t0, ia, t1, ib);
+  const float kth = __shfl_sync(0xffffffffu, a.kth - 1 < 32 ? t0 : t1, (a.kth - 1) & 31);
+  if (lane == 0) a.gtau[j] = have >= a.kth ? ordered_u32(kth) : 0u;
 }
 
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   // large batches with short value lists: a warp per query (A/B: VRS_BLOCK_THRESHOLD forces the block kernel)
   static const bool block_thr = getenv("VRS_BLOCK_THRESHOLD") != nullptr;
-  const size_t wsmem = (size_t)kFinGroup * a.nvals * 4;
+  const size_t wsmem = a.kth > 64 ? (size_t)kFinGroup * a.nvals * 4 : 0;
   if (!block_thr && a.q >= 4 * kSmCountB200 && wsmem <= 96 * 1024) {
     static size_t wattr = 0;
     if (wsmem > 48 * 1024 && wsmem > wattr) {
@@ -942,8 +975,9 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
   if (a.q < 4 * kSmCountB200) return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), 0, s, a);
-  return launch_k(finalize_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32), 0,
-                  s, a);
+  const dim3 grid((unsigned)((a.q + kFinGroup - 1) / kFinGroup));
+  if (a.kprime <= 64) return launch_k(finalize_warp_kernel<256, 64>, grid, dim3(kFinGroup * 32), 0, s, a);
+  return launch_k(finalize_warp_kernel<kBufCap, kFinMaxSel>, grid, dim3(kFinGroup * 32), 0, s, a);
   return cudaGetLastError();
 }
 

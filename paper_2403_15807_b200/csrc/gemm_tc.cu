@@ -47,7 +47,9 @@ namespace vrs {
 __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict__ X, int32_t row_bytes,
                                                           const int32_t *__restrict__ ids,
                                                           const int64_t *__restrict__ count, int64_t n, int allow,
-                                                          int64_t cap, void *__restrict__ xsel) {
+                                                          int64_t cap, void *__restrict__ xsel,
+                                                          const float *__restrict__ norm_src,
+                                                          float *__restrict__ norm_dst) {
   pdl_wait();
   pdl_trigger();
   const int64_t n_sel = *count;
@@ -62,6 +64,9 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
     const int4 *src = reinterpret_cast<const int4 *>(static_cast<const char *>(X) + (int64_t)__ldg(ids + r) * row_bytes);
     reinterpret_cast<int4 *>(static_cast<char *>(xsel) + r * row_bytes)[v] = __ldg(src + v);
   }
+  if (norm_dst)   // the rows' norm terms, contiguous, for the bias producer
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_sel; r += stride)
+      norm_dst[r] = __ldg(norm_src + __ldg(ids + r));
 }
 
 // fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per
@@ -176,6 +181,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.count = a.count;
   p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
   p.xsel_cap = xcap;
+  p.xsel_norm = a.xsel_norm;
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
   p.inv_nx = a.inv_nx;
@@ -183,6 +189,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.kp = kp_of(a.kprime);
   p.cap = p.kp * tc::CAP_FACTOR;
   p.tile_step = 1;
+  p.probe_div = 0;
   p.min_span = tc_min_span();
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
   static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
@@ -193,7 +200,8 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   if (xcap > 0 && p.allow_gather) {
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
-                 (int)p.allow_gather, xcap, a.xsel);
+                 (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
+                 a.metric == VRS_IP ? (float *)nullptr : a.xsel_norm);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
@@ -227,6 +235,9 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // (C2 measurements: 1/8 best at Q = 4096, 1/16 at Q = 256, 1/32 at Q = 16)
     static const int probe_env = getenv("VRS_PROBE_STEP") ? atoi(getenv("VRS_PROBE_STEP")) : 0;
     pp.tile_step = probe_env > 0 ? probe_env : (a.q >= 1024 ? 8 : (a.q >= 64 ? tc::PROBE_STEP : 32));
+    // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
+    static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
+    pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 ? 8 : 0);
     e = tc_launch_mode<MODE_PROBE>(L, pp, s);
     if (e != cudaSuccess) return e;
     ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,

@@ -169,6 +169,7 @@ struct TcParams {
   int32_t qtiles;
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
+  int32_t probe_div;       // probe: > 0 => step = clamp(span / probe_div, 2, tile_step) (device-side span)
   int32_t min_span;        // used splits span >= this many row tiles (splits_used)
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
@@ -182,6 +183,7 @@ struct TcParams {
   const int64_t *coff;     // RFILL: [q][2P] start of each (query, list) segment in cand_id
   float *probe_max;        // [q][2P][SLOTS] probe slot maxima
   int64_t xsel_cap;        // rows of the materialised-selection buffer
+  const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
   int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
@@ -339,8 +341,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
   const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
   const int64_t span = t_end - t_begin;
-  // probe: every tile_step-th tile of the item (the first tile of a shorter item)
-  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(p.tile_step, std::max<int64_t>(1, span)) : 1;
+  // probe: every step-th tile of the item (the first tile of a shorter item).  With
+  // probe_div, short items (small selections) probe densely: their main pass is
+  // slow-path bound, so a tighter threshold pays more than the denser probe costs
+  int64_t step_cap = p.tile_step;
+  if (p.probe_div > 0) step_cap = std::min<int64_t>(step_cap, std::max<int64_t>(2, span / p.probe_div));
+  const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(step_cap, std::max<int64_t>(1, span)) : 1;
   const int ntiles = (int)((span + step - 1) / step);
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
@@ -402,7 +408,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // Loads for tile t + PF are issued before tile t is written out: the warp is
     // memory-latency bound otherwise (one ~us round trip per tile).
     constexpr int PF = 2;
-    const float *src = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;
+    // norm terms: L2 |x|^2, COS 1/|x|; the inner product needs none (no loads).  Gathered
+    // rows read them contiguously from the gather's norm copy (no dependent load).
+    const bool need_norm = p.metric != VRS_IP;
+    const float *src = gather ? p.xsel_norm : (p.metric == VRS_L2 ? p.nx2 : p.inv_nx);
     constexpr int RPL = BN / 32;   // rows per lane
     float nv[PF][RPL];
     int32_t iv[PF][RPL];
@@ -421,13 +430,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
           for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
         }
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) n8[u] = i8[u] >= 0 ? __ldg(src + i8[u]) : 0.f;
-        w = 0xffffffffu;
-      } else {
-        w = 0xffffffffu;
-        if (p.bitmap && pos0 < p.n_rows) w = __ldg(p.bitmap + (pos0 >> 5));
-        if (pos0 + RPL <= p.n_rows) {
+        if (need_norm && pos0 + RPL <= n_sel) {
 #pragma unroll
           for (int v = 0; v < RPL / 4; ++v) {
             const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + v);
@@ -435,7 +438,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < RPL; ++u) n8[u] = pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
+          for (int u = 0; u < RPL; ++u) n8[u] = need_norm && pos0 + u < n_sel ? __ldg(src + pos0 + u) : 0.f;
+        }
+        w = 0xffffffffu;
+      } else {
+        w = 0xffffffffu;
+        if (p.bitmap && pos0 < p.n_rows) w = __ldg(p.bitmap + (pos0 >> 5));
+        if (need_norm && pos0 + RPL <= p.n_rows) {
+#pragma unroll
+          for (int v = 0; v < RPL / 4; ++v) {
+            const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + v);
+            n8[4 * v] = v0.x; n8[4 * v + 1] = v0.y; n8[4 * v + 2] = v0.z; n8[4 * v + 3] = v0.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) n8[u] = need_norm && pos0 + u < p.n_rows ? __ldg(src + pos0 + u) : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < p.n_rows ? (int32_t)(pos0 + u) : -1;

@@ -492,7 +492,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
-                                   (size_t)(xsel_cap * row_bytes), use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
+                                   (size_t)(xsel_cap * row_bytes), (size_t)xsel_cap * 4,
+                                   use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -504,6 +505,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
   void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
+  float *xsel_norm = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap) : nullptr;
   void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
 
   int launches = 0;
@@ -526,7 +528,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
       const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
       CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
     }
-    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
+    GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
                use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
     {
@@ -616,7 +618,8 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const int L = 2 * gp.P;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
   st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
-                                      (size_t)(xsel_cap * row_bytes), use_bf16 ? qpad_bytes : 0, (size_t)q * 4,
+                                      (size_t)(xsel_cap * row_bytes), (size_t)xsel_cap * 4, use_bf16 ? qpad_bytes : 0,
+                                      (size_t)q * 4,
                                       (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4}));
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -625,6 +628,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int64_t *count = cv.take<int64_t>(1);
   void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
   void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
+  float *xsel_norm = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap) : nullptr;
   void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
   RangeState r;
   r.gtau = cv.take<uint32_t>((size_t)q);
@@ -651,7 +655,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
     const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
     CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
   }
-  GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap,
+  GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
              queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
              use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));

@@ -75,6 +75,7 @@ struct GemmArgs {
   int32_t masked;           // 0 auto (device-side selectivity switch), 1 force masked, 2 force gathered
   void *xsel;               // materialised-selection buffer [xsel_cap x d] fp32 / bf16 (gathered mode)
   int64_t xsel_cap;
+  float *xsel_norm;         // [xsel_cap] the gathered rows' norm terms
   const float *Q;
   int64_t q;
   const float *nx2;
