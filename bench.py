@@ -240,15 +240,18 @@ def main():
         _, cnt, _ = ix.select(preds[s])
         nsel[s] = int(cnt.item())
 
+    # clock sampler first, then the warm-up: the timed steps follow the warm-up
+    # without an idle gap (an idle GPU drops its clocks; the first timed step
+    # would pay for the ramp)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     barrier()
 
     # ---------------- timed region
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()

@@ -552,8 +552,26 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
   return n;
 }
 
+// Sums of 8 per-lane values over the warp: on return every lane holds the total
+// of value (lane >> 2) & 7.  Each step swaps half of the remaining values with
+// the partner lane (xor 16, 8, 4), then a plain butterfly over lane bits 0-1.
+__device__ __forceinline__ double warp_sum8_transpose(const double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double w[4], x[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) x[i] = (b3 ? w[i + 2] : w[i]) + __shfl_xor_sync(0xffffffffu, b3 ? w[i] : w[i + 2], 8);
+  double y = (b2 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
+
 // Step 4 for candidates c0, c0 + cstep*U ... of ids[0..m): the warp reads each
-// row coalesced, U rows in flight, fp64 accumulation, one butterfly per row.
+// row coalesced, U rows in flight, fp64 accumulation, one transposing reduction
+// per U rows.
 __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids, int m, int cfirst, int cstep,
                             double qq, double *sc_out, int64_t *sid_out) {
   const int lane = threadIdx.x & 31;
@@ -600,21 +618,18 @@ __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
-        if (a.metric == VRS_COSINE) xx[u] += __shfl_xor_sync(0xffffffffu, xx[u], o);
-      }
-      const int c = c0 + u;
-      if (lane == u && c < m) {
-        double v = sc[u];
-        if (a.metric == VRS_L2) v = -v;   // sort key: larger is better
-        else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xx[u]));
-        sc_out[c] = v;
-        sid_out[c] = ids[c];
-      }
+    // the U = 8 per-lane partial sums -> row (lane >> 2) & 7's total on every lane,
+    // by a transposing butterfly (9 exchanges instead of 8 x 5)
+    const double tot = warp_sum8_transpose(sc);
+    const double xtot = a.metric == VRS_COSINE ? warp_sum8_transpose(xx) : 0.0;
+    const int u = (lane >> 2) & 7;
+    const int c = c0 + u;
+    if ((lane & 3) == 0 && c < m) {
+      double v = tot;
+      if (a.metric == VRS_L2) v = -v;   // sort key: larger is better
+      else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xtot));
+      sc_out[c] = v;
+      sid_out[c] = ids[c];
     }
   }
 }

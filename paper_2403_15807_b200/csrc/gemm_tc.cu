@@ -106,8 +106,14 @@ static int kp_of(int32_t kprime) {
   return kp;
 }
 
+// Splits that keep the SMs busy on small row spaces (VRS_NO_MIN_P=1: off, for A/B).
+static int32_t tc_min_p(const GemmPlan &plan) {
+  static const bool off = getenv("VRS_NO_MIN_P") != nullptr;
+  return off ? 1 : plan.min_p;
+}
+
 GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms) {
-  GemmPlan g{0, 0, 0};
+  GemmPlan g{0, 0, 0, 1};
   if (d % 4 != 0 || d < 4 || q < 1 || n_upper < 1 || kprime > 256) return g;
   if (!encode_fn()) return g;
   const int64_t qtiles = (q + tc::BM - 1) / tc::BM;
@@ -120,6 +126,9 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
   g.P = (int32_t)P;
   g.qtiles = (int32_t)qtiles;
   g.ok = 1;
+  // (small row spaces: splits of a single tile rather than idle SMs -- C2 Q = 4096, s = 0.1 %:
+  // 975 rows = 4 tiles would otherwise run on 32 CTAs)
+  g.min_p = (int32_t)std::max<int64_t>(1, ((int64_t)num_sms + qtiles - 1) / qtiles);
   return g;
 }
 
@@ -191,6 +200,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.tile_step = 1;
   p.probe_div = 0;
   p.min_span = tc_min_span();
+  p.min_p = tc_min_p(plan);
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
   static const bool epi_skip = getenv("VRS_EPI_SKIP") != nullptr;
   p.epi_skip = epi_skip ? 1 : 0;
@@ -241,7 +251,7 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     e = tc_launch_mode<MODE_PROBE>(L, pp, s);
     if (e != cudaSuccess) return e;
     ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
-                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, p.xsel_cap, tc::BN, p.min_span}};
+                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, p.xsel_cap, tc::BN, p.min_span, p.min_p}};
     ProfScope pt("gemm.threshold", s);
     e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;
@@ -267,7 +277,7 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
   l.stride = kp_of(a.kprime) * tc::CAP_FACTOR;
   l.gtau = gs.gtau;
   l.split = SplitInfo{a.ids, a.count, a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1), plan.P, a.n,
-                      a.ids ? a.xsel_cap : 0, tc::BN, tc_min_span()};
+                      a.ids ? a.xsel_cap : 0, tc::BN, tc_min_span(), tc_min_p(plan)};
   return l;
 }
 

@@ -170,7 +170,8 @@ struct TcParams {
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
   int32_t probe_div;       // probe: > 0 => step = clamp(span / probe_div, 2, tile_step) (device-side span)
-  int32_t min_span;        // used splits span >= this many row tiles (splits_used)
+  int32_t min_span;        // used splits span >= this many row tiles (splits_used) ...
+  int32_t min_p;           // ... unless that leaves fewer than min_p splits
   const uint32_t *bitmap;  // nullptr => every row qualifies
   const float *nx2;
   const float *inv_nx;
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int64_t row_tiles = (n_space + BN - 1) / BN;
   // splits actually used (splits_used): >= 4 row tiles per item when the
   // (device-side) row space allows; CTAs of unused splits publish empty lists
-  const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(p.P, row_tiles / p.min_span));
+  const int64_t p_eff = used_splits(row_tiles, p.P, p.min_span, p.min_p);
   const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
   const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
   const int64_t span = t_end - t_begin;

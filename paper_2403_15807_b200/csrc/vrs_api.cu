@@ -448,7 +448,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
 
   // path choice (A16: per-tuple for small batches, tensor formulation for large ones)
   int path = path_req;
-  GemmPlan gp{0, 0, 0};
+  GemmPlan gp{0, 0, 0, 1};
   // the TMA paths need 16-byte aligned rows and bases
   const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
   if (path != VRS_PATH_SCAN && tma_ok) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
@@ -600,7 +600,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   if (dev != ix->device) return fail(VRS_EINVAL, "current device %d differs from the index device %d", dev, ix->device);
   const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
   const int64_t n = ix->n;
-  GemmPlan gp{0, 0, 0};
+  GemmPlan gp{0, 0, 0, 1};
   if (tma_ok) gp = gemm_plan(q, d, n, 32, ix->num_sms);
   if (!gp.ok)
     return fail(VRS_EUNSUPPORTED, "range search runs on the tensor-core path: d %% 4 == 0 and 16-byte aligned rows");

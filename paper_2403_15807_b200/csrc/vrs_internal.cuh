@@ -121,18 +121,26 @@ struct SplitInfo {
   int64_t n_rows;
   int64_t xsel_cap;
   int32_t bn;              // rows per tile
-  int32_t min_span;        // >= this many row tiles per used split
+  int32_t min_span;        // >= this many row tiles per used split ...
+  int32_t min_p;           // ... unless fewer than min_p splits would leave SMs idle (>= 1 tile each)
 };
 __device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t cap) {
   return ids != nullptr && allow != 0 && n_sel <= cap;
+}
+// The one rule (probe / main kernels, threshold, finalize): >= min_span row tiles
+// per split, but at least min_p splits (about one CTA per SM over the query
+// tiles) while every split keeps >= 1 tile, and never more than P.
+__host__ __device__ __forceinline__ int64_t used_splits(int64_t row_tiles, int64_t P, int64_t min_span, int64_t min_p) {
+  int64_t p = row_tiles / min_span;
+  if (p < min_p) p = min_p < row_tiles ? min_p : row_tiles;
+  if (p > P) p = P;
+  return p > 1 ? p : 1;
 }
 __device__ __forceinline__ int64_t splits_used(const SplitInfo &si) {
   if (si.bn == 0) return si.P;
   const int64_t n_sel = si.ids ? *si.count : si.n_rows;
   const int64_t n_space = gather_mode(si.ids, si.allow_gather, n_sel, si.xsel_cap) ? n_sel : si.n_rows;
-  const int64_t row_tiles = (n_space + si.bn - 1) / si.bn;
-  const int64_t p = row_tiles / si.min_span < si.P ? row_tiles / si.min_span : si.P;
-  return p > 1 ? p : 1;
+  return used_splits((n_space + si.bn - 1) / si.bn, si.P, si.min_span, si.min_p);
 }
 
 // Ranking key used by the selection passes, larger = better for every metric

@@ -62,6 +62,7 @@ struct GemmPlan {
   int32_t P;        // row splits = candidate lists per query
   int32_t qtiles;   // query tiles of 128
   int32_t ok;       // shape supported
+  int32_t min_p;    // splits that keep ~every SM busy over the query tiles (used_splits)
 };
 GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms);
 
