@@ -312,6 +312,28 @@ __device__ __forceinline__ void warp_reg_sort64(float &ka, int32_t &ia, float &k
   }
 }
 
+// Bitonic merge of a 64-element bitonic sequence of (key, id) pairs, two per
+// lane (element lane in (ka, ia), lane + 32 in (kb, ib)), into best-first order.
+__device__ __forceinline__ void warp_merge64_pairs(float &ka, int32_t &ia, float &kb, int32_t &ib) {
+  const int lane = threadIdx.x & 31;
+  if (pair_first(kb, ib, ka, ia)) {
+    const float tk = ka; ka = kb; kb = tk;
+    const int32_t ti = ia; ia = ib; ib = ti;
+  }
+#pragma unroll
+  for (int jj = 16; jj > 0; jj >>= 1) {
+    const bool first = (lane & jj) == 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float &key = h ? kb : ka;
+      int32_t &id = h ? ib : ia;
+      const float pk = __shfl_xor_sync(0xffffffffu, key, jj);
+      const int32_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
+      if (first == pair_first(pk, pid, key, id)) { key = pk; id = pid; }
+    }
+  }
+}
+
 // Keep exactly the K best of the warp's buffer (K <= 64), usually in one
 // histogram pass: keys bucketed linearly over [min, max] (a monotone map), the
 // bucket holding the K-th best found from the top, every entry from that bucket
@@ -731,8 +753,42 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   const int nw = fin_stream(a, j, w, kFinW, s_buf[w]);
   if (lane == 0) s_n[w] = nw;
   __syncthreads();
-  // warp 0 merges the survivors of all warps into its own buffer
-  if (w == 0) {
+  if (a.kprime <= 64) {
+    // k' <= 64: each warp sorts its <= k' survivors, a tree of bitonic merges
+    // (best 64 of two sorted lists: the better of a_e and b_63-e, then one merge)
+    // leaves the 64 best of all warps, sorted, in warp 0 -- exact, ties -> lower id
+    float ka = lane < nw ? s_buf[w].key[lane] : -INFINITY, kb = lane + 32 < nw ? s_buf[w].key[lane + 32] : -INFINITY;
+    int32_t ia = lane < nw ? s_buf[w].id[lane] : INT32_MAX, ib = lane + 32 < nw ? s_buf[w].id[lane + 32] : INT32_MAX;
+    warp_reg_sort64(ka, ia, kb, ib);
+    // (exchange through the free tail of each warp's buffer: survivors sit at [0, nw <= 64))
+    constexpr int X0 = kBufCap - 64;
+#pragma unroll 1
+    for (int stride = kFinW / 2; stride >= 1; stride >>= 1) {
+      if (w < 2 * stride) {
+        s_buf[w].key[X0 + lane] = ka; s_buf[w].key[X0 + lane + 32] = kb;
+        s_buf[w].id[X0 + lane] = ia; s_buf[w].id[X0 + lane + 32] = ib;
+      }
+      __syncthreads();
+      if (w < stride) {
+        const FinBufs &P = s_buf[w + stride];
+        const float pa = P.key[X0 + 63 - lane], pb = P.key[X0 + 31 - lane];
+        const int32_t qa = P.id[X0 + 63 - lane], qb = P.id[X0 + 31 - lane];
+        if (pair_first(pa, qa, ka, ia)) { ka = pa; ia = qa; }
+        if (pair_first(pb, qb, kb, ib)) { kb = pb; ib = qb; }
+        warp_merge64_pairs(ka, ia, kb, ib);
+      }
+      __syncthreads();
+    }
+    if (w == 0) {
+      const int K = a.kprime;
+      const int na = __popc(__ballot_sync(0xffffffffu, lane < K && ia != INT32_MAX));
+      const int nb = __popc(__ballot_sync(0xffffffffu, lane + 32 < K && ib != INT32_MAX));
+      if (lane < K) s_buf[0].id[lane] = ia;
+      if (lane + 32 < K) s_buf[0].id[lane + 32] = ib;
+      if (lane == 0) s_n[0] = na + nb;
+    }
+  } else if (w == 0) {
+    // warp 0 merges the survivors of all warps into its own buffer
     const int K = a.kprime;
     FinBufs &B = s_buf[0];
     int n = nw;
@@ -959,6 +1015,71 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   if (lane == 0) a.gtau[j] = have >= a.kth ? ordered_u32(kth) : 0u;
 }
 
+// Bitonic merge of the 64-element bitonic sequence held two per lane (element
+// lane in ka, lane + 32 in kb) into descending order.
+__device__ __forceinline__ void warp_merge64_desc(float &ka, float &kb) {
+  const int lane = threadIdx.x & 31;
+  const float hi = fmaxf(ka, kb), lo = fminf(ka, kb);
+  ka = hi;
+  kb = lo;
+#pragma unroll
+  for (int jj = 16; jj > 0; jj >>= 1) {
+    const float pa = __shfl_xor_sync(0xffffffffu, ka, jj), pb = __shfl_xor_sync(0xffffffffu, kb, jj);
+    const bool first = (lane & jj) == 0;
+    ka = first ? fmaxf(ka, pa) : fminf(ka, pa);
+    kb = first ? fmaxf(kb, pb) : fminf(kb, pb);
+  }
+}
+
+// Small batches (K <= 64): one CTA of NW warps per query, registers first.  Each
+// lane keeps the two largest of its strided share, each warp sorts its 64, and a
+// tree of bitonic merges (top 64 of two sorted 64-lists: max(a_e, b_63-e), then
+// one merge) leaves the 64 largest of the warps' union in warp 0.  Every stage
+// keeps a subset of the values, so its K-th largest is <= the K-th largest of all
+// values: a valid lower bound of the K-th best key (see threshold_warp_kernel).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs a) {
+  __shared__ float s_f[NW][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  const float *v = a.vals + j * a.nvals;
+  const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
+  constexpr int S = NW * 32;
+  float t0 = -INFINITY, t1 = -INFINITY;
+  int i = w * 32 + lane;
+  for (; i + 3 * S < nvals; i += 4 * S) {
+    float f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) f[u] = __ldg(v + i + S * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { t1 = fmaxf(t1, fminf(t0, f[u])); t0 = fmaxf(t0, f[u]); }
+  }
+  for (; i < nvals; i += S) {
+    const float f = __ldg(v + i);
+    t1 = fmaxf(t1, fminf(t0, f));
+    t0 = fmaxf(t0, f);
+  }
+  int32_t ia = lane, ib = lane + 32;
+  warp_reg_sort64(t0, ia, t1, ib);
+#pragma unroll 1
+  for (int stride = NW / 2; stride >= 1; stride >>= 1) {
+    if (w < 2 * stride) { s_f[w][lane] = t0; s_f[w][lane + 32] = t1; }
+    __syncthreads();
+    if (w < stride) {
+      t0 = fmaxf(t0, s_f[w + stride][63 - lane]);
+      t1 = fmaxf(t1, s_f[w + stride][31 - lane]);
+      warp_merge64_desc(t0, t1);
+    }
+    __syncthreads();
+  }
+  if (w == 0) {
+    const float kth = __shfl_sync(0xffffffffu, a.kth - 1 < 32 ? t0 : t1, (a.kth - 1) & 31);
+    if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
+  }
+}
+
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   // large batches with short value lists: a warp per query (A/B: VRS_BLOCK_THRESHOLD forces the block kernel)
   static const bool block_thr = getenv("VRS_BLOCK_THRESHOLD") != nullptr;
@@ -972,6 +1093,10 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
     }
     return launch_k(threshold_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32),
                     wsmem, s, a);
+  }
+  if (!block_thr && a.kth <= 64) {
+    if (a.q < kSmCountB200) return launch_k(threshold_union_kernel<32>, dim3((unsigned)a.q), dim3(1024), 0, s, a);
+    return launch_k(threshold_union_kernel<8>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr = 0;

@@ -7,7 +7,7 @@ import sys
 
 
 OURS = ("select_count_kernel", "select_scatter_kernel", "gather_copy_kernel", "f32_to_bf16_kernel", "tc_topk_kernel",
-        "threshold_kernel", "threshold_warp_kernel", "finalize_warp_kernel", "finalize_cta_kernel", "scan_topk_kernel",
+        "threshold_kernel", "threshold_warp_kernel", "threshold_union_kernel", "finalize_warp_kernel", "finalize_cta_kernel", "scan_topk_kernel",
         "merge_kernel", "norms_kernel", "range_threshold_kernel", "range_prefix_kernel", "range_verify_kernel",
         "range_write_kernel")
 
