@@ -165,6 +165,8 @@ size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
 
 cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L) {
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
+  // gathered rows without a buffer: TMA gather4 straight from X by id
+  const bool g4 = xcap > 0 && a.xsel == nullptr;
   const bool bf = a.bf16 != 0;
   cudaError_t e = cudaSuccess;
   if (bf && !a.prepped) {   // queries -> bf16 (the corpus shadow was converted at load)
@@ -176,7 +178,8 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   const void *xsrc = bf ? a.Xb : (const void *)a.X;
   if (!make_map(&L->mq, qsrc, bf ? (int64_t)plan.qtiles * tc::BM : a.q, a.d, tc::BM, bf) ||
       !make_map(&L->mx, xsrc, a.n, a.d, tc::BN, bf) ||
-      !make_map(&L->mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf))
+      !(g4 ? make_map(&L->mg, xsrc, a.n, a.d, 1, bf)
+           : make_map(&L->mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf)))
     return cudaErrorInvalidValue;
   TcParams &p = L->p;
   memset(&p, 0, sizeof p);
@@ -191,6 +194,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
   p.xsel_cap = xcap;
   p.xsel_norm = a.xsel_norm;
+  p.g4 = g4 ? 1 : 0;
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
   p.inv_nx = a.inv_nx;
@@ -207,7 +211,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   L->bf = bf;
   L->ar = p.nk <= 4 && !no_ar;
   L->rowscale = a.metric == VRS_COSINE;
-  if (xcap > 0 && p.allow_gather) {
+  if (xcap > 0 && p.allow_gather && !g4) {
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
                  (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,

@@ -78,6 +78,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Four rows (r0..r3) of one 128-byte K block into consecutive 128-byte smem rows
+// (swizzled like a 4-row box): the late-materialisation load of gathered rows.
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -169,7 +179,8 @@ struct TcParams {
   int32_t qtiles;
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
-  int32_t probe_div;       // probe: > 0 => step = clamp(span / probe_div, 2, tile_step) (device-side span)
+  int32_t probe_div;
+  int32_t g4;              // gather mode loads rows by TMA gather4 from X via ids (tmap_g); else from X_sel       // probe: > 0 => step = clamp(span / probe_div, 2, tile_step) (device-side span)
   int32_t min_span;        // used splits span >= this many row tiles (splits_used) ...
   int32_t min_p;           // ... unless that leaves fewer than min_p splits
   const uint32_t *bitmap;  // nullptr => every row qualifies
@@ -352,7 +363,50 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
 
-  if (warp == 0) {
+  if (warp == 0 && gather && p.g4) {
+    // ------------------------------------------------ TMA producer, gathered rows
+    // (late materialisation without a copy: each lane loads the ids of its 8 rows
+    // of the tile one tile ahead and issues two gather4 per K block)
+    int stage = 0;
+    uint32_t phase = 0;
+    if (AR && ntiles > 0 && lane == 0) {
+      mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
+      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+    }
+    static_assert(BN == 256, "8 rows per lane");
+    const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;   // tail rows: any valid row (masked)
+    auto load_ids = [&](int t, int32_t (&r)[8]) {
+      const int64_t pos0 = tile_of(t) * BN + lane * 8;
+      if (pos0 + 8 <= n_sel) {
+        const int4 a0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0));
+        const int4 a1 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + 1);
+        r[0] = a0.x; r[1] = a0.y; r[2] = a0.z; r[3] = a0.w; r[4] = a1.x; r[5] = a1.y; r[6] = a1.z; r[7] = a1.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : pad_row;
+      }
+    };
+    int32_t rid[8], rnext[8];
+    if (ntiles > 0) load_ids(0, rid);
+    for (int t = 0; t < ntiles; ++t) {
+      if (t + 1 < ntiles) load_ids(t + 1, rnext);
+      for (int kb = 0; kb < p.nk; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t *st = b_base + stage * SSTRIDE;
+        if (lane == 0) {
+          mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
+          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
+        }
+        __syncwarp();
+        uint8_t *dst = st + BOFF + lane * 8 * 128;
+        tma_gather4(dst, &tmap_g, &full_bar[stage], kb * KE, rid[0], rid[1], rid[2], rid[3]);
+        tma_gather4(dst + 4 * 128, &tmap_g, &full_bar[stage], kb * KE, rid[4], rid[5], rid[6], rid[7]);
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rid[u] = rnext[u];
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
@@ -412,7 +466,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // norm terms: L2 |x|^2, COS 1/|x|; the inner product needs none (no loads).  Gathered
     // rows read them contiguously from the gather's norm copy (no dependent load).
     const bool need_norm = p.metric != VRS_IP;
-    const float *src = gather ? p.xsel_norm : (p.metric == VRS_L2 ? p.nx2 : p.inv_nx);
+    const float *src_rows = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;   // by row id
+    const float *src = gather && !p.g4 ? p.xsel_norm : src_rows;
     constexpr int RPL = BN / 32;   // rows per lane
     float nv[PF][RPL];
     int32_t iv[PF][RPL];
@@ -431,7 +486,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
           for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
         }
-        if (need_norm && pos0 + RPL <= n_sel) {
+        if (need_norm && p.g4) {   // by row id (dependent loads; the bias warp runs PF tiles ahead)
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) n8[u] = i8[u] >= 0 ? __ldg(src_rows + i8[u]) : 0.f;
+        } else if (need_norm && pos0 + RPL <= n_sel) {
 #pragma unroll
           for (int v = 0; v < RPL / 4; ++v) {
             const float4 v0 = __ldg(reinterpret_cast<const float4 *>(src + pos0) + v);
@@ -790,7 +848,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map over a row-major [rows x d] matrix of fp32 or bf16, boxes of one
-// 128-byte K block x box_rows rows, 128-byte swizzle.
+// 128-byte K block x box_rows rows, 128-byte swizzle (box_rows = 1: the gather4
+// map, four such rows per instruction).
 static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows, bool bf16) {
   auto fn = encode_fn();
   if (!fn) return false;

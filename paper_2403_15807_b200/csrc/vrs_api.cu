@@ -486,13 +486,19 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                               : q >= 1024                 ? n * 9 / 10
                               : q >= 256                  ? n * 9 / 20
                                                           : n / 3;
+  // VRS_GATHER4=1: gather by TMA gather4 straight from X (no X_sel buffer; xsel_cap
+  // is then only the break-even).  Measured slower than the copy at every C2 / C5
+  // cell (gather4 moves ~7 B/clk/SM), so the copy is the default.
+  static const bool gather_copy = getenv("VRS_GATHER4") == nullptr;
   const int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
-                               ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                               ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                                              : gather_rows)
                                : 0;
+  const int64_t xsel_rows = gather_copy ? xsel_cap : 0;   // rows of the X_sel buffer
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
-                                   (size_t)(xsel_cap * row_bytes), (size_t)xsel_cap * 4,
+                                   (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4,
                                    use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
@@ -504,8 +510,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *part_key = cv.take<float>(part_entries);
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
-  void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
-  float *xsel_norm = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap) : nullptr;
+  void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
+  float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
   void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
 
   int launches = 0;
@@ -612,13 +618,16 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
                               : q >= 1024                 ? n * 9 / 10
                               : q >= 256                  ? n * 9 / 20
                                                           : n / 3;
+  static const bool gather_copy = getenv("VRS_GATHER4") == nullptr;   // (as in vrs_search_ex)
   const int64_t xsel_cap = (!identity && rows_req != VRS_ROWS_MASKED)
-                               ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                               ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                                              : gather_rows)
                                : 0;
+  const int64_t xsel_rows = gather_copy ? xsel_cap : 0;
   const int L = 2 * gp.P;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
   st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
-                                      (size_t)(xsel_cap * row_bytes), (size_t)xsel_cap * 4, use_bf16 ? qpad_bytes : 0,
+                                      (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4, use_bf16 ? qpad_bytes : 0,
                                       (size_t)q * 4,
                                       (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4}));
   if (st != VRS_OK) return st;
@@ -627,8 +636,8 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int32_t *sel_ids = identity ? nullptr : cv.take<int32_t>((size_t)n);
   int64_t *count = cv.take<int64_t>(1);
   void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
-  void *xsel = xsel_cap > 0 ? cv.take<char>((size_t)(xsel_cap * row_bytes)) : nullptr;
-  float *xsel_norm = xsel_cap > 0 ? cv.take<float>((size_t)xsel_cap) : nullptr;
+  void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
+  float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
   void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
   RangeState r;
   r.gtau = cv.take<uint32_t>((size_t)q);
