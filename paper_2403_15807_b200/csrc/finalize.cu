@@ -574,32 +574,40 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
   return n;
 }
 
-// Sums of 8 per-lane values over the warp: on return every lane holds the total
-// of value (lane >> 2) & 7.  Each step swaps half of the remaining values with
-// the partner lane (xor 16, 8, 4), then a plain butterfly over lane bits 0-1.
-__device__ __forceinline__ double warp_sum8_transpose(const double (&v)[8]) {
+// Sums of U (4 or 8) per-lane values over the warp: on return every lane holds
+// the total of value (lane >> (5 - log2 U)) & (U - 1).  Each step swaps half of
+// the remaining values with the partner lane (xor 16, 8, ...), then a plain
+// butterfly over the remaining lane bits.
+template <int U>
+constexpr int log2u() { return U == 8 ? 3 : (U == 4 ? 2 : (U == 2 ? 1 : 0)); }
+template <int U>
+__device__ __forceinline__ double warp_sum_transpose(const double (&v)[U]) {
+  static_assert(U == 4 || U == 8, "U = 4 or 8");
   const int lane = threadIdx.x & 31;
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-  double w[4], x[2];
+  double w[U];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) w[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+  for (int i = 0; i < U; ++i) w[i] = v[i];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) x[i] = (b3 ? w[i + 2] : w[i]) + __shfl_xor_sync(0xffffffffu, b3 ? w[i] : w[i + 2], 8);
-  double y = (b2 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4);
-  y += __shfl_xor_sync(0xffffffffu, y, 2);
-  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  for (int h = U / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) w[i] = (up ? w[i + h] : w[i]) + __shfl_xor_sync(0xffffffffu, up ? w[i] : w[i + h], o);
+  }
+  double y = w[0];
+#pragma unroll
+  for (int o = 16 / U; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
   return y;
 }
 
 // Step 4 for candidates c0, c0 + cstep*U ... of ids[0..m): the warp reads each
 // row coalesced, U rows in flight, fp64 accumulation, one transposing reduction
 // per U rows.
+template <int U>
 __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids, int m, int cfirst, int cstep,
                             double qq, double *sc_out, int64_t *sid_out) {
   const int lane = threadIdx.x & 31;
   const float *q = a.Q + j * a.d;
   const bool vec = (a.d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Q)) & 15) == 0;
-  constexpr int U = 8;
   for (int c0 = cfirst * U; c0 < m; c0 += cstep * U) {
     const float *xr[U];
 #pragma unroll
@@ -642,11 +650,11 @@ __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids
     }
     // the U = 8 per-lane partial sums -> row (lane >> 2) & 7's total on every lane,
     // by a transposing butterfly (9 exchanges instead of 8 x 5)
-    const double tot = warp_sum8_transpose(sc);
-    const double xtot = a.metric == VRS_COSINE ? warp_sum8_transpose(xx) : 0.0;
-    const int u = (lane >> 2) & 7;
+    const double tot = warp_sum_transpose<U>(sc);
+    const double xtot = a.metric == VRS_COSINE ? warp_sum_transpose<U>(xx) : 0.0;
+    const int u = (lane >> (5 - log2u<U>())) & (U - 1);
     const int c = c0 + u;
-    if ((lane & 3) == 0 && c < m) {
+    if ((lane & ((32 / U) - 1)) == 0 && c < m) {
       double v = tot;
       if (a.metric == VRS_L2) v = -v;   // sort key: larger is better
       else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xtot));
@@ -722,8 +730,10 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
 // (CAP: candidate buffer per warp, >= 2 k'; SEL: re-scored rows per warp, >= k'.
 // The k' <= 64 variant needs 4 KB of shared memory per warp instead of 9 KB, so
 // a 4096-query batch runs in one wave.)
+// (the k' <= 64 variant is held to 64 registers: 8 CTAs of 4 warps per SM, so a
+// 4096-query batch is one wave -- at 96 registers it was 1.4 waves)
 template <int CAP, int SEL>
-__global__ void __launch_bounds__(kFinGroup * 32) finalize_warp_kernel(FinalizeArgs a) {
+__global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? 8 : 1) finalize_warp_kernel(FinalizeArgs a) {
   __shared__ FinBufsT<CAP> s_buf[kFinGroup];
   __shared__ double s_sc[kFinGroup][SEL];
   __shared__ int64_t s_sid[kFinGroup][SEL];
@@ -734,7 +744,7 @@ __global__ void __launch_bounds__(kFinGroup * 32) finalize_warp_kernel(FinalizeA
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
   const int m = fin_stream(a, j, 0, 1, s_buf[w]);
   const double qq = fin_qq(a, j);
-  fin_rescore(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w]);
+  fin_rescore<SEL <= 64 ? 4 : 8>(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w]);
   __syncwarp();
   fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w]);
 }
@@ -822,7 +832,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   __syncthreads();
   const int m = s_n[0];
   const double qq = fin_qq(a, j);
-  fin_rescore(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid);
+  fin_rescore<8>(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid);
   __syncthreads();
   if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid);
 }
