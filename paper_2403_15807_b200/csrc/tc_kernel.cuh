@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // private staging row
       ++st_slow;
       if (MODE == MODE_MAIN && __any_sync(0xffffffffu, cnt + 32 > p.cap)) compact_needed(p.cap - 32);
+#ifdef VRS_SLOW_GROUPS_VOTE
 #pragma unroll
       for (int g = 0; g < 4; ++g) {   // (unrolled: r must stay in registers)
         if (!__any_sync(0xffffffffu, (pass >> g) & 1u)) continue;
@@ -719,6 +720,59 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
         __syncwarp();
       }
+    #else
+      // each lane walks only its own flagged groups (the warp runs max-over-lanes
+      // iterations, ~1 per slow chunk, instead of every group any lane flagged);
+      // the group's 8 raw dots are picked from the unrolled registers by selects
+      uint32_t pm = pass;
+      float *myrow = wst + lane * STAGE_COLS;
+      while (__any_sync(0xffffffffu, pm != 0)) {
+        if (pm) {
+          const int g = __ffs(pm) - 1;
+          pm &= pm - 1;
+          float kk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t lo = g == 0 ? r[i] : r[8 + i], hi = g == 2 ? r[16 + i] : r[24 + i];
+            kk[i] = __uint_as_float(g < 2 ? lo : hi);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; i += 4) {
+            const float4 bq = *reinterpret_cast<const float4 *>(bb + g * 8 + i);
+            float4 aq = make_float4(sc, sc, sc, sc);
+            if (ROWSCALE) aq = *reinterpret_cast<const float4 *>(ba + g * 8 + i);
+            kk[i] = fmaf(kk[i], aq.x, bq.x);
+            kk[i + 1] = fmaf(kk[i + 1], aq.y, bq.y);
+            kk[i + 2] = fmaf(kk[i + 2], aq.z, bq.z);
+            kk[i + 3] = fmaf(kk[i + 3], aq.w, bq.w);
+          }
+          uint32_t msk = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) msk |= (kk[i] > thr ? 1u : 0u) << i;
+          if (MODE == MODE_RCOUNT) {
+            cnt += __popc(msk);
+          } else if (MODE == MODE_RFILL) {   // the list's segment, rows in ascending order
+            while (msk) {
+              const int i = __ffs(msk) - 1;
+              msk &= msk - 1;
+              cid[cnt++] = rid[g * 8 + i];
+            }
+          } else if (msk) {
+            *reinterpret_cast<float4 *>(myrow) = make_float4(kk[0], kk[1], kk[2], kk[3]);
+            *reinterpret_cast<float4 *>(myrow + 4) = make_float4(kk[4], kk[5], kk[6], kk[7]);
+            st_app += __popc(msk);
+            while (msk) {
+              const int i = __ffs(msk) - 1;
+              msk &= msk - 1;
+              ckey[cnt] = myrow[i];
+              cid[cnt] = rid[g * 8 + i];
+              ++cnt;
+            }
+          }
+        }
+      }
+      __syncwarp();   // (the next compaction's histogram aliases the staging rows)
+#endif
     };
 
     for (int t = 0; t < ntiles; ++t) {
