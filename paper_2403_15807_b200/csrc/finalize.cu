@@ -312,36 +312,87 @@ __device__ __forceinline__ void warp_reg_sort64(float &ka, int32_t &ia, float &k
   }
 }
 
-// Bitonic merge of a 64-element bitonic sequence of (key, id) pairs, two per
-// lane (element lane in (ka, ia), lane + 32 in (kb, ib)), into best-first order.
-__device__ __forceinline__ void warp_merge64_pairs(float &ka, int32_t &ia, float &kb, int32_t &ib) {
+// ---- register bitonic networks over 32 * E (key, id) pairs, E per lane ----------
+// Element e = h * 32 + lane sits in slot h of lane `lane`.  Order: best first
+// (key descending, then id ascending).
+template <int E>
+__device__ __forceinline__ void warp_cmpx_e(float (&k)[E], int32_t (&id)[E], int kk, int jj) {
   const int lane = threadIdx.x & 31;
-  if (pair_first(kb, ib, ka, ia)) {
-    const float tk = ka; ka = kb; kb = tk;
-    const int32_t ti = ia; ia = ib; ib = ti;
-  }
+  if (jj >= 32) {   // partners in the same lane
+    const int hj = jj >> 5;
 #pragma unroll
-  for (int jj = 16; jj > 0; jj >>= 1) {
-    const bool first = (lane & jj) == 0;
+    for (int h = 0; h < E; ++h) {
+      if (h & hj) continue;
+      const int hi = h | hj;
+      const bool lo_first = ((h * 32 + lane) & kk) == 0;   // the lower element takes the better
+      if (pair_first(k[hi], id[hi], k[h], id[h]) == lo_first) {
+        const float tk = k[h]; k[h] = k[hi]; k[hi] = tk;
+        const int32_t ti = id[h]; id[h] = id[hi]; id[hi] = ti;
+      }
+    }
+  } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float &key = h ? kb : ka;
-      int32_t &id = h ? ib : ia;
-      const float pk = __shfl_xor_sync(0xffffffffu, key, jj);
-      const int32_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
-      if (first == pair_first(pk, pid, key, id)) { key = pk; id = pid; }
+    for (int h = 0; h < E; ++h) {
+      const int i = h * 32 + lane;
+      const float pk = __shfl_xor_sync(0xffffffffu, k[h], jj);
+      const int32_t pid = __shfl_xor_sync(0xffffffffu, id[h], jj);
+      const bool keep_first = ((i & kk) == 0) == ((i & jj) == 0);
+      if (keep_first == pair_first(pk, pid, k[h], id[h])) { k[h] = pk; id[h] = pid; }
     }
   }
 }
+// Full sort.
+template <int E>
+__device__ __forceinline__ void warp_sort_e(float (&k)[E], int32_t (&id)[E]) {
+#pragma unroll
+  for (int kk = 2; kk <= 32 * E; kk <<= 1)
+#pragma unroll
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) warp_cmpx_e<E>(k, id, kk, jj);
+}
+// Sort of a bitonic sequence (the last stage of the network).
+template <int E>
+__device__ __forceinline__ void warp_merge_e(float (&k)[E], int32_t (&id)[E]) {
+#pragma unroll
+  for (int jj = 16 * E; jj > 0; jj >>= 1) warp_cmpx_e<E>(k, id, 32 * E, jj);
+}
+// Best 32E of two sorted 32E-lists: mine (registers) and other (smem, element e at
+// ok[e] / oi[e]): the better of mine[e] and other[32E-1-e] is bitonic, then merged.
+template <int E>
+__device__ __forceinline__ void warp_merge_with_e(float (&k)[E], int32_t (&id)[E], const float *ok, const int32_t *oi) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 0; h < E; ++h) {
+    const int e = 32 * E - 1 - (h * 32 + lane);
+    const float pk = ok[e];
+    const int32_t pid = oi[e];
+    if (pair_first(pk, pid, k[h], id[h])) { k[h] = pk; id[h] = pid; }
+  }
+  warp_merge_e<E>(k, id);
+}
+// Insert f into the descending per-lane list t[0] >= t[1] >= ... (keys only).
+template <int E>
+__device__ __forceinline__ void top_insert_e(float (&t)[E], float f) {
+#pragma unroll
+  for (int h = E - 1; h > 0; --h) t[h] = fmaxf(t[h], fminf(t[h - 1], f));
+  t[0] = fmaxf(t[0], f);
+}
+template <int E>
+__device__ __forceinline__ float elem_e(const float (&k)[E], int e) {   // element e (warp-uniform e)
+  float v = k[0];
+#pragma unroll
+  for (int h = 1; h < E; ++h) if ((e >> 5) == h) v = k[h];
+  return __shfl_sync(0xffffffffu, v, e & 31);
+}
 
-// Keep exactly the K best of the warp's buffer (K <= 64), usually in one
+// Keep exactly the K best of the warp's buffer (K <= 128), usually in one
 // histogram pass: keys bucketed linearly over [min, max] (a monotone map), the
 // bucket holding the K-th best found from the top, every entry from that bucket
-// up collected (<= 64 of them in the common case) and sorted in registers.
-// Falls back to the radix select when the collected set is larger (ties, spikes).
-__device__ __noinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
+// up collected (<= 32E of them in the common case, E = 2 for K <= 64, else 4) and
+// sorted in registers.  Falls back to the radix select when the collected set is
+// larger (ties, spikes).
+template <int E>
+__device__ __noinline__ uint32_t warp_keep_best_fast_e(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
   const int lane = threadIdx.x & 31;
-  if (K > 64) return warp_keep_best(bk, bi, n, K, hist);
   float lo = INFINITY, hi = -INFINITY;
   for (int i = lane; i < n; i += 32) { lo = fminf(lo, bk[i]); hi = fmaxf(hi, bk[i]); }
 #pragma unroll
@@ -383,11 +434,11 @@ __device__ __noinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int
   const int src = __ffs(__ballot_sync(0xffffffffu, bstar >= 0)) - 1;
   bstar = __shfl_sync(0xffffffffu, bstar, src);
   upto = __shfl_sync(0xffffffffu, upto, src);
-  if (upto > 64) return warp_keep_best(bk, bi, n, K, hist);
+  if (upto > 32 * E) return warp_keep_best(bk, bi, n, K, hist);
   // collect the candidates from bucket bstar up into the (no longer needed)
-  // histogram space, then two per lane into registers
+  // histogram space (32E keys, 32E ids <= 256 words), then E per lane into registers
   float *ck = reinterpret_cast<float *>(hist);
-  int32_t *ci = reinterpret_cast<int32_t *>(hist + 64);
+  int32_t *ci = reinterpret_cast<int32_t *>(hist + 32 * E);
   __syncwarp();
   int got = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
@@ -402,17 +453,30 @@ __device__ __noinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int
     got += __popc(m);
   }
   __syncwarp();
-  float ka = lane < got ? ck[lane] : -INFINITY, kb2 = lane + 32 < got ? ck[lane + 32] : -INFINITY;
-  int32_t ia = lane < got ? ci[lane] : INT32_MAX, ib = lane + 32 < got ? ci[lane + 32] : INT32_MAX;
-  warp_reg_sort64(ka, ia, kb2, ib);
-  // the K best: elements 0..K-1 (element e sits in lane e & 31, slot e >> 5)
+  float kk[E];
+  int32_t ii[E];
+#pragma unroll
+  for (int h = 0; h < E; ++h) {
+    const int e = h * 32 + lane;
+    kk[h] = e < got ? ck[e] : -INFINITY;
+    ii[h] = e < got ? ci[e] : INT32_MAX;
+  }
+  warp_sort_e<E>(kk, ii);
+  // the K best: elements 0..K-1
   __syncwarp();
-  if (lane < K) { bk[lane] = ka; bi[lane] = ia; }
-  if (lane + 32 < K) { bk[lane + 32] = kb2; bi[lane + 32] = ib; }
+#pragma unroll
+  for (int h = 0; h < E; ++h) {
+    const int e = h * 32 + lane;
+    if (e < K) { bk[e] = kk[h]; bi[e] = ii[h]; }
+  }
   __syncwarp();
   n = K;
-  const float kth = __shfl_sync(0xffffffffu, K - 1 < 32 ? ka : kb2, (K - 1) & 31);
-  return ordered_u32(kth);
+  return ordered_u32(elem_e<E>(kk, K - 1));
+}
+__device__ __forceinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
+  if (K <= 64) return warp_keep_best_fast_e<2>(bk, bi, n, K, hist);
+  if (K <= 128) return warp_keep_best_fast_e<4>(bk, bi, n, K, hist);
+  return warp_keep_best(bk, bi, n, K, hist);
 }
 
 // The K-th largest (K <= 64) of the nonzero ordered-u32 values v[0..n) (0 = no
@@ -750,6 +814,48 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? 8 : 1) finalize_wa
 }
 
 constexpr int kFinW = 8;   // warps per query in the small-batch variant
+// k' <= 32E: each warp of the CTA sorts its <= k' survivors, a tree of bitonic
+// merges (best 32E of two sorted lists) leaves the 32E best of all warps, sorted,
+// in warp 0, which writes the k' best ids to s_buf[0] and their count to s_n[0].
+// Exact; ties -> lower id.  (Exchange through the free tail of each warp's buffer:
+// its survivors sit at [0, nw <= k').)
+template <int E>
+__device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s_buf, int nw, int *s_n) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float k[E];
+  int32_t id[E];
+#pragma unroll
+  for (int h = 0; h < E; ++h) {
+    const int e = h * 32 + lane;
+    k[h] = e < nw ? s_buf[w].key[e] : -INFINITY;
+    id[h] = e < nw ? s_buf[w].id[e] : INT32_MAX;
+  }
+  warp_sort_e<E>(k, id);
+  constexpr int X0 = kBufCap - 32 * E;
+#pragma unroll 1
+  for (int stride = kFinW / 2; stride >= 1; stride >>= 1) {
+    if (w < 2 * stride) {
+#pragma unroll
+      for (int h = 0; h < E; ++h) { s_buf[w].key[X0 + h * 32 + lane] = k[h]; s_buf[w].id[X0 + h * 32 + lane] = id[h]; }
+    }
+    __syncthreads();
+    if (w < stride) warp_merge_with_e<E>(k, id, s_buf[w + stride].key + X0, s_buf[w + stride].id + X0);
+    __syncthreads();
+  }
+  if (w == 0) {
+    const int K = a.kprime;
+    int cnt = 0;
+#pragma unroll
+    for (int h = 0; h < E; ++h) {
+      const int e = h * 32 + lane;
+      cnt += __popc(__ballot_sync(0xffffffffu, e < K && id[h] != INT32_MAX));
+      if (e < K) s_buf[0].id[e] = id[h];
+    }
+    if (lane == 0) s_n[0] = cnt;
+  }
+}
+
+
 __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a) {
   __shared__ FinBufs s_buf[kFinW];
   __shared__ double s_sc[kFinMaxSel];
@@ -764,39 +870,9 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   if (lane == 0) s_n[w] = nw;
   __syncthreads();
   if (a.kprime <= 64) {
-    // k' <= 64: each warp sorts its <= k' survivors, a tree of bitonic merges
-    // (best 64 of two sorted lists: the better of a_e and b_63-e, then one merge)
-    // leaves the 64 best of all warps, sorted, in warp 0 -- exact, ties -> lower id
-    float ka = lane < nw ? s_buf[w].key[lane] : -INFINITY, kb = lane + 32 < nw ? s_buf[w].key[lane + 32] : -INFINITY;
-    int32_t ia = lane < nw ? s_buf[w].id[lane] : INT32_MAX, ib = lane + 32 < nw ? s_buf[w].id[lane + 32] : INT32_MAX;
-    warp_reg_sort64(ka, ia, kb, ib);
-    // (exchange through the free tail of each warp's buffer: survivors sit at [0, nw <= 64))
-    constexpr int X0 = kBufCap - 64;
-#pragma unroll 1
-    for (int stride = kFinW / 2; stride >= 1; stride >>= 1) {
-      if (w < 2 * stride) {
-        s_buf[w].key[X0 + lane] = ka; s_buf[w].key[X0 + lane + 32] = kb;
-        s_buf[w].id[X0 + lane] = ia; s_buf[w].id[X0 + lane + 32] = ib;
-      }
-      __syncthreads();
-      if (w < stride) {
-        const FinBufs &P = s_buf[w + stride];
-        const float pa = P.key[X0 + 63 - lane], pb = P.key[X0 + 31 - lane];
-        const int32_t qa = P.id[X0 + 63 - lane], qb = P.id[X0 + 31 - lane];
-        if (pair_first(pa, qa, ka, ia)) { ka = pa; ia = qa; }
-        if (pair_first(pb, qb, kb, ib)) { kb = pb; ib = qb; }
-        warp_merge64_pairs(ka, ia, kb, ib);
-      }
-      __syncthreads();
-    }
-    if (w == 0) {
-      const int K = a.kprime;
-      const int na = __popc(__ballot_sync(0xffffffffu, lane < K && ia != INT32_MAX));
-      const int nb = __popc(__ballot_sync(0xffffffffu, lane + 32 < K && ib != INT32_MAX));
-      if (lane < K) s_buf[0].id[lane] = ia;
-      if (lane + 32 < K) s_buf[0].id[lane + 32] = ib;
-      if (lane == 0) s_n[0] = na + nb;
-    }
+    fin_tree_merge<2>(a, s_buf, nw, s_n);
+  } else if (a.kprime <= 128) {
+    fin_tree_merge<4>(a, s_buf, nw, s_n);
   } else if (w == 0) {
     // warp 0 merges the survivors of all warps into its own buffer
     const int K = a.kprime;
@@ -975,6 +1051,33 @@ radix:
   if (tid == 0) a.gtau[j] = prefix;
 }
 
+// Per lane the E largest of v[first + S * t] (the warp's lanes at consecutive
+// first), warp-sorted: returns element K-1 of the union (-inf if fewer).
+template <int E, int S>
+__device__ __forceinline__ void lane_top_sorted(const float *v, int nvals, int first, float (&t)[E]) {
+#pragma unroll
+  for (int h = 0; h < E; ++h) t[h] = -INFINITY;
+  int i = first;
+  for (; i + 3 * S < nvals; i += 4 * S) {
+    float f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) f[u] = __ldg(v + i + S * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) top_insert_e<E>(t, f[u]);
+  }
+  for (; i < nvals; i += S) top_insert_e<E>(t, __ldg(v + i));
+  int32_t id[E];
+#pragma unroll
+  for (int h = 0; h < E; ++h) id[h] = h * 32 + (int)(threadIdx.x & 31);
+  warp_sort_e<E>(t, id);
+}
+template <int E, int S>
+__device__ __forceinline__ float lane_top_kth(const float *v, int nvals, int first, int K) {
+  float t[E];
+  lane_top_sorted<E, S>(v, nvals, first, t);
+  return elem_e<E>(t, K - 1);
+}
+
 // Large batches: one warp per query, registers only.  Each lane keeps the two
 // largest of its values (slot `lane` of every list); the K-th largest of that
 // union of 64 values is <= the K-th largest of all values (a subset's K-th
@@ -992,7 +1095,7 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
   const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
-  if (a.kth > 64) {
+  if (a.kth > 128) {
     uint32_t *mine = s_vals + (size_t)w * a.nvals;
     for (int i = lane; i < nvals; i += 32) {
       const float f = __ldg(v + i);
@@ -1004,88 +1107,43 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
     if (lane == 0) a.gtau[j] = ok ? x : 0u;
     return;
   }
-  float t0 = -INFINITY, t1 = -INFINITY;   // this lane's two largest (t0 >= t1)
-  int i = lane;
-  for (; i + 96 < nvals; i += 128) {
-    float f[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) f[u] = __ldg(v + i + 32 * u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { t1 = fmaxf(t1, fminf(t0, f[u])); t0 = fmaxf(t0, f[u]); }
-  }
-  for (; i < nvals; i += 32) {
-    const float f = __ldg(v + i);
-    t1 = fmaxf(t1, fminf(t0, f));
-    t0 = fmaxf(t0, f);
-  }
-  const int have = __popc(__ballot_sync(0xffffffffu, t0 > -INFINITY)) + __popc(__ballot_sync(0xffffffffu, t1 > -INFINITY));
-  int32_t ia = lane, ib = lane + 32;
-  warp_reg_sort64(t0, ia, t1, ib);
-  const float kth = __shfl_sync(0xffffffffu, a.kth - 1 < 32 ? t0 : t1, (a.kth - 1) & 31);
-  if (lane == 0) a.gtau[j] = have >= a.kth ? ordered_u32(kth) : 0u;
+  const float kth = a.kth <= 64 ? lane_top_kth<2, 32>(v, nvals, lane, a.kth) : lane_top_kth<4, 32>(v, nvals, lane, a.kth);
+  if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
 }
 
-// Bitonic merge of the 64-element bitonic sequence held two per lane (element
-// lane in ka, lane + 32 in kb) into descending order.
-__device__ __forceinline__ void warp_merge64_desc(float &ka, float &kb) {
-  const int lane = threadIdx.x & 31;
-  const float hi = fmaxf(ka, kb), lo = fminf(ka, kb);
-  ka = hi;
-  kb = lo;
-#pragma unroll
-  for (int jj = 16; jj > 0; jj >>= 1) {
-    const float pa = __shfl_xor_sync(0xffffffffu, ka, jj), pb = __shfl_xor_sync(0xffffffffu, kb, jj);
-    const bool first = (lane & jj) == 0;
-    ka = first ? fmaxf(ka, pa) : fminf(ka, pa);
-    kb = first ? fmaxf(kb, pb) : fminf(kb, pb);
-  }
-}
-
-// Small batches (K <= 64): one CTA of NW warps per query, registers first.  Each
-// lane keeps the two largest of its strided share, each warp sorts its 64, and a
-// tree of bitonic merges (top 64 of two sorted 64-lists: max(a_e, b_63-e), then
-// one merge) leaves the 64 largest of the warps' union in warp 0.  Every stage
-// keeps a subset of the values, so its K-th largest is <= the K-th largest of all
+// Small batches (K <= 128): one CTA of NW warps per query, registers first.  Each
+// lane keeps the E largest of its strided share (E = 2 for K <= 64, else 4),
+// each warp sorts its 32E, and a tree of bitonic merges (best 32E of two sorted
+// lists) leaves the 32E largest of the warps' union in warp 0.  Every stage keeps
+// a subset of the values, so its K-th largest is <= the K-th largest of all
 // values: a valid lower bound of the K-th best key (see threshold_warp_kernel).
-template <int NW>
+template <int NW, int E>
 __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs a) {
-  __shared__ float s_f[NW][64];
+  __shared__ float s_f[NW][32 * E];
+  __shared__ int32_t s_i[NW][32 * E];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
   pdl_wait();
   pdl_trigger();
   const float *v = a.vals + j * a.nvals;
   const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
-  constexpr int S = NW * 32;
-  float t0 = -INFINITY, t1 = -INFINITY;
-  int i = w * 32 + lane;
-  for (; i + 3 * S < nvals; i += 4 * S) {
-    float f[4];
+  float t[E];
+  lane_top_sorted<E, NW * 32>(v, nvals, w * 32 + lane, t);
+  int32_t id[E];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) f[u] = __ldg(v + i + S * u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { t1 = fmaxf(t1, fminf(t0, f[u])); t0 = fmaxf(t0, f[u]); }
-  }
-  for (; i < nvals; i += S) {
-    const float f = __ldg(v + i);
-    t1 = fmaxf(t1, fminf(t0, f));
-    t0 = fmaxf(t0, f);
-  }
-  int32_t ia = lane, ib = lane + 32;
-  warp_reg_sort64(t0, ia, t1, ib);
+  for (int h = 0; h < E; ++h) id[h] = (w * E + h) * 32 + lane;   // (distinct tie-breakers)
 #pragma unroll 1
   for (int stride = NW / 2; stride >= 1; stride >>= 1) {
-    if (w < 2 * stride) { s_f[w][lane] = t0; s_f[w][lane + 32] = t1; }
-    __syncthreads();
-    if (w < stride) {
-      t0 = fmaxf(t0, s_f[w + stride][63 - lane]);
-      t1 = fmaxf(t1, s_f[w + stride][31 - lane]);
-      warp_merge64_desc(t0, t1);
+    if (w < 2 * stride) {
+#pragma unroll
+      for (int h = 0; h < E; ++h) { s_f[w][h * 32 + lane] = t[h]; s_i[w][h * 32 + lane] = id[h]; }
     }
+    __syncthreads();
+    if (w < stride) warp_merge_with_e<E>(t, id, s_f[w + stride], s_i[w + stride]);
     __syncthreads();
   }
   if (w == 0) {
-    const float kth = __shfl_sync(0xffffffffu, a.kth - 1 < 32 ? t0 : t1, (a.kth - 1) & 31);
+    const float kth = elem_e<E>(t, a.kth - 1);
     if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
   }
 }
@@ -1093,7 +1151,7 @@ __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs 
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   // large batches with short value lists: a warp per query (A/B: VRS_BLOCK_THRESHOLD forces the block kernel)
   static const bool block_thr = getenv("VRS_BLOCK_THRESHOLD") != nullptr;
-  const size_t wsmem = a.kth > 64 ? (size_t)kFinGroup * a.nvals * 4 : 0;
+  const size_t wsmem = a.kth > 128 ? (size_t)kFinGroup * a.nvals * 4 : 0;
   if (!block_thr && a.q >= 4 * kSmCountB200 && wsmem <= 96 * 1024) {
     static size_t wattr = 0;
     if (wsmem > 48 * 1024 && wsmem > wattr) {
@@ -1104,9 +1162,13 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
     return launch_k(threshold_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32),
                     wsmem, s, a);
   }
-  if (!block_thr && a.kth <= 64) {
-    if (a.q < kSmCountB200) return launch_k(threshold_union_kernel<32>, dim3((unsigned)a.q), dim3(1024), 0, s, a);
-    return launch_k(threshold_union_kernel<8>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+  if (!block_thr && a.kth <= 128) {
+    const bool big = a.q < kSmCountB200;   // few queries: more warps per query
+    if (a.kth <= 64)
+      return big ? launch_k(threshold_union_kernel<32, 2>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
+                 : launch_k(threshold_union_kernel<8, 2>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+    return big ? launch_k(threshold_union_kernel<16, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
+               : launch_k(threshold_union_kernel<8, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr = 0;
@@ -1127,6 +1189,7 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
   if (a.q < 4 * kSmCountB200) return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), 0, s, a);
   const dim3 grid((unsigned)((a.q + kFinGroup - 1) / kFinGroup));
   if (a.kprime <= 64) return launch_k(finalize_warp_kernel<256, 64>, grid, dim3(kFinGroup * 32), 0, s, a);
+  if (a.kprime <= 128) return launch_k(finalize_warp_kernel<256, 128>, grid, dim3(kFinGroup * 32), 0, s, a);
   return launch_k(finalize_warp_kernel<kBufCap, kFinMaxSel>, grid, dim3(kFinGroup * 32), 0, s, a);
   return cudaGetLastError();
 }

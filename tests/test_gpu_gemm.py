@@ -42,6 +42,11 @@ GEMM_CASES = [
     (20000, 256, 64, 240, oracle.IP, [(0, I32MIN, 9)]),   # k = K_MAX, ~1 % selectivity
     (12000, 768, 9, 100, oracle.L2, [(0, 0, 299)]),
     (2000, 128, 16, 10, oracle.IP, [(0, 5000, 6000)]),    # selectivity 0
+    # q >= 592: the warp-per-query threshold / finalize kernels, k' <= 64 / <= 128 / > 128
+    (6000, 128, 1000, 10, oracle.IP, [(0, 0, 299)]),
+    (12000, 64, 700, 50, oracle.COS, [(0, 0, 499)]),
+    (8000, 128, 600, 100, oracle.L2, []),
+    (5000, 64, 640, 200, oracle.IP, [(0, 0, 799)]),
 ]
 
 
