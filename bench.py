@@ -357,7 +357,10 @@ def main():
         t = a.elapsed_time(b) / reps / 1e3
         ns = nsel[s]
         fl = 2.0 * q * ns * d
-        by = n_loc * sum(1 if cfg.attrs[i][0] == "u8" else 4 for i in range(len(cfg.attrs))) + ns * 4.0 * d + q * 4.0 * d + q * k * 12
+        # algorithmic bytes: attribute columns, the selected rows once (bf16 shadow on the
+        # bf16 tensor-core path, else fp32), the queries, the results
+        esz = 2.0 if (vrs.last_path() == vrs.PATH_GEMM and ix.precision == vrs.PREC_BF16) else 4.0
+        by = n_loc * sum(1 if cfg.attrs[i][0] == "u8" else 4 for i in range(len(cfg.attrs))) + ns * esz * d + q * 4.0 * d + q * k * 12
         cell_out.append({"sel": s, "q": q, "n_sel": ns, "ms": t * 1e3, "qps": q / t,
                          "path": "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan",
                          "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac": fl / t / 1e12 / tc_peak_sus})
