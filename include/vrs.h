@@ -175,8 +175,13 @@ typedef struct {
   int32_t path;      /* vrs_path */
   int32_t rows;      /* vrs_rows */
   int32_t precision; /* vrs_precision of the tensor-core selection (DEFAULT: bf16 if the index has the shadow) */
-  int32_t host_async; /* vrs_search_host only: 1 = do not synchronise; the caller synchronises cuda_stream
-                         before reading h_ids / h_dists, and the host buffers must be pinned */
+  int32_t host_async; /* vrs_search_host only (the host buffers must then be pinned):
+                         0 = synchronise cuda_stream before returning;
+                         1 = do not synchronise; cuda_stream is ordered after the device->host copies,
+                             the caller synchronises it before reading h_ids / h_dists;
+                         2 = overlap: cuda_stream is NOT ordered after the copies (the next call's
+                             kernels overlap this call's download); h_ids / h_dists are complete once
+                             vrs_host_fence(ix, s) has been enqueued on a stream s and s has synchronised */
   int32_t reserved[4];
 } vrs_search_options;
 
@@ -195,6 +200,13 @@ VRS_API vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q,
 VRS_API vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int32_t d,
                            const vrs_predicate *pred, int32_t k, vrs_metric metric, int64_t *h_ids,
                            float *h_dists, const vrs_search_options *opts, void *cuda_stream);
+
+/*
+ * vrs_host_fence -- orders cuda_stream after every device->host result copy that
+ * vrs_search_host has issued on `ix` so far (for host_async = 2).  Enqueues a
+ * wait only; never blocks the host.  Errors: VRS_EINVAL (ix NULL), VRS_ECUDA.
+ */
+VRS_API vrs_status vrs_host_fence(vrs_index *ix, void *cuda_stream);
 
 /*
  * vrs_range_search -- threshold selection instead of top-k: eps = "the score

@@ -52,14 +52,14 @@ _opt_cache = {}
 def _options(path, rows, precision=None, host_async=False):
     if path is None and rows is None and precision is None and not host_async:
         return None
-    key = (path, rows, precision, bool(host_async))
+    key = (path, rows, precision, int(host_async))
     if key in _opt_cache:
         return _opt_cache[key][1]
     o = _lib.SearchOptions()
     o.path = PATH_AUTO if path is None else int(path)
     o.rows = ROWS_AUTO if rows is None else int(rows)
     o.precision = PREC_DEFAULT if precision is None else int(precision)
-    o.host_async = 1 if host_async else 0
+    o.host_async = int(host_async)   # False / True (1) / 2 = overlap (see vrs.h)
     _opt_cache[key] = (o, ctypes.byref(o))   # the struct stays alive with its reference
     return _opt_cache[key][1]
 
@@ -161,7 +161,8 @@ class Index:
     def search_host(self, queries_h: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
                     out=None, stream=None, precision=None, host_async=False):
         """End-to-end call on host buffers (H2D + search + D2H inside libvrs).  Synchronous,
-        unless host_async: then the caller synchronises the stream (pinned buffers)."""
+        unless host_async: True -> the caller synchronises the stream (pinned buffers);
+        2 -> overlap: results are complete after host_fence(stream) + a stream sync."""
         lib = library()
         q, d = queries_h.shape
         if out is None:
@@ -175,6 +176,10 @@ class Index:
                                  _stream(stream))
         _lib.check(st, "vrs_search_host")
         return ids, dists
+
+    def host_fence(self, stream=None):
+        """vrs_host_fence: order `stream` after every result download search_host issued."""
+        _lib.check(library().vrs_host_fence(self._h, _stream(stream)), "vrs_host_fence")
 
     def range_search(self, queries: torch.Tensor, pred=None, tau: float = 0.9, metric="cos", capacity=None,
                      rows=None, precision=None, stream=None):

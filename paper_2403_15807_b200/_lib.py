@@ -26,7 +26,7 @@ K_MAX = 240
 MAX_CLAUSES = 8
 
 # every symbol include/vrs.h declares (tests check the library exports them)
-EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free",
+EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_host_fence", "vrs_select", "vrs_merge", "vrs_free",
            "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
            "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset")
 
@@ -83,10 +83,12 @@ def load_library():
     lib.vrs_search_host.argtypes = [p, p, i64, i32, p, i32, ctypes.c_int, p, p, p, p]
     lib.vrs_range_search.argtypes = [p, p, i64, i32, p, ctypes.c_double, ctypes.c_int, i64, p, p, p,
                                      ctypes.POINTER(i64), p, p]
+    lib.vrs_host_fence.argtypes = [p, p]
     lib.vrs_select.argtypes = [p, p, p, p, p, p]
     lib.vrs_merge.argtypes = [p, p, i32, i64, i32, ctypes.c_int, p, p, p]
     lib.vrs_free.argtypes = [p]
-    for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_select", "vrs_merge", "vrs_free"):
+    for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_host_fence",
+              "vrs_select", "vrs_merge", "vrs_free"):
         getattr(lib, f).restype = ctypes.c_int
     lib.vrs_last_error.restype = ctypes.c_char_p
     lib.vrs_last_path.restype = i32

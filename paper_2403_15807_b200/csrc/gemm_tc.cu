@@ -122,6 +122,8 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
   // items >= ~128 row tiles
   int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, row_tiles * qtiles / ((int64_t)num_sms * 128)));
   int64_t P = std::max<int64_t>(1, (int64_t)num_sms * waves / qtiles);
+  static const int p_env = getenv("VRS_P") ? atoi(getenv("VRS_P")) : 0;   // (experiments)
+  if (p_env > 0) P = p_env;
   P = std::min<int64_t>(std::min<int64_t>(P, row_tiles), 2 * num_sms);
   g.P = (int32_t)P;
   g.qtiles = (int32_t)qtiles;

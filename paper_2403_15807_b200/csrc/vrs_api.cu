@@ -32,7 +32,7 @@ struct vrs_index {
   float *inv_nx;
   int32_t has_zero_row;
   float xmax;              // max row norm (range search error bound)
-  void *xb;
+  void *xb;               // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
   // vrs_search_host staging: two device slots (queries in, ids / dists out) so
   // that the upload of one call overlaps the compute of the previous one; the
   // copies run on their own streams, ordered by events.
@@ -41,7 +41,8 @@ struct vrs_index {
   void *slot_buf[2] = {nullptr, nullptr};
   size_t slot_cap[2] = {0, 0};
   cudaEvent_t slot_free[2] = {nullptr, nullptr}, up_done[2] = {nullptr, nullptr}, comp_done[2] = {nullptr, nullptr};
-  int slot_next = 0;                // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
+  int slot_next = 0;
+  int last_down = -1;     // slot of the last download issued (vrs_host_fence)
   int32_t device;
   int32_t num_sms;
 };
@@ -748,8 +749,20 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
   CUDA_TRY(cudaMemcpyAsync(h_ids, di, ib, cudaMemcpyDeviceToHost, ix->down_stream));
   CUDA_TRY(cudaMemcpyAsync(h_dists, dd, db, cudaMemcpyDeviceToHost, ix->down_stream));
   CUDA_TRY(cudaEventRecord(ix->slot_free[slot], ix->down_stream));
-  CUDA_TRY(cudaStreamWaitEvent(stream, ix->slot_free[slot], 0));
-  if (!(opts && opts->host_async)) CUDA_TRY(cudaStreamSynchronize(stream));
+  ix->last_down = slot;
+  const int mode = opts ? opts->host_async : 0;
+  if (mode != 2) CUDA_TRY(cudaStreamWaitEvent(stream, ix->slot_free[slot], 0));
+  if (mode == 0) CUDA_TRY(cudaStreamSynchronize(stream));
+  return VRS_OK;
+}
+
+vrs_status vrs_host_fence(vrs_index *ix, void *cuda_stream) {
+  g_err[0] = 0;
+  if (!ix) return fail(VRS_EINVAL, "index is NULL");
+  std::lock_guard<std::mutex> guard(ix->host_mu);
+  // the download stream is in order: its last recorded event covers every earlier copy
+  if (ix->down_stream && ix->last_down >= 0)
+    CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)cuda_stream, ix->slot_free[ix->last_down], 0));
   return VRS_OK;
 }
 

@@ -196,6 +196,17 @@ def test_search_host_end_to_end(vrs):
     torch.cuda.synchronize()
     for lo, (i2, d2) in zip((0, 100, 200), outs):
         check_topk(i2.numpy(), d2.numpy(), X, attrs, [(0, lo, lo + 399)], Q, 7, oracle.IP)
+    # host_async = 2 (overlap): the stream is not ordered after the downloads; host_fence
+    # on a separate stream + its synchronisation completes the results
+    outs = []
+    for lo in (0, 100, 200, 300):
+        outs.append(ix.search_host(torch.from_numpy(Q).pin_memory(), [(0, lo, lo + 399)], k=7, metric="ip",
+                                   host_async=2))
+    s2 = torch.cuda.Stream()
+    ix.host_fence(s2)
+    s2.synchronize()
+    for lo, (i2, d2) in zip((0, 100, 200, 300), outs):
+        check_topk(i2.numpy(), d2.numpy(), X, attrs, [(0, lo, lo + 399)], Q, 7, oracle.IP)
 
 
 @pytest.mark.parametrize("dups", [3, 200], ids=["few-dups", "many-dups"])
