@@ -69,6 +69,106 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
       norm_dst[r] = __ldg(norm_src + __ldg(ids + r));
 }
 
+// select_finish (after launch_select_local): every CTA turns the per-chunk counts
+// into an exclusive prefix table in shared memory; CTA 0 writes the count; in
+// gathered mode (decided here from the count, like gather_copy_kernel) each warp
+// takes 32 consecutive dense positions, each lane resolves its position's chunk
+// by binary search and writes the dense id (and the norm term), then the warp
+// copies the 32 rows with 16-byte vectors.  One launch replaces select_scatter +
+// gather_copy.
+__global__ void __launch_bounds__(256) select_finish_kernel(const uint32_t *__restrict__ chunk_count, int nchunks,
+                                                            const int32_t *__restrict__ ids_local,
+                                                            int64_t *__restrict__ count, int32_t *__restrict__ ids,
+                                                            int allow, int64_t cap, const void *__restrict__ X,
+                                                            int32_t row_bytes, void *__restrict__ xsel,
+                                                            const float *__restrict__ norm_src,
+                                                            float *__restrict__ norm_dst) {
+  extern __shared__ uint32_t s_pre[];   // [nchunks + 1]
+  __shared__ uint32_t s_wsum[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  pdl_trigger();
+  // exclusive prefix of the chunk counts: thread t sums a contiguous segment
+  const int seg = (nchunks + 255) / 256;
+  const int c0 = min(nchunks, tid * seg), c1 = min(nchunks, c0 + seg);
+  uint32_t sum = 0;
+  for (int c = c0; c < c1; ++c) sum += __ldg(chunk_count + c);
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t run = incl - sum;
+  for (int i = 0; i < warp; ++i) run += s_wsum[i];
+  for (int c = c0; c < c1; ++c) {
+    s_pre[c] = run;
+    run += __ldg(chunk_count + c);
+  }
+  if (tid == 255) s_pre[nchunks] = run;
+  __syncthreads();
+  const int64_t total = s_pre[nchunks];
+  if (blockIdx.x == 0 && tid == 0) *count = total;
+  if (!gather_mode(ids, allow, total, cap)) return;
+  const int v16 = row_bytes >> 4;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 32; base < total; base += nwarps * 32) {
+    const int64_t r = base + lane;
+    int32_t src = 0;
+    if (r < total) {
+      int lo = 0, hi = nchunks;   // s_pre[lo] <= r < s_pre[hi]: lo = the last chunk starting at or before r
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)s_pre[mid] <= r) lo = mid; else hi = mid;
+      }
+      src = __ldg(ids_local + (int64_t)lo * kSelChunkRows + (r - s_pre[lo]));
+      ids[r] = src;
+      if (norm_dst) norm_dst[r] = __ldg(norm_src + src);
+    }
+    if (xsel) {
+      const int nr = (int)min((int64_t)32, total - base);
+      // the warp's 32 rows, 32 x v16 vectors, 8 loads in flight per lane
+      for (int it0 = 0; it0 < v16; it0 += 8) {
+        int4 v[8];
+        int64_t dst[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = (it0 + u) * 32 + lane;
+          const int rr = i / v16, vv = i - rr * v16;
+          const int32_t sr = __shfl_sync(0xffffffffu, src, rr & 31);
+          dst[u] = -1;
+          if (it0 + u < v16 && rr < nr) {
+            v[u] = __ldg(reinterpret_cast<const int4 *>(static_cast<const char *>(X) + (int64_t)sr * row_bytes) + vv);
+            dst[u] = (base + rr) * (int64_t)v16 + vv;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dst[u] >= 0) reinterpret_cast<int4 *>(xsel)[dst[u]] = v[u];
+      }
+    }
+  }
+}
+
+cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, const void *xsrc, int32_t row_bytes,
+                                 bool copy, cudaStream_t s) {
+  const int nchunks = (int)select_chunks(a.n);
+  const size_t smem = (size_t)(nchunks + 1) * 4;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(select_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  static const int blocks = getenv("VRS_FINISH_BLOCKS") ? atoi(getenv("VRS_FINISH_BLOCKS")) : 2 * 148;
+  return launch_k(select_finish_kernel, dim3(blocks), dim3(256), smem, s, a.chunk_count, nchunks, a.ids_local,
+                  const_cast<int64_t *>(a.count), const_cast<int32_t *>(a.ids), allow, xcap, xsrc, row_bytes,
+                  copy ? a.xsel : (void *)nullptr, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
+                  copy && a.metric != VRS_IP ? a.xsel_norm : (float *)nullptr);
+}
+
 // fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per
 // search; elements [count, total) are zero (query tiles padded to whole 128-row
 // tiles, so the TMA loads of the query operand never fall out of bounds).
@@ -213,7 +313,12 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   L->bf = bf;
   L->ar = p.nk <= 4 && !no_ar;
   L->rowscale = a.metric == VRS_COSINE;
-  if (xcap > 0 && p.allow_gather && !g4) {
+  if (a.ids_local) {   // count + dense ids (+ gathered rows) from launch_select_local's output
+    ProfScope ps("gemm.gather", s);
+    e = launch_select_finish(a, xcap, xcap > 0 ? (int)p.allow_gather : 0, xsrc, a.d * (bf ? 2 : 4), !g4, s);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+  } else if (xcap > 0 && p.allow_gather && !g4) {
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
                  (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,

@@ -30,10 +30,12 @@ constexpr int kSelWordsPerWarp = 32;
 constexpr int kSelWords = kSelWarps * kSelWordsPerWarp;  // 256 words
 constexpr int kSelRows = kSelWords * 32;                 // 8192 rows per block
 
+static_assert(kSelRows == kSelChunkRows, "chunk size shared with select_finish");
+
 __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred, int64_t n,
                                                                    uint32_t *__restrict__ bitmap,
                                                                    uint32_t *__restrict__ chunk_count,
-                                                                   SelectFuse fz) {
+                                                                   SelectFuse fz, int32_t *__restrict__ ids_local) {
   __shared__ uint32_t s_cnt[kSelWarps];
   pdl_wait();
   pdl_trigger();
@@ -118,6 +120,26 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
     for (int i = 0; i < kSelWarps; ++i) t += s_cnt[i];
     chunk_count[blockIdx.x] = t;
   }
+  if (ids_local != nullptr) {
+    // chunk-local ids (no global prefix needed): warp-cooperative, coalesced, as in
+    // select_scatter_kernel but relative to this chunk's slot range
+    uint32_t wpre = 0;
+    for (int i = 0; i < warp; ++i) wpre += s_cnt[i];
+    const uint32_t pc = __popc(my_word);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int32_t *out = ids_local + (int64_t)blockIdx.x * kSelRows + wpre;
+#pragma unroll 4
+    for (int w = 0; w < 32; ++w) {
+      const uint32_t ww = __shfl_sync(0xffffffffu, my_word, w);
+      const uint32_t before = __shfl_sync(0xffffffffu, incl - pc, w);
+      if ((ww >> lane) & 1u) out[before + __popc(ww & lanemask_lt())] = (int32_t)(base + w * 32 + lane);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, const uint32_t *__restrict__ bitmap,
@@ -173,13 +195,25 @@ cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int3
   const SelectFuse fz = fuse ? *fuse : SelectFuse{};
   const uint32_t nchunks = (uint32_t)((n + kSelRows - 1) / kSelRows);
   uint32_t *chunk_count = static_cast<uint32_t *>(scratch);
-  cudaError_t e0 = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap, chunk_count, fz);
+  cudaError_t e0 = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap, chunk_count, fz,
+                            (int32_t *)nullptr);
   if (e0 != cudaSuccess) return e0;
   if (launches) *launches += 1;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = launch_k(select_scatter_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, n, (const uint32_t *)bitmap,
                (const uint32_t *)chunk_count, ids, count);
+  if (e != cudaSuccess) return e;
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_local(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids_local, void *scratch,
+                                cudaStream_t stream, int *launches, const SelectFuse *fuse) {
+  const SelectFuse fz = fuse ? *fuse : SelectFuse{};
+  const uint32_t nchunks = (uint32_t)((n + kSelRows - 1) / kSelRows);
+  cudaError_t e = launch_k(select_count_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, pred, n, bitmap,
+                           static_cast<uint32_t *>(scratch), fz, ids_local);
   if (e != cudaSuccess) return e;
   if (launches) *launches += 1;
   return cudaGetLastError();

@@ -496,8 +496,14 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                                               : gather_rows)
                                : 0;
   const int64_t xsel_rows = gather_copy ? xsel_cap : 0;   // rows of the X_sel buffer
+  // VRS_SELECT_LOCAL=1: one-kernel selection (chunk-local ids) + select_finish (count, dense
+  // ids, gathered rows in one launch) instead of select_count + select_scatter + gather_copy.
+  // Measured: equal on C2's small cells, 10-20 % slower gathers on C5 -- so opt-in.
+  static const bool want_local = getenv("VRS_SELECT_LOCAL") != nullptr;
+  const bool sel_local = want_local && path == VRS_PATH_GEMM && !identity && select_chunks(n) <= kSelFinishMaxChunks;
+  const size_t local_ids = sel_local ? (size_t)select_chunks(n) * kSelChunkRows : 0;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
-                                   part_entries * 4, part_entries * 4,
+                                   local_ids * 4, part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
                                    (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4,
                                    use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
@@ -508,6 +514,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   int32_t *sel_ids = identity ? nullptr : cv.take<int32_t>((size_t)n);
   int64_t *count = cv.take<int64_t>(1);
   void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
+  int32_t *ids_local = sel_local ? cv.take<int32_t>(local_ids) : nullptr;
   float *part_key = cv.take<float>(part_entries);
   int32_t *part_id = cv.take<int32_t>(part_entries);
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
@@ -533,11 +540,14 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     if (!identity) {   // (the bf16 query conversion rides along)
       ProfScope ps("select", stream);
       const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
-      CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
+      if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
+      else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
     }
     GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
                use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+    a.ids_local = ids_local;
+    a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
     {
       ProfScope ps("gemm", stream);
       CUDA_TRY(launch_gemm(a, gp, gemm_scr, stream, &launches));
@@ -627,7 +637,10 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const int64_t xsel_rows = gather_copy ? xsel_cap : 0;
   const int L = 2 * gp.P;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
-  st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
+  static const bool want_local = getenv("VRS_SELECT_LOCAL") != nullptr;   // (as in vrs_search_ex)
+  const bool sel_local = want_local && !identity && select_chunks(n) <= kSelFinishMaxChunks;
+  const size_t local_ids = sel_local ? (size_t)select_chunks(n) * kSelChunkRows : 0;
+  st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n), local_ids * 4,
                                       (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4, use_bf16 ? qpad_bytes : 0,
                                       (size_t)q * 4,
                                       (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4}));
@@ -637,6 +650,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int32_t *sel_ids = identity ? nullptr : cv.take<int32_t>((size_t)n);
   int64_t *count = cv.take<int64_t>(1);
   void *sel_scratch = cv.take<char>(select_scratch_bytes(n));
+  int32_t *ids_local = sel_local ? cv.take<int32_t>(local_ids) : nullptr;
   void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
   float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
   void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
@@ -663,11 +677,14 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
   if (!identity) {
     const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
-    CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
+    if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
+    else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
   }
   GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
              queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
              use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+  a.ids_local = ids_local;
+  a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));
   int64_t C = 0;
   CUDA_TRY(cudaMemcpyAsync(&C, r.coff + (size_t)L * q, 8, cudaMemcpyDeviceToHost, stream));

@@ -33,6 +33,15 @@ struct SelectFuse {
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
                           void *scratch, cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
 size_t select_scratch_bytes(int64_t n);
+// One-kernel selection for the tensor-core path: bitmap, per-chunk counts (scratch,
+// select_scratch_bytes) and chunk-local ids (ids_local[c * kSelChunkRows + j], the
+// j-th selected row of chunk c); select_finish (gemm_tc.cu) turns them into the
+// count, the dense ids and -- in gathered mode -- the copied rows.
+constexpr int kSelChunkRows = 8192;
+constexpr int kSelFinishMaxChunks = 56 * 1024;   // prefix table in <= 224 KB of shared memory
+inline int64_t select_chunks(int64_t n) { return (n + kSelChunkRows - 1) / kSelChunkRows; }
+cudaError_t launch_select_local(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids_local, void *scratch,
+                                cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
 
 // scan.cu -- K6' norms, K2' scan + fused top-k
 cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *zero_flag,
@@ -90,6 +99,10 @@ struct GemmArgs {
   const void *Xb;           // bf16 shadow corpus [n x d] (bf16 only)
   void *Qb;                 // scratch [q x d] bf16 queries (bf16 only)
   int32_t prepped;          // 1: the select kernels already converted the queries
+  // launch_select_local's output (nullptr: ids / count were written by launch_select):
+  // the tensor-core pass first runs select_finish -> count, dense ids, gathered rows
+  const int32_t *ids_local = nullptr;
+  const uint32_t *chunk_count = nullptr;
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
 cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s);
