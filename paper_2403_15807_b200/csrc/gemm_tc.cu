@@ -359,10 +359,18 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
     static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
     pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 ? 8 : 0);
+    // one wave: the probe's CTAs are few-tile items, so fixed per-CTA costs (prologue,
+    // pipeline fill / drain) dominate over several waves -- use at most 148 / qtiles
+    // splits (the same density: the step follows the main pass's span)
+    static const bool full_p = getenv("VRS_PROBE_FULLP") != nullptr;
+    const int32_t p_probe = full_p ? plan.P : std::max(1, std::min(plan.P, kSmCountB200 / std::max(1, plan.qtiles)));
+    pp.P = p_probe;
+    pp.P_main = plan.P;
+    pp.min_p_main = p.min_p;
     e = tc_launch_mode<MODE_PROBE>(L, pp, s);
     if (e != cudaSuccess) return e;
-    ThresholdArgs ta{gs.probe_max, plan.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
-                     SplitInfo{a.ids, a.count, p.allow_gather, plan.P, a.n, p.xsel_cap, tc::BN, p.min_span, p.min_p}};
+    ThresholdArgs ta{gs.probe_max, pp.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
+                     SplitInfo{a.ids, a.count, p.allow_gather, pp.P, a.n, p.xsel_cap, tc::BN, p.min_span, p.min_p}};
     ProfScope pt("gemm.threshold", s);
     e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;

@@ -179,8 +179,9 @@ struct TcParams {
   int32_t qtiles;
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
-  int32_t probe_div;
-  int32_t g4;              // gather mode loads rows by TMA gather4 from X via ids (tmap_g); else from X_sel       // probe: > 0 => step = clamp(span / probe_div, 2, tile_step) (device-side span)
+  int32_t probe_div;       // probe: > 0 => step = clamp(main span / probe_div, 2, tile_step) (device-side span)
+  int32_t P_main, min_p_main;   // probe: the main pass's splits (its span sets the density); 0 = P
+  int32_t g4;              // gather mode loads rows by TMA gather4 from X via ids (tmap_g); else from X_sel
   int32_t min_span;        // used splits span >= this many row tiles (splits_used) ...
   int32_t min_p;           // ... unless that leaves fewer than min_p splits
   const uint32_t *bitmap;  // nullptr => every row qualifies
@@ -357,7 +358,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // probe_div, short items (small selections) probe densely: their main pass is
   // slow-path bound, so a tighter threshold pays more than the denser probe costs
   int64_t step_cap = p.tile_step;
-  if (p.probe_div > 0) step_cap = std::min<int64_t>(step_cap, std::max<int64_t>(2, span / p.probe_div));
+  if (p.probe_div > 0) {   // density from the main pass's span (the probe may use fewer, longer splits)
+    const int64_t main_span = p.P_main > 0 ? row_tiles / used_splits(row_tiles, p.P_main, p.min_span, p.min_p_main) : span;
+    step_cap = std::min<int64_t>(step_cap, std::max<int64_t>(2, main_span / p.probe_div));
+  }
   const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(step_cap, std::max<int64_t>(1, span)) : 1;
   const int ntiles = (int)((span + step - 1) / step);
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
