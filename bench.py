@@ -116,6 +116,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of replaying the step's captured CUDA graph (N = 1)")
     return ap.parse_args()
 
 
@@ -258,6 +260,20 @@ def main():
         step()
     torch.cuda.synchronize()
     barrier()
+    # N = 1: the step (every cell's launches, scratch allocation included) is captured
+    # once as a CUDA graph and replayed, so tiny configs measure the GPU, not Python's
+    # launch loop (C1: ~40 us of host time per call against ~40 us of kernels)
+    graph = None
+    if world == 1 and not args.no_graph:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        launches[0] = 0
+        with torch.cuda.graph(graph, stream=cap):
+            step()
+        launches_per_step = launches[0]
+        graph.replay()
+        torch.cuda.synchronize()
 
     # ---------------- timed region
     stream = torch.cuda.current_stream()
@@ -268,7 +284,10 @@ def main():
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
     for i in range(args.steps):
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
         step_ev[i].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -276,7 +295,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     step_ms = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
-    gpu_launches = launches[0]
+    gpu_launches = launches_per_step * args.steps if graph is not None else launches[0]
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -500,6 +519,8 @@ def main():
                 "dtype_note": "tensor-core selection operands (fp32 accumulate); returned dists re-scored in fp64 from fp32",
                 "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+                "timing": ("CUDA graph of the step (captured once, outside the timed region), replayed K times"
+                           if graph is not None else "eager launches"),
                 "parity": parity, "cells": cell_out, "range_search": range_out, "step_ms": [round(x, 4) for x in step_ms],
                 "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
         print(json.dumps(line), flush=True)

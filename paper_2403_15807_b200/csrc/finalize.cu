@@ -743,14 +743,14 @@ __device__ double fin_qq(const FinalizeArgs &a, int64_t j) {
 // Step 5 (one warp).
 // Bitonic sort of <= 32 (score, id) pairs held one per lane: best first (score
 // descending, then id ascending -- ids are unique, so the order is strict).
-__device__ __forceinline__ void warp_reg_sort_desc(double &key, int64_t &id) {
+__device__ __forceinline__ void warp_reg_sort_desc(double &key, int32_t &id) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
       const double pk = __shfl_xor_sync(0xffffffffu, key, jj);
-      const int64_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
+      const int32_t pid = __shfl_xor_sync(0xffffffffu, id, jj);
       const bool partner_first = pk > key || (pk == key && pid < id);
       const bool keep_first = ((lane & k) == 0) == ((lane & jj) == 0);   // this slot holds the better of the pair
       if (keep_first == partner_first) { key = pk; id = pid; }
@@ -760,10 +760,26 @@ __device__ __forceinline__ void warp_reg_sort_desc(double &key, int64_t &id) {
 
 __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double qq, double *sc, int64_t *sid) {
   const int lane = threadIdx.x & 31;
-  if (m <= 32) {   // registers: one candidate per lane
+  const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
+  const int mv = zero_cos ? 0 : min(m, a.k);
+  const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
+  if (m <= 32) {   // registers: one candidate per lane (local row ids fit 32 bits)
     double key = lane < m ? sc[lane] : -INFINITY;
-    int64_t id = lane < m ? sid[lane] : INT64_MAX;
+    int32_t id = lane < m ? (int32_t)sid[lane] : INT32_MAX;
     warp_reg_sort_desc(key, id);
+    if (a.k <= 32) {   // lane r holds rank r: write straight from registers
+      if (lane < a.k) {
+        const int64_t o = j * a.k + lane;
+        if (lane < mv) {
+          a.ids[o] = a.row_offset + id;
+          a.dists[o] = (float)(a.metric == VRS_L2 ? -key : key);
+        } else {
+          a.ids[o] = -1;
+          a.dists[o] = pad;
+        }
+      }
+      return;
+    }
     __syncwarp();
     sc[lane] = key;
     sid[lane] = id;
@@ -775,9 +791,6 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
     __syncwarp();
     warp_sort_desc_d(sc, sid, np);
   }
-  const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
-  const int mv = zero_cos ? 0 : min(m, a.k);
-  const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
   for (int r = lane; r < a.k; r += 32) {
     const int64_t o = j * a.k + r;
     if (r < mv) {
