@@ -24,8 +24,11 @@ def short(name):
             mode = {"0": "main", "1": "probe", "2": "range-count", "3": "range-fill"}[m.group(2)]
             return f"vrs::tc_topk_kernel[{mode}]"
     name = re.sub(r"\(.*", "", name)
-    name = re.sub(r"<.*", "", name)
+    targs = re.search(r"<(.*)>", name)
+    name = re.sub(r"<.*", "", name).replace("void ", "")
     name = name.split("::")[-1].strip()
+    if mine and targs and ("finalize" in name or "threshold" in name):   # template variants, e.g. <256, 64>
+        name += "<" + targs.group(1) + ">"
     return ("vrs::" + name) if mine else name
 
 
