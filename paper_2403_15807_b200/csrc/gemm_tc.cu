@@ -355,7 +355,10 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // bound); small batches are HBM-bound and want the cheapest probe
     // (C2 measurements: 1/8 best at Q = 4096, 1/16 at Q = 256, 1/32 at Q = 16)
     static const int probe_env = getenv("VRS_PROBE_STEP") ? atoi(getenv("VRS_PROBE_STEP")) : 0;
-    pp.tile_step = probe_env > 0 ? probe_env : (a.q >= 1024 ? 8 : (a.q >= 64 ? tc::PROBE_STEP : 32));
+    // (large d: the main pass is MMA-bound and its epilogue has slack, so a sparser probe
+    // costs the main pass nothing -- C3 Q = 1024: 13.4 -> 12.5 ms, C4 Q = 8192 s = 50 %:
+    // 72 -> 68 ms at step 16; step 32 overflows C4's lists, r01_s3_probe_step_large_d.txt)
+    pp.tile_step = probe_env > 0 ? probe_env : (a.q >= 1024 ? (a.d >= 512 ? 16 : 8) : (a.q >= 64 ? tc::PROBE_STEP : 32));
     // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
     static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
     pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 ? 8 : 0);
