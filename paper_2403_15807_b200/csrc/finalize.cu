@@ -1167,11 +1167,8 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   const size_t wsmem = a.kth > 128 ? (size_t)kFinGroup * a.nvals * 4 : 0;
   if (!block_thr && a.q >= 4 * kSmCountB200 && wsmem <= 96 * 1024) {
     static size_t wattr = 0;
-    if (wsmem > 48 * 1024 && wsmem > wattr) {
-      cudaError_t e = cudaFuncSetAttribute(threshold_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
-      if (e != cudaSuccess) return e;
-      wattr = wsmem;
-    }
+    const cudaError_t e = ensure_smem_attr(threshold_warp_kernel, wsmem, wattr);
+    if (e != cudaSuccess) return e;
     return launch_k(threshold_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32),
                     wsmem, s, a);
   }
@@ -1184,14 +1181,10 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
                : launch_k(threshold_union_kernel<8, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(threshold_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(threshold_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static size_t attr1024 = 0, attr256 = 0;
+  cudaError_t e = ensure_smem_attr(threshold_kernel<1024>, smem, attr1024);
+  if (e == cudaSuccess) e = ensure_smem_attr(threshold_kernel<256>, smem, attr256);
+  if (e != cudaSuccess) return e;
   if (a.q < kSmCountB200) return launch_k(threshold_kernel<1024>, dim3((unsigned)a.q), dim3(1024), smem, s, a);
   return launch_k(threshold_kernel<256>, dim3((unsigned)a.q), dim3(256), smem, s, a);
 }

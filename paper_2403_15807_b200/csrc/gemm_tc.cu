@@ -157,11 +157,8 @@ cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, con
   const int nchunks = (int)select_chunks(a.n);
   const size_t smem = (size_t)(nchunks + 1) * 4;
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(select_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  const cudaError_t e = ensure_smem_attr(select_finish_kernel, smem, attr);
+  if (e != cudaSuccess) return e;
   static const int blocks = getenv("VRS_FINISH_BLOCKS") ? atoi(getenv("VRS_FINISH_BLOCKS")) : 2 * 148;
   return launch_k(select_finish_kernel, dim3(blocks), dim3(256), smem, s, a.chunk_count, nchunks, a.ids_local,
                   const_cast<int64_t *>(a.count), const_cast<int32_t *>(a.ids), allow, xcap, xsrc, row_bytes,

@@ -863,20 +863,14 @@ static TcKernel pick_kernel(bool ar, bool rowscale) {
 // translation unit that calls this).  VRS_STATS=1 prints the epilogue counters.
 template <int MODE>
 static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStream_t s) {
-  static bool attr_set = false;
-  cudaError_t e = cudaSuccess;
-  if (!attr_set) {
-    for (bool ar_ : {false, true})
-      for (bool rs : {false, true})
-        for (TcKernel fn : {pick_kernel<MODE, false>(ar_, rs), pick_kernel<MODE, true>(ar_, rs)})
-          if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static size_t attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per variant (AR, ROWSCALE, BF)
+  cudaError_t e = ensure_smem_attr(L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale)
+                                        : pick_kernel<MODE, false>(L.ar, L.rowscale),
+                                   tc::SMEM_BYTES, attr[(L.ar ? 4 : 0) | (L.rowscale ? 2 : 0) | (L.bf ? 1 : 0)]);
+  if (e != cudaSuccess) return e;
   const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale) : pick_kernel<MODE, false>(L.ar, L.rowscale);
   static unsigned long long *stats = nullptr;
-  static const bool want_stats = getenv("VRS_STATS") != nullptr;
+  static const bool want_stats = getenv("VRS_STATS") != nullptr;   // (debug counters, single-threaded use)
   if (want_stats && !stats) cudaMalloc(&stats, 64);
   TcParams p2 = pr;
   p2.stats = want_stats ? stats : nullptr;

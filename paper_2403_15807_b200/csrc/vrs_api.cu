@@ -182,15 +182,18 @@ static vrs_status scratch_alloc(Scratch &s, size_t bytes) {
     if (!s.ptr) return fail(VRS_ENOMEM, "allocator returned NULL for %zu bytes", bytes);
     return VRS_OK;
   }
-  static bool pool_tuned = false;
-  if (!pool_tuned) {  // keep freed scratch in the pool instead of returning it to the driver
+  {  // keep freed scratch in each device's pool instead of returning it to the driver
+    static uint64_t tuned = 0;   // bit per device
     int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
+      std::lock_guard<std::mutex> g(setup_mutex());
+      cudaMemPool_t pool;
+      if (!(tuned >> dev & 1) && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        tuned |= uint64_t(1) << dev;
+      }
     }
-    pool_tuned = true;
   }
   cudaError_t e = cudaMallocAsync(&s.ptr, bytes, s.stream);
   if (e != cudaSuccess) {

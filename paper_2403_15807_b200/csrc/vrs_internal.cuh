@@ -10,6 +10,7 @@
 
 #include <stdlib.h>
 
+#include <mutex>
 #include <utility>
 
 namespace vrs {
@@ -40,6 +41,25 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// ---- host-side one-time setup ---------------------------------------------------
+// Function attributes and pool tuning are set lazily on first use, possibly from
+// several host threads at once: serialised here.
+inline std::mutex &setup_mutex() {
+  static std::mutex m;
+  return m;
+}
+// Raise a kernel's dynamic shared-memory limit to >= bytes (done: the limit this
+// call site already set; idempotent, thread-safe).
+template <typename Kern>
+inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes, size_t &done) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  std::lock_guard<std::mutex> g(setup_mutex());
+  if (bytes <= done) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done = bytes;
+  return e;
 }
 
 // One clause of theta_R in device form: the [lo, hi] interval clamped to the
