@@ -131,7 +131,7 @@ def workload_desc(cfg, world):
             "k": cfg.k, "rows_per_gpu": datagen.rows_of(cfg, world, 0)[1],
             "selectivities": list(cfg.sels), "queries_per_cell": list(cfg.qs), "cells": len(cells_of(cfg)),
             "data": "synthetic, seeded (datagen)", "l2_flush": "inputs > L2 (corpus %.0f MB per GPU)" % (datagen.rows_of(cfg, world, 0)[1] * cfg.d * 4 / 1e6),
-            "parallelism": f"rows sharded over {world} GPU(s), NCCL all-gather + merge" if world > 1 else "1 GPU"}
+            "parallelism": f"rows sharded over {world} GPU(s), one NCCL all-gather per step + merge" if world > 1 else "1 GPU"}
 
 
 # --------------------------------------------------------------------------- oracle legs
@@ -216,8 +216,15 @@ def main():
     cells = cells_of(cfg)
     preds = {s: datagen.predicate(cfg, s) for s in cfg.sels}
     k, metric = cfg.k, cfg.metric
-    bufs = {c: (torch.empty(c[1], k, dtype=torch.int64, device=dev), torch.empty(c[1], k, dtype=torch.float32, device=dev))
-            for c in cells}
+    # every cell's local results are views of two step-wide buffers, so that N > 1 merges
+    # the whole step with ONE all-gather per array and ONE vrs_merge (not one per cell)
+    q_tot = sum(q for _, q in cells)
+    ids_all = torch.empty(q_tot, k, dtype=torch.int64, device=dev)
+    dists_all = torch.empty(q_tot, k, dtype=torch.float32, device=dev)
+    bufs, q0 = {}, 0
+    for c in cells:
+        bufs[c] = (ids_all[q0:q0 + c[1]], dists_all[q0:q0 + c[1]])
+        q0 += c[1]
     if world > 1:
         import torch.distributed as dist
         from paper_2403_15807_b200.dist import gather_merge
@@ -225,12 +232,12 @@ def main():
 
     cell_path = {}
 
-    def run_cell(c):
+    def run_cell(c, merge=True):
         s, q = c
         ids, dists = ix.search(Qall[:q], preds[s], k=k, metric=metric, out=bufs[c])
         launches[0] += vrs.last_launches()
         cell_path[c] = vrs.last_path()
-        if world > 1:
+        if world > 1 and merge:
             out = gather_merge(ids, dists, k, metric)   # NCCL all-gather + vrs_merge
             launches[0] += 1
             return out
@@ -238,7 +245,10 @@ def main():
 
     def step():
         for c in cells:
-            run_cell(c)
+            run_cell(c, merge=False)
+        if world > 1:   # the step's results: one NCCL all-gather per array + one vrs_merge
+            gather_merge(ids_all, dists_all, k, metric)
+            launches[0] += 1
 
     def barrier():
         if world > 1:
@@ -445,10 +455,14 @@ def main():
                 ix.search_host(qh[q], preds[s], k=k, metric=metric, out=hb[c], host_async=2)
             else:
                 qd[q].copy_(qh[q], non_blocking=True)
-                ids, dists = ix.search(qd[q], preds[s], k=k, metric=metric, out=bufs[c])
-                mi, md = gather_merge(ids, dists, k, metric)
-                hb[c][0].copy_(mi, non_blocking=True)
-                hb[c][1].copy_(md, non_blocking=True)
+                ix.search(qd[q], preds[s], k=k, metric=metric, out=bufs[c])
+        if world > 1:   # one all-gather + merge for the step, results to the host
+            mi, md = gather_merge(ids_all, dists_all, k, metric)
+            q0 = 0
+            for c in cells:
+                hb[c][0].copy_(mi[q0:q0 + c[1]], non_blocking=True)
+                hb[c][1].copy_(md[q0:q0 + c[1]], non_blocking=True)
+                q0 += c[1]
         if world == 1:
             ix.host_fence(stream)   # the step's event covers every result download
         step_done[slot].record(stream)
