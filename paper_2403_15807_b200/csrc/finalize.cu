@@ -587,7 +587,7 @@ template <int CAP>
 __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP> &B) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
-  const int lists = a.split.bn ? (int)min((int64_t)a.lists, 2 * splits_used(a.split)) : a.lists;
+  const int lists = a.split.bn ? (int)min((int64_t)a.lists, kListsPerSplit * splits_used(a.split)) : a.lists;
   uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
   if (a.sorted && K <= a.kread) {
     for (int l = lane; l < lists; l += 32) {
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   const float *v = a.vals + j * a.nvals;
   pdl_wait();
   pdl_trigger();
-  const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);   // lists of used splits only
+  const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);   // lists of used splits only
   __shared__ uint32_t s_lo[32], s_hi[32], s_cnt[32], s_cv[64];
   __shared__ int s_bstar, s_upto, s_got;
   // fast path: min / max, one histogram over value buckets, the <= 64 values
@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   pdl_trigger();
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
-  const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
+  const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);
   if (a.kth > 128) {
     uint32_t *mine = s_vals + (size_t)w * a.nvals;
     for (int i = lane; i < nvals; i += 32) {
@@ -1139,7 +1139,7 @@ __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs 
   pdl_wait();
   pdl_trigger();
   const float *v = a.vals + j * a.nvals;
-  const int nvals = (int)min((int64_t)a.nvals, 2 * splits_used(a.split) * 32);
+  const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);
   float t[E];
   lane_top_sorted<E, NW * 32>(v, nvals, w * 32 + lane, t);
   int32_t id[E];

@@ -19,7 +19,7 @@
 //                           satisfies tau (the definition's own comparison)
 //   range_prefix_kernel     per-query result offsets (the caller's), total R
 //   -- host: read R, check the caller's capacity --
-//   range_write_kernel      per query, the two lists of each split merged by row
+//   range_write_kernel      per query, the kListsPerSplit lists of each split merged by row
 //                           id, splits in order -> ascending ids, exact dists
 #include "tc_kernel.cuh"
 
@@ -192,12 +192,13 @@ __global__ void __launch_bounds__(kRwThreads) range_write_kernel(const int32_t *
   __shared__ int64_t s_warp[kRwThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t j = blockIdx.x;
-  const int L = 2 * P;
+  constexpr int LPS = kListsPerSplit;
+  const int L = LPS * P;
   const int per = (P + kRwThreads - 1) / kRwThreads;
   const int s0 = min(P, tid * per), s1 = min(P, s0 + per);
   const int64_t *seg = coff + j * L;
   int64_t mine = 0;
-  for (int64_t c = seg[2 * s0]; c < seg[2 * s1]; ++c) mine += keep[c];
+  for (int64_t c = seg[LPS * s0]; c < seg[LPS * s1]; ++c) mine += keep[c];
   int64_t incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -210,10 +211,21 @@ __global__ void __launch_bounds__(kRwThreads) range_write_kernel(const int32_t *
   for (int i = 0; i < warp; ++i) before += s_warp[i];
   int64_t o = offsets[j] + before + incl - mine;
   for (int s = s0; s < s1; ++s) {
-    int64_t a = seg[2 * s], ae = seg[2 * s + 1], b = seg[2 * s + 1], be = seg[2 * s + 2];
-    while (a < ae || b < be) {
-      const bool take_a = b >= be || (a < ae && cand[a] < cand[b]);
-      const int64_t c = take_a ? a++ : b++;
+    // the split's LPS lists (each ascending, interleaved column ranges) merged by row id
+    int64_t h[LPS], he[LPS];
+#pragma unroll
+    for (int l = 0; l < LPS; ++l) { h[l] = seg[LPS * s + l]; he[l] = seg[LPS * s + l + 1]; }
+    for (;;) {
+      int best = -1;
+      int32_t bid = 0;
+#pragma unroll
+      for (int l = 0; l < LPS; ++l)
+        if (h[l] < he[l] && (best < 0 || cand[h[l]] < bid)) { best = l; bid = cand[h[l]]; }
+      if (best < 0) break;
+      int64_t c = 0;
+#pragma unroll
+      for (int l = 0; l < LPS; ++l)
+        if (l == best) c = h[l]++;
       if (!keep[c]) continue;
       ids[o] = row_offset + cand[c];
       dists[o] = (float)score[c];
@@ -242,7 +254,7 @@ cudaError_t launch_range_count(const GemmArgs &a, const GemmPlan &plan, RangeSta
     e = tc_launch_mode<MODE_RCOUNT>(L, p, s);
     if (e != cudaSuccess) return e;
   }
-  e = launch_k(range_prefix_kernel, dim3(1), dim3(1024), 0, s, (const int32_t *)r.cand_cnt, a.q, 2 * plan.P, r.coff);
+  e = launch_k(range_prefix_kernel, dim3(1), dim3(1024), 0, s, (const int32_t *)r.cand_cnt, a.q, kListsPerSplit * plan.P, r.coff);
   if (launches) *launches += 3;
   return e;
 }
@@ -263,7 +275,7 @@ cudaError_t launch_range_fill(const GemmArgs &a, const GemmPlan &plan, RangeStat
   {
     ProfScope ps("range.verify", s);
     e = launch_k(range_verify_kernel, dim3((unsigned)a.q), dim3(kRvWarps * 32), 0, s, a.X, a.d, a.Q, a.metric, r.tau,
-                 (const int32_t *)r.cand, (const int64_t *)r.coff, 2 * plan.P, r.score, r.keep, r.kept);
+                 (const int32_t *)r.cand, (const int64_t *)r.coff, kListsPerSplit * plan.P, r.score, r.keep, r.kept);
     if (e != cudaSuccess) return e;
   }
   e = launch_k(range_prefix_kernel, dim3(1), dim3(1024), 0, s, (const int32_t *)r.kept, a.q, 1, r.offsets);

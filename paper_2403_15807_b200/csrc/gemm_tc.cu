@@ -242,7 +242,7 @@ struct GemmScratch {
   size_t bytes;
 };
 GemmScratch carve_gemm(void *base, const GemmPlan &plan, int64_t q, int32_t kprime) {
-  const size_t lists = (size_t)plan.P * 2;
+  const size_t lists = (size_t)plan.P * kListsPerSplit;
   const size_t cap = (size_t)kp_of(kprime) * tc::CAP_FACTOR;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   char *p = static_cast<char *>(base);
@@ -369,7 +369,7 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     pp.min_p_main = p.min_p;
     e = tc_launch_mode<MODE_PROBE>(L, pp, s);
     if (e != cudaSuccess) return e;
-    ThresholdArgs ta{gs.probe_max, pp.P * 2 * tc::SLOTS, a.q, a.kprime, gs.gtau,
+    ThresholdArgs ta{gs.probe_max, pp.P * kListsPerSplit * tc::SLOTS, a.q, a.kprime, gs.gtau,
                      SplitInfo{a.ids, a.count, p.allow_gather, pp.P, a.n, p.xsel_cap, tc::BN, p.min_span, p.min_p}};
     ProfScope pt("gemm.threshold", s);
     e = launch_threshold(ta, s);
@@ -392,7 +392,7 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
   l.key = gs.cand_key;
   l.id = gs.cand_id;
   l.cnt = gs.cand_cnt;
-  l.lists = plan.P * 2;
+  l.lists = plan.P * kListsPerSplit;
   l.stride = kp_of(a.kprime) * tc::CAP_FACTOR;
   l.gtau = gs.gtau;
   l.split = SplitInfo{a.ids, a.count, a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1), plan.P, a.n,

@@ -29,12 +29,14 @@ constexpr int B_BYTES = BN * BK * 4;   // 32 KB at BN = 256
 constexpr int ACC_STAGES = 512 / BN;   // accumulator tiles in TMEM (all 512 columns)
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARP0 = 4;
-constexpr int EPI_WARPS = 8;    // 2 per TMEM lane quadrant, each owning half of the tile's columns
-constexpr int EPI_COLS = BN / 2;
+constexpr int LPS = kListsPerSplit;   // lists per split = epilogue warps per TMEM lane quadrant
+constexpr int EPI_WARPS = 4 * LPS;    // each owns BN / LPS columns of a quadrant's 32 rows (queries)
+constexpr int EPI_COLS = BN / LPS;
+static_assert(EPI_COLS % 32 == 0, "whole 32-column chunks per epilogue warp");
 constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int CAP_FACTOR = 4;   // candidate buffer = CAP_FACTOR * KP entries per (list, query)
 constexpr int BIAS_STAGES = 4;
-constexpr int STAGE_COLS = 16;  // per-warp key staging: one private row of 16 fp32 per lane
+constexpr int STAGE_COLS = 8;   // per-warp key staging: one private row of 8 fp32 (a group's keys) per lane
 constexpr int SLOTS = 32;       // probe: row slots per lane (column index mod 32)
 constexpr int PROBE_STEP = 16;  // probe pass: every 16th row tile (8 / 32 for large / small batches)
 constexpr int GROUPS = BN / 8;  // 8-column key-bound groups per tile
@@ -585,13 +587,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // ------------------------------------------------ epilogue
     const int ew = warp - EPI_WARP0;
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;                      // which 128 of the tile's 256 columns
+    const int half = ew >> 2;                      // which BN / LPS of the tile's columns
     const int m = quad * 32 + lane;                // query row within the tile
     const int64_t qg = (int64_t)qtile * BM + m;    // global query index
     const bool active = qg < p.q;
-    const int list = split * 2 + half;             // candidate list index
+    const int list = split * LPS + half;           // candidate list index
     const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
-    const int64_t cbase = MODE == MODE_RFILL ? (active ? p.coff[qg * (2 * p.P) + list] : 0)
+    const int64_t cbase = MODE == MODE_RFILL ? (active ? p.coff[qg * (LPS * p.P) + list] : 0)
                                              : ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
     float *ckey = p.cand_key + (MODE == MODE_RFILL ? 0 : cbase);
     int32_t *cid = p.cand_id + cbase;
@@ -814,7 +816,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     if (active) {
       if (MODE == MODE_PROBE) {
-        float4 *dst = reinterpret_cast<float4 *>(p.probe_max + ((qg * (2 * p.P)) + list) * SLOTS);
+        float4 *dst = reinterpret_cast<float4 *>(p.probe_max + ((qg * (LPS * p.P)) + list) * SLOTS);
 #pragma unroll
         for (int i = 0; i < SLOTS; i += 4) dst[i / 4] = make_float4(smax[i], smax[i + 1], smax[i + 2], smax[i + 3]);
       } else if (MODE != MODE_RFILL) {

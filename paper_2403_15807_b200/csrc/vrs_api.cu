@@ -638,7 +638,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
                                               : gather_rows)
                                : 0;
   const int64_t xsel_rows = gather_copy ? xsel_cap : 0;
-  const int L = 2 * gp.P;
+  const int L = kListsPerSplit * gp.P;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
   static const bool want_local = getenv("VRS_SELECT_LOCAL") != nullptr;   // (as in vrs_search_ex)
   const bool sel_local = want_local && !identity && select_chunks(n) <= kSelFinishMaxChunks;

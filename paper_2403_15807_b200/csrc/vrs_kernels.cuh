@@ -67,6 +67,14 @@ int scan_query_group(int64_t q, int d, int kpe);
 cudaError_t launch_scan(const ScanArgs &a, int qg, int kpe, cudaStream_t s, int *launches);
 
 // gemm_tc.cu -- K3' tcgen05 GEMM + fused top-k epilogue
+// Candidate lists per row split of the tensor-core pass: each of the epilogue's
+// 4 x kListsPerSplit warps (4 TMEM lane quadrants) owns BN / kListsPerSplit
+// columns of every tile and one (list, query) buffer per query.
+#ifndef VRS_LPS
+#define VRS_LPS 2
+#endif
+constexpr int kListsPerSplit = VRS_LPS;
+
 struct GemmPlan {
   int32_t P;        // row splits = candidate lists per query
   int32_t qtiles;   // query tiles of 128
@@ -151,7 +159,7 @@ struct ThresholdArgs {
   int64_t q;
   int32_t kth;
   uint32_t *gtau;          // [q] ordered-u32 out (0 = fewer than kth finite values)
-  SplitInfo split;         // values [list][32] per query: only lists < 2 * splits_used() are read
+  SplitInfo split;         // values [list][32] per query: only lists < kListsPerSplit * splits_used() are read
 };
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s);
 
