@@ -157,6 +157,21 @@ __host__ __device__ constexpr uint32_t mma_idesc(int M, int N, bool bf16) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                  \
       : "r"(taddr))
 
+#define TMEM_LD_32x32b_X64(taddr, r)                                                                              \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,"   \
+      "%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"                            \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),  \
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),      \
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),     \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),     \
+        "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),     \
+        "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),     \
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),     \
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])                  \
+      : "r"(taddr))
+
 // Wait for this thread's outstanding tcgen05.ld; the registers are tied to the
 // wait so no use of them can be scheduled above it.
 #define TMEM_LD_WAIT(r)                                                                                           \
@@ -201,7 +216,7 @@ struct TcParams {
   const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
-  int32_t epi_skip;        // debug: epilogue only drains TMEM (pipeline-bound measurement)
+  int32_t epi_skip;        // debug: 1 = the epilogue skips the read-out (MMA + TMA bound), 2 = read-out only
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -792,15 +807,50 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
       const int g0 = bs * GROUPS + half * (EPI_COLS / 8);   // this warp's first group
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
-      if (!p.epi_skip) {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
+#ifndef VRS_EPI_X64
+      if (p.epi_skip != 1) {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
         uint32_t ra[32];
 #pragma unroll 1
         for (int c = 0; c < EPI_COLS / 32; ++c) {
           TMEM_LD_32x32b_X32(tbase + c * 32, ra);
           TMEM_LD_WAIT(ra);
+          if (p.epi_skip == 2) {   // debug: read-out only (keeps the loads live)
+            uint32_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x ^= ra[i];
+            if (x == 0x9e3779b9u && p.stats) atomicAdd(p.stats + 3, 1ull);
+            continue;
+          }
           chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, g_bmax + g0 + c * 4, g_amax + g0 + c * 4, g_amin + g0 + c * 4);
         }
       }
+#else
+      if (p.epi_skip != 1) {
+        // A/B (VRS_EPI_X64): two chunks per tcgen05.ld (32x32b.x64, 64 registers).  Box-
+        // dependent: -12 % on one box, +4 % on others (r01_s3_tmem_x64_ab.txt) -- opt-in
+        static_assert((EPI_COLS / 32) % 2 == 0, "pairs of chunks");
+        uint32_t ra[64];
+#pragma unroll 1
+        for (int c = 0; c < EPI_COLS / 32; c += 2) {
+          TMEM_LD_32x32b_X64(tbase + c * 32, ra);
+          TMEM_LD_WAIT(ra);
+          TMEM_LD_WAIT(reinterpret_cast<uint32_t(&)[32]>(ra[32]));
+          if (p.epi_skip == 2) {   // debug: read-out only (keeps the loads live)
+            uint32_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) x ^= ra[i];
+            if (x == 0x9e3779b9u && p.stats) atomicAdd(p.stats + 3, 1ull);
+            continue;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = c + h;
+            chunk(reinterpret_cast<uint32_t(&)[32]>(ra[32 * h]), ba + cc * 32, bb + cc * 32, rid + cc * 32,
+                  g_bmax + g0 + cc * 4, g_amax + g0 + cc * 4, g_amin + g0 + cc * 4);
+          }
+        }
+      }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -1,0 +1,12 @@
+#!/bin/bash
+# 64-column TMEM loads (libvrs_exp: -DVRS_EPI_X64) vs 32
+cd $GRAFT_REPO_ROOT
+O=gpurun_out; P=${PFX:-ay}
+VRS_LIB=exp timeout 900 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_range.py -x -q > $O/${P}_pytest.log 2>&1; echo "PYTEST_EXIT $?" >> $O/${P}_pytest.log
+for lib in default exp default exp; do
+  for c in "0.01 4096" "0.1 4096" "1.0 4096" "1.0 256"; do set -- $c
+    VRS_LIB=$lib timeout 120 python tools/run_cell.py --sel $1 --q $2 | sed "s/^/[$lib] /" >> $O/${P}_ab.txt 2>&1
+  done
+  VRS_LIB=$lib timeout 300 python tools/run_cell.py --workload c5 --n 2500000 --sel 0.3 --q 2048 | sed "s/^/[$lib] /" >> $O/${P}_ab.txt 2>&1
+done
+echo done
