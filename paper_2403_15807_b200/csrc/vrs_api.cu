@@ -33,14 +33,17 @@ struct vrs_index {
   int32_t has_zero_row;
   float xmax;              // max row norm (range search error bound)
   void *xb;               // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
-  // vrs_search_host staging: two device slots (queries in, ids / dists out) so
+  // vrs_search_host staging: device slots (queries in, ids / dists out) so
   // that the upload of one call overlaps the compute of the previous one; the
   // copies run on their own streams, ordered by events.
   std::mutex host_mu;
   cudaStream_t up_stream = nullptr, down_stream = nullptr;
-  void *slot_buf[2] = {nullptr, nullptr};
-  size_t slot_cap[2] = {0, 0};
-  cudaEvent_t slot_free[2] = {nullptr, nullptr}, up_done[2] = {nullptr, nullptr}, comp_done[2] = {nullptr, nullptr};
+  // (4 slots: a call's upload waits for the download of the call 4 back, so short
+  // calls in a row do not chain compute -> download -> upload -> compute)
+  static constexpr int kSlots = 4;
+  void *slot_buf[kSlots] = {};
+  size_t slot_cap[kSlots] = {};
+  cudaEvent_t slot_free[kSlots] = {}, up_done[kSlots] = {}, comp_done[kSlots] = {};
   int slot_next = 0;
   int last_down = -1;     // slot of the last download issued (vrs_host_fence)
   int32_t device;
@@ -389,7 +392,7 @@ vrs_status vrs_free(vrs_index *ix) {
   if (ix->up_stream) {
     cudaStreamSynchronize(ix->up_stream);
     cudaStreamSynchronize(ix->down_stream);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < vrs_index::kSlots; ++i) {
       if (ix->slot_buf[i]) cudaFree(ix->slot_buf[i]);
       cudaEventDestroy(ix->slot_free[i]);
       cudaEventDestroy(ix->up_done[i]);
@@ -729,14 +732,14 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
   if (!ix->up_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ix->up_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&ix->down_stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < vrs_index::kSlots; ++i) {
       CUDA_TRY(cudaEventCreateWithFlags(&ix->slot_free[i], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&ix->up_done[i], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&ix->comp_done[i], cudaEventDisableTiming));
     }
   }
   const int slot = ix->slot_next;
-  ix->slot_next ^= 1;
+  ix->slot_next = (slot + 1) % vrs_index::kSlots;
   const size_t qb = (size_t)q * d * 4, ib = (size_t)q * k * 8, db = (size_t)q * k * 4;
   const size_t need = carve_size({qb, ib, db});
   if (ix->slot_cap[slot] < need) {   // grow (rare): wait for the slot's last use, then reallocate
