@@ -681,16 +681,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const float4 b4 = *reinterpret_cast<const float4 *>(gb);
       float4 ax4 = b4, an4 = b4;
       if (ROWSCALE) { ax4 = *reinterpret_cast<const float4 *>(ga); an4 = *reinterpret_cast<const float4 *>(gn); }
-      uint32_t pass = 0;
+      float dmg[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         float dm = __uint_as_float(r[g * 8]);
 #pragma unroll
         for (int i = 1; i < 8; ++i) dm = fmaxf(dm, __uint_as_float(r[g * 8 + i]));
+        dmg[g] = dm;
+      }
+      ++st_chunks;
+      uint32_t pass = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const float dm = dmg[g];
         const float kb = ROWSCALE ? fmaf(dm, dm >= 0.f ? f4(ax4, g) : f4(an4, g), f4(b4, g)) : fmaf(dm, sc, f4(b4, g));
         pass |= (kb > thr ? 1u : 0u) << g;
       }
-      ++st_chunks;
       if (!__any_sync(0xffffffffu, pass != 0)) return;
       // rare once the threshold is in place: exact keys of the flagged groups, make
       // room (<= 8 appends follow; the compaction histogram aliases the staging
