@@ -11,7 +11,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 timeout 120 python tools/run_cell.py --sel 1.0 --q 4096 --reps 1 --graph 0 > $O/${P}_plain.txt 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tc_topk|finalize|threshold" -s 0 -c 4 -o $O/${P}_c2big python tools/run_cell.py --sel 1.0 --q 4096 --reps 1 --graph 0 > $O/${P}_ncu_full.log 2>&1
 echo done
-for w in c1 c5 c3 c4; do
+for w in c1 c5; do
+  timeout 900 python bench.py --workload $w > $O/${P}_bench_$w.json 2> $O/${P}_bench_$w.err
+done
+for w in c3 c4; do
   timeout 900 python bench.py --workload $w --steps 3 --warmup 3 > $O/${P}_bench_$w.json 2> $O/${P}_bench_$w.err
 done
 echo done2
