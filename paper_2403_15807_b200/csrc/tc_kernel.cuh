@@ -387,27 +387,30 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   if (warp == 0 && gather && p.g4) {
     // ------------------------------------------------ TMA producer, gathered rows
     // (late materialisation without a copy: each lane loads the ids of its 8 rows
-    // of the tile one tile ahead and issues two gather4 per K block)
+    // of the tile one tile ahead and issues BN / 128 gather4 per K block)
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0 && lane == 0) {
       mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
       for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
     }
-    static_assert(BN == 256, "8 rows per lane");
+    constexpr int GR = BN / 32;   // rows per lane (whole gather4 groups)
+    static_assert(GR % 4 == 0, "gather4 groups per lane");
     const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;   // tail rows: any valid row (masked)
-    auto load_ids = [&](int t, int32_t (&r)[8]) {
-      const int64_t pos0 = tile_of(t) * BN + lane * 8;
-      if (pos0 + 8 <= n_sel) {
-        const int4 a0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0));
-        const int4 a1 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + 1);
-        r[0] = a0.x; r[1] = a0.y; r[2] = a0.z; r[3] = a0.w; r[4] = a1.x; r[5] = a1.y; r[6] = a1.z; r[7] = a1.w;
+    auto load_ids = [&](int t, int32_t (&r)[GR]) {
+      const int64_t pos0 = tile_of(t) * BN + lane * GR;
+      if (pos0 + GR <= n_sel) {
+#pragma unroll
+        for (int v = 0; v < GR / 4; ++v) {
+          const int4 a0 = __ldg(reinterpret_cast<const int4 *>(p.ids + pos0) + v);
+          r[4 * v] = a0.x; r[4 * v + 1] = a0.y; r[4 * v + 2] = a0.z; r[4 * v + 3] = a0.w;
+        }
       } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : pad_row;
+        for (int u = 0; u < GR; ++u) r[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : pad_row;
       }
     };
-    int32_t rid[8], rnext[8];
+    int32_t rid[GR], rnext[GR];
     if (ntiles > 0) load_ids(0, rid);
     for (int t = 0; t < ntiles; ++t) {
       if (t + 1 < ntiles) load_ids(t + 1, rnext);
@@ -419,13 +422,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
         }
         __syncwarp();
-        uint8_t *dst = st + BOFF + lane * 8 * 128;
-        tma_gather4(dst, &tmap_g, &full_bar[stage], kb * KE, rid[0], rid[1], rid[2], rid[3]);
-        tma_gather4(dst + 4 * 128, &tmap_g, &full_bar[stage], kb * KE, rid[4], rid[5], rid[6], rid[7]);
+        uint8_t *dst = st + BOFF + lane * GR * 128;
+#pragma unroll
+        for (int v = 0; v < GR / 4; ++v)
+          tma_gather4(dst + v * 4 * 128, &tmap_g, &full_bar[stage], kb * KE, rid[4 * v], rid[4 * v + 1],
+                      rid[4 * v + 2], rid[4 * v + 3]);
         if (++stage == NST) { stage = 0; phase ^= 1; }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) rid[u] = rnext[u];
+      for (int u = 0; u < GR; ++u) rid[u] = rnext[u];
     }
   } else if (warp == 0) {
     // ------------------------------------------------ TMA producer
