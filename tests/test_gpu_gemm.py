@@ -47,6 +47,7 @@ GEMM_CASES = [
     (12000, 64, 700, 50, oracle.COS, [(0, 0, 499)]),
     (8000, 128, 600, 100, oracle.L2, []),
     (5000, 64, 640, 200, oracle.IP, [(0, 0, 799)]),
+    (3000, 32, 20000, 10, oracle.L2, [(0, 0, 599)]),   # 157 query tiles, many more CTAs than SMs
 ]
 
 
