@@ -1,0 +1,13 @@
+#!/bin/bash
+# deferred slow path (default) vs immediate (libvrs_exp: -DVRS_NO_DEFER), alternating on one box
+cd $GRAFT_REPO_ROOT
+O=gpurun_out; P=${PFX:-bh}
+timeout 1100 python -m pytest tests -m gpu -x -q --deselect tests/test_gpu_optin.py::test_slow_path_vote_variant > $O/${P}_pytest.log 2>&1; echo "PYTEST_EXIT $?" >> $O/${P}_pytest.log
+for lib in default exp default exp; do
+  for c in "0.01 4096" "0.1 4096" "1.0 4096" "1.0 256" "1.0 16"; do set -- $c
+    VRS_LIB=$lib timeout 120 python tools/run_cell.py --sel $1 --q $2 | sed "s/^/[$lib] /" >> $O/${P}_ab.txt 2>&1
+  done
+  VRS_LIB=$lib timeout 300 python tools/run_cell.py --workload c5 --n 2500000 --sel 0.3 --q 2048 | sed "s/^/[$lib] /" >> $O/${P}_ab.txt 2>&1
+done
+for lib in default exp; do VRS_LIB=$lib timeout 400 python bench.py --no-parity --no-cpu-baseline > $O/${P}_bench_$lib.json 2>&1; done
+echo done
