@@ -49,11 +49,12 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
                                                           const int64_t *__restrict__ count, int64_t n, int allow,
                                                           int64_t cap, void *__restrict__ xsel,
                                                           const float *__restrict__ norm_src,
-                                                          float *__restrict__ norm_dst) {
+                                                          float *__restrict__ norm_dst, int64_t cp_min_bytes) {
   pdl_wait();
   pdl_trigger();
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, cap)) return;
+  if (n_sel * (int64_t)row_bytes >= cp_min_bytes) return;   // the tensor-core pass fetches them by cp.async
   // one 16-byte vector per thread, consecutive threads along a row (coalesced);
   // the row's id is a broadcast load shared by the row's threads
   const int v16 = row_bytes >> 4;
@@ -264,7 +265,7 @@ size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime) {
 
 cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L) {
   const int64_t xcap = a.ids ? a.xsel_cap : 0;
-  // gathered rows without a buffer: TMA gather4 straight from X by id
+  // gathered rows without a buffer: fetched from X by id (cp.async, or TMA gather4)
   const bool g4 = xcap > 0 && a.xsel == nullptr;
   const bool bf = a.bf16 != 0;
   cudaError_t e = cudaSuccess;
@@ -293,7 +294,23 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.allow_gather = a.masked == 1 ? 0 : (a.masked == 2 ? 2 : 1);
   p.xsel_cap = xcap;
   p.xsel_norm = a.xsel_norm;
-  p.g4 = g4 ? 1 : 0;
+  // Gathered row delivery (decided per launch on the device from the selection size):
+  //  * no X_sel buffer (VRS_GATHER4 / VRS_CPGATHER): rows by id from X -- TMA gather4 or cp.async;
+  //  * one query tile: cp.async when the selection holds >= 512 MB of rows, else the X_sel
+  //    copy (r01_s3_cp_gather_ab.txt: C3 s = 10 % Q = 1 0.95 -> 0.74 ms, small selections
+  //    are faster copied);  * several query tiles: the copy (rows are re-read per tile).
+  static const bool tma_gather4 = getenv("VRS_GATHER4") != nullptr;
+  static const bool no_cp = getenv("VRS_NO_CPGATHER") != nullptr;
+  static const int64_t cp_min = getenv("VRS_CP_MIN_MB") ? (int64_t)atoll(getenv("VRS_CP_MIN_MB")) << 20 : int64_t(512) << 20;
+  if (g4) {
+    p.g4 = tma_gather4 ? 1 : 2;
+    p.cp_min_bytes = 0;
+  } else {
+    p.g4 = (plan.qtiles == 1 && !no_cp) ? 2 : 0;
+    p.cp_min_bytes = p.g4 == 2 ? cp_min : INT64_MAX;
+  }
+  p.xrows = xsrc;
+  p.row_bytes = a.d * (bf ? 2 : 4);
   p.bitmap = a.bitmap;
   p.nx2 = a.nx2;
   p.inv_nx = a.inv_nx;
@@ -319,7 +336,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
                  (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
-                 a.metric == VRS_IP ? (float *)nullptr : a.xsel_norm);
+                 a.metric == VRS_IP ? (float *)nullptr : a.xsel_norm, p.cp_min_bytes);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }

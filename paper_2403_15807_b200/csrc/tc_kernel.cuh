@@ -90,6 +90,16 @@ __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
+// cp.async of 16 bytes (zero-filled when !valid) and an mbarrier arrival that fires
+// when all of this thread's earlier cp.async have landed (pending count +1 now,
+// -1 on completion: the barrier's expected count is unchanged)
+__device__ __forceinline__ void cpa16(uint32_t dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_mbar_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -198,7 +208,12 @@ struct TcParams {
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
   int32_t probe_div;       // probe: > 0 => step = clamp(main span / probe_div, 2, tile_step) (device-side span)
   int32_t P_main, min_p_main;   // probe: the main pass's splits (its span sets the density); 0 = P
-  int32_t g4;              // gather mode loads rows by TMA gather4 from X via ids (tmap_g); else from X_sel
+  int32_t g4;              // gather mode: 1 = TMA gather4 from X by id (tmap_g), 2 = cp.async from X by id
+                           // (xrows), 0 = TMA tiles from the X_sel copy
+  const void *xrows;       // g4 == 2: the rows' base (fp32 corpus or its bf16 shadow), row_bytes each
+  int32_t row_bytes;
+  int64_t cp_min_bytes;    // g4 == 2: cp.async only when the selection holds >= this many row bytes
+                           // (below it gather_copy_kernel made X_sel and TMA tiles stream it)
   int32_t min_span;        // used splits span >= this many row tiles (splits_used) ...
   int32_t min_p;           // ... unless that leaves fewer than min_p splits
   const uint32_t *bitmap;  // nullptr => every row qualifies
@@ -363,6 +378,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   //  masked: every row streams by TMA, unqualified rows are masked by the bitmap
   const int64_t n_sel = p.ids ? *p.count : p.n_rows;
   const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.xsel_cap);
+  // rows fetched by cp.async (see the producer): large one-query-tile selections, where
+  // the X_sel copy's extra pass costs more than cp.async's lower streaming rate
+  const bool cpg = gather && p.g4 == 2 && n_sel * (int64_t)p.row_bytes >= p.cp_min_bytes;
+  const bool direct = cpg || (gather && p.g4 == 1);   // rows by id from X (no X_sel)
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;
   // splits actually used (splits_used): >= 4 row tiles per item when the
@@ -384,7 +403,62 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
 
-  if (warp == 0 && gather && p.g4) {
+  if (warp == 0 && cpg) {
+    // ------------------------------------------------ cp.async producer, gathered rows
+    // (late materialisation without a copy: lane l fetches rows l, l + 32, ... of the
+    // tile straight from X by id -- each row's 128-byte K-block segment as 8 x 16 B,
+    // placed in the 128B-swizzled layout the MMA descriptors expect (what a TMA box
+    // load would write); the stage's barrier completes when every lane's copies land)
+    int stage = 0;
+    uint32_t phase = 0;
+    if (AR && ntiles > 0 && lane == 0) {
+      mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
+      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+    }
+    constexpr int GR = BN / 32;   // rows per lane
+    const char *xb = static_cast<const char *>(p.xrows);
+    const int64_t rb = p.row_bytes;
+    const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;
+    auto load_ids = [&](int t, int32_t (&r)[GR]) {
+#pragma unroll
+      for (int u = 0; u < GR; ++u) {
+        const int64_t pos = tile_of(t) * BN + lane + 32 * u;
+        r[u] = pos < n_sel ? __ldg(p.ids + pos) : pad_row;
+      }
+    };
+    int32_t rid[GR], rnext[GR];
+    if (ntiles > 0) load_ids(0, rid);
+    for (int t = 0; t < ntiles; ++t) {
+      if (t + 1 < ntiles) load_ids(t + 1, rnext);
+      for (int kb = 0; kb < p.nk; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t *st = b_base + stage * SSTRIDE;
+        const uint32_t bdst = smem_u32(st + BOFF);
+        const int64_t koff = (int64_t)kb * 128;
+#pragma unroll
+        for (int u = 0; u < GR; ++u) {
+          const int r = lane + 32 * u;
+          const char *src = xb + (int64_t)rid[u] * rb + koff;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), src + c * 16, koff + c * 16 < rb);
+        }
+        cpa_mbar_arrive(&full_bar[stage]);
+        __syncwarp();
+        if (lane == 0) {
+          if (!AR) {
+            mbar_expect_tx(&full_bar[stage], A_BYTES);
+            tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
+          } else {
+            mbar_arrive(&full_bar[stage]);
+          }
+        }
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+#pragma unroll
+      for (int u = 0; u < GR; ++u) rid[u] = rnext[u];
+    }
+  } else if (warp == 0 && gather && p.g4 == 1) {
     // ------------------------------------------------ TMA producer, gathered rows
     // (late materialisation without a copy: each lane loads the ids of its 8 rows
     // of the tile one tile ahead and issues BN / 128 gather4 per K block)
@@ -467,6 +541,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < p.nk; ++kb) {
         mbar_wait(&full_bar[stage], phase);
+        if (cpg) fence_proxy_async_smem();   // cp.async (generic proxy) writes -> the MMA's async-proxy reads
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
@@ -493,7 +568,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // rows read them contiguously from the gather's norm copy (no dependent load).
     const bool need_norm = p.metric != VRS_IP;
     const float *src_rows = p.metric == VRS_L2 ? p.nx2 : p.inv_nx;   // by row id
-    const float *src = gather && !p.g4 ? p.xsel_norm : src_rows;
+    const float *src = gather && !direct ? p.xsel_norm : src_rows;
     constexpr int RPL = BN / 32;   // rows per lane
     float nv[PF][RPL];
     int32_t iv[PF][RPL];
@@ -512,7 +587,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
           for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
         }
-        if (need_norm && p.g4) {   // by row id (dependent loads; the bias warp runs PF tiles ahead)
+        if (need_norm && direct) {   // by row id (dependent loads; the bias warp runs PF tiles ahead)
 #pragma unroll
           for (int u = 0; u < RPL; ++u) n8[u] = i8[u] >= 0 ? __ldg(src_rows + i8[u]) : 0.f;
         } else if (need_norm && pos0 + RPL <= n_sel) {

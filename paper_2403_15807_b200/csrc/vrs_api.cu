@@ -409,6 +409,14 @@ vrs_status vrs_free(vrs_index *ix) {
   return VRS_OK;
 }
 
+// true: an X_sel buffer is allocated (the gather copy may run; the tensor-core pass
+// decides on the device between it and cp.async, gemm_tc.cu); false: the pass always
+// fetches the rows from X by id (VRS_GATHER4: TMA gather4, VRS_CPGATHER: cp.async)
+static bool gather_copy_mode(int32_t) {
+  static const bool direct = getenv("VRS_GATHER4") != nullptr || getenv("VRS_CPGATHER") != nullptr;
+  return !direct;
+}
+
 static int pow2_at_least(int v) {
   int p = 1;
   while (p < v) p <<= 1;
@@ -493,10 +501,9 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                               : q >= 1024                 ? n * 9 / 10
                               : q >= 256                  ? n * 9 / 20
                                                           : n / 3;
-  // VRS_GATHER4=1: gather by TMA gather4 straight from X (no X_sel buffer; xsel_cap
-  // is then only the break-even).  Measured slower than the copy at every C2 / C5
-  // cell (gather4 moves ~7 B/clk/SM), so the copy is the default.
-  static const bool gather_copy = getenv("VRS_GATHER4") == nullptr;
+  // Row delivery of a gathered selection: the X_sel copy + TMA tiles, or (one query
+  // tile, large selections; decided on the device) cp.async straight from X -- gemm_tc.cu.
+  const bool gather_copy = gather_copy_mode(gp.qtiles);
   const int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
                                ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
                                               : gather_rows)
@@ -635,7 +642,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
                               : q >= 1024                 ? n * 9 / 10
                               : q >= 256                  ? n * 9 / 20
                                                           : n / 3;
-  static const bool gather_copy = getenv("VRS_GATHER4") == nullptr;   // (as in vrs_search_ex)
+  const bool gather_copy = gather_copy_mode(gp.qtiles);   // (as in vrs_search_ex)
   const int64_t xsel_cap = (!identity && rows_req != VRS_ROWS_MASKED)
                                ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
                                               : gather_rows)

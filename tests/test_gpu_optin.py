@@ -1,6 +1,7 @@
 """The opt-in variants of the tensor-core path (environment switches read once per
 process, so each runs in a subprocess): TMA gather4 late materialisation
-(VRS_GATHER4), the one-launch selection + select_finish (VRS_SELECT_LOCAL) and the
+(VRS_GATHER4), cp.async gathering straight into the swizzled stages
+(VRS_CPGATHER), the one-launch selection + select_finish (VRS_SELECT_LOCAL) and the
 warp-voted slow path (libvrs_exp.so, -DVRS_SLOW_GROUPS_VOTE, when built).  Each
 must meet the same parity rules as the default path."""
 import os
@@ -27,8 +28,8 @@ for n, d, q, k, metric, pred in cases:
     X = rng.standard_normal((n, d)).astype(np.float32)
     attrs = [rng.integers(0, 1000, n).astype(np.int32)]
     Q = rng.standard_normal((q, d)).astype(np.float32)
-    for rows in (None, 2):
-        ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    for rows, prec in ((None, None), (2, None), (2, 1)):
+        ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], precision=prec)
         ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=M[metric], path=vrs.PATH_GEMM, rows=rows)
         torch.cuda.synchronize()
         check_topk(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, k, metric)
@@ -53,6 +54,10 @@ def _run(env_extra):
 
 def test_gather4(vrs_lib_built):
     _run({"VRS_GATHER4": "1"})
+
+
+def test_cp_async_gather(vrs_lib_built):
+    _run({"VRS_CPGATHER": "1"})
 
 
 def test_select_local(vrs_lib_built):
