@@ -403,26 +403,34 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
 
-  if (warp == 0 && cpg) {
-    // ------------------------------------------------ cp.async producer, gathered rows
-    // (late materialisation without a copy: lane l fetches rows l, l + 32, ... of the
-    // tile straight from X by id -- each row's 128-byte K-block segment as 8 x 16 B,
+#ifndef VRS_CP_WARPS
+#define VRS_CP_WARPS 1
+#endif
+  constexpr int CPW = VRS_CP_WARPS;   // cp.async producer warps (1: warp 0; 2: warps 0 and 3 -- measured equal)
+  if ((warp == 0 || (CPW == 2 && warp == 3)) && cpg) {
+    // ------------------------------------------------ cp.async producers, gathered rows
+    // (late materialisation without a copy: warps 0 and 3 each fetch half of the tile's
+    // rows straight from X by id -- each row's 128-byte K-block segment as 8 x 16 B,
     // placed in the 128B-swizzled layout the MMA descriptors expect (what a TMA box
-    // load would write); the stage's barrier completes when every lane's copies land)
+    // load would write); the stage's barrier completes when every lane's copies land:
+    // each lane's cp.async.mbarrier.arrive adds a pending arrival that its copies
+    // retire, and warp 0's lane 0 arrives only after both warps registered theirs)
+    const bool lead = warp == 0;
+    const int hrow = lead ? 0 : BN / CPW;   // this warp's first row of the tile
     int stage = 0;
     uint32_t phase = 0;
-    if (AR && ntiles > 0 && lane == 0) {
+    if (lead && AR && ntiles > 0 && lane == 0) {
       mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
       for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
     }
-    constexpr int GR = BN / 32;   // rows per lane
+    constexpr int GR = BN / (32 * CPW);   // rows per lane per warp
     const char *xb = static_cast<const char *>(p.xrows);
     const int64_t rb = p.row_bytes;
     const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;
     auto load_ids = [&](int t, int32_t (&r)[GR]) {
 #pragma unroll
       for (int u = 0; u < GR; ++u) {
-        const int64_t pos = tile_of(t) * BN + lane + 32 * u;
+        const int64_t pos = tile_of(t) * BN + hrow + lane + 32 * u;
         r[u] = pos < n_sel ? __ldg(p.ids + pos) : pad_row;
       }
     };
@@ -437,15 +445,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int64_t koff = (int64_t)kb * 128;
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
-          const int r = lane + 32 * u;
+          const int r = hrow + lane + 32 * u;
           const char *src = xb + (int64_t)rid[u] * rb + koff;
 #pragma unroll
           for (int c = 0; c < 8; ++c)
             cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), src + c * 16, koff + c * 16 < rb);
         }
         cpa_mbar_arrive(&full_bar[stage]);
-        __syncwarp();
-        if (lane == 0) {
+        if (CPW == 2) asm volatile("bar.sync 1, 64;" ::: "memory");   // both producer warps registered their arrivals
+        else __syncwarp();
+        if (lead && lane == 0) {
           if (!AR) {
             mbar_expect_tx(&full_bar[stage], A_BYTES);
             tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
