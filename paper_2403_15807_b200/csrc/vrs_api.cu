@@ -749,16 +749,22 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
   ix->slot_next = (slot + 1) % vrs_index::kSlots;
   const size_t qb = (size_t)q * d * 4, ib = (size_t)q * k * 8, db = (size_t)q * k * 4;
   const size_t need = carve_size({qb, ib, db});
-  if (ix->slot_cap[slot] < need) {   // grow (rare): wait for the slot's last use, then reallocate
-    CUDA_TRY(cudaEventSynchronize(ix->slot_free[slot]));
-    if (ix->slot_buf[slot]) cudaFree(ix->slot_buf[slot]);
-    ix->slot_buf[slot] = nullptr;
-    ix->slot_cap[slot] = 0;
-    if (cudaMalloc(&ix->slot_buf[slot], need) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(VRS_ENOMEM, "cudaMalloc(%zu) for the host-call staging failed", need);
+  if (ix->slot_cap[slot] < need) {
+    // grow (rare): every slot at once, to the new largest size -- the slots take turns,
+    // so growing one at a time would stall (sync + free + malloc) on several later calls
+    for (int i = 0; i < vrs_index::kSlots; ++i) {
+      CUDA_TRY(cudaEventSynchronize(ix->slot_free[i]));   // (never-recorded events are complete)
+      if (ix->slot_buf[i]) cudaFree(ix->slot_buf[i]);
+      ix->slot_buf[i] = nullptr;
+      ix->slot_cap[i] = 0;
     }
-    ix->slot_cap[slot] = need;
+    for (int i = 0; i < vrs_index::kSlots; ++i) {
+      if (cudaMalloc(&ix->slot_buf[i], need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(VRS_ENOMEM, "cudaMalloc(%zu) for the host-call staging failed", need);
+      }
+      ix->slot_cap[i] = need;
+    }
   }
   Carve cv(ix->slot_buf[slot]);
   float *dq = cv.take<float>((size_t)q * d);
