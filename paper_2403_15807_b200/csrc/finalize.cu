@@ -583,8 +583,11 @@ using FinBufs = FinBufsT<kBufCap>;
 
 // Steps 1-2 for one warp over lists l = first, first + step, ... (in groups of
 // 32): the warp's buffer ends with at most K entries (or all it saw).
+// (keep: the buffer is cut to the k' best only when it holds more than `keep`
+// entries -- the CTA tree merge takes up to 32E unsorted survivors per warp)
 template <int CAP>
-__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP> &B) {
+__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP> &B,
+                          int keep = -1) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
   const int lists = a.split.bn ? (int)min((int64_t)a.lists, kListsPerSplit * splits_used(a.split)) : a.lists;
@@ -634,7 +637,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
     }
   }
   __syncwarp();
-  if (n > K) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
+  if (n > (keep < 0 ? K : keep)) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
   return n;
 }
 
@@ -826,7 +829,10 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? 8 : 1) finalize_wa
   fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w]);
 }
 
-constexpr int kFinW = 8;   // warps per query in the small-batch variant
+#ifndef VRS_FIN_W
+#define VRS_FIN_W 8
+#endif
+constexpr int kFinW = VRS_FIN_W;   // warps per query in the small-batch variant (16 measured: q = 16 -4 us, q = 256 +10 us)
 // k' <= 32E: each warp of the CTA sorts its <= k' survivors, a tree of bitonic
 // merges (best 32E of two sorted lists) leaves the 32E best of all warps, sorted,
 // in warp 0, which writes the k' best ids to s_buf[0] and their count to s_n[0].
@@ -870,7 +876,8 @@ __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s
 
 
 __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a) {
-  __shared__ FinBufs s_buf[kFinW];
+  extern __shared__ __align__(16) uint8_t fin_dyn[];
+  FinBufs *s_buf = reinterpret_cast<FinBufs *>(fin_dyn);   // [kFinW]
   __shared__ double s_sc[kFinMaxSel];
   __shared__ int64_t s_sid[kFinMaxSel];
   __shared__ int s_n[kFinW];
@@ -878,8 +885,10 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   const int64_t j = blockIdx.x;
   pdl_wait();
   pdl_trigger();
-  // each warp: its share of the lists -> at most k' survivors
-  const int nw = fin_stream(a, j, w, kFinW, s_buf[w]);
+  // each warp: its share of the lists -> its survivors (<= k', or <= 32E unsorted when
+  // the tree merge follows: it sorts them anyway)
+  const int keep = a.kprime <= 64 ? 64 : (a.kprime <= 128 ? 128 : -1);
+  const int nw = fin_stream(a, j, w, kFinW, s_buf[w], keep);
   if (lane == 0) s_n[w] = nw;
   __syncthreads();
   if (a.kprime <= 64) {
@@ -1192,7 +1201,13 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
-  if (a.q < 4 * kSmCountB200) return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), 0, s, a);
+  if (a.q < 4 * kSmCountB200) {
+    const size_t smem = sizeof(FinBufs) * kFinW;
+    static size_t attr = 0;
+    const cudaError_t e = ensure_smem_attr(finalize_cta_kernel, smem, attr);
+    if (e != cudaSuccess) return e;
+    return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), smem, s, a);
+  }
   const dim3 grid((unsigned)((a.q + kFinGroup - 1) / kFinGroup));
   if (a.kprime <= 64) return launch_k(finalize_warp_kernel<256, 64>, grid, dim3(kFinGroup * 32), 0, s, a);
   if (a.kprime <= 128) return launch_k(finalize_warp_kernel<256, 128>, grid, dim3(kFinGroup * 32), 0, s, a);
