@@ -360,6 +360,8 @@ def main():
                                         "TF32 = measured bf16 sustained x nominal tf32/bf16 (1.1/2.25)", "TF32")
         roof = {"kernel": f"tc_topk_kernel main pass (tcgen05 {kind} + fused top-k)", "bound": "tensor",
                 "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                "traffic_evidence": "profiles/r01_ncu_c2big_all_kernels.md: DRAM read / write of one C2 "
+                                    "Q = 4096, s = 100 % main-pass launch (ncu --set full)",
                 "peak_note": note, "frac_vs_burst_peak": ach / peak_b,
                 "algorithmic": "2*Q*N_sel*d per cell, summed over the step's tensor-core cells, / main-pass time"}
     elif dominant is not None:

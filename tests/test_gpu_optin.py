@@ -60,6 +60,13 @@ def test_cp_async_gather(vrs_lib_built):
     _run({"VRS_CPGATHER": "1"})
 
 
+def test_cp_gather_adaptive_threshold(vrs_lib_built):
+    """The default device-side choice between the X_sel copy and cp.async (one query
+    tile, selection >= the threshold), with the threshold lowered to 1 MB so that the
+    cases above take both branches (the gather copy kernel skips itself by the same test)."""
+    _run({"VRS_CP_MIN_MB": "1"})
+
+
 def test_select_local(vrs_lib_built):
     _run({"VRS_SELECT_LOCAL": "1"})
 
