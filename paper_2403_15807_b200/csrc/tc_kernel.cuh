@@ -231,7 +231,8 @@ struct TcParams {
   const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
-  int32_t epi_skip;        // debug: 1 = the epilogue skips the read-out (MMA + TMA bound), 2 = read-out only
+  int32_t epi_skip;        // debug: 1 = the epilogue skips the read-out (MMA + TMA bound); read-out only:
+                           // build with -DVRS_EPI_READOUT_ONLY
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -909,13 +910,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         for (int c = 0; c < EPI_COLS / 32; ++c) {
           TMEM_LD_32x32b_X32(tbase + c * 32, ra);
           TMEM_LD_WAIT(ra);
-          if (p.epi_skip == 2) {   // debug: read-out only (keeps the loads live)
+#ifdef VRS_EPI_READOUT_ONLY   // debug build: read-out only (keeps the loads live)
+          {
             uint32_t x = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) x ^= ra[i];
             if (x == 0x9e3779b9u && p.stats) atomicAdd(p.stats + 3, 1ull);
             continue;
           }
+#endif
           chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, g_bmax + g0 + c * 4, g_amax + g0 + c * 4, g_amin + g0 + c * 4);
         }
       }
@@ -930,13 +933,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           TMEM_LD_32x32b_X64(tbase + c * 32, ra);
           TMEM_LD_WAIT(ra);
           TMEM_LD_WAIT(reinterpret_cast<uint32_t(&)[32]>(ra[32]));
-          if (p.epi_skip == 2) {   // debug: read-out only (keeps the loads live)
-            uint32_t x = 0;
-#pragma unroll
-            for (int i = 0; i < 64; ++i) x ^= ra[i];
-            if (x == 0x9e3779b9u && p.stats) atomicAdd(p.stats + 3, 1ull);
-            continue;
-          }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int cc = c + h;
