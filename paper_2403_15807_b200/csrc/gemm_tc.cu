@@ -322,8 +322,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.min_span = tc_min_span();
   p.min_p = tc_min_p(plan);
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
-  static const int epi_skip = getenv("VRS_EPI_SKIP") ? std::max(1, atoi(getenv("VRS_EPI_SKIP"))) : 0;
-  p.epi_skip = epi_skip;
+  p.epi_skip = 0;
   L->bf = bf;
   L->ar = p.nk <= 4 && !no_ar;
   L->rowscale = a.metric == VRS_COSINE;

@@ -231,8 +231,8 @@ struct TcParams {
   const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
-  int32_t epi_skip;        // debug: 1 = the epilogue skips the read-out (MMA + TMA bound); read-out only:
-                           // build with -DVRS_EPI_READOUT_ONLY
+  int32_t epi_skip;        // (unused: the MMA + TMA-only and read-out-only measurements are debug
+                           // builds, -DVRS_EPI_SKIP_BUILD / -DVRS_EPI_READOUT_ONLY)
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -706,6 +706,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t *whist = reinterpret_cast<uint32_t *>(wst);   // compaction histogram aliases the staging area
     float thr = active ? -INFINITY : INFINITY;     // accept iff key > thr (inactive lanes never accept)
     int cnt = 0;
+    // epilogue counters (VRS_STATS=1 prints them) exist only in builds with
+    // -DVRS_TC_STATS: the hot loop carries no runtime debug state otherwise
+#ifdef VRS_TC_STATS
+#define TC_STAT(x) (x)
+#else
+#define TC_STAT(x) ((void)0)
+#endif
     uint32_t st_chunks = 0, st_slow = 0, st_app = 0, st_comp = 0;
     float smax[SLOTS];
 #pragma unroll
@@ -730,7 +737,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int oc = __shfl_sync(0xffffffffu, cnt, owner);
         const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
         const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
-        ++st_comp;
+        TC_STAT(++st_comp);
         if (lane == owner) {
           cnt = p.kp;
           thr = fmaxf(thr, nt);
@@ -779,7 +786,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         for (int i = 1; i < 8; ++i) dm = fmaxf(dm, __uint_as_float(r[g * 8 + i]));
         dmg[g] = dm;
       }
-      ++st_chunks;
+      TC_STAT(++st_chunks);
       uint32_t pass = 0;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -792,7 +799,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // room (<= 8 appends follow; the compaction histogram aliases the staging
       // rows), then each lane appends its accepted columns in row order from its
       // private staging row
-      ++st_slow;
+      TC_STAT(++st_slow);
       if (MODE == MODE_MAIN && __any_sync(0xffffffffu, cnt + 32 > p.cap)) compact_needed(p.cap - 32);
 #ifdef VRS_SLOW_GROUPS_VOTE
 #pragma unroll
@@ -826,7 +833,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (msk) {
           *reinterpret_cast<float4 *>(myrow) = make_float4(kk[0], kk[1], kk[2], kk[3]);
           *reinterpret_cast<float4 *>(myrow + 4) = make_float4(kk[4], kk[5], kk[6], kk[7]);
-          st_app += __popc(msk);
+          TC_STAT(st_app += __popc(msk));
           while (msk) {
             const int i = __ffs(msk) - 1;
             msk &= msk - 1;
@@ -877,7 +884,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           } else if (msk) {
             *reinterpret_cast<float4 *>(myrow) = make_float4(kk[0], kk[1], kk[2], kk[3]);
             *reinterpret_cast<float4 *>(myrow + 4) = make_float4(kk[4], kk[5], kk[6], kk[7]);
-            st_app += __popc(msk);
+            TC_STAT(st_app += __popc(msk));
             while (msk) {
               const int i = __ffs(msk) - 1;
               msk &= msk - 1;
@@ -903,8 +910,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int32_t *rid = row_id + bs * BN + half * EPI_COLS;
       const int g0 = bs * GROUPS + half * (EPI_COLS / 8);   // this warp's first group
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + half * EPI_COLS);
-#ifndef VRS_EPI_X64
-      if (p.epi_skip != 1) {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
+#if !defined(VRS_EPI_SKIP_BUILD) && !defined(VRS_EPI_X64)
+      {   // one chunk in flight per warp (the other warps hide the TMEM load latency)
         uint32_t ra[32];
 #pragma unroll 1
         for (int c = 0; c < EPI_COLS / 32; ++c) {
@@ -922,10 +929,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           chunk(ra, ba + c * 32, bb + c * 32, rid + c * 32, g_bmax + g0 + c * 4, g_amax + g0 + c * 4, g_amin + g0 + c * 4);
         }
       }
-#else
-      if (p.epi_skip != 1) {
-        // A/B (VRS_EPI_X64): two chunks per tcgen05.ld (32x32b.x64, 64 registers).  Box-
-        // dependent: -12 % on one box, +4 % on others (r01_s3_tmem_x64_ab.txt) -- opt-in
+#elif !defined(VRS_EPI_SKIP_BUILD)
+      {   // A/B (VRS_EPI_X64): two chunks per tcgen05.ld (32x32b.x64) -- measured equal
         static_assert((EPI_COLS / 32) % 2 == 0, "pairs of chunks");
         uint32_t ra[64];
 #pragma unroll 1

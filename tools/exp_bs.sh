@@ -1,5 +1,5 @@
 #!/bin/bash
-# x32 (default) vs x64 TMEM loads (libvrs_exp), both without the old per-chunk debug branch
+# default vs libvrs_exp (variant named in the call), alternating
 cd $GRAFT_REPO_ROOT
 O=gpurun_out; P=${PFX:-bs}
 for lib in default exp default exp; do
