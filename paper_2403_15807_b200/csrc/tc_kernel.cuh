@@ -1008,7 +1008,8 @@ static TcKernel pick_kernel(bool ar, bool rowscale) {
 }
 
 // One launch of the pass in MODE (the kernels of a mode are instantiated in the
-// translation unit that calls this).  VRS_STATS=1 prints the epilogue counters.
+// translation unit that calls this).  VRS_STATS=1 prints the epilogue counters (they count only in
+// builds with -DVRS_TC_STATS).
 template <int MODE>
 static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStream_t s) {
   static size_t attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per variant (AR, ROWSCALE, BF)
