@@ -1,0 +1,60 @@
+"""Seeded random shapes against the oracle: n, d, q, k, metric, predicate (0-2
+clauses over int32 / uint8 columns, including empty and all-rows), path (auto /
+tensor-core / scan), row delivery and selection precision -- the combinations the
+hand-written cases do not enumerate.  Same acceptance rule as every parity test."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from parity import check_topk
+
+pytestmark = pytest.mark.gpu
+METRICS = {oracle.L2: "l2", oracle.IP: "ip", oracle.COS: "cos"}
+N_CASES = 150
+
+
+@pytest.fixture(scope="module")
+def vrs():
+    import paper_2403_15807_b200 as m
+    m.library()
+    return m
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 20000))
+    d = int(rng.choice([4, 8, 16, 32, 64, 96, 128, 136, 256]))
+    q = int(rng.choice([1, 2, 7, 16, 64, 129, 300]))
+    k = int(rng.choice([1, 5, 10, 32, 50, 100]))
+    metric = int(rng.choice([oracle.L2, oracle.IP, oracle.COS]))
+    n_cl = int(rng.integers(0, 3))
+    pred = []
+    for _ in range(n_cl):
+        col = int(rng.integers(0, 2))
+        hi_max = 999 if col == 0 else 255
+        lo = int(rng.integers(0, hi_max + 1))
+        hi = int(rng.integers(lo - 5, hi_max + 1))   # lo > hi sometimes: an empty clause
+        pred.append((col, lo, hi))
+    path = [None, 2, 1][int(rng.integers(0, 3))]
+    rows = [None, 1, 2][int(rng.integers(0, 3))]
+    prec = [None, 1, 2][int(rng.integers(0, 3))]
+    off = int(rng.integers(0, 1 << 20))
+    return rng, n, d, q, k, metric, pred, path, rows, prec, off
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_fuzz_parity(vrs, seed):
+    rng, n, d, q, k, metric, pred, path, rows, prec, off = _case(seed)
+    if prec == 2 and d % 8:
+        prec = None
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    if metric == oracle.COS:
+        X[np.linalg.norm(X, axis=1) == 0] += 1.0
+    attrs = [rng.integers(0, 1000, n).astype(np.int32), rng.integers(0, 256, n).astype(np.uint8)]
+    Q = rng.standard_normal((q, d)).astype(np.float32)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off,
+                   precision=prec)
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=path, rows=rows)
+    torch.cuda.synchronize()
+    check_topk(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, k, metric, row_offset=off)
