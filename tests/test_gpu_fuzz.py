@@ -58,3 +58,31 @@ def test_fuzz_parity(vrs, seed):
     ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=path, rows=rows)
     torch.cuda.synchronize()
     check_topk(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, k, metric, row_offset=off)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_range(vrs, seed):
+    """Threshold mode on random shapes: tau between two scores of the first query
+    (so result counts vary), ids and offsets exact, dists to fp32 rounding."""
+    rng, n, d, q, _, metric, pred, _, rows, prec, off = _case(10_000 + seed)
+    if prec == 2 and d % 8:
+        prec = None
+    q = min(q, 64)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    attrs = [rng.integers(0, 1000, n).astype(np.int32), rng.integers(0, 256, n).astype(np.uint8)]
+    Q = rng.standard_normal((q, d)).astype(np.float32)
+    _, _, _, sc = oracle.range_search(X, attrs, pred, Q[:1], -np.inf if metric != oracle.L2 else np.inf, metric)
+    if len(sc) >= 2:
+        s = np.sort(sc)[::-1] if metric != oracle.L2 else np.sort(sc)
+        r = int(rng.integers(0, min(len(s) - 1, 200)))
+        tau = float((s[r] + s[r + 1]) / 2)
+    else:
+        tau = 0.0
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off,
+                   precision=prec)
+    o, ids, dists = ix.range_search(torch.from_numpy(Q).cuda(), pred, tau=tau, metric=METRICS[metric], rows=rows)
+    torch.cuda.synchronize()
+    ro, rids, rd, _ = oracle.range_search(X, attrs, pred, Q, tau, metric, row_offset=off)
+    assert o.cpu().numpy().tolist() == ro.tolist()
+    assert ids.cpu().numpy().tolist() == rids.tolist()
+    assert np.allclose(dists.cpu().numpy(), rd, rtol=1e-6, atol=1e-7)
