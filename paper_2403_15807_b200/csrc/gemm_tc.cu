@@ -417,3 +417,15 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
 }
 
 }  // namespace vrs
+
+#ifdef VRS_TC_TIMING
+// Debug builds only (-DVRS_TC_TIMING): copy the per-CTA globaltimer stamps of the
+// last tensor-core launches ([mode][cta][8] u64, see TC_TL) to host and clear them.
+extern "C" VRS_API int vrs_debug_tc_timeline(unsigned long long *host) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  void *d = nullptr;
+  if (cudaGetSymbolAddress(&d, vrs::g_tc_tl) != cudaSuccess) return -1;
+  if (cudaMemcpy(host, d, sizeof(vrs::g_tc_tl), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return cudaMemset(d, 0, sizeof(vrs::g_tc_tl)) == cudaSuccess ? 0 : -1;
+}
+#endif

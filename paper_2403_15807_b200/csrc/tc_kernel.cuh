@@ -313,6 +313,18 @@ constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the li
 // MODE: MAIN (fused top-k candidates) or PROBE (slot maxima for the threshold).
 // ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
 // BF: operands are bf16 (shadow corpus, kind::f16) instead of fp32 (kind::tf32).
+#ifdef VRS_TC_TIMING
+// debug build only: per-CTA globaltimer stamps [mode][cta][8] (tools/tc_timeline.py)
+static __device__ unsigned long long g_tc_tl[4][4096][8];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_TL(slot) (blockIdx.x < 4096 ? (void)(g_tc_tl[MODE & 3][blockIdx.x][slot] = tl_now()) : (void)0)
+#else
+#define TC_TL(slot) ((void)0)
+#endif
 template <bool AR, int MODE, bool ROWSCALE, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
@@ -349,6 +361,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qtile = blockIdx.x % p.qtiles;
   const int split = blockIdx.x / p.qtiles;
+  if (threadIdx.x == 0) TC_TL(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&afull_bar, 1);
@@ -373,6 +386,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // (the prologue above overlaps the predecessor kernel's tail; global memory from here on)
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) TC_TL(1);
   // Selectivity-driven row delivery (decided on the device, no host sync):
   //  gather: the selection was materialised densely (gather_copy_kernel, late
   //          materialization) and streams by TMA from X_sel; ids map rows back
@@ -551,6 +565,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < p.nk; ++kb) {
         mbar_wait(&full_bar[stage], phase);
+        if (t == 0 && kb == 0 && lane == 0) TC_TL(2);
         if (cpg) fence_proxy_async_smem();   // cp.async (generic proxy) writes -> the MMA's async-proxy reads
         tc_fence_after();
         if (lane == 0) {
@@ -904,6 +919,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int bs = t % BIAS_STAGES;
       mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
       mbar_wait(&tfull_bar[acc], (t / ACC_STAGES) & 1);
+      if (t == 0 && ew == 0 && lane == 0) TC_TL(3);
       tc_fence_after();
       const float *ba = bias_a + bs * BN + half * EPI_COLS;
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
@@ -954,6 +970,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_arrive(&bempty_bar[bs]);
       }
     }
+    if (ew == 0 && lane == 0) TC_TL(4);
     if (p.stats && lane == 0) {
       atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
       atomicAdd(p.stats + 1, (unsigned long long)st_slow);
@@ -973,6 +990,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    TC_TL(5);
+#ifdef VRS_TC_TIMING
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tc_tl[MODE & 3][blockIdx.x < 4096 ? blockIdx.x : 4095][6] = smid;
+    g_tc_tl[MODE & 3][blockIdx.x < 4096 ? blockIdx.x : 4095][7] = (unsigned long long)ntiles;
+#endif
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
