@@ -11,8 +11,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvrs.so")
-if os.environ.get("VRS_LIB") == "exp":   # experiment build of the same sources (csrc/Makefile `exp`)
-    LIB_PATH = os.path.join(_HERE, "libvrs_exp.so")
+if os.environ.get("VRS_LIB"):   # experiment builds of the same sources (csrc/Makefile `exp`): libvrs_<VRS_LIB>.so
+    LIB_PATH = os.path.join(_HERE, "libvrs_%s.so" % os.environ["VRS_LIB"])
 
 OK, EINVAL, ENOTFOUND, EDEGENERATE, ENOMEM, ECUDA, ECOMM, EUNSUPPORTED, ERANGE = range(9)
 STATUS_NAMES = ["VRS_OK", "VRS_EINVAL", "VRS_ENOTFOUND", "VRS_EDEGENERATE", "VRS_ENOMEM", "VRS_ECUDA",

@@ -812,8 +812,12 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
 // a 4096-query batch runs in one wave.)
 // (the k' <= 64 variant is held to 64 registers: 8 CTAs of 4 warps per SM, so a
 // 4096-query batch is one wave -- at 96 registers it was 1.4 waves)
+// resident CTAs per SM the <256, 64> variant is register-limited to (A/B: -DVRS_FIN_MINB)
+#ifndef VRS_FIN_MINB
+#define VRS_FIN_MINB 8
+#endif
 template <int CAP, int SEL>
-__global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? 8 : 1) finalize_warp_kernel(FinalizeArgs a) {
+__global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) finalize_warp_kernel(FinalizeArgs a) {
   __shared__ FinBufsT<CAP> s_buf[kFinGroup];
   __shared__ double s_sc[kFinGroup][SEL];
   __shared__ int64_t s_sid[kFinGroup][SEL];
