@@ -322,7 +322,6 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.min_span = tc_min_span();
   p.min_p = tc_min_p(plan);
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;
-  p.epi_skip = 0;
   L->bf = bf;
   L->ar = p.nk <= 4 && !no_ar;
   L->rowscale = a.metric == VRS_COSINE;

@@ -231,8 +231,6 @@ struct TcParams {
   const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
-  int32_t epi_skip;        // (unused: the MMA + TMA-only and read-out-only measurements are debug
-                           // builds, -DVRS_EPI_SKIP_BUILD / -DVRS_EPI_READOUT_ONLY)
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
