@@ -64,3 +64,13 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(L, "_lib", None)
     with pytest.raises(ImportError):
         L.load_library()
+
+
+def test_product_library_exports_exactly_the_header():
+    """libvrs.so's dynamic symbol table is the boundary and nothing else: no debug-only
+    entry points (e.g. the -DVRS_TC_TIMING timeline reader) and no leaked internals."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_2403_15807_b200", "libvrs.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    exported = sorted(line.split()[-1] for line in out.splitlines() if line.strip())
+    assert exported == _declared()
