@@ -818,12 +818,14 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
 #endif
 template <int CAP, int SEL>
 __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) finalize_warp_kernel(FinalizeArgs a) {
+  TL_SCOPE(1);
   __shared__ FinBufsT<CAP> s_buf[kFinGroup];
   __shared__ double s_sc[kFinGroup][SEL];
   __shared__ int64_t s_sid[kFinGroup][SEL];
   const int w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
   pdl_wait();
+  TL_WAITED(1);
   pdl_trigger();
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
   const int m = fin_stream(a, j, 0, 1, s_buf[w]);
@@ -880,6 +882,7 @@ __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s
 
 
 __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a) {
+  TL_SCOPE(1);
   extern __shared__ __align__(16) uint8_t fin_dyn[];
   FinBufs *s_buf = reinterpret_cast<FinBufs *>(fin_dyn);   // [kFinW]
   __shared__ double s_sc[kFinMaxSel];
@@ -888,6 +891,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
   pdl_wait();
+  TL_WAITED(1);
   pdl_trigger();
   // each warp: its share of the lists -> its survivors (<= k', or <= 32E unsorted when
   // the tree merge follows: it sorts them anyway)
@@ -895,6 +899,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   const int nw = fin_stream(a, j, w, kFinW, s_buf[w], keep);
   if (lane == 0) s_n[w] = nw;
   __syncthreads();
+  TL_STAMP(1, 2);
   if (a.kprime <= 64) {
     fin_tree_merge<2>(a, s_buf, nw, s_n);
   } else if (a.kprime <= 128) {
@@ -932,10 +937,12 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
     if (lane == 0) s_n[0] = n;
   }
   __syncthreads();
+  TL_STAMP(1, 3);
   const int m = s_n[0];
   const double qq = fin_qq(a, j);
   fin_rescore<8>(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid);
   __syncthreads();
+  TL_STAMP(1, 4);
   if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid);
 }
 
@@ -947,6 +954,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
 // long value lists, so more threads per query)
 template <int kThrThreads>
 __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a) {
+  TL_SCOPE(0);
   extern __shared__ uint32_t s_val[];
   __shared__ uint32_t hist[256];
   __shared__ uint32_t s_bin, s_above, s_total;
@@ -954,6 +962,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(ThresholdArgs a)
   const int64_t j = blockIdx.x;
   const float *v = a.vals + j * a.nvals;
   pdl_wait();
+  TL_WAITED(0);
   pdl_trigger();
   const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);   // lists of used splits only
   __shared__ uint32_t s_lo[32], s_hi[32], s_cnt[32], s_cv[64];
@@ -1112,11 +1121,13 @@ __device__ __forceinline__ float lane_top_kth(const float *v, int nvals, int fir
 // the top K.  Exact when every lane holds <= 2 values.
 // K > 64 stages the values in shared memory for the radix select.
 __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(ThresholdArgs a) {
+  TL_SCOPE(0);
   extern __shared__ uint32_t s_vals[];
   __shared__ uint32_t s_hist[kFinGroup][256];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = (int64_t)blockIdx.x * kFinGroup + w;
   pdl_wait();
+  TL_WAITED(0);
   pdl_trigger();
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
@@ -1145,16 +1156,20 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
 // values: a valid lower bound of the K-th best key (see threshold_warp_kernel).
 template <int NW, int E>
 __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs a) {
+  TL_SCOPE(0);
   __shared__ float s_f[NW][32 * E];
   __shared__ int32_t s_i[NW][32 * E];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
   pdl_wait();
+  TL_WAITED(0);
   pdl_trigger();
   const float *v = a.vals + j * a.nvals;
   const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);
+  TL_STAMP(0, 2);
   float t[E];
   lane_top_sorted<E, NW * 32>(v, nvals, w * 32 + lane, t);
+  TL_STAMP(0, 3);
   int32_t id[E];
 #pragma unroll
   for (int h = 0; h < E; ++h) id[h] = (w * E + h) * 32 + lane;   // (distinct tie-breakers)
@@ -1168,6 +1183,7 @@ __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs 
     if (w < stride) warp_merge_with_e<E>(t, id, s_f[w + stride], s_i[w + stride]);
     __syncthreads();
   }
+  TL_STAMP(0, 4);
   if (w == 0) {
     const float kth = elem_e<E>(t, a.kth - 1);
     if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
@@ -1222,12 +1238,14 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
 // ------------------------------------------------------------------ K10' merge
 
 __global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
+  TL_SCOPE(2);
   __shared__ int64_t s_id[kFinMaxSel];
   __shared__ float s_key[kFinMaxSel];
   __shared__ double s_k2[kFinMaxSel];
   __shared__ int64_t s_i2[kFinMaxSel];
   const int64_t j = blockIdx.x;
   pdl_wait();
+  TL_WAITED(2);
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5;
   auto get = [&](int64_t c, float &key, int64_t &id) -> bool {
@@ -1269,3 +1287,9 @@ cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s, int *launches) {
 }
 
 }  // namespace vrs
+
+#ifdef VRS_TC_TIMING
+namespace vrs {
+int tl_read_fin(unsigned long long *host) { return tl_read(host); }
+}
+#endif

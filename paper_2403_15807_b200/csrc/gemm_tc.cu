@@ -50,7 +50,9 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
                                                           int64_t cap, void *__restrict__ xsel,
                                                           const float *__restrict__ norm_src,
                                                           float *__restrict__ norm_dst, int64_t cp_min_bytes) {
+  TL_SCOPE(4);
   pdl_wait();
+  TL_WAITED(4);
   pdl_trigger();
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, cap)) return;
@@ -84,10 +86,12 @@ __global__ void __launch_bounds__(256) select_finish_kernel(const uint32_t *__re
                                                             int32_t row_bytes, void *__restrict__ xsel,
                                                             const float *__restrict__ norm_src,
                                                             float *__restrict__ norm_dst) {
+  TL_SCOPE(6);
   extern __shared__ uint32_t s_pre[];   // [nchunks + 1]
   __shared__ uint32_t s_wsum[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_wait();
+  TL_WAITED(6);
   pdl_trigger();
   // exclusive prefix of the chunk counts: thread t sums a contiguous segment
   const int seg = (nchunks + 255) / 256;
@@ -172,7 +176,9 @@ cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, con
 // tiles, so the TMA loads of the query operand never fall out of bounds).
 __global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count,
                                    int64_t total) {
+  TL_SCOPE(5);
   pdl_wait();
+  TL_WAITED(5);
   pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = count + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
@@ -418,13 +424,7 @@ GemmLists gemm_lists(const GemmArgs &a, const GemmPlan &plan, void *scratch) {
 }  // namespace vrs
 
 #ifdef VRS_TC_TIMING
-// Debug builds only (-DVRS_TC_TIMING): copy the per-CTA globaltimer stamps of the
-// last tensor-core launches ([mode][cta][8] u64, see TC_TL) to host and clear them.
-extern "C" VRS_API int vrs_debug_tc_timeline(unsigned long long *host) {
-  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-  void *d = nullptr;
-  if (cudaGetSymbolAddress(&d, vrs::g_tc_tl) != cudaSuccess) return -1;
-  if (cudaMemcpy(host, d, sizeof(vrs::g_tc_tl), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return cudaMemset(d, 0, sizeof(vrs::g_tc_tl)) == cudaSuccess ? 0 : -1;
+namespace vrs {
+int tl_read_gemm(unsigned long long *host) { return tl_read(host); }
 }
 #endif

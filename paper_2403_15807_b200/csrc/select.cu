@@ -36,8 +36,10 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
                                                                    uint32_t *__restrict__ bitmap,
                                                                    uint32_t *__restrict__ chunk_count,
                                                                    SelectFuse fz, int32_t *__restrict__ ids_local) {
+  TL_SCOPE(0);
   __shared__ uint32_t s_cnt[kSelWarps];
   pdl_wait();
+  TL_WAITED(0);
   pdl_trigger();
   if (fz.q_out) {   // folded in: this block's slice of the fp32 -> bf16 query conversion (zero padding)
     const int64_t per = ((fz.q_total + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
@@ -146,8 +148,10 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, 
                                                                      const uint32_t *__restrict__ chunk_count,
                                                                      int32_t *__restrict__ ids,
                                                                      int64_t *__restrict__ count) {
+  TL_SCOPE(1);
   __shared__ uint64_t s_red[kSelWarps];
   pdl_wait();
+  TL_WAITED(1);
   pdl_trigger();
   __shared__ uint32_t s_wsum[kSelWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,3 +226,9 @@ cudaError_t launch_select_local(const PredDev &pred, int64_t n, uint32_t *bitmap
 size_t select_scratch_bytes(int64_t n) { return (size_t)((n + kSelRows - 1) / kSelRows) * 4 + 8; }
 
 }  // namespace vrs
+
+#ifdef VRS_TC_TIMING
+namespace vrs {
+int tl_read_select(unsigned long long *host) { return tl_read(host); }
+}
+#endif

@@ -311,18 +311,7 @@ constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the li
 // MODE: MAIN (fused top-k candidates) or PROBE (slot maxima for the threshold).
 // ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
 // BF: operands are bf16 (shadow corpus, kind::f16) instead of fp32 (kind::tf32).
-#ifdef VRS_TC_TIMING
-// debug build only: per-CTA globaltimer stamps [mode][cta][8] (tools/tc_timeline.py)
-static __device__ unsigned long long g_tc_tl[4][4096][8];
-__device__ __forceinline__ unsigned long long tl_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TC_TL(slot) (blockIdx.x < 4096 ? (void)(g_tc_tl[MODE & 3][blockIdx.x][slot] = tl_now()) : (void)0)
-#else
-#define TC_TL(slot) ((void)0)
-#endif
+#define TC_TL(slot) TL_STAMP(MODE & 3, slot)   // (thread-0-only stamps are filtered in TL_STAMP)
 template <bool AR, int MODE, bool ROWSCALE, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
@@ -563,7 +552,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < p.nk; ++kb) {
         mbar_wait(&full_bar[stage], phase);
-        if (t == 0 && kb == 0 && lane == 0) TC_TL(2);
+        if (t == 0 && kb == 0 && lane == 0) TL_STAMP_ANY(MODE & 3, 2);
         if (cpg) fence_proxy_async_smem();   // cp.async (generic proxy) writes -> the MMA's async-proxy reads
         tc_fence_after();
         if (lane == 0) {
@@ -917,7 +906,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int bs = t % BIAS_STAGES;
       mbar_wait(&bfull_bar[bs], (t / BIAS_STAGES) & 1);
       mbar_wait(&tfull_bar[acc], (t / ACC_STAGES) & 1);
-      if (t == 0 && ew == 0 && lane == 0) TC_TL(3);
+      if (t == 0 && ew == 0 && lane == 0) TL_STAMP_ANY(MODE & 3, 3);
       tc_fence_after();
       const float *ba = bias_a + bs * BN + half * EPI_COLS;
       const float *bb = bias_b + bs * BN + half * EPI_COLS;
@@ -968,7 +957,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_arrive(&bempty_bar[bs]);
       }
     }
-    if (ew == 0 && lane == 0) TC_TL(4);
+    if (ew == 0 && lane == 0) TL_STAMP_ANY(MODE & 3, 4);
     if (p.stats && lane == 0) {
       atomicAdd(p.stats + 0, (unsigned long long)st_chunks);
       atomicAdd(p.stats + 1, (unsigned long long)st_slow);
@@ -993,8 +982,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #ifdef VRS_TC_TIMING
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_tc_tl[MODE & 3][blockIdx.x < 4096 ? blockIdx.x : 4095][6] = smid;
-    g_tc_tl[MODE & 3][blockIdx.x < 4096 ? blockIdx.x : 4095][7] = (unsigned long long)ntiles;
+    if (blockIdx.x < 4096) { g_tl[MODE & 3][blockIdx.x][6] = smid; g_tl[MODE & 3][blockIdx.x][7] = (unsigned long long)ntiles; }
 #endif
   }
   if (warp == 1) {

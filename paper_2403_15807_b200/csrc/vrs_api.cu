@@ -844,3 +844,17 @@ vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n
 }
 
 }  // extern "C"
+
+#ifdef VRS_TC_TIMING
+// Debug builds only (-DVRS_TC_TIMING): per-CTA timeline stamps of one translation
+// unit's kernels (0 select.cu, 1 gemm_tc.cu, 2 finalize.cu; [8][4096][8] u64, see
+// TL_STAMP in vrs_internal.cuh) copied to host and cleared.
+namespace vrs {
+int tl_read_select(unsigned long long *);
+int tl_read_gemm(unsigned long long *);
+int tl_read_fin(unsigned long long *);
+}
+extern "C" VRS_API int vrs_debug_timeline(int tu, unsigned long long *host) {
+  return tu == 0 ? vrs::tl_read_select(host) : tu == 1 ? vrs::tl_read_gemm(host) : tu == 2 ? vrs::tl_read_fin(host) : -1;
+}
+#endif

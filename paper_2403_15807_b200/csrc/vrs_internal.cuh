@@ -43,6 +43,42 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// ---- debug timeline (compile-time only: -DVRS_TC_TIMING; tools/tc_timeline.py) --
+// Per translation unit: globaltimer stamps [region][cta][8] -- slot 0 kernel entry,
+// 1 after griddepcontrol.wait, 5 thread 0 leaving the kernel (the tensor-core
+// kernels add 2-4 and the SM id / tile count in 6 / 7).  Product builds compile
+// every TL_* to nothing.
+#ifdef VRS_TC_TIMING
+static __device__ unsigned long long g_tl[8][4096][8];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_STAMP(region, slot) \
+  ((blockIdx.x < 4096 && threadIdx.x == 0) ? (void)(g_tl[(region)][blockIdx.x][(slot)] = tl_now()) : (void)0)
+#define TL_STAMP_ANY(region, slot) \
+  (blockIdx.x < 4096 ? (void)(g_tl[(region)][blockIdx.x][(slot)] = tl_now()) : (void)0)
+struct TlEnd {
+  int r;
+  __device__ ~TlEnd() { TL_STAMP(r, 5); }
+};
+#define TL_SCOPE(region) TL_STAMP(region, 0); TlEnd tl_end_{region}
+#define TL_WAITED(region) TL_STAMP(region, 1)
+static inline int tl_read(unsigned long long *host) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  void *d = nullptr;
+  if (cudaGetSymbolAddress(&d, g_tl) != cudaSuccess) return -1;
+  if (cudaMemcpy(host, d, sizeof(g_tl), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return cudaMemset(d, 0, sizeof(g_tl)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define TL_STAMP(region, slot) ((void)0)
+#define TL_STAMP_ANY(region, slot) ((void)0)
+#define TL_SCOPE(region) ((void)0)
+#define TL_WAITED(region) ((void)0)
+#endif
+
 // ---- host-side one-time setup ---------------------------------------------------
 // Function attributes and pool tuning are set lazily on first use, possibly from
 // several host threads at once: serialised here.
