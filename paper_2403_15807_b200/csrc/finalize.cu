@@ -1148,44 +1148,68 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
 }
 
+// Per-lane E largest of a strided share, all loads of a round issued together
+// (U per lane), then sorted warp-wide (element h * 32 + lane).
+template <int E, int S, int U>
+__device__ __forceinline__ void lane_top_sorted_1r(const float *v, int nvals, int first, float (&t)[E]) {
+#pragma unroll
+  for (int h = 0; h < E; ++h) t[h] = -INFINITY;
+#pragma unroll 1
+  for (int i0 = first; i0 < nvals; i0 += U * S) {
+    float f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) f[u] = i0 + u * S < nvals ? __ldg(v + i0 + u * S) : -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) top_insert_e<E>(t, f[u]);
+  }
+  int32_t id[E];
+#pragma unroll
+  for (int h = 0; h < E; ++h) id[h] = h * 32 + (int)(threadIdx.x & 31);
+  warp_sort_e<E>(t, id);
+}
+
 // Small batches (K <= 128): one CTA of NW warps per query, registers first.  Each
 // lane keeps the E largest of its strided share (E = 2 for K <= 64, else 4),
-// each warp sorts its 32E, and a tree of bitonic merges (best 32E of two sorted
-// lists) leaves the 32E largest of the warps' union in warp 0.  Every stage keeps
-// a subset of the values, so its K-th largest is <= the K-th largest of all
-// values: a valid lower bound of the K-th best key (see threshold_warp_kernel).
-template <int NW, int E>
+// each warp sorts its 32E and keeps its best 32M (M = 1 for K <= 32), and a tree
+// of bitonic merges (best 32M of two sorted lists) leaves the 32M largest of the
+// warps' union in warp 0.  Every stage keeps a subset of the values that holds
+// that subset's K best, so its K-th largest is <= the K-th largest of all values:
+// a valid lower bound of the K-th best key (see threshold_warp_kernel).  Every
+// probe slot is written (CTAs of unused splits publish -inf), so all a.nvals
+// values are read -- no wait on the selection count -- in one round of loads.
+template <int NW, int E, int M>
 __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs a) {
+  static_assert(M <= E, "merged width within the per-lane lists");
   TL_SCOPE(0);
-  __shared__ float s_f[NW][32 * E];
-  __shared__ int32_t s_i[NW][32 * E];
+  __shared__ float s_f[NW][32 * M];
+  __shared__ int32_t s_i[NW][32 * M];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
   pdl_wait();
   TL_WAITED(0);
   pdl_trigger();
   const float *v = a.vals + j * a.nvals;
-  const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);
   TL_STAMP(0, 2);
   float t[E];
-  lane_top_sorted<E, NW * 32>(v, nvals, w * 32 + lane, t);
+  lane_top_sorted_1r<E, NW * 32, 12>(v, (int)a.nvals, w * 32 + lane, t);
   TL_STAMP(0, 3);
-  int32_t id[E];
+  float tm[M];
+  int32_t id[M];
 #pragma unroll
-  for (int h = 0; h < E; ++h) id[h] = (w * E + h) * 32 + lane;   // (distinct tie-breakers)
+  for (int h = 0; h < M; ++h) { tm[h] = t[h]; id[h] = (w * M + h) * 32 + lane; }   // (distinct tie-breakers)
 #pragma unroll 1
   for (int stride = NW / 2; stride >= 1; stride >>= 1) {
     if (w < 2 * stride) {
 #pragma unroll
-      for (int h = 0; h < E; ++h) { s_f[w][h * 32 + lane] = t[h]; s_i[w][h * 32 + lane] = id[h]; }
+      for (int h = 0; h < M; ++h) { s_f[w][h * 32 + lane] = tm[h]; s_i[w][h * 32 + lane] = id[h]; }
     }
     __syncthreads();
-    if (w < stride) warp_merge_with_e<E>(t, id, s_f[w + stride], s_i[w + stride]);
+    if (w < stride) warp_merge_with_e<M>(tm, id, s_f[w + stride], s_i[w + stride]);
     __syncthreads();
   }
   TL_STAMP(0, 4);
   if (w == 0) {
-    const float kth = elem_e<E>(t, a.kth - 1);
+    const float kth = elem_e<M>(tm, a.kth - 1);
     if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
   }
 }
@@ -1203,11 +1227,14 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   }
   if (!block_thr && a.kth <= 128) {
     const bool big = a.q < kSmCountB200;   // few queries: more warps per query
+    if (a.kth <= 32)
+      return big ? launch_k(threshold_union_kernel<32, 2, 1>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
+                 : launch_k(threshold_union_kernel<8, 2, 1>, dim3((unsigned)a.q), dim3(256), 0, s, a);
     if (a.kth <= 64)
-      return big ? launch_k(threshold_union_kernel<32, 2>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
-                 : launch_k(threshold_union_kernel<8, 2>, dim3((unsigned)a.q), dim3(256), 0, s, a);
-    return big ? launch_k(threshold_union_kernel<16, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
-               : launch_k(threshold_union_kernel<8, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+      return big ? launch_k(threshold_union_kernel<32, 2, 2>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
+                 : launch_k(threshold_union_kernel<8, 2, 2>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+    return big ? launch_k(threshold_union_kernel<16, 4, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
+               : launch_k(threshold_union_kernel<8, 4, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr1024 = 0, attr256 = 0;
