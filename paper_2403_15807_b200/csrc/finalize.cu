@@ -590,7 +590,9 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
                           int keep = -1) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
-  const int lists = a.split.bn ? (int)min((int64_t)a.lists, kListsPerSplit * splits_used(a.split)) : a.lists;
+  // (every list's count is written -- lists of unused splits as 0 -- so all a.lists
+  // are read without waiting on the selection count)
+  const int lists = a.lists;
   uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
   if (a.sorted && K <= a.kread) {
     for (int l = lane; l < lists; l += 32) {
@@ -601,10 +603,12 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
     for (int o = 16; o > 0; o >>= 1) thr = max(thr, __shfl_xor_sync(0xffffffffu, thr, o));
   }
   int n = 0;
+  auto count_of = [&](int l) { return l < lists ? (a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread) : 0; };
+  int c_next = count_of(first_group * 32 + lane);   // (the next group's counts load under this group's keys)
   for (int l0 = first_group * 32; l0 < lists; l0 += group_step * 32) {
     const int l = l0 + lane;
-    int c = 0;
-    if (l < lists) c = a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread;
+    const int c = c_next;
+    c_next = count_of(l0 + group_step * 32 + lane);
     const int64_t base = ((int64_t)(l < lists ? l : 0) * a.q + j) * a.stride;
     for (int r0 = 0; __any_sync(0xffffffffu, r0 < c); r0 += 8) {
       float kv[8];
