@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
   pdl_trigger();
   if (j >= a.q) return;
   const float *v = a.vals + j * a.nvals;
-  const int nvals = (int)min((int64_t)a.nvals, kListsPerSplit * splits_used(a.split) * 32);
+  const int nvals = (int)a.nvals;   // (every probe slot is written, unused splits as -inf: no wait on the count)
   if (a.kth > 128) {
     uint32_t *mine = s_vals + (size_t)w * a.nvals;
     for (int i = lane; i < nvals; i += 32) {
