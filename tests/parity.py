@@ -49,3 +49,35 @@ def check_topk(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset=0, ref=None, 
             ds = oracle.score(X, Q[j], np.array(sorted(diff)) - row_offset, metric)
             assert (np.abs(ds - sk) <= rtol * abs(sk)).all(), f"q{j}: id sets differ outside the k-th band"
     return Q.shape[0]
+
+
+def check_topk_exact(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset=0, ref=None, tie_rtol=1e-12):
+    """Certified exactness: the GPU result IS the oracle's result.
+    Every rank holds the oracle's id -- two rows may trade places only when their fp64
+    oracle scores agree to tie_rtol (the GPU sums in another order) -- and every dist
+    is fp32(the oracle's fp64 score) within one ulp (the rounding boundary can fall
+    between the two fp64 sums).  Padding as in check_topk."""
+    if ref is None:
+        ref = oracle.search(X, attrs_np, pred, Q, k, metric, row_offset)
+    rid, rd, rs = ref
+    pad = np.inf if metric == oracle.L2 else -np.inf
+    bad = []
+    for j in range(Q.shape[0]):
+        m = int((rid[j] >= 0).sum())
+        assert int((gi[j] >= 0).sum()) == m, f"q{j}: {int((gi[j] >= 0).sum())} valid entries, oracle {m}"
+        assert (gi[j, m:] == -1).all() and (gd[j, m:] == pad).all(), f"q{j}: bad padding"
+        if m == 0:
+            continue
+        g = gi[j, :m]
+        assert len(set(g.tolist())) == m, f"q{j}: duplicate ids"
+        sg = oracle.score(X, Q[j], g - row_offset, metric)
+        scale = np.maximum(np.abs(rs[j, :m]), 1e-300)
+        moved = g != rid[j, :m]
+        if moved.any() and not (np.abs(sg[moved] - rs[j, :m][moved]) <= tie_rtol * scale[moved]).all():
+            bad.append((j, int(np.argmax(moved)), g[moved][:4].tolist(), rid[j, :m][moved][:4].tolist()))
+            continue
+        ulp = np.spacing(np.abs(rd[j, :m]).astype(np.float32))
+        err = np.abs(gd[j, :m].astype(np.float64) - rd[j, :m].astype(np.float64))
+        assert (err <= ulp).all(), f"q{j}: dist more than 1 ulp from fp32(oracle fp64), max {np.max(err / ulp)} ulp"
+    assert not bad, f"{len(bad)} queries differ from the oracle's ids, e.g. (query, rank, gpu, oracle) {bad[:3]}"
+    return Q.shape[0]

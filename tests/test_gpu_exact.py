@@ -1,0 +1,105 @@
+"""Certified exact top-k: adversarial inputs where the
+tensor-core selection precision cannot separate the true top-k from other rows.
+
+The acceptance rule here is the strict one (tests/parity.py check_topk_exact):
+the returned ids are the oracle's, rank for rank, and every dist is
+fp32(oracle fp64) within one ulp -- no 1e-3 band.  PAPER.md L1417 (Table 1,
+"Accuracy: Exact") and L26 ("the accurate but exhaustive scan-based search")."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from parity import check_topk_exact
+
+pytestmark = pytest.mark.gpu
+
+METRICS = {oracle.L2: "l2", oracle.IP: "ip", oracle.COS: "cos"}
+
+
+@pytest.fixture(scope="module")
+def vrs():
+    import paper_2403_15807_b200 as m
+    m.library()
+    return m
+
+
+def _tie_corpus(n, d, lo_scale, hi_scale, seed=0):
+    """q = e0.  Rows 0-29 are e0 * lo_scale, rows 30-39 e0 * hi_scale (the true top 10
+    under IP), every other row has <q, x> < 0.9.  When lo_scale and hi_scale round to
+    the same value in the selection precision, the 40 keys tie and a selection by key
+    (ties -> lower id) alone keeps rows 0-25."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)).astype(np.float32) * 0.05
+    X[:, 0] = rng.uniform(-0.9, 0.85, n).astype(np.float32)
+    X[:40] = 0.0
+    X[:30, 0] = np.float32(lo_scale)
+    X[30:40, 0] = np.float32(hi_scale)
+    perm = rng.permutation(n)          # scatter the 40 rows over the corpus, keep their order
+    order = np.sort(perm[:40])
+    rest = np.setdiff1d(np.arange(n), order)
+    Y = np.empty_like(X)
+    Y[order] = X[:40]
+    Y[rest] = X[40:]
+    Q = np.zeros((1, d), dtype=np.float32)
+    Q[0, 0] = 1.0
+    return Y, Q
+
+
+def _search(vrs, X, Q, k, metric, attrs=None, pred=(), precision=None, path=None):
+    n = X.shape[0]
+    attrs = attrs if attrs is not None else [np.zeros(n, dtype=np.int32)]
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], precision=precision)
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), list(pred), k=k, metric=METRICS[metric], path=path)
+    torch.cuda.synchronize()
+    return ids.cpu().numpy(), dists.cpu().numpy(), attrs
+
+
+@pytest.mark.parametrize("hi", [1 + 3.5e-3, 1 + 2e-4], ids=["gap3.5e-3", "gap2e-4"])
+def test_selection_ties_default_precision(vrs, hi):
+    """The judge's construction (What's weak #1): gap 3.5e-3 ties in bf16;
+    gap 2e-4 also ties in fp16 / TF32."""
+    X, Q = _tie_corpus(50000, 128, 1 + 1e-5, hi)
+    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP)
+    check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.IP)
+    assert sorted((gi[0] >= 0).nonzero()[0].tolist()) == list(range(10))
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_selection_ties_every_precision(vrs, prec):
+    p = {"tf32": vrs.PREC_TF32, "bf16": vrs.PREC_BF16}[prec]
+    X, Q = _tie_corpus(50000, 128, 1 + 1e-5, 1 + 3.5e-3, seed=1)
+    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP, precision=p)
+    check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.IP)
+
+
+def test_near_zero_cosine_window(vrs):
+    """C5-like: clustered rows, a narrow predicate window that excludes the query's
+    own cluster, so the k-th cosine is near 0 and many rows crowd the boundary."""
+    rng = np.random.default_rng(5)
+    n, d, C = 200000, 256, 1024
+    cent = rng.standard_normal((C, d)).astype(np.float32)
+    cid = rng.integers(0, C, n)
+    X = (cent[cid] + 0.1 * rng.standard_normal((n, d))).astype(np.float32)
+    attrs = [(cid + rng.integers(0, 8, n)).astype(np.int32)]
+    qc = rng.integers(200, C, 16)
+    Q = (cent[qc] + 0.1 * rng.standard_normal((16, d))).astype(np.float32)
+    pred = [(0, 7, 7)]            # w = 1 window far from the queries' clusters
+    gi, gd, _ = _search(vrs, X, Q, 50, oracle.COS, attrs=attrs, pred=pred)
+    check_topk_exact(gi, gd, X, attrs, pred, Q, 50, oracle.COS)
+
+
+def test_l2_near_duplicates(vrs):
+    """L2: 64 near-copies of the query at distances that differ below the selection
+    precision; the true 10 nearest must come back in order."""
+    rng = np.random.default_rng(7)
+    n, d = 60000, 384
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Q = rng.standard_normal((3, d)).astype(np.float32)
+    pos = rng.choice(n, 3 * 64, replace=False)
+    for j in range(3):
+        for i in range(64):
+            X[pos[64 * j + i]] = Q[j] + np.float32(1e-2) * (1.0 + 1e-4 * i) * np.sign(rng.standard_normal(d)).astype(np.float32)
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    gi, gd, _ = _search(vrs, X, Q, 10, oracle.L2, attrs=attrs)
+    check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.L2)
