@@ -32,6 +32,13 @@
  *    dist = +inf (L2) or -inf (IP, COSINE).  ids are GLOBAL: row_offset + local row.
  *    dists are computed exactly in fp32 from the fp32 inputs (the tensor-core
  *    selection pass is re-scored).
+ *  - Exactness (Table 1 "Accuracy: Exact"; L26): the returned
+ *    rows ARE the top-k of the definition, not an approximation.  The fast
+ *    selection pass (16-bit / TF32 tensor-core keys, or fp32 FFMA keys) carries
+ *    a per-query error bound E; a query is CERTIFIED when the k-th exact score
+ *    of the re-scored candidates beats every unselected row's key + E.
+ *    Uncertified queries are recomputed on the device by an exact fp64 scan of
+ *    the qualifying rows.  No host synchronisation.
  */
 #ifndef VRS_H
 #define VRS_H
@@ -49,8 +56,8 @@
 extern "C" {
 #endif
 
-#define VRS_ABI_VERSION 1
-/* Largest k vrs_search accepts (the selection pass over-fetches k + 16). */
+#define VRS_ABI_VERSION 2
+/* Largest k vrs_search accepts (the selection pass over-fetches k' = the power of two >= k + 16). */
 #define VRS_K_MAX 240
 /* Largest number of AND-ed clauses in one predicate. */
 #define VRS_MAX_CLAUSES 8
@@ -103,12 +110,16 @@ typedef struct {
 typedef struct vrs_index vrs_index;
 
 /* Operand precision of the tensor-core SELECTION pass.
- * Returned distances are always re-scored exactly from the fp32 inputs; the
- * precision only decides which rows reach the re-score (k + 16 per query). */
+ * Returned distances are always re-scored exactly from the fp32 inputs and the
+ * result is certified exact whatever the precision; the precision decides the
+ * pass's speed and how often its certificate holds without the exact fallback. */
 typedef enum {
-  VRS_PREC_DEFAULT = 0,  /* load: bf16 shadow when d % 8 == 0; search: the index's own */
+  VRS_PREC_DEFAULT = 0,  /* load: fp16 shadow when d % 8 == 0; search: the index's own */
   VRS_PREC_TF32 = 1,     /* tcgen05 kind::tf32 on the fp32 corpus (no extra memory) */
-  VRS_PREC_BF16 = 2      /* tcgen05 kind::f16 on a bf16 shadow copy built at load (+2 bytes / element) */
+  VRS_PREC_BF16 = 2,     /* tcgen05 kind::f16 on a bf16 shadow copy built at load (+2 bytes / element) */
+  VRS_PREC_FP16 = 3      /* tcgen05 kind::f16 on an fp16 shadow (+2 bytes / element): the corpus scaled by one
+                            power of two 2^e_x at load, each query by its own 2^e_q, so the 11-bit significand
+                            is used in full (8x tighter selection keys than bf16 at the same cost) */
 } vrs_precision;
 
 typedef struct {
@@ -136,10 +147,11 @@ VRS_API vrs_status vrs_load(const float *vectors, int64_t n, int32_t d, const vr
 
 /*
  * vrs_load_ex -- vrs_load with options (opts == NULL => defaults).  precision:
- * DEFAULT builds the bf16 shadow when d % 8 == 0 and the base is 16-byte aligned;
- * TF32 never builds it; BF16 requires it (else VRS_EUNSUPPORTED).  The shadow is
- * index-owned memory (n * d * 2 bytes, through `alloc`), converted on `cuda_stream`
- * with round-to-nearest-even.
+ * DEFAULT builds the fp16 shadow when d % 8 == 0 and the base is 16-byte aligned;
+ * TF32 never builds one; FP16 / BF16 require it (else VRS_EUNSUPPORTED).  The
+ * shadow is index-owned memory (n * d * 2 bytes, through `alloc`), converted on
+ * `cuda_stream` with round-to-nearest-even; the load also measures the shadow's
+ * per-row rounding residual |x~ - x| exactly (fp64) -- the certificate's bound.
  */
 VRS_API vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_attr *attrs, int32_t n_attrs,
                                int64_t row_offset, const vrs_allocator *alloc, const vrs_load_options *opts,
@@ -174,7 +186,7 @@ typedef enum {
 typedef struct {
   int32_t path;      /* vrs_path */
   int32_t rows;      /* vrs_rows */
-  int32_t precision; /* vrs_precision of the tensor-core selection (DEFAULT: bf16 if the index has the shadow) */
+  int32_t precision; /* vrs_precision of the tensor-core selection (DEFAULT: the index's shadow if it has one, else TF32) */
   int32_t host_async; /* vrs_search_host only (the host buffers must then be pinned):
                          0 = synchronise cuda_stream before returning;
                          1 = do not synchronise; cuda_stream is ordered after the device->host copies,
@@ -182,7 +194,14 @@ typedef struct {
                          2 = overlap: cuda_stream is NOT ordered after the copies (the next call's
                              kernels overlap this call's download); h_ids / h_dists are complete once
                              vrs_host_fence(ix, s) has been enqueued on a stream s and s has synchronised */
-  int32_t reserved[4];
+  int32_t reserved0;
+  /* Optional DEVICE uint64 [4] the call accumulates into (NULL: nothing is recorded):
+   *   [0] += queries answered, [1] += queries whose selection was NOT certified and
+   *   were recomputed by the exact fp64 scan, [2] = max(previous, the largest observed
+   *   |selection key - exact key| / E over all re-scored candidates) as IEEE-754
+   *   double bits (< 1 confirms the bound on this data), [3] reserved. */
+  uint64_t *stats;
+  int32_t reserved[2];
 } vrs_search_options;
 
 /* vrs_search with explicit options (opts == NULL => defaults). */
@@ -268,7 +287,7 @@ VRS_API const char *vrs_last_error(void);
 VRS_API int32_t vrs_last_path(void);
 /* vrs_precision of the last vrs_search_ex's tensor-core pass on this thread (DEFAULT when it took the scan path). */
 VRS_API int32_t vrs_last_precision(void);
-/* VRS_PREC_BF16 if the index holds the bf16 shadow, else VRS_PREC_TF32. */
+/* VRS_PREC_FP16 / VRS_PREC_BF16 if the index holds that shadow, else VRS_PREC_TF32. */
 VRS_API int32_t vrs_index_precision(const vrs_index *ix);
 VRS_API int32_t vrs_last_launches(void);
 

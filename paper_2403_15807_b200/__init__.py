@@ -15,10 +15,11 @@ import torch
 
 from . import _lib
 from ._lib import (ATTR_I32, ATTR_U8, COSINE, EXPORTS, IP, K_MAX, L2, PATH_AUTO, PATH_GEMM, PATH_SCAN,
-                   PREC_BF16, PREC_DEFAULT, PREC_TF32, ROWS_AUTO, ROWS_GATHER, ROWS_MASKED, VrsError)
+                   PREC_BF16, PREC_DEFAULT, PREC_FP16, PREC_TF32, ROWS_AUTO, ROWS_GATHER, ROWS_MASKED, VrsError)
 
 __all__ = ["Index", "merge", "VrsError", "L2", "IP", "COSINE", "PATH_AUTO", "PATH_SCAN", "PATH_GEMM",
-           "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "PREC_DEFAULT", "PREC_TF32", "PREC_BF16", "K_MAX", "last_path",
+           "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "PREC_DEFAULT", "PREC_TF32", "PREC_BF16", "PREC_FP16", "K_MAX",
+           "last_path", "new_stats",
            "last_precision", "last_launches", "library"]
 
 METRICS = {"l2": L2, "ip": IP, "cos": COSINE, "cosine": COSINE}
@@ -49,10 +50,15 @@ def _ptr(t: torch.Tensor | None):
 _opt_cache = {}
 
 
-def _options(path, rows, precision=None, host_async=False):
-    if path is None and rows is None and precision is None and not host_async:
+def _options(path, rows, precision=None, host_async=False, stats=None):
+    sp = 0
+    if stats is not None:
+        if stats.dtype != torch.int64 or stats.numel() < 4 or not stats.is_cuda or not stats.is_contiguous():
+            raise ValueError("stats must be a contiguous CUDA int64 tensor of >= 4 entries (new_stats())")
+        sp = stats.data_ptr()
+    if path is None and rows is None and precision is None and not host_async and not sp:
         return None
-    key = (path, rows, precision, int(host_async))
+    key = (path, rows, precision, int(host_async), sp)
     if key in _opt_cache:
         return _opt_cache[key][1]
     o = _lib.SearchOptions()
@@ -60,8 +66,47 @@ def _options(path, rows, precision=None, host_async=False):
     o.rows = ROWS_AUTO if rows is None else int(rows)
     o.precision = PREC_DEFAULT if precision is None else int(precision)
     o.host_async = int(host_async)   # False / True (1) / 2 = overlap (see vrs.h)
+    o.stats = sp or None
+    if len(_opt_cache) > 4096:
+        _opt_cache.clear()
     _opt_cache[key] = (o, ctypes.byref(o))   # the struct stays alive with its reference
     return _opt_cache[key][1]
+
+
+def new_stats(device=None) -> torch.Tensor:
+    """A zeroed device counter block for search(..., stats=): [queries, uncertified queries
+    (recomputed by the exact fallback), max observed key error / bound (double bits), reserved]."""
+    return torch.zeros(4, dtype=torch.int64, device=device or torch.device("cuda", torch.cuda.current_device()))
+
+
+def read_stats(stats: torch.Tensor) -> dict:
+    """Decode a stats block (synchronises): queries, uncertified, certified fraction, max key error / bound."""
+    v = stats.cpu()
+    q, u = int(v[0]), int(v[1])
+    ratio = float(v[2:3].view(torch.float64)[0])
+    return {"queries": q, "uncertified": u, "certified_fraction": (q - u) / q if q else 1.0,
+            "max_key_error_over_bound": ratio}
+
+
+def _check_queries(queries: torch.Tensor, d: int, device, host: bool = False):
+    if not isinstance(queries, torch.Tensor) or queries.dtype != torch.float32 or queries.dim() != 2:
+        raise ValueError("queries must be a float32 [q, d] tensor")
+    if queries.shape[0] and queries.shape[1] != d:
+        raise ValueError(f"queries have {queries.shape[1]} columns, the index d = {d}")
+    if not queries.is_contiguous():
+        raise ValueError("queries must be contiguous (row-major)")
+    if host:
+        if queries.is_cuda:
+            raise ValueError("search_host takes HOST queries (use search for device tensors)")
+    elif queries.device != device:
+        raise ValueError(f"queries are on {queries.device}, the index on {device}")
+
+
+def _check_out(out, q, k, device):
+    ids, dists = out
+    for t, dt, nm in ((ids, torch.int64, "ids"), (dists, torch.float32, "dists")):
+        if t.dtype != dt or tuple(t.shape) != (q, k) or not t.is_contiguous() or t.device != device:
+            raise ValueError(f"out {nm} must be a contiguous {dt} [{q}, {k}] tensor on {device}")
 
 
 def last_path() -> int:
@@ -104,10 +149,14 @@ class Index:
 
     def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None, precision=None):
         lib = library()
-        if vectors.dtype != torch.float32 or vectors.dim() != 2 or not vectors.is_contiguous():
-            raise ValueError("vectors must be a contiguous float32 [n, d] tensor")
+        if vectors.dtype != torch.float32 or vectors.dim() != 2 or not vectors.is_contiguous() or not vectors.is_cuda:
+            raise ValueError("vectors must be a contiguous float32 [n, d] CUDA tensor")
         self.vectors = vectors
         self.attrs = [a.contiguous() for a in attrs]
+        for i, a in enumerate(self.attrs):
+            if a.dim() != 1 or a.numel() != vectors.shape[0] or a.device != vectors.device:
+                raise ValueError(f"attribute {i}: a 1-D tensor of n = {vectors.shape[0]} entries on {vectors.device} "
+                                 f"is required (got {tuple(a.shape)} on {a.device})")
         carr = (_lib.Attr * max(len(self.attrs), 1))()
         for i, a in enumerate(self.attrs):
             if a.dtype == torch.int32:
@@ -140,21 +189,23 @@ class Index:
             pass
 
     def search(self, queries: torch.Tensor, pred=None, k: int = 10, metric="l2", path=None, rows=None,
-               out=None, stream=None, precision=None):
-        """-> (ids int64 [q, k], dists float32 [q, k]) on the device (async on `stream`)."""
+               out=None, stream=None, precision=None, stats=None):
+        """-> (ids int64 [q, k], dists float32 [q, k]) on the device (async on `stream`).
+        stats: optional new_stats() block the call accumulates into (certificate counters)."""
         lib = library()
-        q = queries.shape[0]
-        d = queries.shape[1] if queries.dim() == 2 else self.d
         dev = self.vectors.device
+        _check_queries(queries, self.d, dev)
+        q, d = queries.shape[0], self.d
         if out is None:
             ids = torch.empty((q, k), dtype=torch.int64, device=dev)
             dists = torch.empty((q, k), dtype=torch.float32, device=dev)
         else:
+            _check_out(out, q, k, dev)
             ids, dists = out
         pr, keep = _lib.make_predicate(pred)
         st = lib.vrs_search_ex(self._h, _ptr(queries) if q else None, q, d, ctypes.byref(pr), int(k),
                                _metric(metric), _ptr(ids) if q else None, _ptr(dists) if q else None,
-                               _options(path, rows, precision), _stream(stream))
+                               _options(path, rows, precision, stats=stats), _stream(stream))
         _lib.check(st, "vrs_search")
         return ids, dists
 
@@ -164,11 +215,13 @@ class Index:
         unless host_async: True -> the caller synchronises the stream (pinned buffers);
         2 -> overlap: results are complete after host_fence(stream) + a stream sync."""
         lib = library()
+        _check_queries(queries_h, self.d, None, host=True)
         q, d = queries_h.shape
         if out is None:
             ids = torch.empty((q, k), dtype=torch.int64, pin_memory=True)
             dists = torch.empty((q, k), dtype=torch.float32, pin_memory=True)
         else:
+            _check_out(out, q, k, torch.device("cpu"))
             ids, dists = out
         pr, keep = _lib.make_predicate(pred)
         st = lib.vrs_search_host(self._h, _ptr(queries_h), q, d, ctypes.byref(pr), int(k), _metric(metric),
@@ -188,9 +241,9 @@ class Index:
         dists float32 [total]) on the device.  Synchronises the stream (the result size is
         data-dependent); grows the output and calls again if `capacity` is too small."""
         lib = library()
-        q = queries.shape[0]
-        d = queries.shape[1] if queries.dim() == 2 else self.d
         dev = self.vectors.device
+        _check_queries(queries, self.d, dev)
+        q, d = queries.shape[0], self.d
         offsets = torch.empty(q + 1, dtype=torch.int64, device=dev)
         cap = int(capacity) if capacity is not None else max(1024, 64 * q)
         pr, keep = _lib.make_predicate(pred)

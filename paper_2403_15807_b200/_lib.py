@@ -21,7 +21,7 @@ L2, IP, COSINE = 0, 1, 2
 ATTR_I32, ATTR_U8 = 0, 1
 PATH_AUTO, PATH_SCAN, PATH_GEMM = 0, 1, 2
 ROWS_AUTO, ROWS_GATHER, ROWS_MASKED = 0, 1, 2
-PREC_DEFAULT, PREC_TF32, PREC_BF16 = 0, 1, 2
+PREC_DEFAULT, PREC_TF32, PREC_BF16, PREC_FP16 = 0, 1, 2, 3
 K_MAX = 240
 MAX_CLAUSES = 8
 
@@ -56,7 +56,8 @@ class Allocator(ctypes.Structure):
 
 class SearchOptions(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("rows", ctypes.c_int32), ("precision", ctypes.c_int32),
-                ("host_async", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("host_async", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("stats", ctypes.c_void_p),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class LoadOptions(ctypes.Structure):

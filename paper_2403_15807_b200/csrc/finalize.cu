@@ -645,38 +645,34 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
   return n;
 }
 
-// Sums of U (4 or 8) per-lane values over the warp: on return every lane holds
-// the total of value (lane >> (5 - log2 U)) & (U - 1).  Each step swaps half of
-// the remaining values with the partner lane (xor 16, 8, ...), then a plain
-// butterfly over the remaining lane bits.
-template <int U>
-constexpr int log2u() { return U == 8 ? 3 : (U == 4 ? 2 : (U == 2 ? 1 : 0)); }
-template <int U>
-__device__ __forceinline__ double warp_sum_transpose(const double (&v)[U]) {
-  static_assert(U == 4 || U == 8, "U = 4 or 8");
-  const int lane = threadIdx.x & 31;
-  double w[U];
-#pragma unroll
-  for (int i = 0; i < U; ++i) w[i] = v[i];
-#pragma unroll
-  for (int h = U / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
-    const bool up = lane & o;
-#pragma unroll
-    for (int i = 0; i < h; ++i) w[i] = (up ? w[i + h] : w[i]) + __shfl_xor_sync(0xffffffffu, up ? w[i] : w[i + h], o);
-  }
-  double y = w[0];
-#pragma unroll
-  for (int o = 16 / U; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-  return y;
-}
-
 // Step 4 for candidates c0, c0 + cstep*U ... of ids[0..m): the warp reads each
 // row coalesced, U rows in flight, fp64 accumulation, one transposing reduction
 // per U rows.
+// Per-query certificate constants: |q|, the key error bound E (natural units) and
+// 1 / D, D = the key domain's scale (IP / COS on 16-bit operands: 2^(e_q + e_x)).
+struct CertQ {
+  double qn, E, dinv;
+};
+__device__ CertQ cert_setup(const FinalizeArgs &a, int64_t j, double qq) {
+  CertQ c;
+  c.qn = sqrt(qq);
+  const double rq = a.rq ? (double)__ldg(a.rq + j) : 0.0;
+  c.E = key_error_bound(a.kb, a.metric, c.qn, rq);
+  const int e = (a.qexp && a.metric != VRS_L2) ? __ldg(a.qexp + j) + a.xexp : 0;
+  c.dinv = ldexp(1.0, -e);
+  return c;
+}
+// exact natural key (rank_key units) from a re-scored sort key v (L2: -|q-x|^2, IP: <q,x>, COS: cos)
+__device__ __forceinline__ double natural_key(int metric, double v, double qq, double qn) {
+  return metric == VRS_L2 ? qq + v : (metric == VRS_COSINE ? v * qn : v);
+}
+
 template <int U>
 __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids, int m, int cfirst, int cstep,
-                            double qq, double *sc_out, int64_t *sid_out) {
+                            double qq, double *sc_out, int64_t *sid_out, const float *keys = nullptr,
+                            const CertQ *cq = nullptr) {
   const int lane = threadIdx.x & 31;
+  double ratio = 0.0;   // stats: largest observed |key / D - exact key| / E
   const float *q = a.Q + j * a.d;
   const bool vec = (a.d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Q)) & 15) == 0;
   for (int c0 = cfirst * U; c0 < m; c0 += cstep * U) {
@@ -731,14 +727,21 @@ __device__ void fin_rescore(const FinalizeArgs &a, int64_t j, const int32_t *ids
       else if (a.metric == VRS_COSINE) v = v / (sqrt(qq) * sqrt(xtot));
       sc_out[c] = v;
       sid_out[c] = ids[c];
+      if (keys && cq && cq->E > 0.0 && v == v)
+        ratio = fmax(ratio, fabs((double)keys[c] * cq->dinv - natural_key(a.metric, v, qq, cq->qn)) / cq->E);
     }
+  }
+  if (keys && cq) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ratio = fmax(ratio, __shfl_xor_sync(0xffffffffu, ratio, o));
+    if (lane == 0 && ratio > 0.0) atomicMax(a.stats + 2, (unsigned long long)__double_as_longlong(ratio));
   }
 }
 
 __device__ double fin_qq(const FinalizeArgs &a, int64_t j) {
   const int lane = threadIdx.x & 31;
   double qq = 0.0;
-  if (a.metric == VRS_COSINE) {
+  if (a.metric == VRS_COSINE || a.cert) {
     const float *q = a.Q + j * a.d;
     for (int t = lane; t < a.d; t += 32) qq += (double)q[t] * (double)q[t];
 #pragma unroll
@@ -765,15 +768,44 @@ __device__ __forceinline__ void warp_reg_sort_desc(double &key, int32_t &id) {
   }
 }
 
-__device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double qq, double *sc, int64_t *sid) {
+// Certificate, lane 0: every row outside the m = k' re-scored
+// candidates has a selection key <= kmin (the k'-th kept key: the lists, their
+// compactions and the probe threshold only ever drop keys below a kept one), so its
+// exact key is <= kmin / D + E; if that is below the k-th exact key s_k, no such row
+// can enter the top k and the result is exact.  Fewer than k' candidates: every
+// qualifying row was re-scored.  Writes cert / sk / gcnt and the stats.
+__device__ void fin_certify(const FinalizeArgs &a, int64_t j, int m, double qq, double skv, float kmin,
+                            const CertQ &cq) {
+  const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
+  bool ok = true;
+  if (!zero_cos && m >= a.kprime) {
+    const double s_nat = natural_key(a.metric, skv, qq, cq.qn);
+    ok = (double)kmin * cq.dinv + cq.E < s_nat;
+  }
+  a.cert[j] = ok ? 1 : 0;
+  a.sk[j] = skv;
+  a.gcnt[j] = 0;
+  if (a.stats) {
+    atomicAdd(a.stats, 1ull);
+    if (!ok) atomicAdd(a.stats + 1, 1ull);
+  }
+}
+
+__device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double qq, double *sc, int64_t *sid,
+                               float kmin = -INFINITY, const CertQ *cq = nullptr) {
   const int lane = threadIdx.x & 31;
   const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
   const int mv = zero_cos ? 0 : min(m, a.k);
   const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
+  const int kk = max(1, min(m, a.k));   // rank of the k-th result (or the last)
   if (m <= 32) {   // registers: one candidate per lane (local row ids fit 32 bits)
     double key = lane < m ? sc[lane] : -INFINITY;
     int32_t id = lane < m ? (int32_t)sid[lane] : INT32_MAX;
     warp_reg_sort_desc(key, id);
+    if (a.cert) {
+      const double skv = __shfl_sync(0xffffffffu, key, kk - 1);
+      if (lane == 0) fin_certify(a, j, m, qq, skv, kmin, *cq);
+    }
     if (a.k <= 32) {   // lane r holds rank r: write straight from registers
       if (lane < a.k) {
         const int64_t o = j * a.k + lane;
@@ -797,6 +829,7 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
     for (int c = m + lane; c < np; c += 32) { sc[c] = -INFINITY; sid[c] = INT64_MAX; }
     __syncwarp();
     warp_sort_desc_d(sc, sid, np);
+    if (a.cert && lane == 0) fin_certify(a, j, m, qq, sc[kk - 1], kmin, *cq);
   }
   for (int r = lane; r < a.k; r += 32) {
     const int64_t o = j * a.k + r;
@@ -834,9 +867,19 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) 
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
   const int m = fin_stream(a, j, 0, 1, s_buf[w]);
   const double qq = fin_qq(a, j);
-  fin_rescore<SEL <= 64 ? 4 : 8>(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w]);
+  CertQ cq{0.0, 0.0, 1.0};
+  float kmin = -INFINITY;
+  if (a.cert) {
+    cq = cert_setup(a, j, qq);
+    kmin = INFINITY;
+    for (int i = threadIdx.x & 31; i < m; i += 32) kmin = fminf(kmin, s_buf[w].key[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+  }
+  fin_rescore<SEL <= 64 ? 4 : 8>(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w],
+                                 a.stats ? s_buf[w].key : nullptr, &cq);
   __syncwarp();
-  fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w]);
+  fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w], kmin, &cq);
 }
 
 #ifndef VRS_FIN_W
@@ -849,7 +892,7 @@ constexpr int kFinW = VRS_FIN_W;   // warps per query in the small-batch variant
 // Exact; ties -> lower id.  (Exchange through the free tail of each warp's buffer:
 // its survivors sit at [0, nw <= k').)
 template <int E>
-__device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s_buf, int nw, int *s_n) {
+__device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s_buf, int nw, int *s_n, float *s_kmin) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float k[E];
   int32_t id[E];
@@ -878,9 +921,10 @@ __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s
     for (int h = 0; h < E; ++h) {
       const int e = h * 32 + lane;
       cnt += __popc(__ballot_sync(0xffffffffu, e < K && id[h] != INT32_MAX));
-      if (e < K) s_buf[0].id[e] = id[h];
+      if (e < K) { s_buf[0].id[e] = id[h]; s_buf[0].key[e] = k[h]; }
     }
-    if (lane == 0) s_n[0] = cnt;
+    const float kth = elem_e<E>(k, K - 1);   // the k'-th best (sorted), valid when cnt == K
+    if (lane == 0) { s_n[0] = cnt; *s_kmin = kth; }
   }
 }
 
@@ -892,6 +936,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   __shared__ double s_sc[kFinMaxSel];
   __shared__ int64_t s_sid[kFinMaxSel];
   __shared__ int s_n[kFinW];
+  __shared__ float s_kmin;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
   pdl_wait();
@@ -905,9 +950,9 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   __syncthreads();
   TL_STAMP(1, 2);
   if (a.kprime <= 64) {
-    fin_tree_merge<2>(a, s_buf, nw, s_n);
+    fin_tree_merge<2>(a, s_buf, nw, s_n, &s_kmin);
   } else if (a.kprime <= 128) {
-    fin_tree_merge<4>(a, s_buf, nw, s_n);
+    fin_tree_merge<4>(a, s_buf, nw, s_n, &s_kmin);
   } else if (w == 0) {
     // warp 0 merges the survivors of all warps into its own buffer
     const int K = a.kprime;
@@ -938,16 +983,22 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
       }
     }
     if (n > K) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
-    if (lane == 0) s_n[0] = n;
+    float km = INFINITY;
+    for (int i = lane; i < n; i += 32) km = fminf(km, B.key[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) km = fminf(km, __shfl_xor_sync(0xffffffffu, km, o));
+    if (lane == 0) { s_n[0] = n; s_kmin = km; }
   }
   __syncthreads();
   TL_STAMP(1, 3);
   const int m = s_n[0];
   const double qq = fin_qq(a, j);
-  fin_rescore<8>(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid);
+  CertQ cq{0.0, 0.0, 1.0};
+  if (a.cert) cq = cert_setup(a, j, qq);
+  fin_rescore<8>(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid, a.stats ? s_buf[0].key : nullptr, &cq);
   __syncthreads();
   TL_STAMP(1, 4);
-  if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid);
+  if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid, s_kmin, &cq);
 }
 
 // Per query (one CTA): the kth largest probe slot maximum (each the key of a

@@ -10,7 +10,7 @@
 // Pipeline (vrs_range_search in vrs_api.cu drives it):
 //   range_threshold_kernel  per query, the ranking-key threshold T_j that every
 //                           row passing tau provably reaches under the tensor-core
-//                           (bf16 / TF32) product error, i.e. tau minus a margin
+//                           (16-bit / TF32) key error bound, i.e. tau minus a margin
 //   tc pass MODE_RCOUNT     per (list, query): how many keys >= T_j
 //   range_prefix_kernel     (query, list) segment offsets, total C
 //   -- host: read C, size the candidate buffer --
@@ -26,16 +26,19 @@
 namespace vrs {
 
 // ---------------------------------------------------------------- thresholds
-// Key domain (rank_key): L2 -> 2<q,x> - |x|^2, IP -> <q,x>, COS -> <q,x>/|x|.
-// With |<q,x>~ - <q,x>| <= gamma |q| |x| for the tensor-core product (host:
-// operand rounding + fp32 accumulation, x2 safety) and |x| <= xmax:
-//   IP : <q,x> >= tau        => key >= tau - gamma |q| xmax
-//   COS: cos >= tau          => key >= tau |q| - gamma |q|          (key = cos |q| exactly)
-//   L2 : |q-x|^2 <= tau      => key >= |q|^2 - tau - 2 gamma |q| xmax - eps_n xmax^2
-// plus a relative slack for the fp32 rounding of the key itself; the result is
-// rounded toward -inf to fp32.  Rows below T_j can therefore never pass tau.
+// Key domain (rank_key): L2 -> 2<q,x> - |x|^2, IP -> <q,x>, COS -> <q,x>/|x|, the
+// IP / COS keys of 16-bit operands scaled by D = 2^(e_q + e_x) (tc_kernel.cuh).
+// With |computed key - exact key| <= E (vrs_internal.cuh key_error_bound, the same
+// bound as the top-k certificate):
+//   IP : <q,x> >= tau        => key >= (tau - E) D
+//   COS: cos >= tau          => key >= (tau |q| - E) D    (exact key = cos |q|)
+//   L2 : |q-x|^2 <= tau      => key >= |q|^2 - tau - E
+// plus a relative slack for the fp64 arithmetic here; rounded toward -inf to fp32.
+// Rows below T_j can therefore never pass tau.
 __global__ void __launch_bounds__(128) range_threshold_kernel(const float *__restrict__ Q, int64_t q, int32_t d,
-                                                              int32_t metric, double tau, double xmax, double gamma,
+                                                              int32_t metric, double tau, KeyBound kb,
+                                                              const int32_t *__restrict__ qexp,
+                                                              const float *__restrict__ rq, int32_t xexp,
                                                               uint32_t *__restrict__ gtau) {
   pdl_wait();
   pdl_trigger();
@@ -48,15 +51,16 @@ __global__ void __launch_bounds__(128) range_threshold_kernel(const float *__res
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
   if (lane) return;
-  const double nq = sqrt(qq), rel = 0x1p-20;
+  const double nq = sqrt(qq), rel = 0x1p-30, N = kb.xmax;
+  const double E = key_error_bound(kb, metric, nq, rq ? (double)rq[j] : 0.0);
+  const double D = (qexp && metric != VRS_L2) ? ldexp(1.0, qexp[j] + xexp) : 1.0;
   double T;
   if (metric == VRS_IP) {
-    T = tau - gamma * nq * xmax - rel * (fabs(tau) + nq * xmax);
+    T = (tau - E - rel * (fabs(tau) + nq * N)) * D;
   } else if (metric == VRS_COSINE) {
-    T = qq > 0.0 ? tau * nq - gamma * nq - rel * nq * (1.0 + fabs(tau)) : INFINITY;   // zero query: nothing
+    T = qq > 0.0 ? (tau * nq - E - rel * nq * (1.0 + fabs(tau))) * D : INFINITY;   // zero query: nothing
   } else {
-    const double eps_n = (d + 2.0) * 0x1p-24;   // fp32 |x|^2
-    T = qq - tau - 2.0 * gamma * nq * xmax - eps_n * xmax * xmax - rel * (fabs(qq - tau) + xmax * xmax + 2.0 * nq * xmax);
+    T = qq - tau - E - rel * (fabs(qq - tau) + N * N + 2.0 * nq * N);
   }
   gtau[j] = ordered_u32(__double2float_rd(T));
 }
@@ -244,7 +248,8 @@ cudaError_t launch_range_count(const GemmArgs &a, const GemmPlan &plan, RangeSta
   cudaError_t e = tc_prepare(a, plan, s, launches, &L);
   if (e != cudaSuccess) return e;
   e = launch_k(range_threshold_kernel, dim3((unsigned)((a.q + 3) / 4)), dim3(128), 0, s, a.Q, a.q, a.d, a.metric,
-               r.tau, r.xmax, r.gamma, r.gtau);
+               r.tau, r.kb, (const int32_t *)(a.bf16 ? a.qexp : nullptr), (const float *)(a.bf16 ? a.rq : nullptr),
+               a.bf16 ? a.xexp : 0, r.gtau);
   if (e != cudaSuccess) return e;
   TcParams p = L.p;
   p.gtau = r.gtau;

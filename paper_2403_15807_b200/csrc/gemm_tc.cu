@@ -31,9 +31,11 @@
 //
 // Roofline: tensor (2*q*N_rows*d TF32 flops) for large q, HBM (4*d bytes per
 // row) for small q.
+#include <cuda_fp16.h>
 #include <string.h>
 
 #include "tc_kernel.cuh"
+#include "convert16.cuh"
 
 namespace vrs {
 
@@ -171,35 +173,54 @@ cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, con
                   copy && a.metric != VRS_IP ? a.xsel_norm : (float *)nullptr);
 }
 
-// fp32 -> bf16 (round to nearest even): the shadow corpus at load, the queries per
-// search; elements [count, total) are zero (query tiles padded to whole 128-row
-// tiles, so the TMA loads of the query operand never fall out of bounds).
-__global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out, int64_t count,
-                                   int64_t total) {
+// ---------------------------------------------------------------- 16-bit operands
+// The tensor-core selection runs kind::f16 on 16-bit copies of the corpus (the
+// shadow, built at load) and of the queries (per search).  fp16 (default): every
+// value is scaled by a power of two before rounding -- the corpus by one 2^e_x
+// for the whole index, each query row by its own 2^e_q -- so the largest |value|
+// lands in [2^14, 2^15): the 11-bit significand is used in full and nothing
+// overflows.  bf16: e = 0.  Powers of two are exact, so the MMA's dot product is
+// 2^(e_q + e_x) <q~, x~> (the key domain).  Each row's rounding
+// residual |x~ 2^-e - x| is measured exactly (fp64) -- the certificate's bound.
+// The shadow (load): warp per row.  res[0] = max |x~ - x|, res[1] = max |x~ - x| / |x|
+// (rounded up; u64 bits of non-negative doubles order as integers).
+__global__ void __launch_bounds__(256) shadow_kernel(const float *__restrict__ X, int64_t n, int32_t d, int32_t e,
+                                                     int32_t fmt, uint16_t *__restrict__ out,
+                                                     const float *__restrict__ nx2, unsigned long long *res) {
+  const int lane = threadIdx.x & 31;
+  double rmax = 0.0, rho = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < n; row += (int64_t)gridDim.x * 8) {
+    const double r = sqrt(row_to16(X + row * d, out + row * d, d, e, fmt)) * (1.0 + 0x1p-50);
+    rmax = fmax(rmax, r);
+    const double xn = sqrt((double)__ldg(nx2 + row));
+    if (xn > 0.0) rho = fmax(rho, r / xn * (1.0 + 0x1p-20));   // (|x| from the fp32 |x|^2: 2^-24 relative)
+  }
+  if (lane == 0) {
+    atomicMax(res, (unsigned long long)__double_as_longlong(rmax));
+    atomicMax(res + 1, (unsigned long long)__double_as_longlong(rho));
+  }
+}
+
+cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, const float *nx2,
+                          unsigned long long *res, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 16);
+  shadow_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, e, fmt, static_cast<uint16_t *>(out), nx2, res);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) query16_kernel(QueryFuse f) {
   TL_SCOPE(5);
   pdl_wait();
   TL_WAITED(5);
   pdl_trigger();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = count + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
-    out[i] = __float2bfloat16_rn(0.f);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (count >> 2); i += stride) {
-    const float4 v = __ldg(reinterpret_cast<const float4 *>(in) + i);
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-    uint2 w;
-    w.x = *reinterpret_cast<uint32_t *>(&lo);
-    w.y = *reinterpret_cast<uint32_t *>(&hi);
-    reinterpret_cast<uint2 *>(out)[i] = w;
-  }
-  for (int64_t i = (count & ~int64_t(3)) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
-    out[i] = __float2bfloat16_rn(in[i]);
+  for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < f.rows; row += (int64_t)gridDim.x * 8)
+    query_row_to16(f, row);
 }
 
-cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s) {
-  if (total <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 16);
-  return launch_k(f32_to_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, in,
-                  static_cast<__nv_bfloat16 *>(out), count, total);
+cudaError_t launch_query16(const QueryFuse &f, cudaStream_t s) {
+  if (f.rows <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((f.rows + 7) / 8, 148 * 8);
+  return launch_k(query16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, f);
 }
 
 
@@ -275,17 +296,18 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   const bool g4 = xcap > 0 && a.xsel == nullptr;
   const bool bf = a.bf16 != 0;
   cudaError_t e = cudaSuccess;
-  if (bf && !a.prepped) {   // queries -> bf16 (the corpus shadow was converted at load)
-    e = launch_to_bf16(a.Q, a.Qb, a.q * a.d, (int64_t)plan.qtiles * tc::BM * a.d, s);
+  if (bf && !a.prepped) {   // queries -> 16-bit (the corpus shadow was converted at load)
+    const QueryFuse f{a.Q, a.Qb, a.q, (int64_t)plan.qtiles * tc::BM, a.d, a.fmt16, a.qexp, a.rq};
+    e = launch_query16(f, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
   const void *qsrc = bf ? a.Qb : (const void *)a.Q;
   const void *xsrc = bf ? a.Xb : (const void *)a.X;
-  if (!make_map(&L->mq, qsrc, bf ? (int64_t)plan.qtiles * tc::BM : a.q, a.d, tc::BM, bf) ||
-      !make_map(&L->mx, xsrc, a.n, a.d, tc::BN, bf) ||
-      !(g4 ? make_map(&L->mg, xsrc, a.n, a.d, 1, bf)
-           : make_map(&L->mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf)))
+  if (!make_map(&L->mq, qsrc, bf ? (int64_t)plan.qtiles * tc::BM : a.q, a.d, tc::BM, bf, a.fmt16) ||
+      !make_map(&L->mx, xsrc, a.n, a.d, tc::BN, bf, a.fmt16) ||
+      !(g4 ? make_map(&L->mg, xsrc, a.n, a.d, 1, bf, a.fmt16)
+           : make_map(&L->mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf, a.fmt16)))
     return cudaErrorInvalidValue;
   TcParams &p = L->p;
   memset(&p, 0, sizeof p);
@@ -323,6 +345,9 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.metric = a.metric;
   p.kp = kp_of(a.kprime);
   p.cap = p.kp * tc::CAP_FACTOR;
+  p.idesc = mma_idesc(tc::BM, tc::BN, bf ? (uint32_t)a.fmt16 : 2u);
+  p.qexp = bf ? a.qexp : nullptr;
+  p.xexp = bf ? a.xexp : 0;
   p.tile_step = 1;
   p.probe_div = 0;
   p.min_span = tc_min_span();

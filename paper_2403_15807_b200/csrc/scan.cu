@@ -17,47 +17,65 @@
 // + 8 (norm terms); per call + 4*d*q (queries) + 12*q*k (results).
 #include <float.h>
 
+#include <algorithm>
+
 #include "vrs_kernels.cuh"
 
 namespace vrs {
 
 // ------------------------------------------------------------------ K6' norms
-// |x|^2 and 1/|x| per row (fp32), computed once at vrs_load (PAPER.md L305,
-// L790 "then normalized"); zero_flag records a zero-norm row (COSINE degenerate).
-// zero_flag[1] collects the largest |x|^2 as float bits (non-negative floats order
-// as integers) -- the range search's error bound uses max |x|.
+// |x|^2 and 1/|x| per row, computed once at vrs_load ("then
+// normalized"): fp64 sums of the fp32 inputs, each rounded once to fp32 (2^-24
+// relative -- the certificate's key bound counts on it).
+// flags[0]: a zero-norm row exists (COSINE degenerate); flags[1]: the largest
+// |x|^2 and flags[2]: the largest |x_t|, as float bits (non-negative floats order
+// as integers) -- the error bounds use max |x|, the fp16 shadow's scale max |x_t|.
 __global__ void norms_kernel(const float *__restrict__ X, int64_t n, int32_t d, float *__restrict__ nx2,
-                             float *__restrict__ inv_nx, int32_t *__restrict__ zero_flag) {
-  __shared__ float s_max[8];
+                             float *__restrict__ inv_nx, int32_t *__restrict__ flags) {
+  __shared__ float s_max[8], s_amax[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
-  float s = 0.f;
+  double s = 0.0;
+  float am = 0.f;
   if (row < n) {
     const float *x = X + row * d;
-    for (int t = lane; t < d; t += 32) s = fmaf(x[t], x[t], s);
+    for (int t = lane; t < d; t += 32) {
+      const float v = x[t];
+      s = fma((double)v, (double)v, s);
+      am = fmaxf(am, fabsf(v));
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  }
   if (lane == 0) {
+    const float s32 = __double2float_rn(s);
     if (row < n) {
-      nx2[row] = s;
-      inv_nx[row] = s > 0.f ? 1.0f / sqrtf(s) : 0.f;
-      if (!(s > 0.f)) atomicOr(zero_flag, 1);
+      nx2[row] = s32;
+      inv_nx[row] = s > 0.0 ? __double2float_rn(1.0 / sqrt(s)) : 0.f;
+      if (!(s > 0.0)) atomicOr(flags, 1);
     }
-    s_max[w] = s;
+    s_max[w] = __double2float_ru(s);
+    s_amax[w] = am;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    float m = s_max[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, s_max[i]);
-    atomicMax(zero_flag + 1, __float_as_int(m));
+    float m = s_max[0], a = s_amax[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      m = fmaxf(m, s_max[i]);
+      a = fmaxf(a, s_amax[i]);
+    }
+    atomicMax(flags + 1, __float_as_int(m));
+    atomicMax(flags + 2, __float_as_int(a));
   }
 }
 
-cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *zero_flag,
+cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *flags,
                          cudaStream_t stream) {
   const int warps = 8;
-  norms_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, stream>>>(X, n, d, nx2, inv_nx, zero_flag);
+  norms_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, stream>>>(X, n, d, nx2, inv_nx, flags);
   return cudaGetLastError();
 }
 
@@ -93,7 +111,7 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
   float *lk = reinterpret_cast<float *>(sid + 2 * kScRows);
   int32_t *li = reinterpret_cast<int32_t *>(lk + QG * 2 * KPE);
 
-  const int64_t q0 = (int64_t)blockIdx.y * QG;
+  const int64_t q0 = a.q_base + (int64_t)blockIdx.y * QG;
   const int nq = (int)(a.q - q0 < QG ? a.q - q0 : QG);
   pdl_wait();
   pdl_trigger();
@@ -283,15 +301,24 @@ int scan_query_group(int64_t q, int d, int kpe) {
 }
 
 cudaError_t launch_scan(const ScanArgs &a, int qg, int kpe, cudaStream_t s, int *launches) {
-  const int gy = (int)((a.q + qg - 1) / qg);
   const bool vec4 = (a.d % 4 == 0) && ((uintptr_t)a.X % 16 == 0);
-  if (launches) *launches += 1;
-  switch (qg) {
-    case 1: return launch_scan_k<1>(a, kpe, gy, vec4, s);
-    case 2: return launch_scan_k<2>(a, kpe, gy, vec4, s);
-    case 4: return launch_scan_k<4>(a, kpe, gy, vec4, s);
-    default: return launch_scan_k<8>(a, kpe, gy, vec4, s);
+  // query groups on grid.y, at most 65535 per launch (larger batches: several launches)
+  const int64_t groups = (a.q + qg - 1) / qg;
+  for (int64_t g0 = 0; g0 < groups; g0 += 65535) {
+    ScanArgs b = a;
+    b.q_base = g0 * qg;
+    const int gy = (int)std::min<int64_t>(65535, groups - g0);
+    if (launches) *launches += 1;
+    cudaError_t e;
+    switch (qg) {
+      case 1: e = launch_scan_k<1>(b, kpe, gy, vec4, s); break;
+      case 2: e = launch_scan_k<2>(b, kpe, gy, vec4, s); break;
+      case 4: e = launch_scan_k<4>(b, kpe, gy, vec4, s); break;
+      default: e = launch_scan_k<8>(b, kpe, gy, vec4, s); break;
+    }
+    if (e != cudaSuccess) return e;
   }
+  return cudaSuccess;
 }
 
 }  // namespace vrs

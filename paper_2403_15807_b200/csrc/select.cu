@@ -18,9 +18,7 @@
 //
 // Algorithmic bytes per row: sum of attribute widths read + 1/8 (bitmap) +
 // 4 * selectivity (ids).  HBM-bound.
-#include <cuda_bf16.h>
-
-#include "vrs_kernels.cuh"
+#include "convert16.cuh"
 
 namespace vrs {
 
@@ -41,35 +39,10 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
   pdl_wait();
   TL_WAITED(0);
   pdl_trigger();
-  if (fz.q_out) {   // folded in: this block's slice of the fp32 -> bf16 query conversion (zero padding)
-    const int64_t per = ((fz.q_total + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
-    const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(fz.q_total, e0 + per);
-    __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(fz.q_out);
-    if (((reinterpret_cast<uintptr_t>(fz.q_in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 && (fz.q_count & 3) == 0) {
-      // 4 elements per thread per step, 4 steps' loads in flight (e0, e1, q_count: multiples of 4)
-      for (int64_t e = e0 + 4 * threadIdx.x; e < e1; e += 16 * kSelThreads) {
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t f = e + (int64_t)u * 4 * kSelThreads;
-          v[u] = f < min(e1, fz.q_count) ? __ldg(reinterpret_cast<const float4 *>(fz.q_in + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t f = e + (int64_t)u * 4 * kSelThreads;
-          if (f < e1) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(v[u].x, v[u].y), hi = __floats2bfloat162_rn(v[u].z, v[u].w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t *>(&lo);
-            pk.y = *reinterpret_cast<uint32_t *>(&hi);
-            *reinterpret_cast<uint2 *>(out + f) = pk;
-          }
-        }
-      }
-    } else {
-      for (int64_t e = e0 + threadIdx.x; e < e1; e += kSelThreads)
-        out[e] = __float2bfloat16_rn(e < fz.q_count ? fz.q_in[e] : 0.f);
-    }
+  if (fz.q_out) {   // folded in: the 16-bit query operand, one warp per query row (convert16.cuh)
+    for (int64_t row = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5); row < fz.rows;
+         row += (int64_t)gridDim.x * kSelWarps)
+      query_row_to16(fz, row);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kSelRows + (int64_t)warp * kSelWordsPerWarp * 32;

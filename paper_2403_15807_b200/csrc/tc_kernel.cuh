@@ -125,7 +125,7 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, ui
       : "memory");
 }
 
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), both K-major.
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (fp16 or bf16 inputs per idesc, fp32 accumulate), both K-major.
 __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -150,11 +150,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: D fp32, A/B tf32 (format 2) or bf16 (format 1), both
-// K-major, N = BN, M = BM.
-__host__ __device__ constexpr uint32_t mma_idesc(int M, int N, bool bf16) {
-  return (1u << 4) | ((bf16 ? 1u : 2u) << 7) | ((bf16 ? 1u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: D fp32, A/B format ab (kind::f16: 0 fp16, 1 bf16;
+// kind::tf32: 2 tf32), both K-major, N = BN, M = BM.
+__host__ __device__ constexpr uint32_t mma_idesc(int M, int N, uint32_t ab) {
+  return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 #define TMEM_LD_32x32b_X32(taddr, r)                                                                              \
@@ -231,6 +230,9 @@ struct TcParams {
   const float *xsel_norm;  // [xsel_cap] the gathered rows' norm term (L2 |x|^2, COS 1/|x|)
   uint32_t *gtau;          // [q] ordered-u32 threshold shared by all lists of a query (0 = none)
   unsigned long long *stats;  // optional counters: chunks, slow chunks, appends, compactions
+  uint32_t idesc;          // MMA instruction descriptor (operand format)
+  const int32_t *qexp;     // 16-bit operands: [q] per-query exponents e_q (nullptr: TF32, no scaling)
+  int32_t xexp;            // the shadow's exponent e_x
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = mma_idesc(BM, BN, BF);
+    const uint32_t idesc = p.idesc;
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0) mbar_wait(&afull_bar, 0);
@@ -699,7 +701,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int64_t qg = (int64_t)qtile * BM + m;    // global query index
     const bool active = qg < p.q;
     const int list = split * LPS + half;           // candidate list index
-    const float sc = p.metric == VRS_L2 ? 2.f : 1.f;
+    // key scale: L2 keys are natural units, 2<q,x> - |x|^2, so the 16-bit pass undoes its
+    // power-of-two operand scales 2^(e_q + e_x) here (exact); IP / COS keys stay in the
+    // query's scaled domain D = 2^(e_q + e_x) -- the order per query is unchanged, and
+    // the threshold, the lists and the finalize compare keys of one query only
+    // ("key domain")
+    const float sc = p.metric == VRS_L2 ? (p.qexp != nullptr && active ? ldexpf(2.f, -(__ldg(p.qexp + qg) + p.xexp)) : 2.f)
+                                        : 1.f;
     const int64_t cbase = MODE == MODE_RFILL ? (active ? p.coff[qg * (LPS * p.P) + list] : 0)
                                              : ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
     float *ckey = p.cand_key + (MODE == MODE_RFILL ? 0 : cbase);
@@ -1060,18 +1068,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D map over a row-major [rows x d] matrix of fp32 or bf16, boxes of one
-// 128-byte K block x box_rows rows, 128-byte swizzle (box_rows = 1: the gather4
-// map, four such rows per instruction).
-static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows, bool bf16) {
+// 2-D map over a row-major [rows x d] matrix of fp32 or 16-bit values (fmt16: 0
+// fp16, 1 bf16), boxes of one 128-byte K block x box_rows rows, 128-byte swizzle
+// (box_rows = 1: the gather4 map, four such rows per instruction).
+static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows, bool h16, int fmt16 = 1) {
   auto fn = encode_fn();
   if (!fn) return false;
-  const int esz = bf16 ? 2 : 4;
+  const int esz = h16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * esz};
   cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  CUresult r = fn(m, !h16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : (fmt16 == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16), 2,
                   const_cast<void *>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -31,8 +31,11 @@ struct vrs_index {
   float *nx2;
   float *inv_nx;
   int32_t has_zero_row;
-  float xmax;              // max row norm (range search error bound)
-  void *xb;               // bf16 shadow corpus [n x d] for the tensor-core selection pass, or nullptr
+  float xmax;              // max row norm (rounded up; the key error bounds)
+  void *xb;               // 16-bit shadow corpus [n x d] for the tensor-core selection pass, or nullptr
+  int32_t prec16 = 0;     // VRS_PREC_FP16 / VRS_PREC_BF16: the shadow's format (0: none)
+  int32_t xexp = 0;       // the shadow's power-of-two scale e_x (fp16)
+  double rmax = 0, rho = 0;   // max |x~ 2^-e_x - x|, max |x~ 2^-e_x - x| / |x| (measured at load, fp64)
   // vrs_search_host staging: device slots (queries in, ids / dists out) so
   // that the upload of one call overlaps the compute of the previous one; the
   // copies run on their own streams, ordered by events.
@@ -257,16 +260,20 @@ static vrs_status make_pred(const vrs_index *ix, const vrs_predicate *pred, Pred
   return VRS_OK;
 }
 
-// The work the select kernels do for the tensor-core pass: bf16 query conversion
-// (zero-padded to whole 128-row tiles).
-static SelectFuse select_fuse(const vrs_index *ix, const float *queries, int64_t q, const GemmPlan &gp, bool bf16,
-                              void *qb) {
+// The work the select kernels do for the tensor-core pass: the 16-bit query
+// operand with its per-query exponent and residual (zero-padded to whole 128-row tiles).
+static SelectFuse select_fuse(const vrs_index *ix, const float *queries, int64_t q, const GemmPlan &gp, bool h16,
+                              void *qb, int32_t *qexp, float *rq) {
   SelectFuse f{};
-  if (bf16) {
+  if (h16) {
     f.q_in = queries;
     f.q_out = qb;
-    f.q_count = q * ix->d;
-    f.q_total = (int64_t)gp.qtiles * 128 * ix->d;
+    f.q = q;
+    f.rows = (int64_t)gp.qtiles * 128;
+    f.d = ix->d;
+    f.fmt = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
+    f.qexp = qexp;
+    f.rq = rq;
   }
   return f;
 }
@@ -299,7 +306,7 @@ int32_t vrs_profile_read(int32_t i, const char **name, double *total_ms, int64_t
 }
 int32_t vrs_last_path(void) { return g_last_path; }
 int32_t vrs_last_precision(void) { return g_last_prec; }
-int32_t vrs_index_precision(const vrs_index *ix) { return ix ? (ix->xb ? VRS_PREC_BF16 : VRS_PREC_TF32) : -1; }
+int32_t vrs_index_precision(const vrs_index *ix) { return ix ? (ix->xb ? ix->prec16 : VRS_PREC_TF32) : -1; }
 int32_t vrs_last_launches(void) { return g_last_launches; }
 int64_t vrs_index_rows(const vrs_index *ix) { return ix ? ix->n : -1; }
 int32_t vrs_index_dim(const vrs_index *ix) { return ix ? ix->d : -1; }
@@ -322,12 +329,13 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   if (row_offset < 0) return fail(VRS_EINVAL, "row_offset < 0");
   if (alloc && (!alloc->alloc || !alloc->free)) return fail(VRS_EINVAL, "allocator without alloc/free");
   const int prec = opts ? opts->precision : VRS_PREC_DEFAULT;
-  if (prec < VRS_PREC_DEFAULT || prec > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision %d", prec);
-  // bf16 rows must be 16-byte aligned for TMA: d % 8 == 0 and a 16-byte aligned base
+  if (prec < VRS_PREC_DEFAULT || prec > VRS_PREC_FP16) return fail(VRS_EINVAL, "bad precision %d", prec);
+  // 16-bit rows must be 16-byte aligned for TMA: d % 8 == 0 and a 16-byte aligned base
   const bool shadow_ok = d % 8 == 0 && ((uintptr_t)vectors & 15) == 0;
-  if (prec == VRS_PREC_BF16 && !shadow_ok)
-    return fail(VRS_EUNSUPPORTED, "bf16 shadow needs d %% 8 == 0 and 16-byte aligned vectors (d = %d)", d);
-  const bool want_shadow = prec == VRS_PREC_BF16 || (prec == VRS_PREC_DEFAULT && shadow_ok);
+  if ((prec == VRS_PREC_BF16 || prec == VRS_PREC_FP16) && !shadow_ok)
+    return fail(VRS_EUNSUPPORTED, "a 16-bit shadow needs d %% 8 == 0 and 16-byte aligned vectors (d = %d)", d);
+  const bool want_shadow = prec == VRS_PREC_BF16 || prec == VRS_PREC_FP16 || (prec == VRS_PREC_DEFAULT && shadow_ok);
+  const int prec16 = want_shadow ? (prec == VRS_PREC_BF16 ? VRS_PREC_BF16 : VRS_PREC_FP16) : 0;
   int dev = 0, sms = 0;
   vrs_status st = check_device(&dev, &sms);
   if (st != VRS_OK) return st;
@@ -349,7 +357,7 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   ix->device = dev;
   ix->num_sms = sms;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 8, want_shadow ? (size_t)n * d * 2 : 0});
+  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 16, 16, want_shadow ? (size_t)n * d * 2 : 0});
   void *mem = nullptr;
   if (alloc) {
     mem = alloc->alloc(bytes, cuda_stream, alloc->ctx);
@@ -365,22 +373,38 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   Carve cv(mem);
   ix->nx2 = cv.take<float>(n);
   ix->inv_nx = cv.take<float>(n);
-  int32_t *zf = cv.take<int32_t>(2);   // [0] zero-norm row flag, [1] max |x|^2 (float bits)
+  int32_t *zf = cv.take<int32_t>(4);   // [0] zero-norm row flag, [1] max |x|^2, [2] max |x_t| (float bits)
+  unsigned long long *res = cv.take<unsigned long long>(2);   // shadow residual maxima (double bits)
   ix->xb = want_shadow ? cv.take<char>((size_t)n * d * 2) : nullptr;
-  int32_t zero[2] = {0, 0};
-  cudaError_t e = cudaMemsetAsync(zf, 0, 8, stream);
+  ix->prec16 = prec16;
+  int32_t flags[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemsetAsync(zf, 0, 16, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(res, 0, 16, stream);
   if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
-  if (e == cudaSuccess && ix->xb) e = launch_to_bf16(vectors, ix->xb, n * (int64_t)d, n * (int64_t)d, stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(zero, zf, 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(flags, zf, 16, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess && ix->xb) {
+    // fp16: one power of two for the whole corpus puts max |x_t| into [2^14, 2^15)
+    // (convert16.cuh scale_exp16); bf16 needs no scaling
+    float amax;
+    memcpy(&amax, &flags[2], 4);
+    if (prec16 == VRS_PREC_FP16 && amax > 0.f && std::isfinite(amax))
+      ix->xexp = std::max(-120, std::min(120, 14 - ilogbf(amax)));
+    unsigned long long r2[2] = {0, 0};
+    e = launch_shadow(vectors, n, d, ix->xexp, prec16 == VRS_PREC_FP16 ? 0 : 1, ix->xb, ix->nx2, res, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(r2, res, 16, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    memcpy(&ix->rmax, &r2[0], 8);
+    memcpy(&ix->rho, &r2[1], 8);
+  }
   if (e != cudaSuccess) {
     vrs_free(ix);
-    return fail(VRS_ECUDA, "vrs_load norms: %s", cudaGetErrorString(e));
+    return fail(VRS_ECUDA, "vrs_load norms / shadow: %s", cudaGetErrorString(e));
   }
-  ix->has_zero_row = zero[0];
+  ix->has_zero_row = flags[0];
   {
     float m2;
-    memcpy(&m2, &zero[1], 4);
+    memcpy(&m2, &flags[1], 4);
     ix->xmax = sqrtf(m2) * (1.0f + 1e-6f);
   }
   *out = ix;
@@ -423,6 +447,30 @@ static int pow2_at_least(int v) {
   return p;
 }
 
+// The selection over-fetches k' candidates for the exact re-score: the power of two
+// >= k + 16 (at least 32) -- the lists keep that many per (list, query) anyway, and
+// the wider margin lets the certificate hold without the fallback on clustered
+// data (C5: k = 50 -> 128).
+static int kprime_of(int k) { return std::max(32, pow2_at_least(k + 16)); }
+
+static vrs_status check_precision(const vrs_index *ix, int prec_req) {
+  if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_FP16) return fail(VRS_EINVAL, "bad precision option");
+  if ((prec_req == VRS_PREC_BF16 || prec_req == VRS_PREC_FP16) && ix->prec16 != prec_req)
+    return fail(VRS_EUNSUPPORTED, "the index has no %s shadow", prec_req == VRS_PREC_BF16 ? "bf16" : "fp16");
+  return VRS_OK;
+}
+
+// Error-bound constants of the selection pass (vrs_internal.cuh key_error_bound).
+static KeyBound key_bound(const vrs_index *ix, bool gemm, bool h16) {
+  KeyBound b{};
+  b.kind = !gemm ? KEY_FP32 : (h16 ? KEY_H16 : KEY_TF32);
+  b.d = ix->d;
+  b.rmax = ix->rmax;
+  b.rho = ix->rho;
+  b.xmax = ix->xmax;
+  return b;
+}
+
 vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t d, const vrs_predicate *pred,
                          int32_t k, vrs_metric metric, int64_t *ids, float *dists,
                          const vrs_search_options *opts, void *cuda_stream) {
@@ -439,11 +487,11 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   if (path_req < VRS_PATH_AUTO || path_req > VRS_PATH_GEMM) return fail(VRS_EINVAL, "bad path option");
   if (rows_req < VRS_ROWS_AUTO || rows_req > VRS_ROWS_MASKED) return fail(VRS_EINVAL, "bad rows option");
   const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
-  if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision option");
-  if (prec_req == VRS_PREC_BF16 && !ix->xb) return fail(VRS_EUNSUPPORTED, "the index has no bf16 shadow");
-  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;
+  vrs_status st = check_precision(ix, prec_req);
+  if (st != VRS_OK) return st;
+  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
   PredDev pd;
-  vrs_status st = make_pred(ix, pred, &pd);
+  st = make_pred(ix, pred, &pd);
   if (st != VRS_OK) return st;
   if (k > VRS_K_MAX) return fail(VRS_EUNSUPPORTED, "k = %d > VRS_K_MAX (%d)", k, VRS_K_MAX);
   if (metric == VRS_COSINE && ix->has_zero_row)
@@ -456,7 +504,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   if (dev != ix->device) return fail(VRS_EINVAL, "current device %d differs from the index device %d", dev, ix->device);
 
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const int32_t kprime = k + 16;  // over-fetch for the exact re-score
+  const int32_t kprime = kprime_of(k);  // over-fetch for the exact re-score
   const int kpe = std::max(64, pow2_at_least(kprime));
   const bool identity = (pd.n == 0);
   const int64_t n = ix->n;
@@ -515,11 +563,20 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   static const bool want_local = getenv("VRS_SELECT_LOCAL") != nullptr;
   const bool sel_local = want_local && path == VRS_PATH_GEMM && !identity && select_chunks(n) <= kSelFinishMaxChunks;
   const size_t local_ids = sel_local ? (size_t)select_chunks(n) * kSelChunkRows : 0;
+  // certificate + exact fallback: per query the exponent / residual of
+  // the 16-bit operand, the certificate, finalize's k-th sort key, a group counter; the
+  // fallback's per-(item, query) slots of k results
+  int ex_qsmem = 0;
+  const int ex_qg = exact_group_size(d, &ex_qsmem);
+  const int64_t ex_items = exact_items_max(q, ex_qg);
+  const size_t ex_slots = (size_t)ex_items * ex_qg;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
                                    local_ids * 4, part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
                                    (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4,
-                                   use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0});
+                                   use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0,
+                                   (size_t)q * 4, (size_t)q * 4, (size_t)q, (size_t)q * 8, (size_t)q * 4,
+                                   ex_slots * k * 8, ex_slots * k * 8, ex_slots * 4});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -534,6 +591,15 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
   float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
   void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
+  int32_t *qexp = cv.take<int32_t>((size_t)q);
+  float *rq = cv.take<float>((size_t)q);
+  uint8_t *cert = cv.take<uint8_t>((size_t)q);
+  double *skey = cv.take<double>((size_t)q);
+  int32_t *gcnt = cv.take<int32_t>((size_t)q);
+  double *slot_key = cv.take<double>(ex_slots * k);
+  int64_t *slot_id = cv.take<int64_t>(ex_slots * k);
+  int32_t *slot_cnt = cv.take<int32_t>(ex_slots);
+  const bool h16 = use_bf16 && path == VRS_PATH_GEMM;
 
   int launches = 0;
   FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, SplitInfo{}, kprime, q, ix->X, d,
@@ -552,13 +618,17 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
     if (!identity) {   // (the bf16 query conversion rides along)
       ProfScope ps("select", stream);
-      const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
+      const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb, qexp, rq);
       if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
       else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
     }
     GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
                use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+    a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
+    a.xexp = ix->xexp;
+    a.qexp = qexp;
+    a.rq = rq;
     a.ids_local = ids_local;
     a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
     {
@@ -576,12 +646,28 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     f.gtau = gl.gtau;
     f.split = gl.split;
   }
+  // the certificate (finalize) and its fallback (exact.cu): every query's result is the
+  // exact top-k of the definition -- no host synchronisation
+  f.kb = key_bound(ix, path == VRS_PATH_GEMM, h16);
+  f.qexp = h16 ? qexp : nullptr;
+  f.rq = h16 ? rq : nullptr;
+  f.xexp = h16 ? ix->xexp : 0;
+  f.cert = cert;
+  f.sk = skey;
+  f.gcnt = gcnt;
+  f.stats = opts ? reinterpret_cast<unsigned long long *>(opts->stats) : nullptr;
   {
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));
   }
+  {
+    ExactArgs ea{cert, skey, gcnt, ix->X, d, n, identity ? nullptr : sel_ids, count, queries, q, (int32_t)metric, k,
+                 ix->row_offset, (double)ix->xmax, ids, dists, slot_key, slot_id, slot_cnt, ex_qg, ex_qsmem};
+    ProfScope ps("exact", stream);
+    CUDA_TRY(launch_exact(ea, stream, &launches));
+  }
   g_last_path = path;
-  g_last_prec = path == VRS_PATH_GEMM ? (use_bf16 ? VRS_PREC_BF16 : VRS_PREC_TF32) : VRS_PREC_DEFAULT;
+  g_last_prec = path == VRS_PATH_GEMM ? (use_bf16 ? ix->prec16 : VRS_PREC_TF32) : VRS_PREC_DEFAULT;
   g_last_launches = launches;
   return VRS_OK;
 }
@@ -607,11 +693,11 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const int rows_req = opts ? opts->rows : VRS_ROWS_AUTO;
   if (rows_req < VRS_ROWS_AUTO || rows_req > VRS_ROWS_MASKED) return fail(VRS_EINVAL, "bad rows option");
   const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
-  if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_BF16) return fail(VRS_EINVAL, "bad precision option");
-  if (prec_req == VRS_PREC_BF16 && !ix->xb) return fail(VRS_EUNSUPPORTED, "the index has no bf16 shadow");
-  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;
+  vrs_status st = check_precision(ix, prec_req);
+  if (st != VRS_OK) return st;
+  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
   PredDev pd;
-  vrs_status st = make_pred(ix, pred, &pd);
+  st = make_pred(ix, pred, &pd);
   if (st != VRS_OK) return st;
   if (metric == VRS_COSINE && ix->has_zero_row)
     return fail(VRS_EDEGENERATE, "COSINE over a corpus with a zero-norm row");
@@ -656,7 +742,8 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n), local_ids * 4,
                                       (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4, use_bf16 ? qpad_bytes : 0,
                                       (size_t)q * 4,
-                                      (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4}));
+                                      (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4, (size_t)q * 4,
+                                      (size_t)q * 4}));
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
   uint32_t *bitmap = cv.take<uint32_t>(nwords);
@@ -667,16 +754,15 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
   float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
   void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
+  int32_t *qexp = cv.take<int32_t>((size_t)q);
+  float *rq = cv.take<float>((size_t)q);
   RangeState r;
   r.gtau = cv.take<uint32_t>((size_t)q);
   r.cand_cnt = cv.take<int32_t>((size_t)L * q);
   r.coff = cv.take<int64_t>((size_t)L * q + 1);
   r.kept = cv.take<int32_t>((size_t)q);
   r.tau = tau;
-  r.xmax = ix->xmax;
-  // |<q,x>~ - <q,x>| <= gamma |q| |x|: operand rounding (bf16 RN 2^-9 each, TF32
-  // <= 2^-10 each) plus fp32 accumulation (d 2^-24), doubled for safety
-  r.gamma = use_bf16 ? 2.0 * (0x1p-8 + 0x1p-18 + d * 0x1p-23) : 2.0 * (0x1p-9 + 0x1p-20 + d * 0x1p-23);
+  r.kb = key_bound(ix, true, use_bf16);
   r.offsets = offsets;
   r.ids = ids;
   r.dists = dists;
@@ -689,13 +775,17 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int launches = 0;
   const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
   if (!identity) {
-    const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb);
+    const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb, qexp, rq);
     if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
     else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
   }
   GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
              queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
              use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+  a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
+  a.xexp = ix->xexp;
+  a.qexp = qexp;
+  a.rq = rq;
   a.ids_local = ids_local;
   a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));
@@ -715,7 +805,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   CUDA_TRY(cudaStreamSynchronize(stream));
   *total = R;
   g_last_path = VRS_PATH_GEMM;
-  g_last_prec = use_bf16 ? VRS_PREC_BF16 : VRS_PREC_TF32;
+  g_last_prec = use_bf16 ? ix->prec16 : VRS_PREC_TF32;
   if (R > capacity) {
     g_last_launches = launches;
     return fail(VRS_ERANGE, "%lld results > capacity %lld", (long long)R, (long long)capacity);

@@ -208,6 +208,58 @@ __device__ __forceinline__ float rank_key(int metric, float dot, float nx2, floa
   return dot * inv_nx;
 }
 
+// ---- selection-key error bound ("Certified exactness") -------
+// The selection passes rank rows by a computed key (rank_key units, "natural"
+// units below: L2 2<q,x> - |x|^2, IP <q,x>, COS <q,x>/|x|).  For one query q
+// and ANY row x, |computed key - exact key| <= E(q) with E from:
+//   operands   x~ = x + eps_x, q~ = q + eta (the 16-bit shadow / query, natural
+//              units):  |<q~,x~> - <q,x>| <= |q| |eps_x| + |eta| |x| + |eta| |eps_x|
+//              (Cauchy-Schwarz), with |eps_x| <= rmax and |eps_x| / |x| <= rho
+//              MEASURED at load (fp64, exact) and |eta| = rq measured per query;
+//              TF32 (hardware rounding of the fp32 operands, truncation or RN):
+//              |eps| <= 2^-10 |x| per element, likewise for q;
+//   accumulation  fp32 sums of exact products (16-bit x 16-bit fits fp32's 24-bit
+//              significand; TF32 11 x 11 bits too): <= c (|q~| |x~|) with
+//              c = (#MMA instructions along K + K per instruction) 2^-22 -- every
+//              accumulate and every in-instruction add within 2 ulp of the largest
+//              partial magnitude; fp32 FFMA scan: c = (d + 4) 2^-24;
+//   key arithmetic  |x|^2 and 1/|x| are fp32 roundings of fp64 values (2^-24
+//              relative), the key's own fma / product rounding (2^-24 relative);
+// each term rounded up generously (x2 on the fp32 rounding terms), then
+// x (1 + 2^-6) and an absolute 2^-40 slack for the fp64 arithmetic of the caller.
+enum KeyKind : int32_t { KEY_H16 = 0, KEY_TF32 = 1, KEY_FP32 = 2 };
+struct KeyBound {
+  int32_t kind;   // KeyKind
+  int32_t d;
+  double rmax;    // KEY_H16: max over rows of |x~ - x| (natural units, rounded up)
+  double rho;     // KEY_H16: max over rows of |x~ - x| / |x|
+  double xmax;    // max row norm (rounded up)
+};
+__host__ __device__ inline double key_error_bound(const KeyBound &b, int metric, double qn, double rq) {
+  double R = b.rmax, rho = b.rho, N = b.xmax, c;
+  if (b.kind == KEY_TF32) {
+    rq = 0x1p-10 * qn;
+    R = 0x1p-10 * N;
+    rho = 0x1p-10;
+    c = (double)((b.d + 7) / 8 + 8) * 0x1p-22;
+  } else if (b.kind == KEY_FP32) {
+    rq = 0.0;
+    R = 0.0;
+    rho = 0.0;
+    c = (double)(b.d + 4) * 0x1p-24;
+  } else {
+    c = (double)((b.d + 15) / 16 + 16) * 0x1p-22;
+  }
+  double E;
+  if (metric == VRS_COSINE) {
+    E = qn * rho + rq + rq * rho + c * (qn + rq) * (1.0 + rho) + 0x1p-21 * qn;
+  } else {
+    const double ed = qn * R + rq * N + rq * R + c * (qn + rq) * (N + R);
+    E = metric == VRS_IP ? ed + 0x1p-23 * qn * N : 2.0 * ed + 0x1p-22 * N * N + 0x1p-22 * qn * N;
+  }
+  return E * (1.0 + 0x1p-6) + 0x1p-40 * (qn * N + N * N + qn * qn);
+}
+
 // Candidate (key, id) total order: key descending, then id ascending.
 __device__ __forceinline__ bool cand_better(float ka, int32_t ia, float kb, int32_t ib) {
   return (ka > kb) || (ka == kb && ia < ib);
@@ -235,6 +287,31 @@ __device__ __forceinline__ void warp_bitonic_sort_desc(float *key, int32_t *id, 
     }
   }
   __syncwarp();
+}
+
+// Sums of U (4 or 8) per-lane values over the warp: on return every lane holds
+// the total of value (lane >> (5 - log2 U)) & (U - 1).  Each step swaps half of
+// the remaining values with the partner lane (xor 16, 8, ...), then a plain
+// butterfly over the remaining lane bits.
+template <int U>
+constexpr int log2u() { return U == 8 ? 3 : (U == 4 ? 2 : (U == 2 ? 1 : 0)); }
+template <int U>
+__device__ __forceinline__ double warp_sum_transpose(const double (&v)[U]) {
+  static_assert(U == 4 || U == 8, "U = 4 or 8");
+  const int lane = threadIdx.x & 31;
+  double w[U];
+#pragma unroll
+  for (int i = 0; i < U; ++i) w[i] = v[i];
+#pragma unroll
+  for (int h = U / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) w[i] = (up ? w[i + h] : w[i]) + __shfl_xor_sync(0xffffffffu, up ? w[i] : w[i + h], o);
+  }
+  double y = w[0];
+#pragma unroll
+  for (int o = 16 / U; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+  return y;
 }
 
 }  // namespace vrs

@@ -21,15 +21,25 @@ struct ProfScope {
   ProfScope &operator=(const ProfScope &) = delete;
 };
 
-// select.cu -- K4'/K5'.  Optional work folded into the count kernel (saves a
-// launch on the tensor-core path): the bf16 conversion of the queries.  (Folding
-// the row gather into the 1-CTA-per-8192-rows scatter kernel was measured slower
-// than the separate gather_copy_kernel.)
-struct SelectFuse {
-  const float *q_in;       // fp32 queries (nullptr: no conversion)
-  void *q_out;             // bf16 [q_total]: q_count converted values, zero padding after
-  int64_t q_count, q_total;
+// The per-search 16-bit query operand of the tensor-core pass (convert16.cuh
+// query_row_to16: per-row power-of-two exponent, 16-bit row, exact residual):
+// folded into select_count_kernel (select.cu; saves a launch), or its own
+// launch (launch_query16) when there is no predicate.
+struct QueryFuse {
+  const float *q_in;       // fp32 queries [q x d] (nullptr: no conversion)
+  void *q_out;             // 16-bit [rows x d]; rows q..rows-1 are zero (whole 128-row tiles)
+  int64_t q, rows;
+  int32_t d;
+  int32_t fmt;             // 0 fp16, 1 bf16
+  int32_t *qexp;           // [q] out: the row's exponent e_q (q~ = 16-bit(q * 2^e_q))
+  float *rq;               // [q] out: |q~ 2^-e_q - q| (fp64, rounded up)
 };
+using SelectFuse = QueryFuse;
+cudaError_t launch_query16(const QueryFuse &f, cudaStream_t s);
+// the fp16 / bf16 shadow at load; res (device u64[2], zeroed): max |x~ - x|, max |x~ - x| / |x| as double bits
+cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, const float *nx2,
+                          unsigned long long *res, cudaStream_t s);
+// select.cu -- K4'/K5' (the query conversion rides along when `fuse` is given)
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
                           void *scratch, cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
 size_t select_scratch_bytes(int64_t n);
@@ -44,7 +54,7 @@ cudaError_t launch_select_local(const PredDev &pred, int64_t n, uint32_t *bitmap
                                 cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
 
 // scan.cu -- K6' norms, K2' scan + fused top-k
-cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *zero_flag,
+cudaError_t launch_norms(const float *X, int64_t n, int32_t d, float *nx2, float *inv_nx, int32_t *flags,
                          cudaStream_t stream);
 
 struct ScanArgs {
@@ -62,6 +72,7 @@ struct ScanArgs {
   float *part_key;        // [P][q][kprime]
   int32_t *part_id;       // [P][q][kprime], -1 = padding
   int32_t P;
+  int64_t q_base = 0;     // first query of this launch (launch_scan splits batches over grid.y's limit)
 };
 int scan_query_group(int64_t q, int d, int kpe);
 cudaError_t launch_scan(const ScanArgs &a, int qg, int kpe, cudaStream_t s, int *launches);
@@ -103,17 +114,20 @@ struct GemmArgs {
   float *part_key;          // [P][q][kprime]
   int32_t *part_id;
   int32_t P;
-  int32_t bf16;             // select on the bf16 shadow (kind::f16) instead of fp32 (kind::tf32)
-  const void *Xb;           // bf16 shadow corpus [n x d] (bf16 only)
-  void *Qb;                 // scratch [q x d] bf16 queries (bf16 only)
+  int32_t bf16;             // select on the 16-bit shadow (kind::f16) instead of fp32 (kind::tf32)
+  const void *Xb;           // 16-bit shadow corpus [n x d] (16-bit only)
+  void *Qb;                 // scratch [qtiles * 128 x d] 16-bit queries (16-bit only)
   int32_t prepped;          // 1: the select kernels already converted the queries
+  int32_t fmt16 = 0;        // 16-bit format: 0 fp16, 1 bf16
+  int32_t xexp = 0;         // the shadow's exponent e_x
+  int32_t *qexp = nullptr;  // [q] per-query exponents e_q (written by the conversion)
+  float *rq = nullptr;      // [q] per-query residuals |q~ - q|
   // launch_select_local's output (nullptr: ids / count were written by launch_select):
   // the tensor-core pass first runs select_finish -> count, dense ids, gathered rows
   const int32_t *ids_local = nullptr;
   const uint32_t *chunk_count = nullptr;
 };
 size_t gemm_scratch_bytes(const GemmPlan &plan, int64_t q, int32_t kprime);
-cudaError_t launch_to_bf16(const float *in, void *out, int64_t count, int64_t total, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, cudaStream_t s, int *launches);
 // the tensor-core pass's candidate lists, as finalize reads them
 struct GemmLists {
@@ -148,6 +162,15 @@ struct FinalizeArgs {
   int64_t row_offset;
   int64_t *ids;            // [q][k]
   float *dists;            // [q][k]
+  // certificate: computed when cert != nullptr
+  KeyBound kb{};                   // error-bound constants of the selection pass that produced the keys
+  const int32_t *qexp = nullptr;   // [q] 16-bit operand exponents: IP / COS keys are in the domain 2^(e_q + xexp)
+  const float *rq = nullptr;       // [q] query residuals |q~ - q| (KEY_H16)
+  int32_t xexp = 0;
+  uint8_t *cert = nullptr;         // [q] out: 1 = the selection is certified exact
+  double *sk = nullptr;            // [q] out: exact sort key of the k-th result (L2: -dist, IP / COS: score)
+  int32_t *gcnt = nullptr;         // [q] out: zeroed (the exact fallback's per-group completion counters)
+  unsigned long long *stats = nullptr;   // optional vrs_search_options.stats
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches);
 
@@ -168,8 +191,7 @@ struct TcLaunch;   // tc_kernel.cuh
 struct RangeState {
   TcLaunch *tc;            // from range_tc_alloc (tensor maps + parameters shared by the passes)
   double tau;              // the caller's threshold (score >= tau; squared L2 <= tau)
-  double xmax;             // max row norm of the index
-  double gamma;            // tensor-core product error bound / (|q| |x|)
+  KeyBound kb;             // the selection pass's key error bound constants
   uint32_t *gtau;          // [q] key thresholds (ordered u32)
   int32_t *cand_cnt;       // [2P][q] candidate counts
   int64_t *coff;           // [q * 2P + 1] candidate segment offsets, query-major; coff[q*2P] = C
@@ -187,6 +209,35 @@ void range_tc_free(TcLaunch *t);
 cudaError_t launch_range_count(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
 cudaError_t launch_range_fill(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
 cudaError_t launch_range_write(const GemmArgs &a, const GemmPlan &plan, RangeState &r, cudaStream_t s, int *launches);
+
+// exact.cu -- the certificate's fallback: exact fp64 top-k of the queries whose
+// selection was not certified (finalize wrote cert = 0), over every qualifying row.
+struct ExactArgs {
+  const uint8_t *cert;     // [q] from finalize
+  const double *sk;        // [q] sort key of finalize's k-th result: rows below it cannot enter
+  int32_t *gcnt;           // [q] group completion counters (zeroed by finalize)
+  const float *X;
+  int32_t d;
+  int64_t n;
+  const int32_t *ids;      // selection (nullptr: all n rows)
+  const int64_t *count;
+  const float *Q;
+  int64_t q;
+  int32_t metric;
+  int32_t k;
+  int64_t row_offset;
+  double xmax;
+  int64_t *out_ids;        // [q][k] (overwritten for the uncertified queries)
+  float *out_dists;
+  double *slot_key;        // [items_max][qg][k]
+  int64_t *slot_id;
+  int32_t *slot_cnt;       // [items_max][qg]
+  int32_t qg;              // queries per group (<= 8)
+  int32_t q_smem;          // 1: the group's queries staged in shared memory
+};
+int exact_group_size(int32_t d, int *q_smem);
+int64_t exact_items_max(int64_t q, int qg);
+cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches);
 
 struct MergeArgs {
   const int64_t *cand_ids;

@@ -2,7 +2,10 @@
 bitmap / count bit-exact; exactly min(k, N_sel) valid entries with exact padding;
 ids unique, in range, 100 % qualifying; every returned dist within 1e-3 relative of
 the oracle's fp64 score of that id and of the oracle's dist at the same rank; id sets
-identical except rows whose oracle score lies within 1e-3 relative of the k-th."""
+identical except rows whose oracle score lies within 1e-3 relative of the k-th.
+On top of these (check_topk exact=True, the default), the certified-exact contract
+of DESIGN.md Sec. 7: ids identical to the oracle's rank for rank and dists equal to
+fp32(oracle fp64) within one ulp (check_topk_exact)."""
 import numpy as np
 
 import oracle
@@ -20,7 +23,7 @@ def check_select(bitmap_dev, count_dev, ids_dev, attrs_np, n, pred):
     return rc
 
 
-def check_topk(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset=0, ref=None, rtol=RTOL):
+def check_topk(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset=0, ref=None, rtol=RTOL, exact=True):
     """gi, gd: numpy [q, k] from the GPU.  X, Q: numpy fp32.  Returns #queries checked."""
     if ref is None:
         ref = oracle.search(X, attrs_np, pred, Q, k, metric, row_offset)
@@ -48,6 +51,8 @@ def check_topk(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset=0, ref=None, 
         if diff:
             ds = oracle.score(X, Q[j], np.array(sorted(diff)) - row_offset, metric)
             assert (np.abs(ds - sk) <= rtol * abs(sk)).all(), f"q{j}: id sets differ outside the k-th band"
+    if exact:   # the certified-exact contract on top of north_star's band rules
+        check_topk_exact(gi, gd, X, attrs_np, pred, Q, k, metric, row_offset, ref=ref)
     return Q.shape[0]
 
 

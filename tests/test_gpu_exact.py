@@ -46,12 +46,15 @@ def _tie_corpus(n, d, lo_scale, hi_scale, seed=0):
     return Y, Q
 
 
-def _search(vrs, X, Q, k, metric, attrs=None, pred=(), precision=None, path=None):
+def _search(vrs, X, Q, k, metric, attrs=None, pred=(), precision=None, path=None, stats_out=None):
     n = X.shape[0]
     attrs = attrs if attrs is not None else [np.zeros(n, dtype=np.int32)]
     ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], precision=precision)
-    ids, dists = ix.search(torch.from_numpy(Q).cuda(), list(pred), k=k, metric=METRICS[metric], path=path)
+    st = vrs.new_stats()
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), list(pred), k=k, metric=METRICS[metric], path=path, stats=st)
     torch.cuda.synchronize()
+    if stats_out is not None:
+        stats_out.update(vrs.read_stats(st))
     return ids.cpu().numpy(), dists.cpu().numpy(), attrs
 
 
@@ -60,17 +63,24 @@ def test_selection_ties_default_precision(vrs, hi):
     """The judge's construction (What's weak #1): gap 3.5e-3 ties in bf16;
     gap 2e-4 also ties in fp16 / TF32."""
     X, Q = _tie_corpus(50000, 128, 1 + 1e-5, hi)
-    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP)
+    st = {}
+    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP, stats_out=st)
     check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.IP)
-    assert sorted((gi[0] >= 0).nonzero()[0].tolist()) == list(range(10))
+    if hi < 1 + 5e-4:   # below fp16's resolution at 1: the certificate must fail -> exact fallback
+        assert st["uncertified"] == 1, st
+    assert st["max_key_error_over_bound"] < 1.0, st
 
 
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
 def test_selection_ties_every_precision(vrs, prec):
     p = {"tf32": vrs.PREC_TF32, "bf16": vrs.PREC_BF16}[prec]
     X, Q = _tie_corpus(50000, 128, 1 + 1e-5, 1 + 3.5e-3, seed=1)
-    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP, precision=p)
+    st = {}
+    gi, gd, attrs = _search(vrs, X, Q, 10, oracle.IP, precision=p, stats_out=st)
     check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.IP)
+    if prec == "bf16":
+        assert st["uncertified"] == 1, st
+    assert st["max_key_error_over_bound"] < 1.0, st
 
 
 def test_near_zero_cosine_window(vrs):
@@ -103,3 +113,61 @@ def test_l2_near_duplicates(vrs):
     attrs = [rng.integers(0, 1000, n).astype(np.int32)]
     gi, gd, _ = _search(vrs, X, Q, 10, oracle.L2, attrs=attrs)
     check_topk_exact(gi, gd, X, attrs, [], Q, 10, oracle.L2)
+
+
+@pytest.mark.parametrize("path", ["gemm", "scan"])
+def test_fallback_many_queries(vrs, path):
+    """Many uncertified queries at once (> one fallback group, ragged): 40 queries whose
+    top-10 ties in every selection precision, among 300 ordinary ones."""
+    rng = np.random.default_rng(11)
+    n, d = 30000, 128
+    X = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    Q = rng.standard_normal((300, d)).astype(np.float32)
+    hard = rng.choice(300, 40, replace=False)
+    pos = rng.choice(n, 40 * 30, replace=False)
+    for h, j in enumerate(hard):
+        u = Q[j] / np.linalg.norm(Q[j])
+        for i in range(30):   # 30 rows along q at scales below every precision's resolution
+            X[pos[30 * h + i]] = (u * np.float32(1.0 + 1e-7 * (i % 7) + (2e-6 if i >= 20 else 0.0))).astype(np.float32)
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    st = {}
+    p = vrs.PATH_SCAN if path == "scan" else vrs.PATH_GEMM
+    gi, gd, _ = _search(vrs, X, Q, 10, oracle.IP, attrs=attrs, pred=[(0, 0, 899)], path=p, stats_out=st)
+    check_topk_exact(gi, gd, X, attrs, [(0, 0, 899)], Q, 10, oracle.IP)
+    assert st["queries"] == 300 and st["uncertified"] >= 1, st
+    assert st["max_key_error_over_bound"] < 1.0, st
+
+
+@pytest.mark.parametrize("metric", [oracle.IP, oracle.L2, oracle.COS])
+def test_accumulation_bound_cancellation(vrs, metric):
+    """Operands exactly representable in fp16 (the measured residuals are 0, so the
+    bound is its accumulation term alone) with large cancelling partial sums: the
+    observed key error must stay below the modelled bound, and the result exact."""
+    rng = np.random.default_rng(13 + metric)
+    n, d = 20000, 256
+    big = rng.integers(512, 1024, (n, 1)).astype(np.float32)
+    sgn = np.where(np.arange(d) % 2 == 0, 1.0, -1.0).astype(np.float32)
+    X = (big * sgn[None, :] + rng.integers(-64, 64, (n, d))).astype(np.float32) / 8
+    Q = (rng.integers(-64, 64, (8, d)) + 512 * sgn[None, :]).astype(np.float32) / 8
+    st = {}
+    gi, gd, attrs = _search(vrs, X, Q, 20, metric, precision=vrs.PREC_FP16, stats_out=st)
+    check_topk_exact(gi, gd, X, attrs, [], Q, 20, metric)
+    assert st["max_key_error_over_bound"] < 1.0, st
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "fp16"])
+@pytest.mark.parametrize("metric", [oracle.IP, oracle.L2, oracle.COS])
+def test_bound_holds_random(vrs, prec, metric):
+    """Gaussian data, every precision x metric: the certificate's bound is never
+    exceeded by an observed key error, and on this data it certifies every query."""
+    rng = np.random.default_rng(17 + metric)
+    n, d = 40000, 256
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Q = rng.standard_normal((64, d)).astype(np.float32)
+    p = {"tf32": vrs.PREC_TF32, "bf16": vrs.PREC_BF16, "fp16": vrs.PREC_FP16}[prec]
+    st = {}
+    gi, gd, attrs = _search(vrs, X, Q, 10, metric, precision=p, stats_out=st)
+    check_topk_exact(gi, gd, X, attrs, [], Q, 10, metric)
+    assert st["max_key_error_over_bound"] < 1.0, st
+    if prec == "fp16":
+        assert st["uncertified"] == 0, st

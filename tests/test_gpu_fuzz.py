@@ -38,7 +38,7 @@ def _case(seed):
         pred.append((col, lo, hi))
     path = [None, 2, 1][int(rng.integers(0, 3))]
     rows = [None, 1, 2][int(rng.integers(0, 3))]
-    prec = [None, 1, 2][int(rng.integers(0, 3))]
+    prec = [None, 1, 2, 3][int(rng.integers(0, 4))]
     off = int(rng.integers(0, 1 << 20))
     return rng, n, d, q, k, metric, pred, path, rows, prec, off
 
@@ -46,7 +46,7 @@ def _case(seed):
 @pytest.mark.parametrize("seed", range(N_CASES))
 def test_fuzz_parity(vrs, seed):
     rng, n, d, q, k, metric, pred, path, rows, prec, off = _case(seed)
-    if prec == 2 and d % 8:
+    if prec in (2, 3) and d % 8:
         prec = None
     X = rng.standard_normal((n, d)).astype(np.float32)
     if metric == oracle.COS:
@@ -65,7 +65,7 @@ def test_fuzz_range(vrs, seed):
     """Threshold mode on random shapes: tau between two scores of the first query
     (so result counts vary), ids and offsets exact, dists to fp32 rounding."""
     rng, n, d, q, _, metric, pred, _, rows, prec, off = _case(10_000 + seed)
-    if prec == 2 and d % 8:
+    if prec in (2, 3) and d % 8:
         prec = None
     q = min(q, 64)
     X = rng.standard_normal((n, d)).astype(np.float32)

@@ -53,11 +53,11 @@ GEMM_CASES = [
 
 @pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: f"n{c[0]}-d{c[1]}-q{c[2]}-k{c[3]}-m{c[4]}")
 @pytest.mark.parametrize("rows", [0, 1, 2], ids=["auto", "gather", "masked"])
-@pytest.mark.parametrize("prec", [1, 2], ids=["tf32", "bf16"])
+@pytest.mark.parametrize("prec", [1, 2, 3], ids=["tf32", "bf16", "fp16"])
 def test_gemm_parity(vrs, case, rows, prec):
     n, d, q, k, metric, pred = case
-    if prec == 2 and d % 8:
-        pytest.skip("bf16 shadow needs d % 8 == 0")
+    if prec in (2, 3) and d % 8:
+        pytest.skip("a 16-bit shadow needs d % 8 == 0")
     rng = np.random.default_rng(n * 7 + d)
     X = rng.standard_normal((n, d)).astype(np.float32)
     attrs = [rng.integers(0, 1000, n).astype(np.int32)]

@@ -130,12 +130,26 @@ def test_q_zero_and_errors(vrs):
         with pytest.raises(vrs.VrsError) as e:
             ix.search(Qd, **args)
         assert e.value.status == status, kw
-    with pytest.raises(vrs.VrsError) as e:                  # host pointer
-        ix.search(torch.zeros(2, 16), [], k=5)
-    assert e.value.status == 1
-    with pytest.raises(vrs.VrsError) as e:                  # d mismatch
-        ix.search(torch.zeros(2, 8, device="cuda"), [], k=5)
-    assert e.value.status == 1
+    # the binding validates tensors before the call ...
+    for bad in (torch.zeros(2, 16), torch.zeros(2, 8, device="cuda"), torch.zeros(2, 16, device="cuda").double(),
+                torch.zeros(16, 2, device="cuda").t()):
+        with pytest.raises(ValueError):
+            ix.search(bad, [], k=5)
+    with pytest.raises(ValueError):                          # wrong out shape / dtype
+        ix.search(Qd, [], k=5, out=(torch.empty(2, 4, dtype=torch.int64, device="cuda"),
+                                    torch.empty(2, 5, device="cuda")))
+    # ... and the C ABI itself still rejects a host pointer and a d mismatch (EINVAL)
+    import ctypes
+    from paper_2403_15807_b200 import _lib
+    lib = vrs.library()
+    pr, keep = _lib.make_predicate([])
+    out_i = torch.empty(2, 5, dtype=torch.int64, device="cuda")
+    out_d = torch.empty(2, 5, device="cuda")
+    host_q = torch.zeros(2, 16)
+    for qptr, dd in ((host_q.data_ptr(), 16), (Qd.data_ptr(), 8)):
+        st = lib.vrs_search_ex(ix._h, ctypes.c_void_p(qptr), 2, dd, ctypes.byref(pr), 5, 0,
+                               ctypes.c_void_p(out_i.data_ptr()), ctypes.c_void_p(out_d.data_ptr()), None, None)
+        assert st == 1
     Z = X.copy()
     Z[3] = 0
     iz = vrs.Index(torch.from_numpy(Z).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
@@ -228,3 +242,16 @@ def test_exact_ties_go_to_lower_ids(vrs, dups, k):
         ri, rd, _ = oracle.search(X, attrs, [(0, 0, 899)], Q, k, metric)
         assert (gi == ri).all()
         assert np.allclose(gd, rd, rtol=1e-6)
+
+
+def test_binding_rejects_bad_columns(vrs):
+    """a short / misplaced attribute column would be read out of bounds by
+    select_count_kernel -- the binding refuses it before vrs_load."""
+    X = torch.zeros(100, 8, device="cuda")
+    for bad in ([torch.zeros(99, dtype=torch.int32, device="cuda")],
+                [torch.zeros(100, dtype=torch.int32)],
+                [torch.zeros(100, 2, dtype=torch.int32, device="cuda")]):
+        with pytest.raises(ValueError):
+            vrs.Index(X, bad)
+    with pytest.raises(ValueError):
+        vrs.Index(X.double(), [])

@@ -45,12 +45,14 @@ CASES = [
     (4099, 32, 130, COS, [(0, 100, 899)], 60),
     (20000, 256, 7, IP, [(0, 0, 9)], 5),        # ~1 % selectivity
     (2000, 768, 2, L2, [(0, 0, 699)], 30),
+    (4000, 8, 4, IP, [], 50),                    # small d: the bound's rounding terms dominate
+    (4000, 16, 4, L2, [(0, 0, 799)], 30),
 ]
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}-d{c[1]}-q{c[2]}-m{c[3]}")
 @pytest.mark.parametrize("rows", [0, 1, 2], ids=["auto", "gather", "masked"])
-@pytest.mark.parametrize("prec", [1, 2], ids=["tf32", "bf16"])
+@pytest.mark.parametrize("prec", [1, 2, 3], ids=["tf32", "bf16", "fp16"])
 def test_range_parity(vrs, case, rows, prec):
     n, d, q, metric, pred, rank = case
     rng = np.random.default_rng(n + d + q)
