@@ -473,9 +473,14 @@ __device__ __noinline__ uint32_t warp_keep_best_fast_e(float *bk, int32_t *bi, i
   n = K;
   return ordered_u32(elem_e<E>(kk, K - 1));
 }
+// (collection capacity 32E >= 2K, else the K-th best's bucket would almost never fit
+// and every compaction would take the radix path; E = 8 collects 2 x 256 words, so it
+// needs a 512-word histogram area)
+template <int HIST>
 __device__ __forceinline__ uint32_t warp_keep_best_fast(float *bk, int32_t *bi, int &n, int K, uint32_t *hist) {
-  if (K <= 64) return warp_keep_best_fast_e<2>(bk, bi, n, K, hist);
-  if (K <= 128) return warp_keep_best_fast_e<4>(bk, bi, n, K, hist);
+  if (K <= 32) return warp_keep_best_fast_e<2>(bk, bi, n, K, hist);
+  if (K <= 64) return warp_keep_best_fast_e<4>(bk, bi, n, K, hist);
+  if (HIST >= 512 && K <= 128) return warp_keep_best_fast_e<8>(bk, bi, n, K, hist);
   return warp_keep_best(bk, bi, n, K, hist);
 }
 
@@ -573,20 +578,21 @@ __device__ bool warp_kth_value_fast(const uint32_t *v, int n, int K, uint32_t *h
 // per-warp survivors merged by warp 0) so small batches are not latency-bound.
 constexpr int kFinGroup = 4;   // queries per CTA when W == 1
 
-template <int CAP>
+template <int CAP, int HIST = 256>
 struct FinBufsT {
+  static constexpr int kHist = HIST;
   float key[CAP];
   int32_t id[CAP];
-  uint32_t hist[256];
+  uint32_t hist[HIST];
 };
-using FinBufs = FinBufsT<kBufCap>;
+using FinBufs = FinBufsT<kBufCap, 512>;
 
 // Steps 1-2 for one warp over lists l = first, first + step, ... (in groups of
 // 32): the warp's buffer ends with at most K entries (or all it saw).
 // (keep: the buffer is cut to the k' best only when it holds more than `keep`
 // entries -- the CTA tree merge takes up to 32E unsorted survivors per warp)
-template <int CAP>
-__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP> &B,
+template <int CAP, int HIST>
+__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP, HIST> &B,
                           int keep = -1) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
@@ -625,7 +631,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (m == 0) continue;
         if (n + __popc(m) > CAP) {
-          thr = max(thr, warp_keep_best_fast(B.key, B.id, n, K, B.hist));
+          thr = max(thr, warp_keep_best_fast<HIST>(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv[u]) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
         }
@@ -641,7 +647,7 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
     }
   }
   __syncwarp();
-  if (n > (keep < 0 ? K : keep)) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
+  if (n > (keep < 0 ? K : keep)) warp_keep_best_fast<HIST>(B.key, B.id, n, K, B.hist);
   return n;
 }
 
@@ -856,7 +862,7 @@ __device__ void fin_sort_write(const FinalizeArgs &a, int64_t j, int m, double q
 template <int CAP, int SEL>
 __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) finalize_warp_kernel(FinalizeArgs a) {
   TL_SCOPE(1);
-  __shared__ FinBufsT<CAP> s_buf[kFinGroup];
+  __shared__ FinBufsT<CAP, SEL <= 64 ? 256 : 512> s_buf[kFinGroup];
   __shared__ double s_sc[kFinGroup][SEL];
   __shared__ int64_t s_sid[kFinGroup][SEL];
   const int w = threadIdx.x >> 5;
@@ -969,7 +975,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
         bool keep = i < nv && ordered_u32(kv) >= thr;
         uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (n + __popc(m) > kBufCap) {
-          thr = max(thr, warp_keep_best_fast(B.key, B.id, n, K, B.hist));
+          thr = max(thr, warp_keep_best_fast<FinBufs::kHist>(B.key, B.id, n, K, B.hist));
           keep = keep && ordered_u32(kv) >= thr;
           m = __ballot_sync(0xffffffffu, keep);
         }
@@ -982,7 +988,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
         __syncwarp();
       }
     }
-    if (n > K) warp_keep_best_fast(B.key, B.id, n, K, B.hist);
+    if (n > K) warp_keep_best_fast<FinBufs::kHist>(B.key, B.id, n, K, B.hist);
     float km = INFINITY;
     for (int i = lane; i < n; i += 32) km = fminf(km, B.key[i]);
 #pragma unroll
@@ -1199,7 +1205,11 @@ __global__ void __launch_bounds__(kFinGroup * 32) threshold_warp_kernel(Threshol
     if (lane == 0) a.gtau[j] = ok ? x : 0u;
     return;
   }
-  const float kth = a.kth <= 64 ? lane_top_kth<2, 32>(v, nvals, lane, a.kth) : lane_top_kth<4, 32>(v, nvals, lane, a.kth);
+  // (the union keeps 32E values, at least 2K: with 32E == K its K-th largest would be its
+  // minimum, a far looser bound -- C4 k' = 128 at E = 4 cost the main pass 40 %)
+  const float kth = a.kth <= 32   ? lane_top_kth<2, 32>(v, nvals, lane, a.kth)
+                    : a.kth <= 64 ? lane_top_kth<4, 32>(v, nvals, lane, a.kth)
+                                  : lane_top_kth<8, 32>(v, nvals, lane, a.kth);
   if (lane == 0) a.gtau[j] = kth > -INFINITY ? ordered_u32(kth) : 0u;
 }
 
@@ -1281,15 +1291,17 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
                     wsmem, s, a);
   }
   if (!block_thr && a.kth <= 128) {
+    // per lane E values, merged width 32M >= 2K (M = E): the K-th of the kept union stays
+    // close to the K-th of all values (see threshold_warp_kernel)
     const bool big = a.q < kSmCountB200;   // few queries: more warps per query
     if (a.kth <= 32)
-      return big ? launch_k(threshold_union_kernel<32, 2, 1>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
-                 : launch_k(threshold_union_kernel<8, 2, 1>, dim3((unsigned)a.q), dim3(256), 0, s, a);
-    if (a.kth <= 64)
       return big ? launch_k(threshold_union_kernel<32, 2, 2>, dim3((unsigned)a.q), dim3(1024), 0, s, a)
                  : launch_k(threshold_union_kernel<8, 2, 2>, dim3((unsigned)a.q), dim3(256), 0, s, a);
-    return big ? launch_k(threshold_union_kernel<16, 4, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
-               : launch_k(threshold_union_kernel<8, 4, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+    if (a.kth <= 64)
+      return big ? launch_k(threshold_union_kernel<16, 4, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
+                 : launch_k(threshold_union_kernel<8, 4, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+    return big ? launch_k(threshold_union_kernel<16, 8, 8>, dim3((unsigned)a.q), dim3(512), 0, s, a)
+               : launch_k(threshold_union_kernel<8, 8, 8>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr1024 = 0, attr256 = 0;

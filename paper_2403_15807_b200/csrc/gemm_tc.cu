@@ -409,7 +409,12 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // pipeline fill / drain) dominate over several waves -- use at most 148 / qtiles
     // splits (the same density: the step follows the main pass's span)
     static const bool full_p = getenv("VRS_PROBE_FULLP") != nullptr;
-    const int32_t p_probe = full_p ? plan.P : std::max(1, std::min(plan.P, kSmCountB200 / std::max(1, plan.qtiles)));
+    // ... but enough splits that a query has >= 4 k' probe values (2 lists x 32 slots per split):
+    // gtau is the k'-th largest of them, and with k' near their count it degenerates to their
+    // minimum (C4 Q = 8192: 128 values for k' = 128 doubled the main pass's survivors)
+    const int32_t p_probe = full_p ? plan.P
+                                   : std::max(1, std::min(plan.P, std::max(kSmCountB200 / std::max(1, plan.qtiles),
+                                                                           (4 * a.kprime + 63) / 64)));
     pp.P = p_probe;
     pp.P_main = plan.P;
     pp.min_p_main = p.min_p;

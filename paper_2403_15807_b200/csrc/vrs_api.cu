@@ -451,7 +451,12 @@ static int pow2_at_least(int v) {
 // >= k + 16 (at least 32) -- the lists keep that many per (list, query) anyway, and
 // the wider margin lets the certificate hold without the fallback on clustered
 // data (C5: k = 50 -> 128).
-static int kprime_of(int k) { return std::max(32, pow2_at_least(k + 16)); }
+static int kprime_of(int k) {
+  static const bool old = getenv("VRS_KPRIME_K16") != nullptr;   // (A/B only: r01's k + 16)
+  static const int forced = getenv("VRS_KPRIME") ? atoi(getenv("VRS_KPRIME")) : 0;   // (A/B only)
+  if (forced > 0) return std::max(k + 1, std::min(256, forced));
+  return old ? k + 16 : std::max(32, pow2_at_least(k + 16));
+}
 
 static vrs_status check_precision(const vrs_index *ix, int prec_req) {
   if (prec_req < VRS_PREC_DEFAULT || prec_req > VRS_PREC_FP16) return fail(VRS_EINVAL, "bad precision option");
@@ -660,7 +665,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));
   }
-  {
+  static const bool no_fallback = getenv("VRS_NO_FALLBACK") != nullptr;   // (A/B timing only: results unverified)
+  if (!no_fallback) {
     ExactArgs ea{cert, skey, gcnt, ix->X, d, n, identity ? nullptr : sel_ids, count, queries, q, (int32_t)metric, k,
                  ix->row_offset, (double)ix->xmax, ids, dists, slot_key, slot_id, slot_cnt, ex_qg, ex_qsmem};
     ProfScope ps("exact", stream);

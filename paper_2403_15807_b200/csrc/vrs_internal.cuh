@@ -90,7 +90,7 @@ inline std::mutex &setup_mutex() {
 // call site already set; idempotent, thread-safe).
 template <typename Kern>
 inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes, size_t &done) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  if (bytes <= 32 * 1024) return cudaSuccess;   // (static shared memory adds to the 48 KB default limit)
   std::lock_guard<std::mutex> g(setup_mutex());
   if (bytes <= done) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

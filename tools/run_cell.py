@@ -19,7 +19,7 @@ ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--rows", type=int, default=0)
-ap.add_argument("--prec", type=int, default=0, help="0 default (bf16 shadow), 1 tf32, 2 bf16")
+ap.add_argument("--prec", type=int, default=0, help="0 default (the index shadow), 1 tf32, 2 bf16, 3 fp16")
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.workload]
 n = a.n or cfg.n

@@ -18,4 +18,4 @@ for path in sys.argv[1:]:
     print("   kernels ms/step", {k: round(v, 3) for k, v in d.get("kernels_ms_per_step", {}).items()})
     for c in d.get("cells", []):
         print(f"   s={c['sel']:<8g} q={c['q']:<5d} nsel={c['n_sel']:<9d} {c['ms']:8.3f} ms {c['qps']:12.0f} q/s "
-              f"hbm={c['hbm_frac']:.2f} tc={c['tensor_frac']:.2f}")
+              f"hbm={c['hbm_frac']:.2f} tc={c.get('tensor_frac', c.get('tensor_frac_burst', 0)):.2f}")
