@@ -3,20 +3,29 @@
 // finalize.cu certifies each query's result: the k-th exact score of the
 // re-scored candidates must beat every unselected row's selection key plus the
 // key error bound.  A query that fails (selection-precision ties, clustered
-// data, adversarial inputs) is recomputed here from the definition itself
-// (sigma_eps(v x sigma_theta(R)); Table 1 "Accuracy:
-// Exact"): the exact fp64 score of EVERY qualifying row, the k best by (score,
-// lower id).  One launch, no host synchronisation: the kernel reads the
+// data, adversarial inputs) is recomputed here from the definition (PAPER.md
+// L285-L288: sigma_eps(v x sigma_theta(R)); Table 1 "Accuracy: Exact"):
+// every qualifying row is examined, and the k best by (exact score, lower id)
+// are returned.  One launch, no host synchronisation: the kernel reads the
 // certificate flags itself and returns at once when every query is certified.
 //
-// Work: the uncertified queries in groups of up to 8 (the rows are read once per
-// group), each group's row space split over the grid.  Each CTA keeps, per query,
-// the rows scoring at least finalize's k-th sort key (no row below it can enter:
-// k rows already reach it) in a shared-memory buffer, compacted to the k best
-// when it fills; its best k go to a slot; the CTA finishing a group's last split
-// merges the group's slots and overwrites the queries' results.
+// Per work item (a group of up to QG uncertified queries x a split of the row
+// space), two stages:
+//   filter  lane-per-row fp32 FFMA dot products of each qualifying row with the
+//           group's queries (rows staged HBM -> shared memory by 16-byte
+//           cp.async in a per-warp ring; queries in shared memory), keys as in
+//           rank_key; a row survives for a query when its fp32 key reaches
+//           s_k - E32, where s_k is finalize's k-th EXACT key -- k rows reach s_k,
+//           and E32 bounds the fp32 key's error (vrs_internal.cuh, KEY_FP32), so no
+//           row of the true top k is dropped;
+//   exact   each survivor's fp64 score (coalesced warp re-read of the row); rows
+//           at or above the k-th sort key go to a per-query shared buffer,
+//           compacted to the k best by (score, lower id) when it fills.
+// Each item's k best go to a slot; the CTA finishing a group's last split merges
+// the group's slots and overwrites those queries' results.
 //
-// Roofline: HBM (4d bytes per qualifying row per group) -- rarely launched work.
+// Roofline: HBM (4d bytes per qualifying row per query group) -- launched on
+// every search, it works only when a certificate failed.
 #include <float.h>
 
 #include <algorithm>
@@ -27,10 +36,28 @@ namespace vrs {
 
 constexpr int kExWarps = 8;
 constexpr int kExThreads = kExWarps * 32;
-constexpr int kExQG = 8;       // queries per group (max)
-constexpr int kExCap = 512;    // buffered rows per query (>= k + 16 per batch; k <= VRS_K_MAX)
-constexpr int kExGrid = 148;   // one CTA per SM
-constexpr int kExQSmem = 96 * 1024;
+constexpr int kExCap = 512;     // exact-scored rows buffered per query (>= k + 256 per flush batch)
+constexpr int kExGrid = 148;    // one CTA per SM
+constexpr int kExKC = 16;       // fp32 columns per staged chunk
+constexpr int kExPad = kExKC + 4;
+constexpr int kExStages = 2;
+constexpr int kExSurv = 4096;   // survivor list; flushed once it holds >= kExSurv / 2
+constexpr int kExQMax = 8;
+
+__host__ __device__ constexpr size_t exact_smem_bytes(int qg, int dpad) {
+  return (size_t)qg * kExCap * 16                              // exact buffers (key, id)
+         + (size_t)kExWarps * kExStages * 32 * kExPad * 4      // row stages
+         + (size_t)kExSurv * 8                                 // survivors (row, query slot)
+         + (size_t)qg * dpad * 4;                              // queries
+}
+
+int exact_group_size(int32_t d) {
+  const int dpad = (d + kExKC - 1) / kExKC * kExKC;
+  int qg = kExQMax;
+  while (qg > 1 && exact_smem_bytes(qg, dpad) > 200 * 1024) qg >>= 1;
+  return qg;
+}
+int64_t exact_items_max(int64_t q, int qg) { return std::max<int64_t>(4 * kExGrid, (q + qg - 1) / qg); }
 
 // descending (key, id asc) bitonic sort of n = 2^p (double, int64) pairs in shared memory, one warp
 __device__ void ex_sort_desc(double *key, int64_t *id, int n) {
@@ -59,24 +86,56 @@ __device__ void ex_compact(double *key, int64_t *id, int &cnt, int k) {
   cnt = min(cnt, k);
 }
 
-int exact_group_size(int32_t d, int *q_smem) {
-  const int64_t per = (int64_t)d * 4;
-  int qg = (int)std::min<int64_t>(kExQG, std::max<int64_t>(1, kExQSmem / per));
-  *q_smem = (int64_t)qg * per <= kExQSmem ? 1 : 0;
-  return qg;
+// exact fp64 sort key of row `rid` for query row qv (one warp, coalesced): L2 -|q-x|^2, IP <q,x>, COS cos
+template <bool VEC4>
+__device__ double ex_exact(const ExactArgs &a, const float *qv, double qq, int32_t rid) {
+  const int lane = threadIdx.x & 31;
+  const float *x = a.X + (int64_t)rid * a.d;
+  double s = 0.0, xx = 0.0;
+  if (VEC4) {
+    for (int t = 4 * lane; t < a.d; t += 128) {
+      const float4 xv = __ldg(reinterpret_cast<const float4 *>(x + t));
+      const float4 q4 = *reinterpret_cast<const float4 *>(qv + t);
+      if (a.metric == VRS_L2) {
+        const double d0 = (double)q4.x - xv.x, d1 = (double)q4.y - xv.y, d2 = (double)q4.z - xv.z, d3 = (double)q4.w - xv.w;
+        s += d0 * d0; s += d1 * d1; s += d2 * d2; s += d3 * d3;
+      } else {
+        s += (double)q4.x * xv.x; s += (double)q4.y * xv.y; s += (double)q4.z * xv.z; s += (double)q4.w * xv.w;
+        xx += (double)xv.x * xv.x + (double)xv.y * xv.y + (double)xv.z * xv.z + (double)xv.w * xv.w;
+      }
+    }
+  } else {
+    for (int t = lane; t < a.d; t += 32) {
+      const double xv = __ldg(x + t), q1 = qv[t];
+      if (a.metric == VRS_L2) { const double df = q1 - xv; s += df * df; }
+      else { s += q1 * xv; xx += xv * xv; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    xx += __shfl_xor_sync(0xffffffffu, xx, o);
+  }
+  if (a.metric == VRS_L2) return -s;
+  if (a.metric == VRS_COSINE) return qq > 0.0 && xx > 0.0 ? s / (sqrt(qq) * sqrt(xx)) : -INFINITY;
+  return s;
 }
-int64_t exact_items_max(int64_t q, int qg) { return std::max<int64_t>(kExGrid, (q + qg - 1) / qg); }
 
-template <bool VEC>
+template <int QG, bool VEC4>
 __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs a) {
   extern __shared__ __align__(16) uint8_t ex_smem[];
-  double *s_key = reinterpret_cast<double *>(ex_smem);                  // [qg][kExCap]
-  int64_t *s_id = reinterpret_cast<int64_t *>(s_key + kExQG * kExCap);   // [qg][kExCap]
-  float *s_q = reinterpret_cast<float *>(s_id + kExQG * kExCap);         // [qg][d] (q_smem)
-  __shared__ int s_cnt[kExQG];
-  __shared__ double s_thr[kExQG], s_qq[kExQG];
-  __shared__ int64_t s_qid[kExQG];
-  __shared__ int s_wsum[kExWarps], s_last, s_full;
+  const int dpad = (a.d + kExKC - 1) / kExKC * kExKC;
+  const int nk = dpad / kExKC;
+  double *s_key = reinterpret_cast<double *>(ex_smem);                       // [QG][kExCap]
+  int64_t *s_id = reinterpret_cast<int64_t *>(s_key + QG * kExCap);           // [QG][kExCap]
+  float *s_stage = reinterpret_cast<float *>(s_id + QG * kExCap);             // [warps][stages][32][kExPad]
+  uint2 *s_surv = reinterpret_cast<uint2 *>(s_stage + kExWarps * kExStages * 32 * kExPad);   // (row, slot)
+  float *s_q = reinterpret_cast<float *>(s_surv + kExSurv);                   // [QG][dpad]
+  __shared__ int s_cnt[QG], s_nsurv;
+  __shared__ double s_thr[QG], s_qq[QG];
+  __shared__ float s_thr32[QG];
+  __shared__ int64_t s_qid[QG];
+  __shared__ int s_wsum[kExWarps], s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_wait();
   pdl_trigger();
@@ -91,10 +150,44 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
 #pragma unroll
   for (int w = 0; w < kExWarps; ++w) U += s_wsum[w];
   if (U == 0) return;
-  const int QG = a.qg;
   const int64_t ngroups = (U + QG - 1) / QG;
-  const int64_t R = std::max<int64_t>(1, (int64_t)gridDim.x / ngroups);
+  const int64_t R = std::max<int64_t>(1, (2 * (int64_t)gridDim.x + ngroups - 1) / ngroups);
   const int64_t n_space = a.ids ? *a.count : a.n;
+  KeyBound kb32{};
+  kb32.kind = KEY_FP32;
+  kb32.d = a.d;
+  kb32.xmax = a.xmax;
+  float *wst = s_stage + warp * kExStages * 32 * kExPad;
+
+  // survivors -> exact fp64 scores -> per-query buffers (all threads; clears the list)
+  auto flush = [&]() {
+    const int ns = s_nsurv;
+    for (int b0 = 0; b0 < ns; b0 += 256) {
+      for (int e = b0 + warp; e < min(ns, b0 + 256); e += kExWarps) {
+        const uint2 sv = s_surv[e];
+        const int i = (int)sv.y;
+        const double v = ex_exact<VEC4>(a, s_q + i * dpad, s_qq[i], (int32_t)sv.x);
+        if (lane == 0 && v >= s_thr[i]) {
+          const int p = atomicAdd(&s_cnt[i], 1);
+          s_key[i * kExCap + p] = v;
+          s_id[i * kExCap + p] = (int32_t)sv.x;
+        }
+      }
+      __syncthreads();
+      if (warp < QG && s_cnt[warp] > kExCap - 256) {   // room for the next batch
+        int c = s_cnt[warp];
+        ex_compact(s_key + warp * kExCap, s_id + warp * kExCap, c, a.k);
+        if (lane == 0) {
+          s_cnt[warp] = c;
+          if (c >= a.k) s_thr[warp] = fmax(s_thr[warp], s_key[warp * kExCap + a.k - 1]);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_nsurv = 0;
+    __syncthreads();
+  };
+
   for (int64_t item = blockIdx.x; item < ngroups * R; item += gridDim.x) {
     const int64_t g = item / R, r = item - g * R;
     const int nq = (int)std::min<int64_t>(QG, U - g * QG);
@@ -119,137 +212,110 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
       }
     }
     __syncthreads();
-    if (tid < nq) {
-      const int64_t j = s_qid[tid];
-      s_cnt[tid] = 0;
-      const double skv = a.sk[j];
-      // (fp64 sums in another order than finalize's: a slack of 2^-40 of the scale)
-      s_thr[tid] = skv - 0x1p-40 * (fabs(skv) + a.xmax * a.xmax + 1e-300);
+    for (int i = tid; i < QG * dpad; i += kExThreads) {
+      const int qi = i / dpad, t = i - qi * dpad;
+      s_q[i] = (qi < nq && t < a.d) ? __ldg(a.Q + s_qid[qi] * a.d + t) : 0.f;
     }
-    if (a.q_smem)
-      for (int i = tid; i < nq * a.d; i += kExThreads) {
-        const int qi = i / a.d;
-        s_q[i] = __ldg(a.Q + s_qid[qi] * a.d + (i - qi * a.d));
-      }
+    if (tid == 0) s_nsurv = 0;
     __syncthreads();
-    if (warp < nq) {   // |q|^2 (COS)
-      const float *qv = a.Q + s_qid[warp] * a.d;
+    if (warp < QG) {   // |q|^2, thresholds
       double qq = 0.0;
-      for (int t = lane; t < a.d; t += 32) qq += (double)__ldg(qv + t) * (double)__ldg(qv + t);
+      for (int t = lane; t < a.d; t += 32) qq += (double)s_q[warp * dpad + t] * (double)s_q[warp * dpad + t];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
-      if (lane == 0) s_qq[warp] = qq;
+      if (lane == 0) {
+        s_qq[warp] = qq;
+        s_cnt[warp] = 0;
+        if (warp < nq) {
+          const double skv = a.sk[s_qid[warp]], qn = sqrt(qq);
+          // exact stage: finalize's k-th sort key, less a slack for fp64 sums in another order
+          s_thr[warp] = skv - 0x1p-40 * (fabs(skv) + (qn + a.xmax) * (qn + a.xmax));
+          // filter: the fp32 key of a row scoring >= s_k is >= s_k (natural units) - E32
+          const double nat = a.metric == VRS_L2 ? qq + skv : (a.metric == VRS_COSINE ? skv * qn : skv);
+          s_thr32[warp] = __double2float_rd(nat - key_error_bound(kb32, a.metric, qn, 0.0));
+        } else {
+          s_thr[warp] = INFINITY;
+          s_thr32[warp] = INFINITY;
+        }
+      }
     }
     __syncthreads();
-    const float *qbase[kExQG];
-#pragma unroll
-    for (int i = 0; i < kExQG; ++i)
-      qbase[i] = i < nq ? (a.q_smem ? s_q + i * a.d : a.Q + s_qid[i] * a.d) : (a.q_smem ? s_q : a.Q + s_qid[0] * a.d);
-    // ---- this split's rows, 2 per warp per step
+    // ---- filter: this split's rows, 256 per block step, one per lane
     const int64_t r0 = n_space * r / R, r1 = n_space * (r + 1) / R;
-    for (int64_t b0 = r0; b0 < r1; b0 += 2 * kExWarps) {
-      double acc[2][kExQG], xx[2];
-      int32_t rid[2];
+    for (int64_t b0 = r0; b0 < r1; b0 += kExThreads) {
+      const int64_t pos = b0 + warp * 32 + lane;
+      const int32_t myid = pos < r1 ? (a.ids ? __ldg(a.ids + pos) : (int32_t)pos) : -1;
+      auto issue = [&](int kc) {
+        float *buf = wst + (kc % kExStages) * 32 * kExPad;
+        if (VEC4) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t pos = b0 + 2 * warp + h;
-        rid[h] = pos < r1 ? (a.ids ? __ldg(a.ids + pos) : (int32_t)pos) : -1;
-        xx[h] = 0.0;
-#pragma unroll
-        for (int i = 0; i < kExQG; ++i) acc[h][i] = 0.0;
-      }
-      if (VEC) {
-        for (int t = 4 * lane; t < a.d; t += 128) {
-          float4 xv[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            xv[h] = rid[h] >= 0 ? __ldg(reinterpret_cast<const float4 *>(a.X + (int64_t)rid[h] * a.d + t))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int i = 0; i < kExQG; ++i) {
-            if (i >= nq) break;
-            const float4 qv = *reinterpret_cast<const float4 *>(qbase[i] + t);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (a.metric == VRS_L2) {
-                const double d0 = (double)qv.x - xv[h].x, d1 = (double)qv.y - xv[h].y, d2 = (double)qv.z - xv[h].z,
-                             d3 = (double)qv.w - xv[h].w;
-                acc[h][i] += d0 * d0; acc[h][i] += d1 * d1; acc[h][i] += d2 * d2; acc[h][i] += d3 * d3;
-              } else {
-                acc[h][i] += (double)qv.x * xv[h].x; acc[h][i] += (double)qv.y * xv[h].y;
-                acc[h][i] += (double)qv.z * xv[h].z; acc[h][i] += (double)qv.w * xv[h].w;
-              }
+          for (int h = 0; h < 4; ++h) {   // 32 rows x 4 x 16 B: lane -> (row lane/4 + 8h, part lane % 4)
+            const int rr = (lane >> 2) + 8 * h, part = lane & 3;
+            const int32_t idr = __shfl_sync(0xffffffffu, myid, rr);
+            const int col = kc * kExKC + part * 4;
+            const bool ok = idr >= 0 && col < a.d;
+            cp_async16(buf + rr * kExPad + part * 4, ok ? (const void *)(a.X + (int64_t)idr * a.d + col) : a.X, ok);
+          }
+        } else {
+#pragma unroll 4
+          for (int rr = 0; rr < 32; ++rr) {
+            const int32_t idr = __shfl_sync(0xffffffffu, myid, rr);
+            for (int c = lane; c < kExKC; c += 32) {
+              const int col = kc * kExKC + c;
+              const bool ok = idr >= 0 && col < a.d;
+              cp_async4(buf + rr * kExPad + c, ok ? (const void *)(a.X + (int64_t)idr * a.d + col) : a.X, ok);
             }
           }
-          if (a.metric == VRS_COSINE)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              xx[h] += (double)xv[h].x * xv[h].x + (double)xv[h].y * xv[h].y + (double)xv[h].z * xv[h].z +
-                       (double)xv[h].w * xv[h].w;
         }
-      } else {
-        for (int t = lane; t < a.d; t += 32) {
-          double xv[2];
+        cp_async_commit();
+      };
+      float acc[QG];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) xv[h] = rid[h] >= 0 ? (double)__ldg(a.X + (int64_t)rid[h] * a.d + t) : 0.0;
+      for (int i = 0; i < QG; ++i) acc[i] = 0.f;
+      issue(0);
+      for (int kc = 0; kc < nk; ++kc) {
+        if (kc + 1 < nk) issue(kc + 1);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const float *xb = wst + (kc % kExStages) * 32 * kExPad + lane * kExPad;
+        const float *qk = s_q + kc * kExKC;
 #pragma unroll
-          for (int i = 0; i < kExQG; ++i) {
-            if (i >= nq) break;
-            const double qv = qbase[i][t];
+        for (int c4 = 0; c4 < kExKC / 4; ++c4) {
+          const float4 xv = *reinterpret_cast<const float4 *>(xb + c4 * 4);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (a.metric == VRS_L2) { const double df = qv - xv[h]; acc[h][i] += df * df; }
-              else acc[h][i] += qv * xv[h];
-            }
+          for (int i = 0; i < QG; ++i) {   // sequential in t: the KEY_FP32 bound's accumulation model
+            const float4 qv = *reinterpret_cast<const float4 *>(qk + i * dpad + c4 * 4);
+            acc[i] = fmaf(xv.x, qv.x, acc[i]);
+            acc[i] = fmaf(xv.y, qv.y, acc[i]);
+            acc[i] = fmaf(xv.z, qv.z, acc[i]);
+            acc[i] = fmaf(xv.w, qv.w, acc[i]);
           }
-          if (a.metric == VRS_COSINE)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) xx[h] += xv[h] * xv[h];
         }
+        __syncwarp();
       }
+      cp_async_wait<0>();
+      if (myid >= 0) {
+        const float nx2 = a.metric == VRS_L2 ? __ldg(a.nx2 + myid) : 0.f;
+        const float inx = a.metric == VRS_COSINE ? __ldg(a.inv_nx + myid) : 0.f;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double tot = warp_sum_transpose<kExQG>(acc[h]);   // lane: query (lane >> 2) & 7
-        double xt = xx[h];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) xt += __shfl_xor_sync(0xffffffffu, xt, o);
-        const int i = (lane >> 2) & 7;
-        if ((lane & 3) == 0 && i < nq && rid[h] >= 0) {
-          double v = tot;
-          if (a.metric == VRS_L2) v = -v;
-          else if (a.metric == VRS_COSINE) v = s_qq[i] > 0.0 ? v / (sqrt(s_qq[i]) * sqrt(xt)) : -INFINITY;
-          if (v >= s_thr[i]) {
-            const int p = atomicAdd(&s_cnt[i], 1);
-            s_key[i * kExCap + p] = v;
-            s_id[i * kExCap + p] = rid[h];
+        for (int i = 0; i < QG; ++i) {
+          const float key = rank_key(a.metric, acc[i], nx2, inx);
+          if (key >= s_thr32[i]) {
+            const int p = atomicAdd(&s_nsurv, 1);
+            s_surv[p] = make_uint2((uint32_t)myid, (uint32_t)i);
           }
         }
       }
       __syncthreads();
-      // make room for the next step's <= 2 * kExWarps appends per query
-      if (tid == 0) {
-        int full = 0;
-        for (int i = 0; i < nq; ++i) full |= s_cnt[i] > kExCap - 2 * kExWarps;
-        s_full = full;
-      }
-      __syncthreads();
-      if (s_full) {
-        if (warp < nq && s_cnt[warp] > kExCap - 2 * kExWarps) {
-          int c = s_cnt[warp];
-          ex_compact(s_key + warp * kExCap, s_id + warp * kExCap, c, a.k);
-          if (lane == 0) {
-            s_cnt[warp] = c;
-            if (c >= a.k) s_thr[warp] = fmax(s_thr[warp], s_key[warp * kExCap + a.k - 1]);
-          }
-        }
-        __syncthreads();
-      }
+      if (s_nsurv >= kExSurv / 2) flush();   // (a step adds <= 256 * QG <= kExSurv / 2)
     }
+    flush();
     // ---- this split's k best per query -> its slot
     if (warp < nq) {
       int c = s_cnt[warp];
       ex_compact(s_key + warp * kExCap, s_id + warp * kExCap, c, a.k);
-      const int64_t so = (item * a.qg + warp);
+      const int64_t so = item * a.qg + warp;
       for (int e = lane; e < c; e += 32) {
         a.slot_key[so * a.k + e] = s_key[warp * kExCap + e];
         a.slot_id[so * a.k + e] = s_id[warp * kExCap + e];
@@ -268,7 +334,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
       int64_t *bi = s_id + warp * kExCap;
       int c = 0;
       for (int64_t rr = 0; rr < R; ++rr) {
-        const int64_t so = ((g * R + rr) * a.qg + warp);
+        const int64_t so = (g * R + rr) * a.qg + warp;
         const int sc = __ldcg(a.slot_cnt + so);
         if (c + sc > kExCap) ex_compact(bk, bi, c, a.k);
         for (int e = lane; e < sc; e += 32) {
@@ -295,15 +361,27 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
   }
 }
 
-cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches) {
-  const bool vec = (a.d % 4 == 0) && (((uintptr_t)a.X | (uintptr_t)a.Q) % 16 == 0);
-  const size_t smem = (size_t)kExQG * kExCap * 16 + (a.q_smem ? (size_t)a.qg * a.d * 4 : 0);
+template <int QG>
+static cudaError_t launch_exact_qg(const ExactArgs &a, bool vec, size_t smem, cudaStream_t s) {
   static size_t attr[2] = {0, 0};
-  auto kern = vec ? exact_fallback_kernel<true> : exact_fallback_kernel<false>;
+  auto kern = vec ? exact_fallback_kernel<QG, true> : exact_fallback_kernel<QG, false>;
   const cudaError_t e = ensure_smem_attr(kern, smem, attr[vec ? 1 : 0]);
   if (e != cudaSuccess) return e;
-  if (launches) *launches += 1;
   return launch_k(kern, dim3(kExGrid), dim3(kExThreads), smem, s, a);
+}
+
+cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches) {
+  const bool vec = (a.d % 4 == 0) && (((uintptr_t)a.X | (uintptr_t)a.Q) % 16 == 0);
+  const int dpad = (a.d + kExKC - 1) / kExKC * kExKC;
+  const size_t smem = exact_smem_bytes(a.qg, dpad);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;   // (d beyond ~40k)
+  if (launches) *launches += 1;
+  switch (a.qg) {
+    case 1: return launch_exact_qg<1>(a, vec, smem, s);
+    case 2: return launch_exact_qg<2>(a, vec, smem, s);
+    case 4: return launch_exact_qg<4>(a, vec, smem, s);
+    default: return launch_exact_qg<8>(a, vec, smem, s);
+  }
 }
 
 }  // namespace vrs

@@ -571,8 +571,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // certificate + exact fallback: per query the exponent / residual of
   // the 16-bit operand, the certificate, finalize's k-th sort key, a group counter; the
   // fallback's per-(item, query) slots of k results
-  int ex_qsmem = 0;
-  const int ex_qg = exact_group_size(d, &ex_qsmem);
+  const int ex_qg = exact_group_size(d);
   const int64_t ex_items = exact_items_max(q, ex_qg);
   const size_t ex_slots = (size_t)ex_items * ex_qg;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
@@ -668,7 +667,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   static const bool no_fallback = getenv("VRS_NO_FALLBACK") != nullptr;   // (A/B timing only: results unverified)
   if (!no_fallback) {
     ExactArgs ea{cert, skey, gcnt, ix->X, d, n, identity ? nullptr : sel_ids, count, queries, q, (int32_t)metric, k,
-                 ix->row_offset, (double)ix->xmax, ids, dists, slot_key, slot_id, slot_cnt, ex_qg, ex_qsmem};
+                 ix->row_offset, (double)ix->xmax, ix->nx2, ix->inv_nx, ids, dists, slot_key, slot_id, slot_cnt, ex_qg};
     ProfScope ps("exact", stream);
     CUDA_TRY(launch_exact(ea, stream, &launches));
   }

@@ -227,15 +227,16 @@ struct ExactArgs {
   int32_t k;
   int64_t row_offset;
   double xmax;
+  const float *nx2;        // the index's |x|^2 and 1/|x| (the fp32 filter keys)
+  const float *inv_nx;
   int64_t *out_ids;        // [q][k] (overwritten for the uncertified queries)
   float *out_dists;
   double *slot_key;        // [items_max][qg][k]
   int64_t *slot_id;
   int32_t *slot_cnt;       // [items_max][qg]
-  int32_t qg;              // queries per group (<= 8)
-  int32_t q_smem;          // 1: the group's queries staged in shared memory
+  int32_t qg;              // queries per group (1, 2, 4 or 8)
 };
-int exact_group_size(int32_t d, int *q_smem);
+int exact_group_size(int32_t d);
 int64_t exact_items_max(int64_t q, int qg);
 cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches);
 
