@@ -36,25 +36,30 @@ namespace vrs {
 
 constexpr int kExWarps = 8;
 constexpr int kExThreads = kExWarps * 32;
-constexpr int kExCap = 512;     // exact-scored rows buffered per query (>= k + 256 per flush batch)
+constexpr int kExBatch = 64;    // survivors exact-scored between buffer checks (buffer: pow2 >= k + kExBatch)
 constexpr int kExGrid = 148;    // one CTA per SM
 constexpr int kExKC = 16;       // fp32 columns per staged chunk
 constexpr int kExPad = kExKC + 4;
 constexpr int kExStages = 2;
-constexpr int kExSurv = 4096;   // survivor list; flushed once it holds >= kExSurv / 2
-constexpr int kExQMax = 8;
+constexpr int kExSurv = 8192;   // survivor list; flushed before a step could overflow it
+constexpr int kExQMax = 16;
 
-__host__ __device__ constexpr size_t exact_smem_bytes(int qg, int dpad) {
-  return (size_t)qg * kExCap * 16                              // exact buffers (key, id)
+__host__ __device__ constexpr int exact_cap(int k) {
+  int c = 128;
+  while (c < k + kExBatch) c <<= 1;
+  return c;
+}
+__host__ __device__ constexpr size_t exact_smem_bytes(int qg, int dpad, int cap) {
+  return (size_t)qg * cap * 16                                 // exact buffers (key, id)
          + (size_t)kExWarps * kExStages * 32 * kExPad * 4      // row stages
          + (size_t)kExSurv * 8                                 // survivors (row, query slot)
          + (size_t)qg * dpad * 4;                              // queries
 }
 
-int exact_group_size(int32_t d) {
+int exact_group_size(int32_t d, int32_t k) {
   const int dpad = (d + kExKC - 1) / kExKC * kExKC;
   int qg = kExQMax;
-  while (qg > 1 && exact_smem_bytes(qg, dpad) > 200 * 1024) qg >>= 1;
+  while (qg > 1 && exact_smem_bytes(qg, dpad, exact_cap(k)) > 200 * 1024) qg >>= 1;
   return qg;
 }
 int64_t exact_items_max(int64_t q, int qg) { return std::max<int64_t>(4 * kExGrid, (q + qg - 1) / qg); }
@@ -78,11 +83,11 @@ __device__ void ex_sort_desc(double *key, int64_t *id, int n) {
   __syncwarp();
 }
 
-// one warp: sort the query's buffer and keep its k best (count -> min(count, k))
-__device__ void ex_compact(double *key, int64_t *id, int &cnt, int k) {
+// one warp: sort the query's buffer (cap entries, a power of two) and keep its k best
+__device__ void ex_compact(double *key, int64_t *id, int &cnt, int k, int cap) {
   const int lane = threadIdx.x & 31;
-  for (int i = cnt + lane; i < kExCap; i += 32) { key[i] = -INFINITY; id[i] = INT64_MAX; }
-  ex_sort_desc(key, id, kExCap);
+  for (int i = cnt + lane; i < cap; i += 32) { key[i] = -INFINITY; id[i] = INT64_MAX; }
+  ex_sort_desc(key, id, cap);
   cnt = min(cnt, k);
 }
 
@@ -126,9 +131,10 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
   extern __shared__ __align__(16) uint8_t ex_smem[];
   const int dpad = (a.d + kExKC - 1) / kExKC * kExKC;
   const int nk = dpad / kExKC;
-  double *s_key = reinterpret_cast<double *>(ex_smem);                       // [QG][kExCap]
-  int64_t *s_id = reinterpret_cast<int64_t *>(s_key + QG * kExCap);           // [QG][kExCap]
-  float *s_stage = reinterpret_cast<float *>(s_id + QG * kExCap);             // [warps][stages][32][kExPad]
+  const int cap = exact_cap(a.k);
+  double *s_key = reinterpret_cast<double *>(ex_smem);                       // [QG][cap]
+  int64_t *s_id = reinterpret_cast<int64_t *>(s_key + QG * cap);              // [QG][cap]
+  float *s_stage = reinterpret_cast<float *>(s_id + QG * cap);                // [warps][stages][32][kExPad]
   uint2 *s_surv = reinterpret_cast<uint2 *>(s_stage + kExWarps * kExStages * 32 * kExPad);   // (row, slot)
   float *s_q = reinterpret_cast<float *>(s_surv + kExSurv);                   // [QG][dpad]
   __shared__ int s_cnt[QG], s_nsurv;
@@ -162,26 +168,27 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
   // survivors -> exact fp64 scores -> per-query buffers (all threads; clears the list)
   auto flush = [&]() {
     const int ns = s_nsurv;
-    for (int b0 = 0; b0 < ns; b0 += 256) {
-      for (int e = b0 + warp; e < min(ns, b0 + 256); e += kExWarps) {
+    for (int b0 = 0; b0 < ns; b0 += kExBatch) {
+      for (int e = b0 + warp; e < min(ns, b0 + kExBatch); e += kExWarps) {
         const uint2 sv = s_surv[e];
         const int i = (int)sv.y;
         const double v = ex_exact<VEC4>(a, s_q + i * dpad, s_qq[i], (int32_t)sv.x);
         if (lane == 0 && v >= s_thr[i]) {
           const int p = atomicAdd(&s_cnt[i], 1);
-          s_key[i * kExCap + p] = v;
-          s_id[i * kExCap + p] = (int32_t)sv.x;
+          s_key[i * cap + p] = v;
+          s_id[i * cap + p] = (int32_t)sv.x;
         }
       }
       __syncthreads();
-      if (warp < QG && s_cnt[warp] > kExCap - 256) {   // room for the next batch
-        int c = s_cnt[warp];
-        ex_compact(s_key + warp * kExCap, s_id + warp * kExCap, c, a.k);
-        if (lane == 0) {
-          s_cnt[warp] = c;
-          if (c >= a.k) s_thr[warp] = fmax(s_thr[warp], s_key[warp * kExCap + a.k - 1]);
+      for (int w = warp; w < QG; w += kExWarps)   // room for the next batch
+        if (s_cnt[w] > cap - kExBatch) {
+          int c = s_cnt[w];
+          ex_compact(s_key + w * cap, s_id + w * cap, c, a.k, cap);
+          if (lane == 0) {
+            s_cnt[w] = c;
+            if (c >= a.k) s_thr[w] = fmax(s_thr[w], s_key[w * cap + a.k - 1]);
+          }
         }
-      }
       __syncthreads();
     }
     if (tid == 0) s_nsurv = 0;
@@ -218,24 +225,24 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
     }
     if (tid == 0) s_nsurv = 0;
     __syncthreads();
-    if (warp < QG) {   // |q|^2, thresholds
+    for (int w = warp; w < QG; w += kExWarps) {   // |q|^2, thresholds
       double qq = 0.0;
-      for (int t = lane; t < a.d; t += 32) qq += (double)s_q[warp * dpad + t] * (double)s_q[warp * dpad + t];
+      for (int t = lane; t < a.d; t += 32) qq += (double)s_q[w * dpad + t] * (double)s_q[w * dpad + t];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
       if (lane == 0) {
-        s_qq[warp] = qq;
-        s_cnt[warp] = 0;
-        if (warp < nq) {
-          const double skv = a.sk[s_qid[warp]], qn = sqrt(qq);
+        s_qq[w] = qq;
+        s_cnt[w] = 0;
+        if (w < nq) {
+          const double skv = a.sk[s_qid[w]], qn = sqrt(qq);
           // exact stage: finalize's k-th sort key, less a slack for fp64 sums in another order
-          s_thr[warp] = skv - 0x1p-40 * (fabs(skv) + (qn + a.xmax) * (qn + a.xmax));
+          s_thr[w] = skv - 0x1p-40 * (fabs(skv) + (qn + a.xmax) * (qn + a.xmax));
           // filter: the fp32 key of a row scoring >= s_k is >= s_k (natural units) - E32
           const double nat = a.metric == VRS_L2 ? qq + skv : (a.metric == VRS_COSINE ? skv * qn : skv);
-          s_thr32[warp] = __double2float_rd(nat - key_error_bound(kb32, a.metric, qn, 0.0));
+          s_thr32[w] = __double2float_rd(nat - key_error_bound(kb32, a.metric, qn, 0.0));
         } else {
-          s_thr[warp] = INFINITY;
-          s_thr32[warp] = INFINITY;
+          s_thr[w] = INFINITY;
+          s_thr32[w] = INFINITY;
         }
       }
     }
@@ -308,17 +315,17 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
         }
       }
       __syncthreads();
-      if (s_nsurv >= kExSurv / 2) flush();   // (a step adds <= 256 * QG <= kExSurv / 2)
+      if (s_nsurv > kExSurv - kExThreads * QG) flush();   // (a step adds <= 256 * QG)
     }
     flush();
     // ---- this split's k best per query -> its slot
-    if (warp < nq) {
-      int c = s_cnt[warp];
-      ex_compact(s_key + warp * kExCap, s_id + warp * kExCap, c, a.k);
-      const int64_t so = item * a.qg + warp;
+    for (int w = warp; w < nq; w += kExWarps) {
+      int c = s_cnt[w];
+      ex_compact(s_key + w * cap, s_id + w * cap, c, a.k, cap);
+      const int64_t so = item * a.qg + w;
       for (int e = lane; e < c; e += 32) {
-        a.slot_key[so * a.k + e] = s_key[warp * kExCap + e];
-        a.slot_id[so * a.k + e] = s_id[warp * kExCap + e];
+        a.slot_key[so * a.k + e] = s_key[w * cap + e];
+        a.slot_id[so * a.k + e] = s_id[w * cap + e];
       }
       if (lane == 0) a.slot_cnt[so] = c;
     }
@@ -329,14 +336,14 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
     if (!s_last) continue;
     __threadfence();
     // ---- the group's last split: merge every split's slot, write the k best
-    if (warp < nq) {
-      double *bk = s_key + warp * kExCap;
-      int64_t *bi = s_id + warp * kExCap;
+    for (int w = warp; w < nq; w += kExWarps) {
+      double *bk = s_key + w * cap;
+      int64_t *bi = s_id + w * cap;
       int c = 0;
       for (int64_t rr = 0; rr < R; ++rr) {
-        const int64_t so = (g * R + rr) * a.qg + warp;
+        const int64_t so = (g * R + rr) * a.qg + w;
         const int sc = __ldcg(a.slot_cnt + so);
-        if (c + sc > kExCap) ex_compact(bk, bi, c, a.k);
+        if (c + sc > cap) ex_compact(bk, bi, c, a.k, cap);
         for (int e = lane; e < sc; e += 32) {
           bk[c + e] = __ldcg(a.slot_key + so * a.k + e);
           bi[c + e] = __ldcg(a.slot_id + so * a.k + e);
@@ -344,8 +351,8 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
         c += sc;
         __syncwarp();
       }
-      ex_compact(bk, bi, c, a.k);
-      const int64_t j = s_qid[warp];
+      ex_compact(bk, bi, c, a.k, cap);
+      const int64_t j = s_qid[w];
       const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
       for (int e = lane; e < a.k; e += 32) {
         const int64_t o = j * a.k + e;
@@ -373,14 +380,15 @@ static cudaError_t launch_exact_qg(const ExactArgs &a, bool vec, size_t smem, cu
 cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches) {
   const bool vec = (a.d % 4 == 0) && (((uintptr_t)a.X | (uintptr_t)a.Q) % 16 == 0);
   const int dpad = (a.d + kExKC - 1) / kExKC * kExKC;
-  const size_t smem = exact_smem_bytes(a.qg, dpad);
+  const size_t smem = exact_smem_bytes(a.qg, dpad, exact_cap(a.k));
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;   // (d beyond ~40k)
   if (launches) *launches += 1;
   switch (a.qg) {
     case 1: return launch_exact_qg<1>(a, vec, smem, s);
     case 2: return launch_exact_qg<2>(a, vec, smem, s);
     case 4: return launch_exact_qg<4>(a, vec, smem, s);
-    default: return launch_exact_qg<8>(a, vec, smem, s);
+    case 8: return launch_exact_qg<8>(a, vec, smem, s);
+    default: return launch_exact_qg<16>(a, vec, smem, s);
   }
 }
 

@@ -571,7 +571,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // certificate + exact fallback: per query the exponent / residual of
   // the 16-bit operand, the certificate, finalize's k-th sort key, a group counter; the
   // fallback's per-(item, query) slots of k results
-  const int ex_qg = exact_group_size(d);
+  const int ex_qg = exact_group_size(d, k);
   const int64_t ex_items = exact_items_max(q, ex_qg);
   const size_t ex_slots = (size_t)ex_items * ex_qg;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),

@@ -234,9 +234,9 @@ struct ExactArgs {
   double *slot_key;        // [items_max][qg][k]
   int64_t *slot_id;
   int32_t *slot_cnt;       // [items_max][qg]
-  int32_t qg;              // queries per group (1, 2, 4 or 8)
+  int32_t qg;              // queries per group (1, 2, 4, 8 or 16)
 };
-int exact_group_size(int32_t d);
+int exact_group_size(int32_t d, int32_t k);
 int64_t exact_items_max(int64_t q, int qg);
 cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches);
 
