@@ -9,7 +9,7 @@ import sys
 OURS = ("select_count_kernel", "select_scatter_kernel", "gather_copy_kernel", "f32_to_bf16_kernel", "tc_topk_kernel",
         "threshold_kernel", "threshold_warp_kernel", "threshold_union_kernel", "finalize_warp_kernel", "finalize_cta_kernel", "scan_topk_kernel",
         "merge_kernel", "norms_kernel", "range_threshold_kernel", "range_prefix_kernel", "range_verify_kernel",
-        "range_write_kernel")
+        "range_write_kernel", "exact_fallback_kernel", "shadow_kernel", "query16_kernel", "select_finish_kernel")
 
 
 def short(name):
@@ -27,7 +27,7 @@ def short(name):
     targs = re.search(r"<(.*)>", name)
     name = re.sub(r"<.*", "", name).replace("void ", "")
     name = name.split("::")[-1].strip()
-    if mine and targs and ("finalize" in name or "threshold" in name):   # template variants, e.g. <256, 64>
+    if mine and targs and ("finalize" in name or "threshold" in name or "exact" in name):   # template variants, e.g. <256, 64>
         name += "<" + targs.group(1) + ">"
     return ("vrs::" + name) if mine else name
 
