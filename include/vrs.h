@@ -99,8 +99,11 @@ typedef struct {
   const vrs_clause *clauses;
 } vrs_predicate;
 
-/* Optional stream-ordered allocator for the library's own device memory
- * (norms at load, per-call scratch).  NULL => cudaMallocAsync / cudaFreeAsync. */
+/* Optional stream-ordered allocator for ALL of the library's own device memory (norms and
+ * shadow at load, per-call scratch on the call's stream, vrs_search_host staging with
+ * stream NULL).  NULL => cudaMalloc / cudaMallocAsync + cudaFreeAsync.  alloc returning
+ * NULL makes the call fail with VRS_ENOMEM.  The Python binding passes torch's caching
+ * allocator. */
 typedef struct {
   void *(*alloc)(size_t bytes, void *cuda_stream, void *ctx);
   void (*free)(void *ptr, void *cuda_stream, void *ctx);
@@ -301,6 +304,11 @@ VRS_API int32_t vrs_last_launches(void);
 VRS_API void vrs_profile_enable(int32_t on);
 VRS_API int32_t vrs_profile_read(int32_t i, const char **name, double *total_ms, int64_t *launches);
 VRS_API void vrs_profile_reset(void);
+
+/* Bytes the library's own stream-ordered pool (cudaMallocAsync, used for per-call scratch
+ * when the index has no allocator) currently reserves on the current device; it keeps at
+ * most 2 GiB of freed scratch cached and releases the rest at synchronisation.  -1 on error. */
+VRS_API int64_t vrs_pool_reserved_bytes(void);
 
 /* Loaded index properties. */
 VRS_API int64_t vrs_index_rows(const vrs_index *ix);

@@ -19,7 +19,7 @@ from ._lib import (ATTR_I32, ATTR_U8, COSINE, EXPORTS, IP, K_MAX, L2, PATH_AUTO,
 
 __all__ = ["Index", "merge", "VrsError", "L2", "IP", "COSINE", "PATH_AUTO", "PATH_SCAN", "PATH_GEMM",
            "ROWS_AUTO", "ROWS_GATHER", "ROWS_MASKED", "PREC_DEFAULT", "PREC_TF32", "PREC_BF16", "PREC_FP16", "K_MAX",
-           "last_path", "new_stats",
+           "last_path", "new_stats", "read_stats", "pool_reserved_bytes",
            "last_precision", "last_launches", "library"]
 
 METRICS = {"l2": L2, "ip": IP, "cos": COSINE, "cosine": COSINE}
@@ -88,6 +88,31 @@ def read_stats(stats: torch.Tensor) -> dict:
             "max_key_error_over_bound": ratio}
 
 
+def _torch_allocator():
+    """vrs_allocator backed by torch's caching allocator (SURVEY 8(b) "Ownership": the index's
+    derived data and every call's scratch come from torch's pool; a failed allocation makes the
+    call return VRS_ENOMEM).  Blocks are tied to the stream they are allocated on, so a block
+    freed right after the call's kernels were enqueued is reused only in stream order."""
+    def alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+        except Exception:   # noqa: BLE001 -- out of memory: NULL -> VRS_ENOMEM
+            return None
+
+    def free(ptr, stream, ctx):
+        if ptr:
+            torch.cuda.caching_allocator_delete(ptr)
+
+    a = _lib.Allocator(_lib.ALLOC_FN(alloc), _lib.FREE_FN(free), None)
+    return a
+
+
+def pool_reserved_bytes() -> int:
+    """Bytes libvrs's own cudaMallocAsync pool reserves on the current device (0 when every
+    index uses the torch allocator)."""
+    return int(library().vrs_pool_reserved_bytes())
+
+
 def _check_queries(queries: torch.Tensor, d: int, device, host: bool = False):
     if not isinstance(queries, torch.Tensor) or queries.dtype != torch.float32 or queries.dim() != 2:
         raise ValueError("queries must be a float32 [q, d] tensor")
@@ -147,7 +172,11 @@ class Index:
     """vrs_load over one (shard of a) relation: fp32 vectors [n, d] and
     int32 / uint8 attribute columns, all CUDA tensors (borrowed, kept alive here)."""
 
-    def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None, precision=None):
+    def __init__(self, vectors: torch.Tensor, attrs=(), row_offset: int = 0, stream=None, precision=None,
+                 allocator="torch"):
+        """allocator: "torch" (default) -- the library's own memory (norms, 16-bit shadow, per-call
+        scratch) comes from torch's caching allocator; None -- libvrs's bounded cudaMallocAsync
+        pool; or a ready _lib.Allocator (tests)."""
         lib = library()
         if vectors.dtype != torch.float32 or vectors.dim() != 2 or not vectors.is_contiguous() or not vectors.is_cuda:
             raise ValueError("vectors must be a contiguous float32 [n, d] CUDA tensor")
@@ -170,7 +199,11 @@ class Index:
         n, d = vectors.shape
         opts = _lib.LoadOptions()
         opts.precision = PREC_DEFAULT if precision is None else int(precision)
-        st = lib.vrs_load_ex(_ptr(vectors), n, d, carr, len(self.attrs), int(row_offset), None, ctypes.byref(opts),
+        if allocator == "torch":
+            allocator = _torch_allocator()
+        self._alloc = allocator   # (the callbacks must outlive the index)
+        st = lib.vrs_load_ex(_ptr(vectors), n, d, carr, len(self.attrs), int(row_offset),
+                             ctypes.byref(allocator) if allocator is not None else None, ctypes.byref(opts),
                              _stream(stream), ctypes.byref(h))
         _lib.check(st, "vrs_load_ex")
         self.precision = int(lib.vrs_index_precision(h))

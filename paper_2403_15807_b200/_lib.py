@@ -28,7 +28,7 @@ MAX_CLAUSES = 8
 # every symbol include/vrs.h declares (tests check the library exports them)
 EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_host_fence", "vrs_select", "vrs_merge", "vrs_free",
            "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
-           "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset")
+           "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset", "vrs_pool_reserved_bytes")
 
 
 class VrsError(RuntimeError):
@@ -50,8 +50,12 @@ class Predicate(ctypes.Structure):
     _fields_ = [("n_clauses", ctypes.c_int32), ("clauses", ctypes.POINTER(Clause))]
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Allocator(ctypes.Structure):
-    _fields_ = [("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("ctx", ctypes.c_void_p)]
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("ctx", ctypes.c_void_p)]
 
 
 class SearchOptions(ctypes.Structure):
@@ -107,6 +111,7 @@ def load_library():
     lib.vrs_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(i64)]
     lib.vrs_profile_read.restype = i32
+    lib.vrs_pool_reserved_bytes.restype = i64
     _lib = lib
     return lib
 

@@ -172,6 +172,8 @@ struct Scratch {
   }
 };
 
+static constexpr uint64_t kPoolKeep = uint64_t(2) << 30;   // 2 GiB
+
 static vrs_status scratch_alloc(Scratch &s, size_t bytes) {
   // size classes of 1/8 of a power of two: consecutive searches of different
   // shapes then reuse the stream-ordered pool's blocks instead of mapping new
@@ -188,14 +190,16 @@ static vrs_status scratch_alloc(Scratch &s, size_t bytes) {
     if (!s.ptr) return fail(VRS_ENOMEM, "allocator returned NULL for %zu bytes", bytes);
     return VRS_OK;
   }
-  {  // keep freed scratch in each device's pool instead of returning it to the driver
+  {  // keep up to kPoolKeep of freed scratch in the device's pool (consecutive searches reuse
+     // it instead of mapping new memory); above that the pool returns memory to the driver at
+     // the next synchronisation -- bounded, it never holds a large gather buffer for good
     static uint64_t tuned = 0;   // bit per device
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
       std::lock_guard<std::mutex> g(setup_mutex());
       cudaMemPool_t pool;
       if (!(tuned >> dev & 1) && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
+        uint64_t thr = kPoolKeep;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         tuned |= uint64_t(1) << dev;
       }
@@ -278,6 +282,14 @@ static SelectFuse select_fuse(const vrs_index *ix, const float *queries, int64_t
   return f;
 }
 
+static void slot_release(vrs_index *ix, int i) {
+  if (!ix->slot_buf[i]) return;
+  if (ix->has_alloc) ix->alloc.free(ix->slot_buf[i], nullptr, ix->alloc.ctx);
+  else cudaFree(ix->slot_buf[i]);
+  ix->slot_buf[i] = nullptr;
+  ix->slot_cap[i] = 0;
+}
+
 // ---- ABI ----------------------------------------------------------------------------
 extern "C" {
 
@@ -308,6 +320,18 @@ int32_t vrs_last_path(void) { return g_last_path; }
 int32_t vrs_last_precision(void) { return g_last_prec; }
 int32_t vrs_index_precision(const vrs_index *ix) { return ix ? (ix->xb ? ix->prec16 : VRS_PREC_TF32) : -1; }
 int32_t vrs_last_launches(void) { return g_last_launches; }
+
+int64_t vrs_pool_reserved_bytes(void) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  uint64_t v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess ||
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return (int64_t)v;
+}
 int64_t vrs_index_rows(const vrs_index *ix) { return ix ? ix->n : -1; }
 int32_t vrs_index_dim(const vrs_index *ix) { return ix ? ix->d : -1; }
 
@@ -417,7 +441,7 @@ vrs_status vrs_free(vrs_index *ix) {
     cudaStreamSynchronize(ix->up_stream);
     cudaStreamSynchronize(ix->down_stream);
     for (int i = 0; i < vrs_index::kSlots; ++i) {
-      if (ix->slot_buf[i]) cudaFree(ix->slot_buf[i]);
+      slot_release(ix, i);
       cudaEventDestroy(ix->slot_free[i]);
       cudaEventDestroy(ix->up_done[i]);
       cudaEventDestroy(ix->comp_done[i]);
@@ -439,6 +463,19 @@ vrs_status vrs_free(vrs_index *ix) {
 static bool gather_copy_mode(int32_t) {
   static const bool direct = getenv("VRS_GATHER4") != nullptr || getenv("VRS_CPGATHER") != nullptr;
   return !direct;
+}
+
+// The materialised-selection buffer is sized for the worst case (every row up to the
+// break-even selectivity); above 1 GiB it is also capped at half the device's free
+// memory (selections that do not fit then stream masked -- the same result).
+static int64_t cap_by_free_memory(int64_t rows, int64_t row_bytes) {
+  if (rows * row_bytes <= (int64_t(1) << 30)) return rows;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return rows;
+  }
+  return std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)(fr / 2) / row_bytes));
 }
 
 static int pow2_at_least(int v) {
@@ -557,10 +594,11 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // Row delivery of a gathered selection: the X_sel copy + TMA tiles, or (one query
   // tile, large selections; decided on the device) cp.async straight from X -- gemm_tc.cu.
   const bool gather_copy = gather_copy_mode(gp.qtiles);
-  const int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
-                               ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
-                                              : gather_rows)
-                               : 0;
+  int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
+                         ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
+                                        : gather_rows)
+                         : 0;
+  if (gather_copy) xsel_cap = cap_by_free_memory(xsel_cap, row_bytes);
   const int64_t xsel_rows = gather_copy ? xsel_cap : 0;   // rows of the X_sel buffer
   // VRS_SELECT_LOCAL=1: one-kernel selection (chunk-local ids) + select_finish (count, dense
   // ids, gathered rows in one launch) instead of select_count + select_scatter + gather_copy.
@@ -849,15 +887,14 @@ vrs_status vrs_search_host(vrs_index *ix, const float *h_queries, int64_t q, int
     // so growing one at a time would stall (sync + free + malloc) on several later calls
     for (int i = 0; i < vrs_index::kSlots; ++i) {
       CUDA_TRY(cudaEventSynchronize(ix->slot_free[i]));   // (never-recorded events are complete)
-      if (ix->slot_buf[i]) cudaFree(ix->slot_buf[i]);
-      ix->slot_buf[i] = nullptr;
-      ix->slot_cap[i] = 0;
+      slot_release(ix, i);
     }
     for (int i = 0; i < vrs_index::kSlots; ++i) {
-      if (cudaMalloc(&ix->slot_buf[i], need) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(VRS_ENOMEM, "cudaMalloc(%zu) for the host-call staging failed", need);
-      }
+      void *p = nullptr;
+      if (ix->has_alloc) p = ix->alloc.alloc(need, nullptr, ix->alloc.ctx);   // (index-owned, stream-free use)
+      else if (cudaMalloc(&p, need) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
+      if (!p) return fail(VRS_ENOMEM, "allocation of %zu bytes for the host-call staging failed", need);
+      ix->slot_buf[i] = p;
       ix->slot_cap[i] = need;
     }
   }
