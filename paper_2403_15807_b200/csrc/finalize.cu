@@ -897,7 +897,7 @@ constexpr int kFinW = VRS_FIN_W;   // warps per query in the small-batch variant
 // in warp 0, which writes the k' best ids to s_buf[0] and their count to s_n[0].
 // Exact; ties -> lower id.  (Exchange through the free tail of each warp's buffer:
 // its survivors sit at [0, nw <= k').)
-template <int E>
+template <int E, int W>
 __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s_buf, int nw, int *s_n, float *s_kmin) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float k[E];
@@ -911,7 +911,7 @@ __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s
   warp_sort_e<E>(k, id);
   constexpr int X0 = kBufCap - 32 * E;
 #pragma unroll 1
-  for (int stride = kFinW / 2; stride >= 1; stride >>= 1) {
+  for (int stride = W / 2; stride >= 1; stride >>= 1) {
     if (w < 2 * stride) {
 #pragma unroll
       for (int h = 0; h < E; ++h) { s_buf[w].key[X0 + h * 32 + lane] = k[h]; s_buf[w].id[X0 + h * 32 + lane] = id[h]; }
@@ -935,13 +935,17 @@ __device__ __forceinline__ void fin_tree_merge(const FinalizeArgs &a, FinBufs *s
 }
 
 
-__global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a) {
+// W warps per query: 8, or 32 for tiny batches (each warp then sees few enough
+// candidates to skip the buffer compactions, and the re-score is 4x as wide: C4
+// s = 5 %, Q = 1 spent 104 us in the 8-warp kernel, most of it in compactions)
+template <int W>
+__global__ void __launch_bounds__(W * 32) finalize_cta_kernel(FinalizeArgs a) {
   TL_SCOPE(1);
   extern __shared__ __align__(16) uint8_t fin_dyn[];
-  FinBufs *s_buf = reinterpret_cast<FinBufs *>(fin_dyn);   // [kFinW]
+  FinBufs *s_buf = reinterpret_cast<FinBufs *>(fin_dyn);   // [W]
   __shared__ double s_sc[kFinMaxSel];
   __shared__ int64_t s_sid[kFinMaxSel];
-  __shared__ int s_n[kFinW];
+  __shared__ int s_n[W];
   __shared__ float s_kmin;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x;
@@ -951,21 +955,21 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   // each warp: its share of the lists -> its survivors (<= k', or <= 32E unsorted when
   // the tree merge follows: it sorts them anyway)
   const int keep = a.kprime <= 64 ? 64 : (a.kprime <= 128 ? 128 : -1);
-  const int nw = fin_stream(a, j, w, kFinW, s_buf[w], keep);
+  const int nw = fin_stream(a, j, w, W, s_buf[w], keep);
   if (lane == 0) s_n[w] = nw;
   __syncthreads();
   TL_STAMP(1, 2);
   if (a.kprime <= 64) {
-    fin_tree_merge<2>(a, s_buf, nw, s_n, &s_kmin);
+    fin_tree_merge<2, W>(a, s_buf, nw, s_n, &s_kmin);
   } else if (a.kprime <= 128) {
-    fin_tree_merge<4>(a, s_buf, nw, s_n, &s_kmin);
+    fin_tree_merge<4, W>(a, s_buf, nw, s_n, &s_kmin);
   } else if (w == 0) {
     // warp 0 merges the survivors of all warps into its own buffer
     const int K = a.kprime;
     FinBufs &B = s_buf[0];
     int n = nw;
     uint32_t thr = 0u;
-    for (int v = 1; v < kFinW; ++v) {
+    for (int v = 1; v < W; ++v) {
       const int nv = s_n[v];
       for (int i0 = 0; i0 < nv; i0 += 32) {
         const int i = i0 + lane;
@@ -1001,7 +1005,7 @@ __global__ void __launch_bounds__(kFinW * 32) finalize_cta_kernel(FinalizeArgs a
   const double qq = fin_qq(a, j);
   CertQ cq{0.0, 0.0, 1.0};
   if (a.cert) cq = cert_setup(a, j, qq);
-  fin_rescore<8>(a, j, s_buf[0].id, m, w, kFinW, qq, s_sc, s_sid, a.stats ? s_buf[0].key : nullptr, &cq);
+  fin_rescore<8>(a, j, s_buf[0].id, m, w, W, qq, s_sc, s_sid, a.stats ? s_buf[0].key : nullptr, &cq);
   __syncthreads();
   TL_STAMP(1, 4);
   if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid, s_kmin, &cq);
@@ -1300,8 +1304,8 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
     if (a.kth <= 64)
       return big ? launch_k(threshold_union_kernel<16, 4, 4>, dim3((unsigned)a.q), dim3(512), 0, s, a)
                  : launch_k(threshold_union_kernel<8, 4, 4>, dim3((unsigned)a.q), dim3(256), 0, s, a);
-    return big ? launch_k(threshold_union_kernel<16, 8, 8>, dim3((unsigned)a.q), dim3(512), 0, s, a)
-               : launch_k(threshold_union_kernel<8, 8, 8>, dim3((unsigned)a.q), dim3(256), 0, s, a);
+    // (E = 8: a warp's register sort is costly -- 8 warps, each lane with more values, beat 16 / 32)
+    return launch_k(threshold_union_kernel<8, 8, 8>, dim3((unsigned)a.q), dim3(256), 0, s, a);
   }
   const size_t smem = (size_t)a.nvals * 4;
   static size_t attr1024 = 0, attr256 = 0;
@@ -1316,11 +1320,30 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
   if (a.q < 4 * kSmCountB200) {
+    // (16 warps per query for <= 64 queries with k' >= 64: C4 s = 5 %, Q = 1 finalize 93 -> 48 us;
+    // k' = 32 (C2) gains nothing; 32 warps spill at 64 registers, r02_finalize_width_ab.txt)
+    static const int wide_q_env = getenv("VRS_FIN_WIDE_Q") ? atoi(getenv("VRS_FIN_WIDE_Q")) : -1;
+    const int wide_q = wide_q_env >= 0 ? wide_q_env : (a.kprime >= 64 ? 64 : 0);
+    static const int wide_w = getenv("VRS_FIN_WIDE_W") ? atoi(getenv("VRS_FIN_WIDE_W")) : 16;   // (A/B: 16 or 32)
+    if (a.q <= wide_q && wide_w == 32) {
+      const size_t smem = sizeof(FinBufs) * 32;
+      static size_t attr32 = 0;
+      const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<32>, smem, attr32);
+      if (e != cudaSuccess) return e;
+      return launch_k(finalize_cta_kernel<32>, dim3((unsigned)a.q), dim3(32 * 32), smem, s, a);
+    }
+    if (a.q <= wide_q && wide_w == 16) {
+      const size_t smem = sizeof(FinBufs) * 16;
+      static size_t attr16 = 0;
+      const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<16>, smem, attr16);
+      if (e != cudaSuccess) return e;
+      return launch_k(finalize_cta_kernel<16>, dim3((unsigned)a.q), dim3(16 * 32), smem, s, a);
+    }
     const size_t smem = sizeof(FinBufs) * kFinW;
     static size_t attr = 0;
-    const cudaError_t e = ensure_smem_attr(finalize_cta_kernel, smem, attr);
+    const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<kFinW>, smem, attr);
     if (e != cudaSuccess) return e;
-    return launch_k(finalize_cta_kernel, dim3((unsigned)a.q), dim3(kFinW * 32), smem, s, a);
+    return launch_k(finalize_cta_kernel<kFinW>, dim3((unsigned)a.q), dim3(kFinW * 32), smem, s, a);
   }
   const dim3 grid((unsigned)((a.q + kFinGroup - 1) / kFinGroup));
   if (a.kprime <= 64) return launch_k(finalize_warp_kernel<256, 64>, grid, dim3(kFinGroup * 32), 0, s, a);

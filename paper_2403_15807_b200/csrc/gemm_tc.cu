@@ -328,14 +328,12 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   //    copy (r01_s3_cp_gather_ab.txt: C3 s = 10 % Q = 1 0.95 -> 0.74 ms, small selections
   //    are faster copied);  * several query tiles: the copy (rows are re-read per tile).
   static const bool tma_gather4 = getenv("VRS_GATHER4") != nullptr;
-  static const bool no_cp = getenv("VRS_NO_CPGATHER") != nullptr;
-  static const int64_t cp_min = getenv("VRS_CP_MIN_MB") ? (int64_t)atoll(getenv("VRS_CP_MIN_MB")) << 20 : int64_t(512) << 20;
   if (g4) {
     p.g4 = tma_gather4 ? 1 : 2;
     p.cp_min_bytes = 0;
   } else {
-    p.g4 = (plan.qtiles == 1 && !no_cp) ? 2 : 0;
-    p.cp_min_bytes = p.g4 == 2 ? cp_min : INT64_MAX;
+    p.g4 = a.cp_min_bytes < INT64_MAX ? 2 : 0;
+    p.cp_min_bytes = a.cp_min_bytes;
   }
   p.xrows = xsrc;
   p.row_bytes = a.d * (bf ? 2 : 4);
@@ -401,10 +399,14 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // (large d: the main pass is MMA-bound and its epilogue has slack, so a sparser probe
     // costs the main pass nothing -- C3 Q = 1024: 13.4 -> 12.5 ms, C4 Q = 8192 s = 50 %:
     // 72 -> 68 ms at step 16; step 32 overflows C4's lists, r01_s3_probe_step_large_d.txt)
-    pp.tile_step = probe_env > 0 ? probe_env : (a.q >= 1024 ? (a.d >= 512 ? 16 : 8) : (a.q >= 64 ? tc::PROBE_STEP : 32));
+    // (d >= 512 below 1024 queries: the main pass is HBM-bound, its epilogue has slack -- the
+    // sparsest probe; C3 s = 10 %, Q = 64: the dense probe took 193 us of a 608 us search)
+    const bool hbm_bound = a.d >= 512 && a.q < 1024;
+    pp.tile_step = probe_env > 0 ? probe_env
+                                 : (a.q >= 1024 ? (a.d >= 512 ? 16 : 8) : (a.q >= 64 && !hbm_bound ? tc::PROBE_STEP : 32));
     // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
     static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
-    pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 ? 8 : 0);
+    pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 && !hbm_bound ? 8 : 0);
     // one wave: the probe's CTAs are few-tile items, so fixed per-CTA costs (prologue,
     // pipeline fill / drain) dominate over several waves -- use at most 148 / qtiles
     // splits (the same density: the step follows the main pass's span)

@@ -447,13 +447,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         uint8_t *st = b_base + stage * SSTRIDE;
         const uint32_t bdst = smem_u32(st + BOFF);
         const int64_t koff = (int64_t)kb * 128;
+        // coalesced: 8 lanes copy one row's 128-byte segment (16 B each), a warp
+        // instruction 4 whole rows; the row ids (lane j holds rows j + 32v) by shuffle
+        const int c = lane & 7;
+        const bool cvalid = koff + c * 16 < rb;
 #pragma unroll
-        for (int u = 0; u < GR; ++u) {
-          const int r = hrow + lane + 32 * u;
-          const char *src = xb + (int64_t)rid[u] * rb + koff;
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), src + c * 16, koff + c * 16 < rb);
+        for (int u = 0; u < BN / (4 * CPW); ++u) {
+          const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
+          const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
+          const int r = hrow + rl;
+          cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xb + (int64_t)id * rb + koff + c * 16, cvalid);
         }
         cpa_mbar_arrive(&full_bar[stage]);
         if (CPW == 2) asm volatile("bar.sync 1, 64;" ::: "memory");   // both producer warps registered their arrivals

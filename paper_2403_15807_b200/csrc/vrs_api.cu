@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -457,25 +458,71 @@ vrs_status vrs_free(vrs_index *ix) {
   return VRS_OK;
 }
 
-// true: an X_sel buffer is allocated (the gather copy may run; the tensor-core pass
-// decides on the device between it and cp.async, gemm_tc.cu); false: the pass always
-// fetches the rows from X by id (VRS_GATHER4: TMA gather4, VRS_CPGATHER: cp.async)
-static bool gather_copy_mode(int32_t) {
-  static const bool direct = getenv("VRS_GATHER4") != nullptr || getenv("VRS_CPGATHER") != nullptr;
-  return !direct;
-}
-
-// The materialised-selection buffer is sized for the worst case (every row up to the
-// break-even selectivity); above 1 GiB it is also capped at half the device's free
-// memory (selections that do not fit then stream masked -- the same result).
+// The X_sel copy buffer above 1 GiB is also capped at half the device's free memory
+// (selections that do not fit then stream masked -- the same result).
+// (cudaMemGetInfo costs ~100 us: its answer is reused for 50 ms per device)
 static int64_t cap_by_free_memory(int64_t rows, int64_t row_bytes) {
   if (rows * row_bytes <= (int64_t(1) << 30)) return rows;
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+  static std::mutex mu;
+  static int64_t cached_free[64];
+  static std::chrono::steady_clock::time_point when[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) {
     cudaGetLastError();
     return rows;
   }
-  return std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)(fr / 2) / row_bytes));
+  int64_t fr;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const auto now = std::chrono::steady_clock::now();
+    if (cached_free[dev] <= 0 || now - when[dev] > std::chrono::milliseconds(50)) {
+      size_t f = 0, tot = 0;
+      if (cudaMemGetInfo(&f, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return rows;
+      }
+      cached_free[dev] = (int64_t)f;
+      when[dev] = now;
+    }
+    fr = cached_free[dev];
+  }
+  return std::max<int64_t>(1, std::min<int64_t>(rows, (fr / 2) / row_bytes));
+}
+
+// ---- row delivery plan of the tensor-core pass ("Row delivery") ------
+// A selection is delivered gathered (only its rows; late materialization) iff
+// N_sel <= gather_cap -- decided on the device from the selection count -- else every
+// row streams by TMA with the unqualified ones masked.  Gathered rows reach the pass
+// either through an X_sel copy (gather_copy_kernel, then TMA tiles; 2 x the row bytes,
+// but read once per query tile) or fetched by id with coalesced cp.async straight into
+// the swizzled stages (no copy; each query tile re-reads them) -- the latter for at most
+// cp_qtiles query tiles and selections of >= cp_min_bytes.  Break-even selectivities
+// (B200 measurements, profiles/r02_rowplan_*.txt): masked rows stream at ~6.9 TB/s,
+// cp.async-gathered ones at ~5 TB/s per query tile, copied ones cost a read + write.
+struct RowPlan {
+  int64_t gather_cap;      // gathered iff N_sel <= gather_cap (0: always masked)
+  int64_t xsel_rows;       // rows of the X_sel copy buffer
+  int64_t cp_min_bytes;    // cp.async iff gathered and N_sel * row_bytes >= this (INT64_MAX: never)
+};
+static RowPlan row_plan(int64_t q, int32_t qtiles, int64_t n, int64_t row_bytes, int rows_req, bool identity) {
+  static const int cp_qtiles = getenv("VRS_CP_QTILES") ? atoi(getenv("VRS_CP_QTILES")) : 2;
+  static const int64_t cp_min = (getenv("VRS_CP_MIN_MB") ? (int64_t)atoll(getenv("VRS_CP_MIN_MB")) : 64) << 20;
+  static const double cp_frac = getenv("VRS_GATHER_CP_FRAC") ? atof(getenv("VRS_GATHER_CP_FRAC")) : 0.7;
+  static const bool direct = getenv("VRS_GATHER4") != nullptr || getenv("VRS_CPGATHER") != nullptr;
+  RowPlan r{0, 0, INT64_MAX};
+  if (identity || rows_req == VRS_ROWS_MASKED) return r;
+  const bool cp = qtiles <= cp_qtiles && getenv("VRS_NO_CPGATHER") == nullptr;
+  int64_t cap = q >= 1024 ? n * 9 / 10 : q >= 256 ? n * 9 / 20 : n / 3;
+  if (cp) cap = std::max<int64_t>(cap, (int64_t)(n * cp_frac / qtiles));
+  if (rows_req == VRS_ROWS_GATHER) cap = n;
+  r.gather_cap = cap;
+  if (direct) return r;   // (VRS_GATHER4 / VRS_CPGATHER: rows by id from X, no buffer; tc_prepare)
+  r.cp_min_bytes = cp ? cp_min : INT64_MAX;
+  int64_t buf = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes));
+  if (cp) buf = std::min<int64_t>(buf, std::max<int64_t>(1, (cp_min - 1) / row_bytes));   // copies stay below cp_min
+  r.xsel_rows = cap_by_free_memory(buf, row_bytes);
+  if (!cp) r.gather_cap = std::min(r.gather_cap, r.xsel_rows);
+  return r;
 }
 
 static int pow2_at_least(int v) {
@@ -587,19 +634,10 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // at most 16 GiB of rows.
   const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
   const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;   // bf16 queries, whole 128-row tiles
-  const int64_t gather_rows = rows_req == VRS_ROWS_GATHER ? n
-                              : q >= 1024                 ? n * 9 / 10
-                              : q >= 256                  ? n * 9 / 20
-                                                          : n / 3;
-  // Row delivery of a gathered selection: the X_sel copy + TMA tiles, or (one query
-  // tile, large selections; decided on the device) cp.async straight from X -- gemm_tc.cu.
-  const bool gather_copy = gather_copy_mode(gp.qtiles);
-  int64_t xsel_cap = (path == VRS_PATH_GEMM && !identity && rows_req != VRS_ROWS_MASKED)
-                         ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
-                                        : gather_rows)
-                         : 0;
-  if (gather_copy) xsel_cap = cap_by_free_memory(xsel_cap, row_bytes);
-  const int64_t xsel_rows = gather_copy ? xsel_cap : 0;   // rows of the X_sel buffer
+  const RowPlan rp = path == VRS_PATH_GEMM ? row_plan(q, gp.qtiles, n, row_bytes, rows_req, identity)
+                                           : RowPlan{0, 0, INT64_MAX};
+  const int64_t xsel_cap = rp.gather_cap;
+  const int64_t xsel_rows = rp.xsel_rows;   // rows of the X_sel buffer
   // VRS_SELECT_LOCAL=1: one-kernel selection (chunk-local ids) + select_finish (count, dense
   // ids, gathered rows in one launch) instead of select_count + select_scatter + gather_copy.
   // Measured: equal on C2's small cells, 10-20 % slower gathers on C5 -- so opt-in.
@@ -671,6 +709,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     a.xexp = ix->xexp;
     a.qexp = qexp;
     a.rq = rq;
+    a.cp_min_bytes = rp.cp_min_bytes;
     a.ids_local = ids_local;
     a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
     {
@@ -767,16 +806,9 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const size_t nwords = (size_t)((n + 31) / 32);
   const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
   const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;
-  const int64_t gather_rows = rows_req == VRS_ROWS_GATHER ? n
-                              : q >= 1024                 ? n * 9 / 10
-                              : q >= 256                  ? n * 9 / 20
-                                                          : n / 3;
-  const bool gather_copy = gather_copy_mode(gp.qtiles);   // (as in vrs_search_ex)
-  const int64_t xsel_cap = (!identity && rows_req != VRS_ROWS_MASKED)
-                               ? (gather_copy ? std::min<int64_t>(gather_rows, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes))
-                                              : gather_rows)
-                               : 0;
-  const int64_t xsel_rows = gather_copy ? xsel_cap : 0;
+  const RowPlan rp = row_plan(q, gp.qtiles, n, row_bytes, rows_req, identity);   // (as in vrs_search_ex)
+  const int64_t xsel_cap = rp.gather_cap;
+  const int64_t xsel_rows = rp.xsel_rows;
   const int L = kListsPerSplit * gp.P;
   Scratch scr{ix->has_alloc ? &ix->alloc : nullptr, stream};
   static const bool want_local = getenv("VRS_SELECT_LOCAL") != nullptr;   // (as in vrs_search_ex)
@@ -829,6 +861,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   a.xexp = ix->xexp;
   a.qexp = qexp;
   a.rq = rq;
+  a.cp_min_bytes = rp.cp_min_bytes;
   a.ids_local = ids_local;
   a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));

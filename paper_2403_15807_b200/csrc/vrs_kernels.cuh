@@ -122,6 +122,7 @@ struct GemmArgs {
   int32_t xexp = 0;         // the shadow's exponent e_x
   int32_t *qexp = nullptr;  // [q] per-query exponents e_q (written by the conversion)
   float *rq = nullptr;      // [q] per-query residuals |q~ - q|
+  int64_t cp_min_bytes = INT64_MAX;   // gathered selections of >= this many row bytes: cp.async by id (vrs_api row_plan)
   // launch_select_local's output (nullptr: ids / count were written by launch_select):
   // the tensor-core pass first runs select_finish -> count, dense ids, gathered rows
   const int32_t *ids_local = nullptr;
