@@ -15,6 +15,8 @@
 //
 // Roofline: HBM.  Algorithmic bytes per selected row: 4*d (vector) + 4 (id)
 // + 8 (norm terms); per call + 4*d*q (queries) + 12*q*k (results).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <float.h>
 
 #include <algorithm>
@@ -96,13 +98,18 @@ __host__ __device__ constexpr size_t scan_smem_bytes(int QG, int KPE, int dpad) 
          + (size_t)QG * 2 * KPE * 8;                     // per-query list + append buffer
 }
 
-template <int QG, int KPE, bool VEC4>
+// ESZ: row element size -- 4 (the fp32 corpus) or 2 (the index's 16-bit shadow: half
+// the bytes; the value read is x~ = 16-bit(x 2^e_x), its dot products are scaled back by
+// 2^-e_x exactly, the queries stay fp32).  A stage holds 128 bytes of each row either way.
+template <int QG, int KPE, bool VEC4, int ESZ>
 __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
   extern __shared__ __align__(16) float smem[];
+  constexpr int KCE = kScKC * 4 / ESZ;   // elements per 128-byte stage chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d;
-  const int dpad = (d + kScKC - 1) / kScKC * kScKC;
-  const int nk = dpad / kScKC;
+  const int dpad = (d + KCE - 1) / KCE * KCE;
+  const int nk = dpad / KCE;
+  const char *xbase = ESZ == 4 ? reinterpret_cast<const char *>(a.X) : static_cast<const char *>(a.Xh);
 
   float *q_s = smem;
   float *stage = q_s + QG * dpad;
@@ -150,9 +157,10 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
       for (int i = 0; i < 8; ++i) {
         const int r = (lane >> 3) + 4 * i;
         const int32_t idr = __shfl_sync(0xffffffffu, myid, r);
-        const int col = kc * kScKC + (lane & 7) * 4;
+        const int col = kc * KCE + (lane & 7) * (16 / ESZ);
         const bool ok = idr >= 0 && col < d;
-        cp_async16(buf + r * kScPad + (lane & 7) * 4, ok ? (const void *)(a.X + (int64_t)idr * d + col) : a.X, ok);
+        cp_async16(buf + r * kScPad + (lane & 7) * 4, ok ? (const void *)(xbase + ((int64_t)idr * d + col) * ESZ) : xbase,
+                   ok);
       }
     } else {
 #pragma unroll 4
@@ -197,17 +205,47 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
     __syncwarp();
     const int kc = t % nk;
     const float *buf = wst + (t % kScStages) * 32 * kScPad + lane * kScPad;
-    const float *qk = q_s + kc * kScKC;
+    const float *qk = q_s + kc * KCE;
+    if constexpr (ESZ == 4) {
 #pragma unroll
-    for (int c4 = 0; c4 < kScKC / 4; ++c4) {
-      const float4 rv = *reinterpret_cast<const float4 *>(buf + c4 * 4);
+      for (int c4 = 0; c4 < kScKC / 4; ++c4) {
+        const float4 rv = *reinterpret_cast<const float4 *>(buf + c4 * 4);
 #pragma unroll
-      for (int j = 0; j < QG; ++j) {
-        const float4 qv = *reinterpret_cast<const float4 *>(qk + j * dpad + c4 * 4);
-        acc[j] = fmaf(rv.x, qv.x, acc[j]);
-        acc[j] = fmaf(rv.y, qv.y, acc[j]);
-        acc[j] = fmaf(rv.z, qv.z, acc[j]);
-        acc[j] = fmaf(rv.w, qv.w, acc[j]);
+        for (int j = 0; j < QG; ++j) {
+          const float4 qv = *reinterpret_cast<const float4 *>(qk + j * dpad + c4 * 4);
+          acc[j] = fmaf(rv.x, qv.x, acc[j]);
+          acc[j] = fmaf(rv.y, qv.y, acc[j]);
+          acc[j] = fmaf(rv.z, qv.z, acc[j]);
+          acc[j] = fmaf(rv.w, qv.w, acc[j]);
+        }
+      }
+    } else {   // 16-bit rows: 8 elements per 16 bytes, converted exactly to fp32
+#pragma unroll
+      for (int c8 = 0; c8 < kScKC / 4; ++c8) {
+        const uint4 raw = *reinterpret_cast<const uint4 *>(buf + c8 * 4);
+        float xv[8];
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float2 f;
+          if (a.fmt16 == 0) f = __half22float2(*reinterpret_cast<const __half2 *>(&w[h]));
+          else f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[h]));
+          xv[2 * h] = f.x;
+          xv[2 * h + 1] = f.y;
+        }
+#pragma unroll
+        for (int j = 0; j < QG; ++j) {
+          const float4 q0 = *reinterpret_cast<const float4 *>(qk + j * dpad + c8 * 8);
+          const float4 q1 = *reinterpret_cast<const float4 *>(qk + j * dpad + c8 * 8 + 4);
+          acc[j] = fmaf(xv[0], q0.x, acc[j]);
+          acc[j] = fmaf(xv[1], q0.y, acc[j]);
+          acc[j] = fmaf(xv[2], q0.z, acc[j]);
+          acc[j] = fmaf(xv[3], q0.w, acc[j]);
+          acc[j] = fmaf(xv[4], q1.x, acc[j]);
+          acc[j] = fmaf(xv[5], q1.y, acc[j]);
+          acc[j] = fmaf(xv[6], q1.z, acc[j]);
+          acc[j] = fmaf(xv[7], q1.w, acc[j]);
+        }
       }
     }
     __syncwarp();
@@ -223,7 +261,7 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
 #pragma unroll
       for (int j = 0; j < QG; ++j) {
         sc[(b * QG + j) * kScRows + warp * 32 + lane] =
-            (myid >= 0 && j < nq) ? rank_key(a.metric, acc[j], nx2, inx) : -INFINITY;
+            (myid >= 0 && j < nq) ? rank_key(a.metric, ESZ == 4 ? acc[j] : ldexpf(acc[j], -a.xexp), nx2, inx) : -INFINITY;
         acc[j] = 0.f;
       }
       sid[b * kScRows + warp * 32 + lane] = myid;
@@ -265,11 +303,12 @@ __global__ void __launch_bounds__(kScThreads, 1) scan_topk_kernel(ScanArgs a) {
   }
 }
 
-template <int QG, int KPE, bool VEC4>
+template <int QG, int KPE, bool VEC4, int ESZ>
 static cudaError_t launch_scan_t(const ScanArgs &a, int gy, cudaStream_t stream) {
-  const int dpad = (a.d + kScKC - 1) / kScKC * kScKC;
+  constexpr int KCE = kScKC * 4 / ESZ;
+  const int dpad = (a.d + KCE - 1) / KCE * KCE;
   const size_t smem = scan_smem_bytes(QG, KPE, dpad);
-  auto fn = scan_topk_kernel<QG, KPE, VEC4>;
+  auto fn = scan_topk_kernel<QG, KPE, VEC4, ESZ>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_k(fn, dim3(a.P, gy), dim3(kScThreads), smem, stream, a);
@@ -277,7 +316,8 @@ static cudaError_t launch_scan_t(const ScanArgs &a, int gy, cudaStream_t stream)
 
 template <int QG, int KPE>
 static cudaError_t launch_scan_v(const ScanArgs &a, int gy, bool vec4, cudaStream_t s) {
-  return vec4 ? launch_scan_t<QG, KPE, true>(a, gy, s) : launch_scan_t<QG, KPE, false>(a, gy, s);
+  if (a.Xh) return launch_scan_t<QG, KPE, true, 2>(a, gy, s);   // (the shadow: d % 8 == 0, aligned)
+  return vec4 ? launch_scan_t<QG, KPE, true, 4>(a, gy, s) : launch_scan_t<QG, KPE, false, 4>(a, gy, s);
 }
 
 template <int QG>
@@ -292,7 +332,7 @@ static constexpr size_t kSmemLimit = 227 * 1024;
 // Pick the query group size: the smallest of {1,2,4,8} covering q (8 for q > 8),
 // shrunk until the shared-memory plan fits.
 int scan_query_group(int64_t q, int d, int kpe) {
-  const int dpad = (d + kScKC - 1) / kScKC * kScKC;
+  const int dpad = (d + 2 * kScKC - 1) / (2 * kScKC) * (2 * kScKC);   // (the 16-bit variant's padding)
   int qg = q <= 1 ? 1 : q <= 2 ? 2 : q <= 4 ? 4 : 8;
   const int kp = kpe <= 64 ? 64 : kpe <= 128 ? 128 : 256;
   while (qg > 1 && scan_smem_bytes(qg, kp, dpad) > kSmemLimit) qg >>= 1;

@@ -552,7 +552,7 @@ static vrs_status check_precision(const vrs_index *ix, int prec_req) {
 // Error-bound constants of the selection pass (vrs_internal.cuh key_error_bound).
 static KeyBound key_bound(const vrs_index *ix, bool gemm, bool h16) {
   KeyBound b{};
-  b.kind = !gemm ? KEY_FP32 : (h16 ? KEY_H16 : KEY_TF32);
+  b.kind = !gemm ? (h16 ? KEY_H16_FFMA : KEY_FP32) : (h16 ? KEY_H16 : KEY_TF32);
   b.d = ix->d;
   b.rmax = ix->rmax;
   b.rho = ix->rho;
@@ -679,7 +679,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   double *slot_key = cv.take<double>(ex_slots * k);
   int64_t *slot_id = cv.take<int64_t>(ex_slots * k);
   int32_t *slot_cnt = cv.take<int32_t>(ex_slots);
-  const bool h16 = use_bf16 && path == VRS_PATH_GEMM;
+  const bool h16 = use_bf16 && path == VRS_PATH_GEMM;   // (16-bit query operand of the tensor-core pass)
 
   int launches = 0;
   FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, SplitInfo{}, kprime, q, ix->X, d,
@@ -691,6 +691,11 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     }
     ScanArgs a{ix->X, n, d, sel_ids, count, queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime,
                part_key, part_id, P};
+    if (use_bf16) {   // the scan streams the 16-bit shadow (half the bytes) unless TF32 (= fp32 rows) is asked for
+      a.Xh = ix->xb;
+      a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
+      a.xexp = ix->xexp;
+    }
     ProfScope ps("scan", stream);
     CUDA_TRY(launch_scan(a, qg, kpe, stream, &launches));
   } else {
@@ -729,7 +734,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   }
   // the certificate (finalize) and its fallback (exact.cu): every query's result is the
   // exact top-k of the definition -- no host synchronisation
-  f.kb = key_bound(ix, path == VRS_PATH_GEMM, h16);
+  f.kb = key_bound(ix, path == VRS_PATH_GEMM, use_bf16);
   f.qexp = h16 ? qexp : nullptr;
   f.rq = h16 ? rq : nullptr;
   f.xexp = h16 ? ix->xexp : 0;
@@ -749,7 +754,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     CUDA_TRY(launch_exact(ea, stream, &launches));
   }
   g_last_path = path;
-  g_last_prec = path == VRS_PATH_GEMM ? (use_bf16 ? ix->prec16 : VRS_PREC_TF32) : VRS_PREC_DEFAULT;
+  g_last_prec = use_bf16 ? ix->prec16 : (path == VRS_PATH_GEMM ? VRS_PREC_TF32 : VRS_PREC_DEFAULT);
   g_last_launches = launches;
   return VRS_OK;
 }

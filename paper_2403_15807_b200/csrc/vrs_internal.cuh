@@ -227,7 +227,7 @@ __device__ __forceinline__ float rank_key(int metric, float dot, float nx2, floa
 //              relative), the key's own fma / product rounding (2^-24 relative);
 // each term rounded up generously (x2 on the fp32 rounding terms), then
 // x (1 + 2^-6) and an absolute 2^-40 slack for the fp64 arithmetic of the caller.
-enum KeyKind : int32_t { KEY_H16 = 0, KEY_TF32 = 1, KEY_FP32 = 2 };
+enum KeyKind : int32_t { KEY_H16 = 0, KEY_TF32 = 1, KEY_FP32 = 2, KEY_H16_FFMA = 3 };
 struct KeyBound {
   int32_t kind;   // KeyKind
   int32_t d;
@@ -246,6 +246,9 @@ __host__ __device__ inline double key_error_bound(const KeyBound &b, int metric,
     rq = 0.0;
     R = 0.0;
     rho = 0.0;
+    c = (double)(b.d + 4) * 0x1p-24;
+  } else if (b.kind == KEY_H16_FFMA) {   // 16-bit shadow rows, exact fp32 queries, FFMA (scan path)
+    rq = 0.0;
     c = (double)(b.d + 4) * 0x1p-24;
   } else {
     c = (double)((b.d + 15) / 16 + 16) * 0x1p-22;

@@ -73,6 +73,9 @@ struct ScanArgs {
   int32_t *part_id;       // [P][q][kprime], -1 = padding
   int32_t P;
   int64_t q_base = 0;     // first query of this launch (launch_scan splits batches over grid.y's limit)
+  const void *Xh = nullptr;   // the 16-bit shadow: rows read from it (half the bytes) when set
+  int32_t fmt16 = 0;          // 0 fp16, 1 bf16
+  int32_t xexp = 0;           // the shadow's exponent e_x
 };
 int scan_query_group(int64_t q, int d, int kpe);
 cudaError_t launch_scan(const ScanArgs &a, int qg, int kpe, cudaStream_t s, int *launches);
