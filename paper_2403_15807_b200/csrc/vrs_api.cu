@@ -513,7 +513,9 @@ static RowPlan row_plan(int64_t q, int32_t qtiles, int64_t n, int64_t row_bytes,
   if (identity || rows_req == VRS_ROWS_MASKED) return r;
   const bool cp = qtiles <= cp_qtiles && getenv("VRS_NO_CPGATHER") == nullptr;
   int64_t cap = q >= 1024 ? n * 9 / 10 : q >= 256 ? n * 9 / 20 : n / 3;
-  if (cp) cap = std::max<int64_t>(cap, (int64_t)(n * cp_frac / qtiles));
+  // (masked and cp.async-gathered rows are both re-read per query tile: the break-even
+  // selectivity is the rate ratio, ~0.7, whatever the tile count)
+  if (cp) cap = std::max<int64_t>(cap, (int64_t)(n * cp_frac));
   if (rows_req == VRS_ROWS_GATHER) cap = n;
   r.gather_cap = cap;
   if (direct) return r;   // (VRS_GATHER4 / VRS_CPGATHER: rows by id from X, no buffer; tc_prepare)
