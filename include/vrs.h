@@ -199,10 +199,11 @@ typedef struct {
                              vrs_host_fence(ix, s) has been enqueued on a stream s and s has synchronised */
   int32_t reserved0;
   /* Optional DEVICE uint64 [4] the call accumulates into (NULL: nothing is recorded):
-   *   [0] += queries answered, [1] += queries whose selection was NOT certified and
-   *   were recomputed by the exact fp64 scan, [2] = max(previous, the largest observed
-   *   |selection key - exact key| / E over all re-scored candidates) as IEEE-754
-   *   double bits (< 1 confirms the bound on this data), [3] reserved. */
+   *   [0] += queries answered, [1] += queries whose first selection was NOT certified
+   *   (re-selected by the refine pass when it runs, else recomputed exactly), [2] =
+   *   max(previous, the largest observed |selection key - exact key| / E over all
+   *   re-scored candidates) as IEEE-754 double bits (< 1 confirms the bound on this data),
+   *   [3] += queries recomputed by the exact fp64 fallback. */
   uint64_t *stats;
   int32_t reserved[2];
 } vrs_search_options;

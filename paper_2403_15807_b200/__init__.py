@@ -74,18 +74,19 @@ def _options(path, rows, precision=None, host_async=False, stats=None):
 
 
 def new_stats(device=None) -> torch.Tensor:
-    """A zeroed device counter block for search(..., stats=): [queries, uncertified queries
-    (recomputed by the exact fallback), max observed key error / bound (double bits), reserved]."""
+    """A zeroed device counter block for search(..., stats=): [queries, queries whose fp16
+    selection was not certified, max observed key error / bound (double bits), queries that
+    reached the exact fp64 fallback (the rest were certified by the refine pass)]."""
     return torch.zeros(4, dtype=torch.int64, device=device or torch.device("cuda", torch.cuda.current_device()))
 
 
 def read_stats(stats: torch.Tensor) -> dict:
     """Decode a stats block (synchronises): queries, uncertified, certified fraction, max key error / bound."""
     v = stats.cpu()
-    q, u = int(v[0]), int(v[1])
+    q, u, fb = int(v[0]), int(v[1]), int(v[3])
     ratio = float(v[2:3].view(torch.float64)[0])
     return {"queries": q, "uncertified": u, "certified_fraction": (q - u) / q if q else 1.0,
-            "max_key_error_over_bound": ratio}
+            "refined": u - fb, "exact_fallback": fb, "max_key_error_over_bound": ratio}
 
 
 def _torch_allocator():

@@ -49,6 +49,42 @@ __device__ __forceinline__ double row_to16(const float *__restrict__ in, uint16_
   return r2;
 }
 
+// One row -> a 16-bit pair (fp16 only): hi = fp16(v 2^e), lo = fp16(v 2^e - hi) (the
+// difference is exact in fp32), by one warp; returns |hi 2^-e - v|^2 in .x and
+// |(hi + lo) 2^-e - v|^2 in .y (fp64) on every lane.  The refine pass multiplies
+// q_hi.x_hi + q_hi.x_lo + q_lo.x_hi ("Refine").
+__device__ __forceinline__ double2 row_to16x2(const float *__restrict__ in, uint16_t *__restrict__ hi,
+                                              uint16_t *__restrict__ lo, int d, int e) {
+  const int lane = threadIdx.x & 31;
+  double r1 = 0.0, r2 = 0.0;
+  for (int t = 4 * lane; t < d; t += 128) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(in + t));
+    const float s0 = ldexpf(v.x, e), s1 = ldexpf(v.y, e), s2 = ldexpf(v.z, e), s3 = ldexpf(v.w, e);
+    uint2 wh;
+    wh.x = pack16x2(s0, s1, 0);
+    wh.y = pack16x2(s2, s3, 0);
+    const float2 h01 = unpack16x2(wh.x, 0), h23 = unpack16x2(wh.y, 0);
+    uint2 wl;
+    wl.x = pack16x2(s0 - h01.x, s1 - h01.y, 0);
+    wl.y = pack16x2(s2 - h23.x, s3 - h23.y, 0);
+    *reinterpret_cast<uint2 *>(hi + t) = wh;
+    if (lo) *reinterpret_cast<uint2 *>(lo + t) = wl;
+    const float2 l01 = unpack16x2(wl.x, 0), l23 = unpack16x2(wl.y, 0);
+    const double a0 = ldexp((double)h01.x, -e) - v.x, a1 = ldexp((double)h01.y, -e) - v.y;
+    const double a2 = ldexp((double)h23.x, -e) - v.z, a3 = ldexp((double)h23.y, -e) - v.w;
+    r1 += a0 * a0 + a1 * a1 + a2 * a2 + a3 * a3;
+    const double b0 = ldexp((double)h01.x + l01.x, -e) - v.x, b1 = ldexp((double)h01.y + l01.y, -e) - v.y;
+    const double b2 = ldexp((double)h23.x + l23.x, -e) - v.z, b3 = ldexp((double)h23.y + l23.y, -e) - v.w;
+    r2 += b0 * b0 + b1 * b1 + b2 * b2 + b3 * b3;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  }
+  return make_double2(r1, r2);
+}
+
 // One query row (warp): per-row exponent, 16-bit row, exponent and residual
 // (rounded up) to qexp / rq.  Rows q..rows-1 are zero padding (whole 128-row tiles).
 __device__ __forceinline__ void query_row_to16(const QueryFuse &f, int64_t row) {

@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_fallback_kernel(ExactArgs
 #pragma unroll
   for (int w = 0; w < kExWarps; ++w) U += s_wsum[w];
   if (U == 0) return;
+  if (a.stats && blockIdx.x == 0 && tid == 0) atomicAdd(a.stats + 3, (unsigned long long)U);
   const int64_t ngroups = (U + QG - 1) / QG;
   const int64_t R = std::max<int64_t>(1, (2 * (int64_t)gridDim.x + ngroups - 1) / ngroups);
   const int64_t n_space = a.ids ? *a.count : a.n;

@@ -663,7 +663,8 @@ __device__ CertQ cert_setup(const FinalizeArgs &a, int64_t j, double qq) {
   CertQ c;
   c.qn = sqrt(qq);
   const double rq = a.rq ? (double)__ldg(a.rq + j) : 0.0;
-  c.E = key_error_bound(a.kb, a.metric, c.qn, rq);
+  c.E = a.kb.kind == KEY_H16X3 ? key_error_bound_x3(a.kb, a.metric, c.qn, rq, a.rq2 ? (double)__ldg(a.rq2 + j) : 0.0)
+                               : key_error_bound(a.kb, a.metric, c.qn, rq);
   const int e = (a.qexp && a.metric != VRS_L2) ? __ldg(a.qexp + j) + a.xexp : 0;
   c.dinv = ldexp(1.0, -e);
   return c;
@@ -791,7 +792,8 @@ __device__ void fin_certify(const FinalizeArgs &a, int64_t j, int m, double qq, 
   a.cert[j] = ok ? 1 : 0;
   a.sk[j] = skv;
   a.gcnt[j] = 0;
-  if (a.stats) {
+  if (!ok && a.uncert_seen && !a.qmap) *reinterpret_cast<volatile int32_t *>(a.uncert_seen) = 1;
+  if (a.stats && !a.qmap) {   // (the refine's finalize re-certifies queries already counted)
     atomicAdd(a.stats, 1ull);
     if (!ok) atomicAdd(a.stats + 1, 1ull);
   }
@@ -871,8 +873,10 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) 
   TL_WAITED(1);
   pdl_trigger();
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
+  if (a.qcount && j >= __ldg(a.qcount)) return;
+  const int64_t jq = a.qmap ? __ldg(a.qmap + j) : j;   // (the refine: compacted row -> query)
   const int m = fin_stream(a, j, 0, 1, s_buf[w]);
-  const double qq = fin_qq(a, j);
+  const double qq = fin_qq(a, jq);
   CertQ cq{0.0, 0.0, 1.0};
   float kmin = -INFINITY;
   if (a.cert) {
@@ -882,10 +886,10 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
   }
-  fin_rescore<SEL <= 64 ? 4 : 8>(a, j, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w],
+  fin_rescore<SEL <= 64 ? 4 : 8>(a, jq, s_buf[w].id, m, 0, 1, qq, s_sc[w], s_sid[w],
                                  a.stats ? s_buf[w].key : nullptr, &cq);
   __syncwarp();
-  fin_sort_write(a, j, m, qq, s_sc[w], s_sid[w], kmin, &cq);
+  fin_sort_write(a, jq, m, qq, s_sc[w], s_sid[w], kmin, &cq);
 }
 
 #ifndef VRS_FIN_W
@@ -952,6 +956,8 @@ __global__ void __launch_bounds__(W * 32) finalize_cta_kernel(FinalizeArgs a) {
   pdl_wait();
   TL_WAITED(1);
   pdl_trigger();
+  if (a.qcount && j >= __ldg(a.qcount)) return;   // (whole CTA)
+  const int64_t jq = a.qmap ? __ldg(a.qmap + j) : j;
   // each warp: its share of the lists -> its survivors (<= k', or <= 32E unsorted when
   // the tree merge follows: it sorts them anyway)
   const int keep = a.kprime <= 64 ? 64 : (a.kprime <= 128 ? 128 : -1);
@@ -1002,13 +1008,13 @@ __global__ void __launch_bounds__(W * 32) finalize_cta_kernel(FinalizeArgs a) {
   __syncthreads();
   TL_STAMP(1, 3);
   const int m = s_n[0];
-  const double qq = fin_qq(a, j);
+  const double qq = fin_qq(a, jq);
   CertQ cq{0.0, 0.0, 1.0};
   if (a.cert) cq = cert_setup(a, j, qq);
-  fin_rescore<8>(a, j, s_buf[0].id, m, w, W, qq, s_sc, s_sid, a.stats ? s_buf[0].key : nullptr, &cq);
+  fin_rescore<8>(a, jq, s_buf[0].id, m, w, W, qq, s_sc, s_sid, a.stats ? s_buf[0].key : nullptr, &cq);
   __syncthreads();
   TL_STAMP(1, 4);
-  if (w == 0) fin_sort_write(a, j, m, qq, s_sc, s_sid, s_kmin, &cq);
+  if (w == 0) fin_sort_write(a, jq, m, qq, s_sc, s_sid, s_kmin, &cq);
 }
 
 // Per query (one CTA): the kth largest probe slot maximum (each the key of a

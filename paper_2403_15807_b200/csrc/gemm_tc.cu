@@ -182,29 +182,46 @@ cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, con
 // overflows.  bf16: e = 0.  Powers of two are exact, so the MMA's dot product is
 // 2^(e_q + e_x) <q~, x~> (the key domain).  Each row's rounding
 // residual |x~ 2^-e - x| is measured exactly (fp64) -- the certificate's bound.
-// The shadow (load): warp per row.  res[0] = max |x~ - x|, res[1] = max |x~ - x| / |x|
-// (rounded up; u64 bits of non-negative doubles order as integers).
+// The shadow (load): warp per row.  res[0] = max |x~ - x|, res[1] = max |x~ - x| / |x|;
+// with out_lo (fp16): the refine pass's second half x_lo = fp16(x 2^e - x~), and
+// res[2] / res[3] the same maxima for |(x~ + x_lo) 2^-e - x| (rounded up; u64 bits of
+// non-negative doubles order as integers).
 __global__ void __launch_bounds__(256) shadow_kernel(const float *__restrict__ X, int64_t n, int32_t d, int32_t e,
                                                      int32_t fmt, uint16_t *__restrict__ out,
-                                                     const float *__restrict__ nx2, unsigned long long *res) {
+                                                     uint16_t *__restrict__ out_lo, const float *__restrict__ nx2,
+                                                     unsigned long long *res) {
   const int lane = threadIdx.x & 31;
-  double rmax = 0.0, rho = 0.0;
+  double rmax = 0.0, rho = 0.0, rmax2 = 0.0, rho2 = 0.0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < n; row += (int64_t)gridDim.x * 8) {
-    const double r = sqrt(row_to16(X + row * d, out + row * d, d, e, fmt)) * (1.0 + 0x1p-50);
+    double r, r2 = 0.0;
+    if (out_lo) {
+      const double2 rr = row_to16x2(X + row * d, out + row * d, out_lo + row * d, d, e);
+      r = sqrt(rr.x) * (1.0 + 0x1p-50);
+      r2 = sqrt(rr.y) * (1.0 + 0x1p-50);
+    } else {
+      r = sqrt(row_to16(X + row * d, out + row * d, d, e, fmt)) * (1.0 + 0x1p-50);
+    }
     rmax = fmax(rmax, r);
+    rmax2 = fmax(rmax2, r2);
     const double xn = sqrt((double)__ldg(nx2 + row));
-    if (xn > 0.0) rho = fmax(rho, r / xn * (1.0 + 0x1p-20));   // (|x| from the fp32 |x|^2: 2^-24 relative)
+    if (xn > 0.0) {   // (|x| from the fp32 |x|^2: 2^-24 relative)
+      rho = fmax(rho, r / xn * (1.0 + 0x1p-20));
+      rho2 = fmax(rho2, r2 / xn * (1.0 + 0x1p-20));
+    }
   }
   if (lane == 0) {
     atomicMax(res, (unsigned long long)__double_as_longlong(rmax));
     atomicMax(res + 1, (unsigned long long)__double_as_longlong(rho));
+    atomicMax(res + 2, (unsigned long long)__double_as_longlong(rmax2));
+    atomicMax(res + 3, (unsigned long long)__double_as_longlong(rho2));
   }
 }
 
-cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, const float *nx2,
-                          unsigned long long *res, cudaStream_t s) {
+cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, void *out_lo,
+                          const float *nx2, unsigned long long *res, cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 16);
-  shadow_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, e, fmt, static_cast<uint16_t *>(out), nx2, res);
+  shadow_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, e, fmt, static_cast<uint16_t *>(out),
+                                                 static_cast<uint16_t *>(out_lo), nx2, res);
   return cudaGetLastError();
 }
 
@@ -311,6 +328,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
     return cudaErrorInvalidValue;
   TcParams &p = L->p;
   memset(&p, 0, sizeof p);
+  p.nseg = 1;   // (one K segment; the refine pass sets 3)
   p.n_rows = a.n;
   p.d = a.d;
   p.nk = (a.d + (bf ? 2 * tc::BK : tc::BK) - 1) / (bf ? 2 * tc::BK : tc::BK);
@@ -460,3 +478,133 @@ namespace vrs {
 int tl_read_gemm(unsigned long long *host) { return tl_read(host); }
 }
 #endif
+
+// ---------------------------------------------------------------- the refine pass
+// ("Refine".)  The queries whose fp16 selection was not certified
+// (cert = 0 after finalize) are re-selected with keys that carry fp32-level accuracy:
+// each 16-bit operand is split into hi + lo halves (x_lo built at load, q_lo here) and
+// the pass multiplies q_hi.x_hi + q_hi.x_lo + q_lo.x_hi into one fp32 accumulator --
+// three K segments of the same tcgen05 kernel over masked row tiles.  The threshold is
+// provable from level 0: the true k-th score is >= s_k (k re-scored rows reach it), so a
+// row of the true top k has a refine key >= s_k - E1; the pass needs no probe.
+
+namespace vrs {
+
+// One CTA of 1024 threads: compact the uncertified queries (ascending), then per compacted
+// row (a warp each): the [q_hi | q_lo] fp16 row with its exponent and residuals, and the
+// key threshold (s_k - E1) in the pass's key domain.  Rows past the count up to the tile
+// boundary are zero with an unreachable threshold.
+__global__ void __launch_bounds__(1024) refine_prep_kernel(RefineArgs r) {
+  __shared__ int s_wsum[32];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < r.q; c0 += 1024) {
+    const int64_t j = c0 + tid;
+    const bool f = j < r.q && r.cert[j] == 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_wsum[warp] = __popc(bal);
+    __syncthreads();
+    int before = s_base;
+    for (int w = 0; w < warp; ++w) before += s_wsum[w];
+    if (f) r.qlist[before + __popc(bal & lanemask_lt())] = (int32_t)j;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < 32; ++w) t += s_wsum[w];
+      s_base += t;
+    }
+    __syncthreads();
+  }
+  const int U = s_base;
+  if (tid == 0) *r.ucount = U;
+  if (U == 0) return;
+  const int64_t upad = std::min<int64_t>(r.rows, ((int64_t)U + tc::BM - 1) / tc::BM * tc::BM);
+  for (int64_t row = warp; row < upad; row += 32) {
+    uint16_t *hi = r.qr + row * 2 * r.dpad, *lo = hi + r.dpad;
+    if (row >= U) {   // padding rows of the last tile
+      for (int t = lane; t < 2 * r.dpad; t += 32) hi[t] = 0;
+      if (lane == 0) {
+        r.qexp[row] = 0;
+        r.rqa[row] = 0.f;
+        r.rq2[row] = 0.f;
+        r.gtau[row] = 0xffffffffu;   // (+inf: nothing passes)
+      }
+      continue;
+    }
+    const int64_t j = r.qlist[row];
+    const float *qv = r.Q + j * r.d;
+    float am = 0.f;
+    double qq = 0.0;
+    for (int t = lane; t < r.d; t += 32) {
+      am = fmaxf(am, fabsf(qv[t]));
+      qq += (double)qv[t] * (double)qv[t];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+      qq += __shfl_xor_sync(0xffffffffu, qq, o);
+    }
+    const int e = scale_exp16(am, 0);
+    const double2 rr = row_to16x2(qv, hi, lo, r.d, e);
+    for (int t = r.d + lane; t < r.dpad; t += 32) { hi[t] = 0; lo[t] = 0; }
+    if (lane == 0) {
+      const double r1 = sqrt(rr.x), r2 = sqrt(rr.y) * (1.0 + 0x1p-50);
+      const double rqa = (r1 + r2) * (1.0 + 0x1p-50);   // |q_lo| <= |q_hi - q| + |q_hi + q_lo - q|
+      r.qexp[row] = e;
+      r.rqa[row] = __double2float_ru(rqa);
+      r.rq2[row] = __double2float_ru(r2);
+      const double qn = sqrt(qq), skv = r.sk[j];
+      const double E1 = key_error_bound_x3(r.kb, r.metric, qn, (double)__double2float_ru(rqa), (double)__double2float_ru(r2));
+      const double nat = r.metric == VRS_L2 ? qq + skv : (r.metric == VRS_COSINE ? skv * qn : skv);
+      double T = nat - E1 - 0x1p-30 * (fabs(nat) + qn * r.kb.xmax);
+      if (r.metric != VRS_L2) T = ldexp(T, e + r.xexp);   // IP / COS keys are in the domain 2^(e_q + e_x)
+      r.gtau[row] = ordered_u32(__double2float_rd(T));
+    }
+  }
+}
+
+cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan &plan, void *gemm_scratch,
+                          const void *x_lo, cudaStream_t s, int *launches) {
+  cudaError_t e = launch_k(refine_prep_kernel, dim3(1), dim3(1024), 0, s, r);
+  if (e != cudaSuccess) return e;
+  // row delivery: gathered by cp.async (the hi and lo halves fetched by id, any query-tile
+  // count -- the refine has few tiles) up to the masked break-even, else masked tiles
+  GemmArgs b = a;
+  b.masked = 0;
+  b.xsel_cap = a.ids ? r.gather_cap : 0;
+  b.xsel = nullptr;
+  b.prepped = 1;
+  b.cp_min_bytes = 0;
+  TcLaunch L;
+  e = tc_prepare(b, plan, s, launches, &L);
+  if (e != cudaSuccess) return e;
+  if (!make_map(&L.mq, r.qr, r.rows, 2 * r.dpad, tc::BM, true, 0) || !make_map(&L.mg, x_lo, a.n, a.d, tc::BN, true, 0))
+    return cudaErrorInvalidValue;
+  const GemmScratch gs = carve_gemm(gemm_scratch, plan, a.q, a.kprime);
+  TcParams &p = L.p;
+  p.cand_key = gs.cand_key;   // (level 0's lists: its finalize has read them)
+  p.cand_id = gs.cand_id;
+  p.cand_cnt = gs.cand_cnt;
+  p.probe_max = gs.probe_max;
+  p.gtau = r.gtau;
+  p.qexp = r.qexp;
+  p.nseg = 3;
+  p.a_lo_off = r.dpad;
+  p.qcount = r.ucount;
+  p.xrows_lo = x_lo;
+  p.g4 = 2;
+  p.cp_min_bytes = 0;
+  L.ar = false;
+  {
+    ProfScope pf("refine.main", s);
+    e = tc_launch_mode<MODE_MAIN>(L, p, s);
+  }
+  if (launches) *launches += 2;
+  return e;
+}
+
+}  // namespace vrs

@@ -233,6 +233,13 @@ struct TcParams {
   uint32_t idesc;          // MMA instruction descriptor (operand format)
   const int32_t *qexp;     // 16-bit operands: [q] per-query exponents e_q (nullptr: TF32, no scaling)
   int32_t xexp;            // the shadow's exponent e_x
+  // refine pass: K runs over nseg = 3 segments -- q_hi.x_hi, q_hi.x_lo (x_lo
+  // through tmap_g), q_lo.x_hi (q_lo at column a_lo_off of the query map); query tiles at or
+  // past *qcount (the device-side count of compacted queries) do no work
+  int32_t nseg = 1;
+  int32_t a_lo_off = 0;
+  const int32_t *qcount = nullptr;
+  const void *xrows_lo = nullptr;   // cp.async gather, segment 1: x_lo's base
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -403,7 +410,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     step_cap = std::min<int64_t>(step_cap, std::max<int64_t>(2, main_span / p.probe_div));
   }
   const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(step_cap, std::max<int64_t>(1, span)) : 1;
-  const int ntiles = (int)((span + step - 1) / step);
+  const bool q_idle = p.qcount != nullptr && (int64_t)qtile * BM >= (int64_t)__ldg(p.qcount);
+  const int ntiles = q_idle ? 0 : (int)((span + step - 1) / step);
+  const int nkb = p.nk * p.nseg;   // K blocks per tile (3 segments in the refine pass)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
 
@@ -442,11 +451,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (ntiles > 0) load_ids(0, rid);
     for (int t = 0; t < ntiles; ++t) {
       if (t + 1 < ntiles) load_ids(t + 1, rnext);
-      for (int kb = 0; kb < p.nk; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int seg = kb / p.nk, kk = kb - seg * p.nk;   // (refine: 3 segments, x_lo in segment 1)
+        const char *xs = seg == 1 ? static_cast<const char *>(p.xrows_lo) : xb;
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t *st = b_base + stage * SSTRIDE;
         const uint32_t bdst = smem_u32(st + BOFF);
-        const int64_t koff = (int64_t)kb * 128;
+        const int64_t koff = (int64_t)kk * 128;
         // coalesced: 8 lanes copy one row's 128-byte segment (16 B each), a warp
         // instruction 4 whole rows; the row ids (lane j holds rows j + 32v) by shuffle
         const int c = lane & 7;
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
           const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
           const int r = hrow + rl;
-          cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xb + (int64_t)id * rb + koff + c * 16, cvalid);
+          cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xs + (int64_t)id * rb + koff + c * 16, cvalid);
         }
         cpa_mbar_arrive(&full_bar[stage]);
         if (CPW == 2) asm volatile("bar.sync 1, 64;" ::: "memory");   // both producer warps registered their arrivals
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (lead && lane == 0) {
           if (!AR) {
             mbar_expect_tx(&full_bar[stage], A_BYTES);
-            tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
+            tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
           } else {
             mbar_arrive(&full_bar[stage]);
           }
@@ -533,12 +544,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)(tile_of(t) * BN);
-        for (int kb = 0; kb < p.nk; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int seg = kb / p.nk, kk = kb - seg * p.nk;   // (refine: 3 segments; else seg = 0)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *st = b_base + stage * SSTRIDE;
           mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
-          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], kb * KE, qtile * BM);
-          tma_load_2d(st + BOFF, gather ? &tmap_g : &tmap_x, &full_bar[stage], kb * KE, row0);
+          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
+          tma_load_2d(st + BOFF, (gather || seg == 1) ? &tmap_g : &tmap_x, &full_bar[stage], kk * KE, row0);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
@@ -555,7 +567,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < p.nk; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         if (t == 0 && kb == 0 && lane == 0) TL_STAMP_ANY(MODE & 3, 2);
         if (cpg) fence_proxy_async_smem();   // cp.async (generic proxy) writes -> the MMA's async-proxy reads
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
           // frees the smem slot when these MMAs finish; accumulator ready after the last K block
           tc_commit(&empty_bar[stage]);
-          if (kb == p.nk - 1) tc_commit(&tfull_bar[acc]);
+          if (kb == nkb - 1) tc_commit(&tfull_bar[acc]);
         }
         __syncwarp();
         if (++stage == NST) { stage = 0; phase ^= 1; }

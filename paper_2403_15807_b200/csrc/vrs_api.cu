@@ -37,6 +37,12 @@ struct vrs_index {
   int32_t prec16 = 0;     // VRS_PREC_FP16 / VRS_PREC_BF16: the shadow's format (0: none)
   int32_t xexp = 0;       // the shadow's power-of-two scale e_x (fp16)
   double rmax = 0, rho = 0;   // max |x~ 2^-e_x - x|, max |x~ 2^-e_x - x| / |x| (measured at load, fp64)
+  void *xl = nullptr;        // fp16 only: the refine pass's low half x_lo [n x d]
+  // set (by a plain store from finalize, through mapped pinned memory -- no copy, no sync) once a
+  // query of this index failed its level-0 certificate: the refine pass is launched from then on
+  volatile int32_t *uncert_seen_host = nullptr;
+  int32_t *uncert_seen_dev = nullptr;
+  double rmax2 = 0, rho2 = 0;   // the same maxima after x~ + x_lo
   // vrs_search_host staging: device slots (queries in, ids / dists out) so
   // that the upload of one call overlaps the compute of the previous one; the
   // copies run on their own streams, ordered by events.
@@ -382,7 +388,11 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   ix->device = dev;
   ix->num_sms = sms;
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 16, 16, want_shadow ? (size_t)n * d * 2 : 0});
+  // (the refine pass's x_lo: fp16 shadows, unless VRS_NO_REFINE)
+  static const bool no_refine = getenv("VRS_NO_REFINE") != nullptr;
+  const bool want_lo = want_shadow && prec16 == VRS_PREC_FP16 && !no_refine;
+  const size_t bytes = carve_size({(size_t)n * 4, (size_t)n * 4, 16, 32, want_shadow ? (size_t)n * d * 2 : 0,
+                                   want_lo ? (size_t)n * d * 2 : 0});
   void *mem = nullptr;
   if (alloc) {
     mem = alloc->alloc(bytes, cuda_stream, alloc->ctx);
@@ -399,12 +409,13 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
   ix->nx2 = cv.take<float>(n);
   ix->inv_nx = cv.take<float>(n);
   int32_t *zf = cv.take<int32_t>(4);   // [0] zero-norm row flag, [1] max |x|^2, [2] max |x_t| (float bits)
-  unsigned long long *res = cv.take<unsigned long long>(2);   // shadow residual maxima (double bits)
+  unsigned long long *res = cv.take<unsigned long long>(4);   // shadow residual maxima (double bits)
   ix->xb = want_shadow ? cv.take<char>((size_t)n * d * 2) : nullptr;
+  ix->xl = want_lo ? cv.take<char>((size_t)n * d * 2) : nullptr;
   ix->prec16 = prec16;
   int32_t flags[4] = {0, 0, 0, 0};
   cudaError_t e = cudaMemsetAsync(zf, 0, 16, stream);
-  if (e == cudaSuccess) e = cudaMemsetAsync(res, 0, 16, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(res, 0, 32, stream);
   if (e == cudaSuccess) e = launch_norms(vectors, n, d, ix->nx2, ix->inv_nx, zf, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(flags, zf, 16, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
@@ -415,18 +426,34 @@ vrs_status vrs_load_ex(const float *vectors, int64_t n, int32_t d, const vrs_att
     memcpy(&amax, &flags[2], 4);
     if (prec16 == VRS_PREC_FP16 && amax > 0.f && std::isfinite(amax))
       ix->xexp = std::max(-120, std::min(120, 14 - ilogbf(amax)));
-    unsigned long long r2[2] = {0, 0};
-    e = launch_shadow(vectors, n, d, ix->xexp, prec16 == VRS_PREC_FP16 ? 0 : 1, ix->xb, ix->nx2, res, stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(r2, res, 16, cudaMemcpyDeviceToHost, stream);
+    unsigned long long r2[4] = {0, 0, 0, 0};
+    e = launch_shadow(vectors, n, d, ix->xexp, prec16 == VRS_PREC_FP16 ? 0 : 1, ix->xb, ix->xl, ix->nx2, res, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(r2, res, 32, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     memcpy(&ix->rmax, &r2[0], 8);
     memcpy(&ix->rho, &r2[1], 8);
+    memcpy(&ix->rmax2, &r2[2], 8);
+    memcpy(&ix->rho2, &r2[3], 8);
   }
   if (e != cudaSuccess) {
     vrs_free(ix);
     return fail(VRS_ECUDA, "vrs_load norms / shadow: %s", cudaGetErrorString(e));
   }
   ix->has_zero_row = flags[0];
+  if (ix->xl) {
+    int32_t *h = nullptr;
+    if (cudaHostAlloc(&h, 4, cudaHostAllocMapped) == cudaSuccess) {
+      *h = 0;
+      void *dptr = nullptr;
+      if (cudaHostGetDevicePointer(&dptr, h, 0) == cudaSuccess) {
+        ix->uncert_seen_host = h;
+        ix->uncert_seen_dev = static_cast<int32_t *>(dptr);
+      } else {
+        cudaFreeHost(h);
+      }
+    }
+    cudaGetLastError();
+  }
   {
     float m2;
     memcpy(&m2, &flags[1], 4);
@@ -454,6 +481,7 @@ vrs_status vrs_free(vrs_index *ix) {
     if (ix->has_alloc) ix->alloc.free(ix->nx2, nullptr, ix->alloc.ctx);
     else cudaFree(ix->nx2);
   }
+  if (ix->uncert_seen_host) cudaFreeHost(const_cast<int32_t *>(ix->uncert_seen_host));
   delete ix;
   return VRS_OK;
 }
@@ -560,6 +588,8 @@ static KeyBound key_bound(const vrs_index *ix, bool gemm, bool h16) {
   b.rmax = ix->rmax;
   b.rho = ix->rho;
   b.xmax = ix->xmax;
+  b.rmax2 = ix->rmax2;
+  b.rho2 = ix->rho2;
   return b;
 }
 
@@ -651,6 +681,19 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // the 16-bit operand, the certificate, finalize's k-th sort key, a group counter; the
   // fallback's per-(item, query) slots of k results
   const int ex_qg = exact_group_size(d, k);
+  // the refine pass for batches of >= 128 queries on the fp16 tensor-core
+  // path (below that the exact fallback's row passes cost less than a tensor pass's launch chain)
+  // -- and only once the index has seen a level-0 certificate fail (the flag finalize sets): an
+  // index whose data always certifies pays no launches for it (C2: 8 cells x 3 launches);
+  // VRS_REFINE=always / never for A/B.  Correctness never depends on it: the exact fallback
+  // recomputes whatever stays uncertified.
+  static const int refine_qmin = getenv("VRS_REFINE_QMIN") ? atoi(getenv("VRS_REFINE_QMIN")) : 128;
+  static const int refine_mode = !getenv("VRS_REFINE") ? 0 : (strcmp(getenv("VRS_REFINE"), "always") == 0 ? 1 : -1);
+  const bool refine_seen = refine_mode == 1 || (refine_mode == 0 && ix->uncert_seen_host && *ix->uncert_seen_host != 0);
+  const bool refine = path == VRS_PATH_GEMM && use_bf16 && ix->xl != nullptr && q >= refine_qmin && refine_seen &&
+                      (prec_req == VRS_PREC_DEFAULT || prec_req == VRS_PREC_FP16);
+  const int32_t rf_dpad = (d + 63) / 64 * 64;
+  const size_t rf_rows = (size_t)gp.qtiles * 128;
   const int64_t ex_items = exact_items_max(q, ex_qg);
   const size_t ex_slots = (size_t)ex_items * ex_qg;
   const size_t bytes = carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n),
@@ -659,7 +702,10 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                                    (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4,
                                    use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0,
                                    (size_t)q * 4, (size_t)q * 4, (size_t)q, (size_t)q * 8, (size_t)q * 4,
-                                   ex_slots * k * 8, ex_slots * k * 8, ex_slots * 4});
+                                   ex_slots * k * 8, ex_slots * k * 8, ex_slots * 4,
+                                   refine ? (size_t)q * 4 : 0, refine ? (size_t)16 : 0, refine ? rf_rows * 2 * (size_t)rf_dpad * 2 : 0,
+                                   refine ? (size_t)q * 4 : 0, refine ? (size_t)q * 4 : 0, refine ? (size_t)q * 4 : 0,
+                                   refine ? (size_t)q * 4 : 0});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -682,9 +728,18 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   double *slot_key = cv.take<double>(ex_slots * k);
   int64_t *slot_id = cv.take<int64_t>(ex_slots * k);
   int32_t *slot_cnt = cv.take<int32_t>(ex_slots);
+  int32_t *rf_qlist = refine ? cv.take<int32_t>((size_t)q) : nullptr;
+  int32_t *rf_count = refine ? cv.take<int32_t>(4) : nullptr;
+  uint16_t *rf_qr = refine ? cv.take<uint16_t>(rf_rows * 2 * rf_dpad) : nullptr;
+  int32_t *rf_qexp = refine ? cv.take<int32_t>((size_t)q) : nullptr;
+  float *rf_rqa = refine ? cv.take<float>((size_t)q) : nullptr;
+  float *rf_rq2 = refine ? cv.take<float>((size_t)q) : nullptr;
+  uint32_t *rf_gtau = refine ? cv.take<uint32_t>((size_t)q) : nullptr;
   const bool h16 = use_bf16 && path == VRS_PATH_GEMM;   // (16-bit query operand of the tensor-core pass)
 
   int launches = 0;
+  GemmArgs gemm_args{};   // (the tensor-core pass's arguments, reused by the refine pass)
+  void *gemm_scr_keep = gemm_scr;
   FinalizeArgs f{part_key, part_id, nullptr, P, kprime, kprime, 1, nullptr, SplitInfo{}, kprime, q, ix->X, d,
                  queries, (int32_t)metric, k, ix->row_offset, ids, dists};
   if (path == VRS_PATH_SCAN) {
@@ -719,6 +774,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     a.rq = rq;
     a.cp_min_bytes = rp.cp_min_bytes;
     a.ids_local = ids_local;
+    gemm_args = a;
     a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
     {
       ProfScope ps("gemm", stream);
@@ -745,14 +801,36 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   f.sk = skey;
   f.gcnt = gcnt;
   f.stats = opts ? reinterpret_cast<unsigned long long *>(opts->stats) : nullptr;
+  f.uncert_seen = h16 ? ix->uncert_seen_dev : nullptr;
   {
     ProfScope ps("finalize", stream);
     CUDA_TRY(launch_finalize(f, stream, &launches));
+  }
+  if (refine) {   // level 1: the uncertified queries re-selected with split-fp16 keys, finalized again
+    RefineArgs ra{cert, skey, queries, q, d, rf_dpad, (int32_t)metric, key_bound(ix, true, true), ix->xexp,
+                  (int64_t)rf_rows, rf_qlist, rf_count, rf_qr, rf_qexp, rf_rqa, rf_rq2, rf_gtau};
+    ra.kb.kind = KEY_H16X3;
+    ra.gather_cap = rows_req == VRS_ROWS_MASKED ? 0 : (rows_req == VRS_ROWS_GATHER ? n : n * 7 / 10);
+    {
+      ProfScope ps("refine", stream);
+      CUDA_TRY(launch_refine(ra, gemm_args, gp, gemm_scr_keep, ix->xl, stream, &launches));
+    }
+    FinalizeArgs f2 = f;
+    f2.gtau = rf_gtau;
+    f2.kb = ra.kb;
+    f2.qexp = rf_qexp;
+    f2.rq = rf_rqa;
+    f2.rq2 = rf_rq2;
+    f2.qmap = rf_qlist;
+    f2.qcount = rf_count;
+    ProfScope ps("refine.finalize", stream);
+    CUDA_TRY(launch_finalize(f2, stream, &launches));
   }
   static const bool no_fallback = getenv("VRS_NO_FALLBACK") != nullptr;   // (A/B timing only: results unverified)
   if (!no_fallback) {
     ExactArgs ea{cert, skey, gcnt, ix->X, d, n, identity ? nullptr : sel_ids, count, queries, q, (int32_t)metric, k,
                  ix->row_offset, (double)ix->xmax, ix->nx2, ix->inv_nx, ids, dists, slot_key, slot_id, slot_cnt, ex_qg};
+    ea.stats = f.stats;
     ProfScope ps("exact", stream);
     CUDA_TRY(launch_exact(ea, stream, &launches));
   }

@@ -227,14 +227,33 @@ __device__ __forceinline__ float rank_key(int metric, float dot, float nx2, floa
 //              relative), the key's own fma / product rounding (2^-24 relative);
 // each term rounded up generously (x2 on the fp32 rounding terms), then
 // x (1 + 2^-6) and an absolute 2^-40 slack for the fp64 arithmetic of the caller.
-enum KeyKind : int32_t { KEY_H16 = 0, KEY_TF32 = 1, KEY_FP32 = 2, KEY_H16_FFMA = 3 };
+enum KeyKind : int32_t { KEY_H16 = 0, KEY_TF32 = 1, KEY_FP32 = 2, KEY_H16_FFMA = 3, KEY_H16X3 = 4 };
 struct KeyBound {
   int32_t kind;   // KeyKind
   int32_t d;
   double rmax;    // KEY_H16: max over rows of |x~ - x| (natural units, rounded up)
   double rho;     // KEY_H16: max over rows of |x~ - x| / |x|
   double xmax;    // max row norm (rounded up)
+  double rmax2 = 0, rho2 = 0;   // KEY_H16X3: the same after x~ + x_lo
 };
+// The refine pass (KEY_H16X3): keys from q_hi.x_hi + q_hi.x_lo + q_lo.x_hi with
+// q = q_hi + q_lo + eta2, x = x_hi + x_lo + eps2 (natural units; |q_lo| <= rqa, |eta2| = rq2,
+// |x_lo| <= R + R2, |eps2| <= R2): the exact dot differs from the computed three products by
+// q_lo.x_lo + (q_hi + q_lo).eps2 + eta2.(x_hi + x_lo) + eta2.eps2, and the fp32 accumulation
+// of 3 x ceil(d/16) MMA instructions over partial magnitudes <= (|q| + 2 rqa + rq2)(N + 2R + R2).
+__host__ __device__ inline double key_error_bound_x3(const KeyBound &b, int metric, double qn, double rqa, double rq2) {
+  const double R = b.rmax, R2 = b.rmax2, rho = b.rho, rho2 = b.rho2, N = b.xmax;
+  const double c = (double)(3 * ((b.d + 15) / 16) + 16) * 0x1p-22;
+  double E;
+  if (metric == VRS_COSINE) {   // divided by |x|: |x_lo| <= (rho + rho2)|x|, |eps2| <= rho2 |x|
+    E = rqa * (rho + rho2) + (qn + rq2) * rho2 + rq2 * (1.0 + rho2) +
+        c * (qn + 2.0 * rqa + rq2) * (1.0 + 2.0 * rho + rho2) + 0x1p-21 * qn;
+  } else {
+    const double ed = rqa * (R + R2) + (qn + rq2) * R2 + rq2 * (N + R2) + c * (qn + 2.0 * rqa + rq2) * (N + 2.0 * R + R2);
+    E = metric == VRS_IP ? ed + 0x1p-23 * qn * N : 2.0 * ed + 0x1p-22 * N * N + 0x1p-22 * qn * N;
+  }
+  return E * (1.0 + 0x1p-6) + 0x1p-40 * (qn * N + N * N + qn * qn);
+}
 __host__ __device__ inline double key_error_bound(const KeyBound &b, int metric, double qn, double rq) {
   double R = b.rmax, rho = b.rho, N = b.xmax, c;
   if (b.kind == KEY_TF32) {

@@ -36,9 +36,10 @@ struct QueryFuse {
 };
 using SelectFuse = QueryFuse;
 cudaError_t launch_query16(const QueryFuse &f, cudaStream_t s);
-// the fp16 / bf16 shadow at load; res (device u64[2], zeroed): max |x~ - x|, max |x~ - x| / |x| as double bits
-cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, const float *nx2,
-                          unsigned long long *res, cudaStream_t s);
+// the fp16 / bf16 shadow at load (and with out_lo, fp16 only, the refine pass's low half); res
+// (device u64[4], zeroed): max |x~ - x|, max |x~ - x| / |x|, and the same after hi + lo, as double bits
+cudaError_t launch_shadow(const float *X, int64_t n, int32_t d, int32_t e, int32_t fmt, void *out, void *out_lo,
+                          const float *nx2, unsigned long long *res, cudaStream_t s);
 // select.cu -- K4'/K5' (the query conversion rides along when `fuse` is given)
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
                           void *scratch, cudaStream_t stream, int *launches, const SelectFuse *fuse = nullptr);
@@ -175,6 +176,12 @@ struct FinalizeArgs {
   double *sk = nullptr;            // [q] out: exact sort key of the k-th result (L2: -dist, IP / COS: score)
   int32_t *gcnt = nullptr;         // [q] out: zeroed (the exact fallback's per-group completion counters)
   unsigned long long *stats = nullptr;   // optional vrs_search_options.stats
+  // the refine pass's finalize: row j of the lists is compacted query qmap[j] (its Q row, result
+  // row and certificate); rows j >= *qcount return at once; rq = |q_lo|, rq2 = the residual after lo
+  const int32_t *qmap = nullptr;
+  const int32_t *qcount = nullptr;
+  const float *rq2 = nullptr;
+  int32_t *uncert_seen = nullptr;   // (mapped host flag) set to 1 when a level-0 certificate fails
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches);
 
@@ -239,10 +246,34 @@ struct ExactArgs {
   int64_t *slot_id;
   int32_t *slot_cnt;       // [items_max][qg]
   int32_t qg;              // queries per group (1, 2, 4, 8 or 16)
+  unsigned long long *stats = nullptr;   // [3] += the queries recomputed here
 };
 int exact_group_size(int32_t d, int32_t k);
 int64_t exact_items_max(int64_t q, int qg);
 cudaError_t launch_exact(const ExactArgs &a, cudaStream_t s, int *launches);
+
+// refine.cu -- the refine pass: the uncertified queries, compacted, re-selected
+// with three 16-bit products per dot (q_hi.x_hi + q_hi.x_lo + q_lo.x_hi), then finalized again.
+struct RefineArgs {
+  const uint8_t *cert;     // [q] level-0 certificates
+  const double *sk;        // [q] level-0 k-th sort keys
+  const float *Q;
+  int64_t q;
+  int32_t d, dpad;         // dpad: d rounded up to whole 64-element K blocks
+  int32_t metric;
+  KeyBound kb;             // KEY_H16X3
+  int32_t xexp;
+  int64_t rows;            // rows of qr (whole 128-row tiles of q)
+  int32_t *qlist;          // [q] out: compacted -> original query
+  int32_t *ucount;         // [1] out: the number of uncertified queries
+  uint16_t *qr;            // [rows x 2 dpad] out: fp16 [q_hi | q_lo] per compacted query
+  int32_t *qexp;           // [q] out
+  float *rqa, *rq2;        // [q] out: |q_lo|, |(q_hi + q_lo) 2^-e - q|
+  uint32_t *gtau;          // [q] out: the refine pass's provable key threshold (ordered u32)
+  int64_t gather_cap = 0;  // gathered (cp.async) iff N_sel <= this, else masked
+};
+cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan &plan, void *gemm_scratch,
+                          const void *x_lo, cudaStream_t s, int *launches);
 
 struct MergeArgs {
   const int64_t *cand_ids;

@@ -76,7 +76,7 @@ def test_enomem_mapping(vrs):
         vrs.Index(Xd, A, allocator=_failing_allocator(vrs, 1024))
     assert e.value.status == 4
     # enough for the index (norms + shadow), too little for a search's scratch
-    need = 20000 * (4 + 4) + 20000 * 64 * 2 + 4096
+    need = 20000 * (4 + 4) + 2 * 20000 * 64 * 2 + 4096   # norms + the fp16 shadow's two halves
     ix = vrs.Index(Xd, A, allocator=_failing_allocator(vrs, need))
     with pytest.raises(vrs.VrsError) as e:
         ix.search(torch.from_numpy(Q).cuda(), [], k=10, metric="l2")

@@ -171,3 +171,33 @@ def test_bound_holds_random(vrs, prec, metric):
     assert st["max_key_error_over_bound"] < 1.0, st
     if prec == "fp16":
         assert st["uncertified"] == 0, st
+
+
+def test_refine_pass_certifies_clustered(vrs):
+    """C5-like clustered data, 512 queries from random clusters, a wide window: the fp16
+    selection cannot certify queries whose own cluster is in the window (thousands of rows
+    within fp16's bound of one another); the refine pass (split-fp16 keys, q >= 128)
+    certifies most of them; the rest reach the exact fallback.  Results exact either way."""
+    rng = np.random.default_rng(21)
+    n, d, C = 300000, 256, 256
+    cent = rng.standard_normal((C, d)).astype(np.float32)
+    cid = rng.integers(0, C, n)
+    X = (cent[cid] + 0.1 * rng.standard_normal((n, d))).astype(np.float32)
+    attrs = [(cid + rng.integers(0, 8, n)).astype(np.int32)]
+    qc = rng.integers(0, C, 512)
+    Q = (cent[qc] + 0.1 * rng.standard_normal((512, d))).astype(np.float32)
+    pred = [(0, 7, 200)]
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    Qd = torch.from_numpy(Q).cuda()
+    for call in range(2):   # the first failed certificate enables the refine pass for the index
+        st = vrs.new_stats()
+        ids, dists = ix.search(Qd, pred, k=50, metric="cos", stats=st)
+        torch.cuda.synchronize()
+        s = vrs.read_stats(st)
+        check_topk_exact(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, 50, oracle.COS)
+        assert s["uncertified"] > 50, s
+        assert s["max_key_error_over_bound"] < 1.0, s
+        if call == 0:
+            assert s["exact_fallback"] == s["uncertified"], s     # (no refine yet)
+        else:
+            assert s["exact_fallback"] < s["uncertified"] / 4, s
