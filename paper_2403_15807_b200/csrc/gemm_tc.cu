@@ -59,16 +59,29 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, cap)) return;
   if (n_sel * (int64_t)row_bytes >= cp_min_bytes) return;   // the tensor-core pass fetches them by cp.async
-  // one 16-byte vector per thread, consecutive threads along a row (coalesced);
-  // the row's id is a broadcast load shared by the row's threads
+  // a warp per row (4 rows in flight), lanes along the row's 16-byte vectors (coalesced);
+  // the row id is one broadcast load (round 1 divided a 64-bit element index per vector:
+  // C5 s = 10 %, 128 MB of 512-byte rows took 336 us)
   const int v16 = row_bytes >> 4;
-  const int64_t total = n_sel * v16, stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t r = i / v16;
-    const int v = (int)(i - r * v16);
-    const int4 *src = reinterpret_cast<const int4 *>(static_cast<const char *>(X) + (int64_t)__ldg(ids + r) * row_bytes);
-    reinterpret_cast<int4 *>(static_cast<char *>(xsel) + r * row_bytes)[v] = __ldg(src + v);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const char *Xc = static_cast<const char *>(X);
+  char *Yc = static_cast<char *>(xsel);
+  for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; r0 < n_sel; r0 += warps * 4) {
+    int32_t id[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) id[u] = r0 + u < n_sel ? __ldg(ids + r0 + u) : -1;
+    for (int v = lane; v < v16; v += 32) {
+      int4 w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (id[u] >= 0) w[u] = __ldg(reinterpret_cast<const int4 *>(Xc + (int64_t)id[u] * row_bytes) + v);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (id[u] >= 0) reinterpret_cast<int4 *>(Yc + (r0 + u) * row_bytes)[v] = w[u];
+    }
   }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (norm_dst)   // the rows' norm terms, contiguous, for the bias producer
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_sel; r += stride)
       norm_dst[r] = __ldg(norm_src + __ldg(ids + r));
