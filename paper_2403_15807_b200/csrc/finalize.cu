@@ -1327,18 +1327,11 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
   // small batches: a CTA of 8 warps per query; large: a warp per query
   if (a.q < 4 * kSmCountB200) {
     // (16 warps per query for <= 64 queries with k' >= 64: C4 s = 5 %, Q = 1 finalize 93 -> 48 us;
-    // k' = 32 (C2) gains nothing; 32 warps spill at 64 registers, r02_finalize_width_ab.txt)
+    // k' = 32 (C2) gains nothing; 32 warps measured slower -- they spill at 64 registers,
+    // r02_finalize_width_ab.txt)
     static const int wide_q_env = getenv("VRS_FIN_WIDE_Q") ? atoi(getenv("VRS_FIN_WIDE_Q")) : -1;
     const int wide_q = wide_q_env >= 0 ? wide_q_env : (a.kprime >= 64 ? 64 : 0);
-    static const int wide_w = getenv("VRS_FIN_WIDE_W") ? atoi(getenv("VRS_FIN_WIDE_W")) : 16;   // (A/B: 16 or 32)
-    if (a.q <= wide_q && wide_w == 32) {
-      const size_t smem = sizeof(FinBufs) * 32;
-      static size_t attr32 = 0;
-      const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<32>, smem, attr32);
-      if (e != cudaSuccess) return e;
-      return launch_k(finalize_cta_kernel<32>, dim3((unsigned)a.q), dim3(32 * 32), smem, s, a);
-    }
-    if (a.q <= wide_q && wide_w == 16) {
+    if (a.q <= wide_q) {
       const size_t smem = sizeof(FinBufs) * 16;
       static size_t attr16 = 0;
       const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<16>, smem, attr16);
