@@ -234,7 +234,7 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def oracle_topk_shard(cfg, X_dev, attrs_dev, pred, Q_h, row_offset):
+def oracle_topk_shard(cfg, X_dev, attrs_dev, pred, Q_h, row_offset, threads=0):
     """Oracle top-k of Q_h over one (GPU-resident) shard, reading only the rows the
     ORACLE's own selection keeps: attributes -> host -> oracle.select -> those rows
     copied to the host (torch indexing: plumbing) -> oracle.search over them with the
@@ -254,7 +254,7 @@ def oracle_topk_shard(cfg, X_dev, attrs_dev, pred, Q_h, row_offset):
     for c0 in range(0, cnt, step):   # bounded host memory: the selection in chunks, merged by the oracle
         sl = sel[c0:c0 + step]
         Xs = X_dev.index_select(0, torch.from_numpy(sl).to(X_dev.device)).cpu().numpy()
-        li, ld, _ = oracle.search(Xs, [], [], Q_h, k, cfg.metric)
+        li, ld, _ = oracle.search(Xs, [], [], Q_h, k, cfg.metric, 0, threads)
         gi = np.where(li >= 0, sl[np.clip(li, 0, None)] + row_offset, -1)
         parts_i.append(gi)
         parts_d.append(ld)
@@ -554,9 +554,11 @@ def main():
     if not args.no_parity:
         import oracle
         oracle.build()
-        nq = 3
+        nq = 3 if world == 1 else 2
         Q_h = Qall[:nq].cpu().numpy()
-        pcells = [(s, max(cfg.qs)) for s in cfg.sels]   # (the oracle reads the selection in bounded chunks)
+        # (the oracle reads the selection in bounded chunks; at N > 1 the ranks share the host's
+        # cores, so the largest selectivity is left to the N = 1 run)
+        pcells = [(s, max(cfg.qs)) for s in (cfg.sels if world == 1 else cfg.sels[:-1])]
         res = []
         for s, q in pcells:
             run_cell((s, q))
@@ -566,7 +568,7 @@ def main():
             else:
                 gi_t, gd_t = bufs[(s, q)]
             gi, gd = gi_t[:nq].cpu().numpy(), gd_t[:nq].cpu().numpy()
-            ri, rd = oracle_topk_shard(cfg, X, attrs, preds[s], Q_h, r0)
+            ri, rd = oracle_topk_shard(cfg, X, attrs, preds[s], Q_h, r0, max(1, len(os.sched_getaffinity(0)) // world))
             if world > 1:   # gather every rank's oracle top-k, merge with the oracle's merge
                 ti = torch.from_numpy(ri).to(dev)
                 td = torch.from_numpy(rd).to(dev)
