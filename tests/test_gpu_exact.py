@@ -173,7 +173,8 @@ def test_bound_holds_random(vrs, prec, metric):
         assert st["uncertified"] == 0, st
 
 
-def test_refine_pass_certifies_clustered(vrs):
+@pytest.mark.parametrize("metric", [oracle.COS, oracle.IP, oracle.L2])
+def test_refine_pass_certifies_clustered(vrs, metric):
     """C5-like clustered data, 512 queries from random clusters, a wide window: the fp16
     selection cannot certify queries whose own cluster is in the window (thousands of rows
     within fp16's bound of one another); the refine pass (split-fp16 keys, q >= 128)
@@ -191,12 +192,15 @@ def test_refine_pass_certifies_clustered(vrs):
     Qd = torch.from_numpy(Q).cuda()
     for call in range(2):   # the first failed certificate enables the refine pass for the index
         st = vrs.new_stats()
-        ids, dists = ix.search(Qd, pred, k=50, metric="cos", stats=st)
+        ids, dists = ix.search(Qd, pred, k=50, metric={oracle.COS: "cos", oracle.IP: "ip", oracle.L2: "l2"}[metric],
+                               stats=st)
         torch.cuda.synchronize()
         s = vrs.read_stats(st)
-        check_topk_exact(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, 50, oracle.COS)
-        assert s["uncertified"] > 50, s
+        check_topk_exact(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, 50, metric)
         assert s["max_key_error_over_bound"] < 1.0, s
+        if metric == oracle.L2:   # (squared distances spread enough within a cluster: level 0 certifies)
+            continue
+        assert s["uncertified"] > 50, s
         if call == 0:
             assert s["exact_fallback"] == s["uncertified"], s     # (no refine yet)
         else:
