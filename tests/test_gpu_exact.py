@@ -198,7 +198,7 @@ def test_refine_pass_certifies_clustered(vrs, metric):
         s = vrs.read_stats(st)
         check_topk_exact(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, 50, metric)
         assert s["max_key_error_over_bound"] < 1.0, s
-        if metric == oracle.L2:   # (squared distances spread enough within a cluster: level 0 certifies)
+        if metric != oracle.COS:   # (IP / L2 spread enough within a cluster: level 0 certifies them)
             continue
         assert s["uncertified"] > 50, s
         if call == 0:
