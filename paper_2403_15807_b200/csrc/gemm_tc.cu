@@ -44,7 +44,7 @@ namespace vrs {
 
 // Late materialization ("(re-)materialized into dense
 // vectors"): X_sel[r] = X[ids[r]] (rows of row_bytes, a multiple of 16: the fp32
-// corpus or its bf16 shadow), one warp per row, 16-byte vector copies.
+// corpus or its 16-bit shadow), one warp per row, 16-byte vector copies.
 // HBM-bound: 2 * row_bytes per selected row.
 __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict__ X, int32_t row_bytes,
                                                           const int32_t *__restrict__ ids,
@@ -433,8 +433,11 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // (d >= 512 below 1024 queries: the main pass is HBM-bound, its epilogue has slack -- the
     // sparsest probe; C3 s = 10 %, Q = 64: the dense probe took 193 us of a 608 us search)
     const bool hbm_bound = a.d >= 512 && a.q < 1024;
+    // (d >= 1024, q >= 1024: every 32nd tile -- C4: probe 5.6 -> 3.2 ms per step, main pass and
+    // finalize within noise, +1 % overall, r02_probe_step_c4_ab.txt)
     pp.tile_step = probe_env > 0 ? probe_env
-                                 : (a.q >= 1024 ? (a.d >= 512 ? 16 : 8) : (a.q >= 64 && !hbm_bound ? tc::PROBE_STEP : 32));
+                                 : (a.q >= 1024 ? (a.d >= 1024 ? 32 : (a.d >= 512 ? 16 : 8))
+                                                : (a.q >= 64 && !hbm_bound ? tc::PROBE_STEP : 32));
     // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
     static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
     pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 && !hbm_bound ? 8 : 0);

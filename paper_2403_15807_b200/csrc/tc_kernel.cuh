@@ -209,7 +209,7 @@ struct TcParams {
   int32_t P_main, min_p_main;   // probe: the main pass's splits (its span sets the density); 0 = P
   int32_t g4;              // gather mode: 1 = TMA gather4 from X by id (tmap_g), 2 = cp.async from X by id
                            // (xrows), 0 = TMA tiles from the X_sel copy
-  const void *xrows;       // g4 == 2: the rows' base (fp32 corpus or its bf16 shadow), row_bytes each
+  const void *xrows;       // g4 == 2: the rows' base (fp32 corpus or its 16-bit shadow), row_bytes each
   int32_t row_bytes;
   int64_t cp_min_bytes;    // g4 == 2: cp.async only when the selection holds >= this many row bytes
                            // (below it gather_copy_kernel made X_sel and TMA tiles stream it)

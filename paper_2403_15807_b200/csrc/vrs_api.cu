@@ -611,7 +611,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
   vrs_status st = check_precision(ix, prec_req);
   if (st != VRS_OK) return st;
-  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
+  const bool use16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
   PredDev pd;
   st = make_pred(ix, pred, &pd);
   if (st != VRS_OK) return st;
@@ -637,7 +637,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // the TMA paths need 16-byte aligned rows and bases
   const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
   if (path != VRS_PATH_SCAN && tma_ok) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
-  // (measured on C2: the tensor-core pass over the bf16 shadow is HBM-bound and beats
+  // (measured on C2: the tensor-core pass over the 16-bit shadow is HBM-bound and beats
   // the fp32 FFMA scan already at q = 1 -- it reads half the bytes)
   if (path == VRS_PATH_AUTO) path = gp.ok ? VRS_PATH_GEMM : VRS_PATH_SCAN;
   if (path == VRS_PATH_GEMM && !gp.ok) return fail(VRS_EUNSUPPORTED, "tensor-core path does not support this shape");
@@ -665,8 +665,8 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   // Sec. 6): selectivity 1/3 while the pass is HBM-bound (q < 256), ~0.45 at
   // q = 256, 0.9 once it is tensor / TMEM-bound (q >= 1024).  The buffer holds
   // at most 16 GiB of rows.
-  const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
-  const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;   // bf16 queries, whole 128-row tiles
+  const int64_t row_bytes = (int64_t)d * (use16 ? 2 : 4);
+  const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;   // 16-bit queries, whole 128-row tiles
   const RowPlan rp = path == VRS_PATH_GEMM ? row_plan(q, gp.qtiles, n, row_bytes, rows_req, identity)
                                            : RowPlan{0, 0, INT64_MAX};
   const int64_t xsel_cap = rp.gather_cap;
@@ -690,7 +690,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   static const int refine_qmin = getenv("VRS_REFINE_QMIN") ? atoi(getenv("VRS_REFINE_QMIN")) : 128;
   static const int refine_mode = !getenv("VRS_REFINE") ? 0 : (strcmp(getenv("VRS_REFINE"), "always") == 0 ? 1 : -1);
   const bool refine_seen = refine_mode == 1 || (refine_mode == 0 && ix->uncert_seen_host && *ix->uncert_seen_host != 0);
-  const bool refine = path == VRS_PATH_GEMM && use_bf16 && ix->xl != nullptr && q >= refine_qmin && refine_seen &&
+  const bool refine = path == VRS_PATH_GEMM && use16 && ix->xl != nullptr && q >= refine_qmin && refine_seen &&
                       (prec_req == VRS_PREC_DEFAULT || prec_req == VRS_PREC_FP16);
   const int32_t rf_dpad = (d + 63) / 64 * 64;
   const size_t rf_rows = (size_t)gp.qtiles * 128;
@@ -700,7 +700,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                                    local_ids * 4, part_entries * 4, part_entries * 4,
                                    path == VRS_PATH_GEMM ? gemm_scratch_bytes(gp, q, kprime) : 0,
                                    (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4,
-                                   use_bf16 && path == VRS_PATH_GEMM ? qpad_bytes : 0,
+                                   use16 && path == VRS_PATH_GEMM ? qpad_bytes : 0,
                                    (size_t)q * 4, (size_t)q * 4, (size_t)q, (size_t)q * 8, (size_t)q * 4,
                                    ex_slots * k * 8, ex_slots * k * 8, ex_slots * 4,
                                    refine ? (size_t)q * 4 : 0, refine ? (size_t)16 : 0, refine ? rf_rows * 2 * (size_t)rf_dpad * 2 : 0,
@@ -719,7 +719,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   void *gemm_scr = path == VRS_PATH_GEMM ? cv.take<char>(gemm_scratch_bytes(gp, q, kprime)) : nullptr;
   void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
   float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
-  void *qb = use_bf16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
+  void *qb = use16 && path == VRS_PATH_GEMM ? cv.take<char>(qpad_bytes) : nullptr;
   int32_t *qexp = cv.take<int32_t>((size_t)q);
   float *rq = cv.take<float>((size_t)q);
   uint8_t *cert = cv.take<uint8_t>((size_t)q);
@@ -735,7 +735,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *rf_rqa = refine ? cv.take<float>((size_t)q) : nullptr;
   float *rf_rq2 = refine ? cv.take<float>((size_t)q) : nullptr;
   uint32_t *rf_gtau = refine ? cv.take<uint32_t>((size_t)q) : nullptr;
-  const bool h16 = use_bf16 && path == VRS_PATH_GEMM;   // (16-bit query operand of the tensor-core pass)
+  const bool h16 = use16 && path == VRS_PATH_GEMM;   // (16-bit query operand of the tensor-core pass)
 
   int launches = 0;
   GemmArgs gemm_args{};   // (the tensor-core pass's arguments, reused by the refine pass)
@@ -749,7 +749,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     }
     ScanArgs a{ix->X, n, d, sel_ids, count, queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime,
                part_key, part_id, P};
-    if (use_bf16) {   // the scan streams the 16-bit shadow (half the bytes) unless TF32 (= fp32 rows) is asked for
+    if (use16) {   // the scan streams the 16-bit shadow (half the bytes) unless TF32 (= fp32 rows) is asked for
       a.Xh = ix->xb;
       a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
       a.xexp = ix->xexp;
@@ -759,15 +759,15 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   } else {
     // tensor-core path: gathered selection or bitmap-masked full tiles, chosen on the device
     const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
-    if (!identity) {   // (the bf16 query conversion rides along)
+    if (!identity) {   // (the 16-bit query conversion rides along)
       ProfScope ps("select", stream);
-      const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb, qexp, rq);
+      const SelectFuse fz = select_fuse(ix, queries, q, gp, use16, qb, qexp, rq);
       if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
       else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
     }
     GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
                queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, kprime, part_key, part_id, P,
-               use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+               use16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
     a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
     a.xexp = ix->xexp;
     a.qexp = qexp;
@@ -793,7 +793,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   }
   // the certificate (finalize) and its fallback (exact.cu): every query's result is the
   // exact top-k of the definition -- no host synchronisation
-  f.kb = key_bound(ix, path == VRS_PATH_GEMM, use_bf16);
+  f.kb = key_bound(ix, path == VRS_PATH_GEMM, use16);
   f.qexp = h16 ? qexp : nullptr;
   f.rq = h16 ? rq : nullptr;
   f.xexp = h16 ? ix->xexp : 0;
@@ -835,7 +835,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     CUDA_TRY(launch_exact(ea, stream, &launches));
   }
   g_last_path = path;
-  g_last_prec = use_bf16 ? ix->prec16 : (path == VRS_PATH_GEMM ? VRS_PREC_TF32 : VRS_PREC_DEFAULT);
+  g_last_prec = use16 ? ix->prec16 : (path == VRS_PATH_GEMM ? VRS_PREC_TF32 : VRS_PREC_DEFAULT);
   g_last_launches = launches;
   return VRS_OK;
 }
@@ -863,7 +863,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const int prec_req = opts ? opts->precision : VRS_PREC_DEFAULT;
   vrs_status st = check_precision(ix, prec_req);
   if (st != VRS_OK) return st;
-  const bool use_bf16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
+  const bool use16 = ix->xb && prec_req != VRS_PREC_TF32;   // (16-bit shadow: fp16 or bf16)
   PredDev pd;
   st = make_pred(ix, pred, &pd);
   if (st != VRS_OK) return st;
@@ -890,7 +890,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
     return fail(VRS_EUNSUPPORTED, "range search runs on the tensor-core path: d %% 4 == 0 and 16-byte aligned rows");
   const bool identity = (pd.n == 0);
   const size_t nwords = (size_t)((n + 31) / 32);
-  const int64_t row_bytes = (int64_t)d * (use_bf16 ? 2 : 4);
+  const int64_t row_bytes = (int64_t)d * (use16 ? 2 : 4);
   const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;
   const RowPlan rp = row_plan(q, gp.qtiles, n, row_bytes, rows_req, identity);   // (as in vrs_search_ex)
   const int64_t xsel_cap = rp.gather_cap;
@@ -901,7 +901,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const bool sel_local = want_local && !identity && select_chunks(n) <= kSelFinishMaxChunks;
   const size_t local_ids = sel_local ? (size_t)select_chunks(n) * kSelChunkRows : 0;
   st = scratch_alloc(scr, carve_size({nwords * 4, identity ? 0 : (size_t)n * 4, 8, select_scratch_bytes(n), local_ids * 4,
-                                      (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4, use_bf16 ? qpad_bytes : 0,
+                                      (size_t)(xsel_rows * row_bytes), (size_t)xsel_rows * 4, use16 ? qpad_bytes : 0,
                                       (size_t)q * 4,
                                       (size_t)L * q * 4, ((size_t)L * q + 1) * 8, (size_t)q * 4, (size_t)q * 4,
                                       (size_t)q * 4}));
@@ -914,7 +914,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int32_t *ids_local = sel_local ? cv.take<int32_t>(local_ids) : nullptr;
   void *xsel = xsel_rows > 0 ? cv.take<char>((size_t)(xsel_rows * row_bytes)) : nullptr;
   float *xsel_norm = xsel_rows > 0 ? cv.take<float>((size_t)xsel_rows) : nullptr;
-  void *qb = use_bf16 ? cv.take<char>(qpad_bytes) : nullptr;
+  void *qb = use16 ? cv.take<char>(qpad_bytes) : nullptr;
   int32_t *qexp = cv.take<int32_t>((size_t)q);
   float *rq = cv.take<float>((size_t)q);
   RangeState r;
@@ -923,7 +923,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   r.coff = cv.take<int64_t>((size_t)L * q + 1);
   r.kept = cv.take<int32_t>((size_t)q);
   r.tau = tau;
-  r.kb = key_bound(ix, true, use_bf16);
+  r.kb = key_bound(ix, true, use16);
   r.offsets = offsets;
   r.ids = ids;
   r.dists = dists;
@@ -936,13 +936,13 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   int launches = 0;
   const int32_t rows_mode = rows_req == VRS_ROWS_MASKED ? 1 : (rows_req == VRS_ROWS_GATHER ? 2 : 0);
   if (!identity) {
-    const SelectFuse fz = select_fuse(ix, queries, q, gp, use_bf16, qb, qexp, rq);
+    const SelectFuse fz = select_fuse(ix, queries, q, gp, use16, qb, qexp, rq);
     if (sel_local) CUDA_TRY(launch_select_local(pd, n, bitmap, ids_local, sel_scratch, stream, &launches, &fz));
     else CUDA_TRY(launch_select(pd, n, bitmap, sel_ids, count, sel_scratch, stream, &launches, &fz));
   }
   GemmArgs a{ix->X, n, d, sel_ids, count, identity ? nullptr : bitmap, rows_mode, xsel, xsel_cap, xsel_norm,
              queries, q, ix->nx2, ix->inv_nx, (int32_t)metric, 32, nullptr, nullptr, gp.P,
-             use_bf16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
+             use16 ? 1 : 0, ix->xb, qb, identity ? 0 : 1};
   a.fmt16 = ix->prec16 == VRS_PREC_FP16 ? 0 : 1;
   a.xexp = ix->xexp;
   a.qexp = qexp;
@@ -967,7 +967,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   CUDA_TRY(cudaStreamSynchronize(stream));
   *total = R;
   g_last_path = VRS_PATH_GEMM;
-  g_last_prec = use_bf16 ? ix->prec16 : VRS_PREC_TF32;
+  g_last_prec = use16 ? ix->prec16 : VRS_PREC_TF32;
   if (R > capacity) {
     g_last_launches = launches;
     return fail(VRS_ERANGE, "%lld results > capacity %lld", (long long)R, (long long)capacity);
