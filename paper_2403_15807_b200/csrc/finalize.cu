@@ -591,31 +591,42 @@ using FinBufs = FinBufsT<kBufCap, 512>;
 // 32): the warp's buffer ends with at most K entries (or all it saw).
 // (keep: the buffer is cut to the k' best only when it holds more than `keep`
 // entries -- the CTA tree merge takes up to 32E unsorted survivors per warp)
-template <int CAP, int HIST>
-__device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP, HIST> &B,
-                          int keep = -1) {
+template <bool FOLD, int CAP, int HIST>
+__device__ int fin_stream_impl(const FinalizeArgs &a, int64_t j, int first_group, int group_step, FinBufsT<CAP, HIST> &B,
+                               int keep) {
   const int lane = threadIdx.x & 31;
   const int K = a.kprime;
   // (every list's count is written -- lists of unused splits as 0 -- so all a.lists
   // are read without waiting on the selection count)
-  const int lists = a.lists;
+  // (the refine pass's lists: F groups of a.lists at list rows f Qa + j, refine_fold)
+  const int lists0 = a.lists;
+  int lists = lists0;
+  int64_t Qa = 0;
+  if (FOLD) {
+    const RefineFold rf = refine_fold(__ldg(a.qcount), a.fold_qtiles, a.q);
+    lists = lists0 * rf.F;
+    Qa = rf.Qa;
+  }
+  auto lrow = [&](int l) -> int64_t {
+    return !FOLD ? (int64_t)l * a.q + j : (int64_t)(l % lists0) * a.q + (int64_t)(l / lists0) * Qa + j;
+  };
   uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
   if (a.sorted && K <= a.kread) {
     for (int l = lane; l < lists; l += 32) {
-      const int64_t o = ((int64_t)l * a.q + j) * a.stride + (K - 1);
+      const int64_t o = lrow(l) * a.stride + (K - 1);
       if (__ldg(a.id + o) >= 0) thr = max(thr, ordered_u32(__ldg(a.key + o)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) thr = max(thr, __shfl_xor_sync(0xffffffffu, thr, o));
   }
   int n = 0;
-  auto count_of = [&](int l) { return l < lists ? (a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread) : 0; };
+  auto count_of = [&](int l) { return l < lists ? (a.cnt ? __ldg(a.cnt + lrow(l)) : a.kread) : 0; };
   int c_next = count_of(first_group * 32 + lane);   // (the next group's counts load under this group's keys)
   for (int l0 = first_group * 32; l0 < lists; l0 += group_step * 32) {
     const int l = l0 + lane;
     const int c = c_next;
     c_next = count_of(l0 + group_step * 32 + lane);
-    const int64_t base = ((int64_t)(l < lists ? l : 0) * a.q + j) * a.stride;
+    const int64_t base = lrow(l < lists ? l : 0) * a.stride;
     for (int r0 = 0; __any_sync(0xffffffffu, r0 < c); r0 += 8) {
       float kv[8];
       int32_t iv[8];
@@ -649,6 +660,12 @@ __device__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int
   __syncwarp();
   if (n > (keep < 0 ? K : keep)) warp_keep_best_fast<HIST>(B.key, B.id, n, K, B.hist);
   return n;
+}
+template <int CAP, int HIST>
+__device__ __forceinline__ int fin_stream(const FinalizeArgs &a, int64_t j, int first_group, int group_step,
+                                          FinBufsT<CAP, HIST> &B, int keep = -1) {
+  if (a.qcount != nullptr && a.fold_qtiles > 0) return fin_stream_impl<true>(a, j, first_group, group_step, B, keep);
+  return fin_stream_impl<false>(a, j, first_group, group_step, B, keep);
 }
 
 // Step 4 for candidates c0, c0 + cstep*U ... of ids[0..m): the warp reads each
@@ -875,7 +892,7 @@ __global__ void __launch_bounds__(kFinGroup * 32, SEL <= 64 ? VRS_FIN_MINB : 1) 
   if (j >= a.q) return;   // whole warps only; no block-wide synchronisation below
   if (a.qcount && j >= __ldg(a.qcount)) return;
   const int64_t jq = a.qmap ? __ldg(a.qmap + j) : j;   // (the refine: compacted row -> query)
-  const int m = fin_stream(a, j, 0, 1, s_buf[w]);
+  const int m = fin_stream_impl<false>(a, j, 0, 1, s_buf[w], -1);   // (the refine's finalize runs the CTA kernel)
   const double qq = fin_qq(a, jq);
   CertQ cq{0.0, 0.0, 1.0};
   float kmin = -INFINITY;
@@ -1325,13 +1342,14 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches) {
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
-  if (a.q < 4 * kSmCountB200) {
+  // (the refine's finalize: the CTA kernel -- its queries read F x the lists, refine_fold)
+  if (a.q < 4 * kSmCountB200 || a.fold_qtiles > 0) {
     // (16 warps per query for <= 64 queries with k' >= 64: C4 s = 5 %, Q = 1 finalize 93 -> 48 us;
     // k' = 32 (C2) gains nothing; 32 warps measured slower -- they spill at 64 registers,
     // r02_finalize_width_ab.txt)
     static const int wide_q_env = getenv("VRS_FIN_WIDE_Q") ? atoi(getenv("VRS_FIN_WIDE_Q")) : -1;
     const int wide_q = wide_q_env >= 0 ? wide_q_env : (a.kprime >= 64 ? 64 : 0);
-    if (a.q <= wide_q) {
+    if (a.q <= wide_q && a.fold_qtiles == 0) {
       const size_t smem = sizeof(FinBufs) * 16;
       static size_t attr16 = 0;
       const cudaError_t e = ensure_smem_attr(finalize_cta_kernel<16>, smem, attr16);

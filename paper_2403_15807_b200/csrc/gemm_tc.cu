@@ -339,6 +339,8 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
       !(g4 ? make_map(&L->mg, xsrc, a.n, a.d, 1, bf, a.fmt16)
            : make_map(&L->mg, xcap > 0 ? a.xsel : xsrc, xcap > 0 ? xcap : a.n, a.d, tc::BN, bf, a.fmt16)))
     return cudaErrorInvalidValue;
+  L->ml = L->mx;   // (the refine pass's x_lo maps; launch_refine sets them)
+  L->mlg = L->mx;
   TcParams &p = L->p;
   memset(&p, 0, sizeof p);
   p.nseg = 1;   // (one K segment; the refine pass sets 3)
@@ -390,7 +392,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
     e = launch_select_finish(a, xcap, xcap > 0 ? (int)p.allow_gather : 0, xsrc, a.d * (bf ? 2 : 4), !g4, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
-  } else if (xcap > 0 && p.allow_gather && !g4) {
+  } else if (xcap > 0 && p.allow_gather && !g4 && !a.xsel_ready) {
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
                  (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
@@ -587,19 +589,35 @@ cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan
                           const void *x_lo, cudaStream_t s, int *launches) {
   cudaError_t e = launch_k(refine_prep_kernel, dim3(1), dim3(1024), 0, s, r);
   if (e != cudaSuccess) return e;
-  // row delivery: gathered by cp.async (the hi and lo halves fetched by id, any query-tile
-  // count -- the refine has few tiles) up to the masked break-even, else masked tiles
+  // row delivery: with xsel_lo, level 0's (the same device decision from the same count):
+  // X_sel (its x_hi rows, still in place) + X_sel_lo (x_lo rows, copied here) by TMA, rows by
+  // id (cp.async), or masked tiles.  Without (no memory for it): gathered by cp.async (hi and
+  // lo halves by id) up to the masked break-even, else masked tiles.
   GemmArgs b = a;
-  b.masked = 0;
-  b.xsel_cap = a.ids ? r.gather_cap : 0;
-  b.xsel = nullptr;
   b.prepped = 1;
-  b.cp_min_bytes = 0;
+  b.xsel_ready = 1;
+  const bool own = r.xsel_lo != nullptr && a.xsel != nullptr;
+  if (!own) {
+    b.masked = 0;
+    b.xsel_cap = a.ids ? r.gather_cap : 0;
+    b.xsel = nullptr;
+    b.cp_min_bytes = 0;
+  }
   TcLaunch L;
   e = tc_prepare(b, plan, s, launches, &L);
   if (e != cudaSuccess) return e;
-  if (!make_map(&L.mq, r.qr, r.rows, 2 * r.dpad, tc::BM, true, 0) || !make_map(&L.mg, x_lo, a.n, a.d, tc::BN, true, 0))
+  if (!make_map(&L.mq, r.qr, r.rows, 2 * r.dpad, tc::BM, true, 0) || !make_map(&L.ml, x_lo, a.n, a.d, tc::BN, true, 0))
     return cudaErrorInvalidValue;
+  L.mlg = L.ml;
+  if (own) {
+    if (!make_map(&L.mlg, r.xsel_lo, L.p.xsel_cap, a.d, tc::BN, true, 0)) return cudaErrorInvalidValue;
+    ProfScope pg("refine.gather", s);   // x_lo rows of the selection (exactly when level 0 copied x_hi)
+    e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, x_lo, a.d * 2, a.ids, a.count, a.n,
+                 (int)L.p.allow_gather, L.p.xsel_cap, r.xsel_lo, (const float *)nullptr, (float *)nullptr,
+                 L.p.cp_min_bytes);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+  }
   const GemmScratch gs = carve_gemm(gemm_scratch, plan, a.q, a.kprime);
   TcParams &p = L.p;
   p.cand_key = gs.cand_key;   // (level 0's lists: its finalize has read them)
@@ -612,8 +630,10 @@ cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan
   p.a_lo_off = r.dpad;
   p.qcount = r.ucount;
   p.xrows_lo = x_lo;
-  p.g4 = 2;
-  p.cp_min_bytes = 0;
+  if (!own) {
+    p.g4 = 2;
+    p.cp_min_bytes = 0;
+  }
   L.ar = false;
   {
     ProfScope pf("refine.main", s);

@@ -234,8 +234,8 @@ struct TcParams {
   const int32_t *qexp;     // 16-bit operands: [q] per-query exponents e_q (nullptr: TF32, no scaling)
   int32_t xexp;            // the shadow's exponent e_x
   // refine pass: K runs over nseg = 3 segments -- q_hi.x_hi, q_hi.x_lo (x_lo
-  // through tmap_g), q_lo.x_hi (q_lo at column a_lo_off of the query map); query tiles at or
-  // past *qcount (the device-side count of compacted queries) do no work
+  // through tmap_gl gathered / tmap_xl masked / xrows_lo by id), q_lo.x_hi (q_lo at column
+  // a_lo_off of the query map); the grid folds onto the *qcount compacted queries' tiles
   int32_t nseg = 1;
   int32_t a_lo_off = 0;
   const int32_t *qcount = nullptr;
@@ -324,7 +324,8 @@ constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the li
 template <bool AR, int MODE, bool ROWSCALE, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
-                   const __grid_constant__ CUtensorMap tmap_g, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
+                   const __grid_constant__ CUtensorMap tmap_gl, TcParams p) {
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
@@ -355,8 +356,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qtile = blockIdx.x % p.qtiles;
-  const int split = blockIdx.x / p.qtiles;
+  int qtile = blockIdx.x % p.qtiles;
+  int split = blockIdx.x / p.qtiles;
   if (threadIdx.x == 0) TC_TL(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
@@ -368,7 +369,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_q); prefetch_tmap(&tmap_x); prefetch_tmap(&tmap_g); }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_q);
+    prefetch_tmap(&tmap_x);
+    prefetch_tmap(&tmap_g);
+    if (p.nseg > 1) { prefetch_tmap(&tmap_xl); prefetch_tmap(&tmap_gl); }
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
                  "n"(TMEM_COLS)
@@ -383,6 +389,23 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) TC_TL(1);
+  // the refine pass (qcount: its compacted query count, on the device): the grid folds
+  // onto the active query tiles, P F row splits per tile (refine_fold); split s writes
+  // list split s mod P at list rows (s / P) Qa + query
+  int64_t P_rows = p.P, lrow = 0;
+  int lsplit = split;
+  bool q_idle = false, fold_out = false;
+  if (p.qcount != nullptr) {
+    const int64_t qc = __ldg(p.qcount);
+    const RefineFold rf = refine_fold(qc, p.qtiles, p.q);
+    qtile = blockIdx.x % rf.tiles;
+    split = blockIdx.x / rf.tiles;
+    P_rows = (int64_t)p.P * rf.F;
+    fold_out = split >= P_rows;
+    lsplit = split % p.P;
+    lrow = (int64_t)(split / p.P) * rf.Qa;
+    q_idle = qc == 0 || fold_out;
+  }
   // Selectivity-driven row delivery (decided on the device, no host sync):
   //  gather: the selection was materialised densely (gather_copy_kernel, late
   //          materialization) and streams by TMA from X_sel; ids map rows back
@@ -397,7 +420,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int64_t row_tiles = (n_space + BN - 1) / BN;
   // splits actually used (splits_used): >= 4 row tiles per item when the
   // (device-side) row space allows; CTAs of unused splits publish empty lists
-  const int64_t p_eff = used_splits(row_tiles, p.P, p.min_span, p.min_p);
+  const int64_t p_eff = used_splits(row_tiles, P_rows, p.min_span, p.min_p);
   const int64_t t_begin = split < p_eff ? (row_tiles * split) / p_eff : 0;
   const int64_t t_end = split < p_eff ? (row_tiles * (split + 1)) / p_eff : 0;
   const int64_t span = t_end - t_begin;
@@ -410,7 +433,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     step_cap = std::min<int64_t>(step_cap, std::max<int64_t>(2, main_span / p.probe_div));
   }
   const int step = MODE == MODE_PROBE ? (int)std::min<int64_t>(step_cap, std::max<int64_t>(1, span)) : 1;
-  const bool q_idle = p.qcount != nullptr && (int64_t)qtile * BM >= (int64_t)__ldg(p.qcount);
   const int ntiles = q_idle ? 0 : (int)((span + step - 1) / step);
   const int nkb = p.nk * p.nseg;   // K blocks per tile (3 segments in the refine pass)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
@@ -550,7 +572,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           uint8_t *st = b_base + stage * SSTRIDE;
           mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
           if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
-          tma_load_2d(st + BOFF, (gather || seg == 1) ? &tmap_g : &tmap_x, &full_bar[stage], kk * KE, row0);
+          // (refine: x_lo in segment 1 -- gathered into its own X_sel copy, or masked over the full x_lo)
+          const CUtensorMap *bmap = seg == 1 ? (gather ? &tmap_gl : &tmap_xl) : (gather ? &tmap_g : &tmap_x);
+          tma_load_2d(st + BOFF, bmap, &full_bar[stage], kk * KE, row0);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
@@ -714,8 +738,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int half = ew >> 2;                      // which BN / LPS of the tile's columns
     const int m = quad * 32 + lane;                // query row within the tile
     const int64_t qg = (int64_t)qtile * BM + m;    // global query index
-    const bool active = qg < p.q;
-    const int list = split * LPS + half;           // candidate list index
+    const bool active = qg < p.q && !fold_out;
+    const int list = lsplit * LPS + half;          // candidate list index
     // key scale: L2 keys are natural units, 2<q,x> - |x|^2, so the 16-bit pass undoes its
     // power-of-two operand scales 2^(e_q + e_x) here (exact); IP / COS keys stay in the
     // query's scaled domain D = 2^(e_q + e_x) -- the order per query is unchanged, and
@@ -724,7 +748,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const float sc = p.metric == VRS_L2 ? (p.qexp != nullptr && active ? ldexpf(2.f, -(__ldg(p.qexp + qg) + p.xexp)) : 2.f)
                                         : 1.f;
     const int64_t cbase = MODE == MODE_RFILL ? (active ? p.coff[qg * (LPS * p.P) + list] : 0)
-                                             : ((int64_t)list * p.q + (active ? qg : 0)) * p.cap;
+                                             : ((int64_t)list * p.q + (active ? lrow + qg : 0)) * p.cap;
     float *ckey = p.cand_key + (MODE == MODE_RFILL ? 0 : cbase);
     int32_t *cid = p.cand_id + cbase;
     float *wst = kstage + ew * 32 * STAGE_COLS;
@@ -760,7 +784,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int owner = __ffs(need) - 1;
         need &= need - 1;
         const int oc = __shfl_sync(0xffffffffu, cnt, owner);
-        const int64_t ob = ((int64_t)list * p.q + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
+        const int64_t ob = ((int64_t)list * p.q + lrow + (int64_t)qtile * BM + quad * 32 + owner) * p.cap;
         const float nt = compact_lane(p.cand_key + ob, p.cand_id + ob, oc, p.kp, whist);
         TC_STAT(++st_comp);
         if (lane == owner) {
@@ -993,7 +1017,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < SLOTS; i += 4) dst[i / 4] = make_float4(smax[i], smax[i + 1], smax[i + 2], smax[i + 3]);
       } else if (MODE != MODE_RFILL) {
-        p.cand_cnt[(int64_t)list * p.q + qg] = cnt;
+        p.cand_cnt[(int64_t)list * p.q + lrow + qg] = cnt;
       }
     }
   }
@@ -1021,10 +1045,11 @@ static int tc_min_span() {
 }
 
 // ---------------------------------------------------------------- launch plumbing
-// Everything a tensor-core pass launch needs: the three tensor maps (queries,
-// rows, gathered rows), the mode-independent parameters and the variant flags.
+// Everything a tensor-core pass launch needs: the tensor maps (queries, rows, gathered
+// rows; the refine pass's x_lo rows and gathered x_lo rows -- copies of mx otherwise),
+// the mode-independent parameters and the variant flags.
 struct TcLaunch {
-  CUtensorMap mq, mx, mg;
+  CUtensorMap mq, mx, mg, ml, mlg;
   TcParams p;
   bool bf, ar, rowscale;
 };
@@ -1032,10 +1057,11 @@ struct TcLaunch {
 // when the selection is materialised (gemm_tc.cu).
 cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L);
 
-typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
 template <bool AR, int MODE, bool ROWSCALE, bool BF>
 __global__ void tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
-                               const __grid_constant__ CUtensorMap tmap_g, TcParams p);
+                               const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
+                               const __grid_constant__ CUtensorMap tmap_gl, TcParams p);
 template <int MODE, bool BF>
 static TcKernel pick_kernel(bool ar, bool rowscale) {
   return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF> : tc_topk_kernel<true, MODE, false, BF>)
@@ -1059,7 +1085,7 @@ static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStr
   TcParams p2 = pr;
   p2.stats = want_stats ? stats : nullptr;
   if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
-  e = launch_k(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, L.mq, L.mx, L.mg, p2);
+  e = launch_k(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, L.mq, L.mx, L.mg, L.ml, L.mlg, p2);
   if (want_stats) {
     unsigned long long h[4];
     cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);

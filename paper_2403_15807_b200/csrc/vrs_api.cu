@@ -693,6 +693,10 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const bool refine = path == VRS_PATH_GEMM && use16 && ix->xl != nullptr && q >= refine_qmin && refine_seen &&
                       (prec_req == VRS_PREC_DEFAULT || prec_req == VRS_PREC_FP16);
   const int32_t rf_dpad = (d + 63) / 64 * 64;
+  // the refine's X_sel_lo (x_lo rows of the selection, beside level 0's X_sel of x_hi rows),
+  // when both fit the free-memory share the X_sel alone is capped by; else cp.async by id
+  const int64_t xlo_rows = refine && xsel_rows > 0 && cap_by_free_memory(xsel_rows, 2 * row_bytes) == xsel_rows
+                               ? xsel_rows : 0;
   const size_t rf_rows = (size_t)gp.qtiles * 128;
   const int64_t ex_items = exact_items_max(q, ex_qg);
   const size_t ex_slots = (size_t)ex_items * ex_qg;
@@ -705,7 +709,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                                    ex_slots * k * 8, ex_slots * k * 8, ex_slots * 4,
                                    refine ? (size_t)q * 4 : 0, refine ? (size_t)16 : 0, refine ? rf_rows * 2 * (size_t)rf_dpad * 2 : 0,
                                    refine ? (size_t)q * 4 : 0, refine ? (size_t)q * 4 : 0, refine ? (size_t)q * 4 : 0,
-                                   refine ? (size_t)q * 4 : 0});
+                                   refine ? (size_t)q * 4 : 0, (size_t)(xlo_rows * row_bytes)});
   st = scratch_alloc(scr, bytes);
   if (st != VRS_OK) return st;
   Carve cv(scr.ptr);
@@ -735,6 +739,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   float *rf_rqa = refine ? cv.take<float>((size_t)q) : nullptr;
   float *rf_rq2 = refine ? cv.take<float>((size_t)q) : nullptr;
   uint32_t *rf_gtau = refine ? cv.take<uint32_t>((size_t)q) : nullptr;
+  void *rf_xsel_lo = xlo_rows > 0 ? cv.take<char>((size_t)(xlo_rows * row_bytes)) : nullptr;
   const bool h16 = use16 && path == VRS_PATH_GEMM;   // (16-bit query operand of the tensor-core pass)
 
   int launches = 0;
@@ -811,6 +816,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
                   (int64_t)rf_rows, rf_qlist, rf_count, rf_qr, rf_qexp, rf_rqa, rf_rq2, rf_gtau};
     ra.kb.kind = KEY_H16X3;
     ra.gather_cap = rows_req == VRS_ROWS_MASKED ? 0 : (rows_req == VRS_ROWS_GATHER ? n : n * 7 / 10);
+    ra.xsel_lo = rf_xsel_lo;
     {
       ProfScope ps("refine", stream);
       CUDA_TRY(launch_refine(ra, gemm_args, gp, gemm_scr_keep, ix->xl, stream, &launches));
@@ -823,6 +829,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     f2.rq2 = rf_rq2;
     f2.qmap = rf_qlist;
     f2.qcount = rf_count;
+    f2.fold_qtiles = gp.qtiles;
     ProfScope ps("refine.finalize", stream);
     CUDA_TRY(launch_finalize(f2, stream, &launches));
   }

@@ -192,6 +192,24 @@ __host__ __device__ __forceinline__ int64_t used_splits(int64_t row_tiles, int64
   if (p > P) p = P;
   return p > 1 ? p : 1;
 }
+// The refine pass (qcount set on the device) folds its P x qtiles CTAs onto the
+// `tiles` query tiles its compacted queries fill: F row-split groups per tile (P F
+// splits), group f's lists stored at rows f Qa + j of the level-0 lists ([2P][q]),
+// F Qa <= q.  The refine's main pass and its finalize both map through this.
+struct RefineFold {
+  int32_t tiles;   // active query tiles, ceil(qcount / 128) (>= 1)
+  int32_t F;       // split groups per tile
+  int64_t Qa;      // tiles * 128: list-row stride between groups
+};
+__host__ __device__ __forceinline__ RefineFold refine_fold(int64_t qcount, int64_t qtiles, int64_t q) {
+  RefineFold r;
+  r.tiles = (int32_t)(qcount > 0 ? (qcount + 127) / 128 : 1);
+  r.Qa = (int64_t)r.tiles * 128;
+  int64_t F = qtiles / r.tiles;
+  if (F > q / r.Qa) F = q / r.Qa;
+  r.F = (int32_t)(F > 1 ? F : 1);
+  return r;
+}
 __device__ __forceinline__ int64_t splits_used(const SplitInfo &si) {
   if (si.bn == 0) return si.P;
   const int64_t n_sel = si.ids ? *si.count : si.n_rows;

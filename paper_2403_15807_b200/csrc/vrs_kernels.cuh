@@ -127,6 +127,7 @@ struct GemmArgs {
   int32_t *qexp = nullptr;  // [q] per-query exponents e_q (written by the conversion)
   float *rq = nullptr;      // [q] per-query residuals |q~ - q|
   int64_t cp_min_bytes = INT64_MAX;   // gathered selections of >= this many row bytes: cp.async by id (vrs_api row_plan)
+  int32_t xsel_ready = 0;   // the refine pass: X_sel already holds the gathered rows (no copy launch)
   // launch_select_local's output (nullptr: ids / count were written by launch_select):
   // the tensor-core pass first runs select_finish -> count, dense ids, gathered rows
   const int32_t *ids_local = nullptr;
@@ -180,6 +181,7 @@ struct FinalizeArgs {
   // row and certificate); rows j >= *qcount return at once; rq = |q_lo|, rq2 = the residual after lo
   const int32_t *qmap = nullptr;
   const int32_t *qcount = nullptr;
+  int32_t fold_qtiles = 0;         // the refine's finalize: level 0's query tiles (refine_fold)
   const float *rq2 = nullptr;
   int32_t *uncert_seen = nullptr;   // (mapped host flag) set to 1 when a level-0 certificate fails
 };
@@ -270,7 +272,9 @@ struct RefineArgs {
   int32_t *qexp;           // [q] out
   float *rqa, *rq2;        // [q] out: |q_lo|, |(q_hi + q_lo) 2^-e - q|
   uint32_t *gtau;          // [q] out: the refine pass's provable key threshold (ordered u32)
-  int64_t gather_cap = 0;  // gathered (cp.async) iff N_sel <= this, else masked
+  int64_t gather_cap = 0;  // no xsel_lo: gathered (cp.async by id) iff N_sel <= this, else masked
+  void *xsel_lo = nullptr; // [xsel_cap x d] x_lo rows of the level-0 selection: the refine delivers its rows
+                           // like level 0 (X_sel copies + TMA, cp.async, or masked; the same device decision)
 };
 cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan &plan, void *gemm_scratch,
                           const void *x_lo, cudaStream_t s, int *launches);

@@ -205,3 +205,37 @@ def test_refine_pass_certifies_clustered(vrs, metric):
             assert s["exact_fallback"] == s["uncertified"], s     # (no refine yet)
         else:
             assert s["exact_fallback"] < s["uncertified"] / 4, s
+
+
+@pytest.mark.parametrize("nq,window,rows", [(2048, (0, 7, 200), None), (1024, (0, 7, 40), None),
+                                           (130, (0, 7, 200), None), (512, (0, 7, 200), "masked"),
+                                           (512, (0, 7, 200), "gather"), (256, (0, 20, 60), "gather")])
+def test_refine_fold_many_query_tiles(vrs, nq, window, rows):
+    """The refine pass folds its grid onto the query tiles its (device-side) uncertified
+    count fills (refine_fold: F split groups per tile, lists at rows f Qa + j): batches of
+    many query tiles with a few uncertified queries (large F), a narrow window (short
+    row space: fewer used splits than P F) and a ragged 130-query batch; rows delivered as
+    level 0 chose (X_sel + X_sel_lo copies, cp.async by id, masked), forced either way.
+    Exact results."""
+    rng = np.random.default_rng(23 + nq)
+    n, d, C = 80000, 256, 72
+    cent = rng.standard_normal((C, d)).astype(np.float32)
+    cid = rng.integers(0, C, n)
+    X = (cent[cid] + 0.1 * rng.standard_normal((n, d))).astype(np.float32)
+    attrs = [(cid + rng.integers(0, 8, n)).astype(np.int32)]
+    qc = rng.integers(0, C, nq)
+    Q = (cent[qc] + 0.1 * rng.standard_normal((nq, d))).astype(np.float32)
+    pred = [window]
+    ref = oracle.search(X, attrs, pred, Q, 30, oracle.COS, 0)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    Qd = torch.from_numpy(Q).cuda()
+    for call in range(2):   # (call 1 runs the refine: call 0's failed certificates enable it)
+        st = vrs.new_stats()
+        kw = {} if rows is None else {"rows": {"masked": vrs.ROWS_MASKED, "gather": vrs.ROWS_GATHER}[rows]}
+        ids, dists = ix.search(Qd, pred, k=30, metric="cos", stats=st, **kw)
+        torch.cuda.synchronize()
+        s = vrs.read_stats(st)
+        check_topk_exact(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, 30, oracle.COS, ref=ref)
+        assert s["max_key_error_over_bound"] < 1.0, s
+        if call == 1 and s["uncertified"] > 0:
+            assert s["refined"] > 0, s
