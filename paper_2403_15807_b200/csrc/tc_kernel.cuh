@@ -439,9 +439,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
 
 #ifndef VRS_CP_WARPS
-#define VRS_CP_WARPS 1
+#define VRS_CP_WARPS 2
 #endif
-  constexpr int CPW = VRS_CP_WARPS;   // cp.async producer warps (1: warp 0; 2: warps 0 and 3 -- measured equal)
+  // cp.async producer warps (1: warp 0; 2: warps 0 and 3).  With the coalesced producer two
+  // warps raise the per-SM fetch rate: C4 s = 50 % Q = 1 2.06 -> 1.89 ms, Q = 256 4.00 -> 3.33 ms,
+  // C3 s = 10 % Q = 1 0.51 -> 0.48 ms (r02_cp_warps_ab.txt; round 1's uncoalesced one: equal)
+  constexpr int CPW = VRS_CP_WARPS;
   if ((warp == 0 || (CPW == 2 && warp == 3)) && cpg) {
     // ------------------------------------------------ cp.async producers, gathered rows
     // (late materialisation without a copy: warps 0 and 3 each fetch half of the tile's
