@@ -51,14 +51,15 @@ __global__ void __launch_bounds__(256) gather_copy_kernel(const void *__restrict
                                                           const int64_t *__restrict__ count, int64_t n, int allow,
                                                           int64_t cap, void *__restrict__ xsel,
                                                           const float *__restrict__ norm_src,
-                                                          float *__restrict__ norm_dst, int64_t cp_min_bytes) {
+                                                          float *__restrict__ norm_dst, int64_t cp_min_bytes,
+                                                          int64_t cp_min_rows) {
   TL_SCOPE(4);
   pdl_wait();
   TL_WAITED(4);
   pdl_trigger();
   const int64_t n_sel = *count;
   if (!gather_mode(ids, allow, n_sel, cap)) return;
-  if (n_sel * (int64_t)row_bytes >= cp_min_bytes) return;   // the tensor-core pass fetches them by cp.async
+  if (cp_fetch(n_sel, row_bytes, cp_min_bytes, cp_min_rows)) return;   // the tensor-core pass fetches them by cp.async
   // a warp per row (4 rows in flight), lanes along the row's 16-byte vectors (coalesced);
   // the row id is one broadcast load (round 1 divided a 64-bit element index per vector:
   // C5 s = 10 %, 128 MB of 512-byte rows took 336 us)
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(256) select_finish_kernel(const uint32_t *__re
                                                             int allow, int64_t cap, const void *__restrict__ X,
                                                             int32_t row_bytes, void *__restrict__ xsel,
                                                             const float *__restrict__ norm_src,
-                                                            float *__restrict__ norm_dst) {
+                                                            float *__restrict__ norm_dst, int64_t cp_min_bytes,
+                                                            int64_t cp_min_rows) {
   TL_SCOPE(6);
   extern __shared__ uint32_t s_pre[];   // [nchunks + 1]
   __shared__ uint32_t s_wsum[8];
@@ -132,6 +134,10 @@ __global__ void __launch_bounds__(256) select_finish_kernel(const uint32_t *__re
   const int64_t total = s_pre[nchunks];
   if (blockIdx.x == 0 && tid == 0) *count = total;
   if (!gather_mode(ids, allow, total, cap)) return;
+  if (cp_fetch(total, row_bytes, cp_min_bytes, cp_min_rows)) {   // rows by id in the pass: ids only
+    xsel = nullptr;
+    norm_dst = nullptr;
+  }
   const int v16 = row_bytes >> 4;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 32; base < total; base += nwarps * 32) {
@@ -183,7 +189,8 @@ cudaError_t launch_select_finish(const GemmArgs &a, int64_t xcap, int allow, con
   return launch_k(select_finish_kernel, dim3(blocks), dim3(256), smem, s, a.chunk_count, nchunks, a.ids_local,
                   const_cast<int64_t *>(a.count), const_cast<int32_t *>(a.ids), allow, xcap, xsrc, row_bytes,
                   copy ? a.xsel : (void *)nullptr, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
-                  copy && a.metric != VRS_IP ? a.xsel_norm : (float *)nullptr);
+                  copy && a.metric != VRS_IP ? a.xsel_norm : (float *)nullptr, copy ? a.cp_min_bytes : INT64_MAX,
+                  copy ? a.cp_min_rows : INT64_MAX);
 }
 
 // ---------------------------------------------------------------- 16-bit operands
@@ -357,16 +364,19 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.xsel_norm = a.xsel_norm;
   // Gathered row delivery (decided per launch on the device from the selection size):
   //  * no X_sel buffer (VRS_GATHER4 / VRS_CPGATHER): rows by id from X -- TMA gather4 or cp.async;
-  //  * one query tile: cp.async when the selection holds >= 512 MB of rows, else the X_sel
+  //  * <= 2 query tiles: cp.async when the selection holds >= 64 MB or >= 2 x 148 row tiles
+  //    (cp_fetch), else the X_sel
   //    copy (r01_s3_cp_gather_ab.txt: C3 s = 10 % Q = 1 0.95 -> 0.74 ms, small selections
   //    are faster copied);  * several query tiles: the copy (rows are re-read per tile).
   static const bool tma_gather4 = getenv("VRS_GATHER4") != nullptr;
   if (g4) {
     p.g4 = tma_gather4 ? 1 : 2;
     p.cp_min_bytes = 0;
+    p.cp_min_rows = 0;
   } else {
     p.g4 = a.cp_min_bytes < INT64_MAX ? 2 : 0;
     p.cp_min_bytes = a.cp_min_bytes;
+    p.cp_min_rows = a.cp_min_rows;
   }
   p.xrows = xsrc;
   p.row_bytes = a.d * (bf ? 2 : 4);
@@ -396,7 +406,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
     ProfScope ps("gemm.gather", s);
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, xsrc, a.d * (bf ? 2 : 4), a.ids, a.count, a.n,
                  (int)p.allow_gather, xcap, a.xsel, a.metric == VRS_L2 ? a.nx2 : a.inv_nx,
-                 a.metric == VRS_IP ? (float *)nullptr : a.xsel_norm, p.cp_min_bytes);
+                 a.metric == VRS_IP ? (float *)nullptr : a.xsel_norm, p.cp_min_bytes, p.cp_min_rows);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }
@@ -614,7 +624,7 @@ cudaError_t launch_refine(const RefineArgs &r, const GemmArgs &a, const GemmPlan
     ProfScope pg("refine.gather", s);   // x_lo rows of the selection (exactly when level 0 copied x_hi)
     e = launch_k(gather_copy_kernel, dim3(8 * 148), dim3(256), 0, s, x_lo, a.d * 2, a.ids, a.count, a.n,
                  (int)L.p.allow_gather, L.p.xsel_cap, r.xsel_lo, (const float *)nullptr, (float *)nullptr,
-                 L.p.cp_min_bytes);
+                 L.p.cp_min_bytes, L.p.cp_min_rows);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 1;
   }

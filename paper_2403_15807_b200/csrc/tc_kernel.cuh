@@ -211,7 +211,8 @@ struct TcParams {
                            // (xrows), 0 = TMA tiles from the X_sel copy
   const void *xrows;       // g4 == 2: the rows' base (fp32 corpus or its 16-bit shadow), row_bytes each
   int32_t row_bytes;
-  int64_t cp_min_bytes;    // g4 == 2: cp.async only when the selection holds >= this many row bytes
+  int64_t cp_min_bytes;    // g4 == 2: cp.async only when the selection holds >= this many row bytes ...
+  int64_t cp_min_rows;     // ... or >= this many rows (cp_fetch)
                            // (below it gather_copy_kernel made X_sel and TMA tiles stream it)
   int32_t min_span;        // used splits span >= this many row tiles (splits_used) ...
   int32_t min_p;           // ... unless that leaves fewer than min_p splits
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const bool gather = gather_mode(p.ids, p.allow_gather, n_sel, p.xsel_cap);
   // rows fetched by cp.async (see the producer): large one-query-tile selections, where
   // the X_sel copy's extra pass costs more than cp.async's lower streaming rate
-  const bool cpg = gather && p.g4 == 2 && n_sel * (int64_t)p.row_bytes >= p.cp_min_bytes;
+  const bool cpg = gather && p.g4 == 2 && cp_fetch(n_sel, p.row_bytes, p.cp_min_bytes, p.cp_min_rows);
   const bool direct = cpg || (gather && p.g4 == 1);   // rows by id from X (no X_sel)
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;

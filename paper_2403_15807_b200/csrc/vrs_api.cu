@@ -530,14 +530,21 @@ static int64_t cap_by_free_memory(int64_t rows, int64_t row_bytes) {
 struct RowPlan {
   int64_t gather_cap;      // gathered iff N_sel <= gather_cap (0: always masked)
   int64_t xsel_rows;       // rows of the X_sel copy buffer
-  int64_t cp_min_bytes;    // cp.async iff gathered and N_sel * row_bytes >= this (INT64_MAX: never)
+  int64_t cp_min_bytes;    // cp.async iff gathered and N_sel * row_bytes >= this (INT64_MAX: never) ...
+  int64_t cp_min_rows;     // ... or N_sel >= this (cp_fetch)
 };
 static RowPlan row_plan(int64_t q, int32_t qtiles, int64_t n, int64_t row_bytes, int rows_req, bool identity) {
   static const int cp_qtiles = getenv("VRS_CP_QTILES") ? atoi(getenv("VRS_CP_QTILES")) : 2;
   static const int64_t cp_min = (getenv("VRS_CP_MIN_MB") ? (int64_t)atoll(getenv("VRS_CP_MIN_MB")) : 64) << 20;
   static const double cp_frac = getenv("VRS_GATHER_CP_FRAC") ? atof(getenv("VRS_GATHER_CP_FRAC")) : 0.7;
   static const bool direct = getenv("VRS_GATHER4") != nullptr || getenv("VRS_CPGATHER") != nullptr;
-  RowPlan r{0, 0, INT64_MAX};
+  // (cp.async also for >= 2 x 148 row tiles of any size: enough tiles that the by-id fetch,
+  // ~38 GB/s per SM with two producer warps, runs on every SM -- C2 s = 10 %, Q <= 256: 25.6 MB,
+  // 4-6 us faster than the copy; fewer tiles leave most SMs idle: C4 s = 0.1 %, Q = 1, 25 tiles:
+  // the copy is 10 us faster; r02_planner_c2.txt, r02_planner_c4.txt)
+  static const int64_t cp_min_rows = getenv("VRS_CP_MIN_ROWS") ? atoll(getenv("VRS_CP_MIN_ROWS"))
+                                                               : int64_t(2) * kSmCountB200 * 256;
+  RowPlan r{0, 0, INT64_MAX, INT64_MAX};
   if (identity || rows_req == VRS_ROWS_MASKED) return r;
   const bool cp = qtiles <= cp_qtiles && getenv("VRS_NO_CPGATHER") == nullptr;
   int64_t cap = q >= 1024 ? n * 9 / 10 : q >= 256 ? n * 9 / 20 : n / 3;
@@ -548,8 +555,10 @@ static RowPlan row_plan(int64_t q, int32_t qtiles, int64_t n, int64_t row_bytes,
   r.gather_cap = cap;
   if (direct) return r;   // (VRS_GATHER4 / VRS_CPGATHER: rows by id from X, no buffer; tc_prepare)
   r.cp_min_bytes = cp ? cp_min : INT64_MAX;
+  r.cp_min_rows = cp ? cp_min_rows : INT64_MAX;
   int64_t buf = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(16) << 30) / row_bytes));
-  if (cp) buf = std::min<int64_t>(buf, std::max<int64_t>(1, (cp_min - 1) / row_bytes));   // copies stay below cp_min
+  if (cp)   // copies stay below cp_min and cp_min_rows
+    buf = std::min<int64_t>(buf, std::max<int64_t>(1, std::min((cp_min - 1) / row_bytes, cp_min_rows - 1)));
   r.xsel_rows = cap_by_free_memory(buf, row_bytes);
   if (!cp) r.gather_cap = std::min(r.gather_cap, r.xsel_rows);
   return r;
@@ -668,7 +677,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   const int64_t row_bytes = (int64_t)d * (use16 ? 2 : 4);
   const size_t qpad_bytes = (size_t)gp.qtiles * 128 * d * 2;   // 16-bit queries, whole 128-row tiles
   const RowPlan rp = path == VRS_PATH_GEMM ? row_plan(q, gp.qtiles, n, row_bytes, rows_req, identity)
-                                           : RowPlan{0, 0, INT64_MAX};
+                                           : RowPlan{0, 0, INT64_MAX, INT64_MAX};
   const int64_t xsel_cap = rp.gather_cap;
   const int64_t xsel_rows = rp.xsel_rows;   // rows of the X_sel buffer
   // VRS_SELECT_LOCAL=1: one-kernel selection (chunk-local ids) + select_finish (count, dense
@@ -778,6 +787,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
     a.qexp = qexp;
     a.rq = rq;
     a.cp_min_bytes = rp.cp_min_bytes;
+    a.cp_min_rows = rp.cp_min_rows;
     a.ids_local = ids_local;
     gemm_args = a;
     a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
@@ -955,6 +965,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   a.qexp = qexp;
   a.rq = rq;
   a.cp_min_bytes = rp.cp_min_bytes;
+  a.cp_min_rows = rp.cp_min_rows;
   a.ids_local = ids_local;
   a.chunk_count = sel_local ? static_cast<const uint32_t *>(sel_scratch) : nullptr;
   CUDA_TRY(launch_range_count(a, gp, r, stream, &launches));

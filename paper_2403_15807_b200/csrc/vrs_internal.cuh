@@ -183,6 +183,14 @@ struct SplitInfo {
 __device__ __forceinline__ bool gather_mode(const int32_t *ids, int allow, int64_t n_sel, int64_t cap) {
   return ids != nullptr && allow != 0 && n_sel <= cap;
 }
+// Gathered rows fetched by id (cp.async) rather than through the X_sel copy (vrs_api row_plan's
+// rule, applied on the device to N_sel): selections of >= cp_min bytes, or of >= cp_min_rows
+// rows -- enough row tiles that the per-SM fetch spreads over every SM.  Every kernel that
+// takes the decision (the gather copy, select_finish, the tensor-core pass) calls this.
+__host__ __device__ __forceinline__ bool cp_fetch(int64_t n_sel, int64_t row_bytes, int64_t cp_min_bytes,
+                                                  int64_t cp_min_rows) {
+  return n_sel * row_bytes >= cp_min_bytes || n_sel >= cp_min_rows;
+}
 // The one rule (probe / main kernels, threshold, finalize): >= min_span row tiles
 // per split, but at least min_p splits (about one CTA per SM over the query
 // tiles) while every split keeps >= 1 tile, and never more than P.

@@ -127,6 +127,7 @@ struct GemmArgs {
   int32_t *qexp = nullptr;  // [q] per-query exponents e_q (written by the conversion)
   float *rq = nullptr;      // [q] per-query residuals |q~ - q|
   int64_t cp_min_bytes = INT64_MAX;   // gathered selections of >= this many row bytes: cp.async by id (vrs_api row_plan)
+  int64_t cp_min_rows = INT64_MAX;    // ... or of >= this many rows (cp_fetch)
   int32_t xsel_ready = 0;   // the refine pass: X_sel already holds the gathered rows (no copy launch)
   // launch_select_local's output (nullptr: ids / count were written by launch_select):
   // the tensor-core pass first runs select_finish -> count, dense ids, gathered rows

@@ -22,7 +22,8 @@ M = {oracle.L2: "l2", oracle.IP: "ip", oracle.COS: "cos"}
 cases = [(20000, 128, 300, 10, oracle.IP, [(0, 0, 99)]),       # gathered, 10 %
          (12000, 64, 700, 50, oracle.COS, [(0, 0, 299)]),      # gathered, q >= 592
          (9000, 768, 9, 100, oracle.L2, [(0, 0, 299)]),        # d = 768, 30 %
-         (6000, 128, 64, 10, oracle.L2, [(0, 5000, 6000)])]    # empty selection
+         (6000, 128, 64, 10, oracle.L2, [(0, 5000, 6000)]),    # empty selection
+         (200000, 128, 16, 10, oracle.IP, [(0, 0, 899)])]      # 90 %, >= 2 x 148 row tiles: cp.async (cp_fetch)
 for n, d, q, k, metric, pred in cases:
     rng = np.random.default_rng(n + d)
     X = rng.standard_normal((n, d)).astype(np.float32)
