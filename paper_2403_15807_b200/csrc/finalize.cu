@@ -24,7 +24,7 @@ constexpr int kTieCap = 512;
 
 // Exactly the m best (key desc, id asc) valid candidates -> out (unordered).
 // get(c, &key, &id) returns false for padding.  Block-wide (kFinThreads).
-template <typename IdT, typename Get>
+template <typename IdT, int NT = kFinThreads, typename Get>
 __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, float *out_key) {
   __shared__ uint32_t hist[256];
   __shared__ int s_n, s_out, s_ties, s_bin, s_above;
@@ -34,15 +34,17 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
   if (tid == 0) { s_n = 0; s_out = 0; s_ties = 0; }
   __syncthreads();
   int local = 0;
-  for (int64_t c = tid; c < C; c += kFinThreads) {
+  for (int64_t c = tid; c < C; c += NT) {
     float k; IdT i;
     local += get(c, k, i) ? 1 : 0;
   }
-  atomicAdd(&s_n, local);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0) atomicAdd(&s_n, local);
   __syncthreads();
   const int nvalid = s_n;
   if (nvalid <= m_want) {
-    for (int64_t c = tid; c < C; c += kFinThreads) {
+    for (int64_t c = tid; c < C; c += NT) {
       float k; IdT i;
       if (get(c, k, i)) {
         const int p = atomicAdd(&s_out, 1);
@@ -57,9 +59,9 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
   uint32_t prefix = 0, mask = 0;
   int rem = m;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int b = tid; b < 256; b += kFinThreads) hist[b] = 0;
+    for (int b = tid; b < 256; b += NT) hist[b] = 0;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < C; c0 += kFinThreads) {
+    for (int64_t c0 = 0; c0 < C; c0 += NT) {
       const int64_t c = c0 + tid;
       float k; IdT i;
       uint32_t bin = 256u;
@@ -98,7 +100,7 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
     __syncthreads();
   }
   // strictly better keys are all in; `rem` of the ties at `prefix` go by lowest id
-  for (int64_t c = tid; c < C; c += kFinThreads) {
+  for (int64_t c = tid; c < C; c += NT) {
     float k; IdT i;
     if (get(c, k, i)) {
       const uint32_t ok = ordered_u32(k);
@@ -131,11 +133,11 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
     for (int r = 0; r < rem; ++r) {
       IdT best = (IdT)0x7fffffffffffffffLL;
       if (sizeof(IdT) == 4) best = (IdT)0x7fffffff;
-      for (int64_t c = tid; c < C; c += kFinThreads) {
+      for (int64_t c = tid; c < C; c += NT) {
         float k; IdT i;
         if (get(c, k, i) && ordered_u32(k) == prefix && i > s_last && i < best) best = i;
       }
-      __shared__ IdT s_red[kFinThreads / 32];
+      __shared__ IdT s_red[NT / 32];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         IdT y = __shfl_xor_sync(0xffffffffu, best, o);
@@ -145,7 +147,7 @@ __device__ int block_select_top(Get get, int64_t C, int m_want, IdT *out_id, flo
       __syncthreads();
       if (tid == 0) {
         IdT b = s_red[0];
-        for (int w = 1; w < kFinThreads / 32; ++w) b = s_red[w] < b ? s_red[w] : b;
+        for (int w = 1; w < NT / 32; ++w) b = s_red[w] < b ? s_red[w] : b;
         out_id[gt + r] = b; out_key[gt + r] = tkey; s_last = b;
       }
       __syncthreads();
@@ -1034,6 +1036,276 @@ __global__ void __launch_bounds__(W * 32) finalize_cta_kernel(FinalizeArgs a) {
   if (w == 0) fin_sort_write(a, jq, m, qq, s_sc, s_sid, s_kmin, &cq);
 }
 
+// Small batches (tensor-core lists, q <= VRS_FIN_BLOCK_Q): one CTA of kFinBT threads per
+// query, few block-wide steps (a Q = 1 finalize is a latency chain on one SM):
+//  (1) the per-(split, list) counts, prefix-summed block-wide (a thread per list);
+//  (2) every candidate at or above the probe threshold staged in shared memory;
+//  (3) the k' best (key desc, id asc): min / max, one 2048-bucket histogram over a
+//      monotone linear map of the keys, the bucket holding the k'-th best found from the
+//      top, everything above it taken, the boundary bucket resolved by ranking;
+//  (4) exact re-score (every warp, U rows in flight);
+//  (5) rank sort of the <= k' exact scores, the certificate, the k best written.
+// Replaces the per-warp buffer compactions and tree merge of finalize_cta_kernel
+// (r02_small_q_chain_timeline.txt: 40-90 us at Q = 1).  More than kFinStage candidates,
+// a single-valued key range or a crowded boundary bucket: the radix select
+// (block_select_top) over the lists instead -- the same result.
+constexpr int kFinBT = 512;
+constexpr int kFinStage = 16384;      // staged candidates (128 KB of key + id)
+constexpr int kFinBlockMaxLists = 4096;
+constexpr int kFinNB = 2048;          // histogram buckets
+constexpr int kFinBnd = 1024;         // boundary-bucket capacity of the ranking step
+static size_t finalize_block_smem(int lists) { return (size_t)kFinStage * 8 + (size_t)(lists + 1) * 4; }
+
+struct FinBlockShared {
+  uint32_t hist[kFinNB];
+  float bkey[kFinBnd];
+  int32_t bid[kFinBnd];
+  double sc[kFinMaxSel], sc2[kFinMaxSel];
+  int64_t sid[kFinMaxSel], sid2[kFinMaxSel];
+  int32_t sel[kFinMaxSel];
+  float selk[kFinMaxSel];
+  int32_t wsum[kFinBT / 32];
+  uint32_t wlo[kFinBT / 32], whi[kFinBT / 32], wcnt[kFinBT / 32];
+  float wkmin[kFinBT / 32];
+  int n_out, n_bnd, bstar, above;
+};
+
+// (3) on the staged set: exactly the K best valid (id >= 0) entries -> out (unordered);
+// returns their number, or -1 when the caller must fall back to the radix select.
+template <int NT>
+__device__ int block_select_staged(const float *key, const int32_t *id, int T, int K, FinBlockShared &S) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t lo = 0xffffffffu, hi = 0u, cnt = 0;
+  for (int c = tid; c < T; c += NT)
+    if (id[c] >= 0) {
+      const uint32_t u = ordered_u32(key[c]);
+      lo = min(lo, u); hi = max(hi, u); ++cnt;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) { S.wlo[w] = lo; S.whi[w] = hi; S.wcnt[w] = cnt; }
+  for (int b = tid; b < kFinNB; b += NT) S.hist[b] = 0;
+  if (tid == 0) { S.n_out = 0; S.n_bnd = 0; }
+  __syncthreads();
+  lo = 0xffffffffu; hi = 0u; cnt = 0;
+#pragma unroll
+  for (int v = 0; v < NT / 32; ++v) { lo = min(lo, S.wlo[v]); hi = max(hi, S.whi[v]); cnt += S.wcnt[v]; }
+  if ((int)cnt <= K) {   // every valid entry
+    for (int c = tid; c < T; c += NT)
+      if (id[c] >= 0) {
+        const int p = atomicAdd(&S.n_out, 1);
+        S.sel[p] = id[c]; S.selk[p] = key[c];
+      }
+    __syncthreads();
+    return (int)cnt;
+  }
+  if (hi == lo) return -1;   // (block-uniform) one key value: ties by id -> the radix path
+  const float scale = ((float)kFinNB - 0.5f) / (float)(hi - lo);
+  auto bucket = [&](uint32_t u) { return min(kFinNB - 1, (int)((float)(u - lo) * scale)); };   // monotone
+  for (int c = tid; c < T; c += NT)
+    if (id[c] >= 0) atomicAdd(&S.hist[bucket(ordered_u32(key[c]))], 1u);
+  __syncthreads();
+  // bucket of the K-th best: thread t sums buckets [NB-1-4t-3, NB-1-4t] (descending)
+  constexpr int PB = kFinNB / NT;
+  uint32_t v[PB], s = 0;
+#pragma unroll
+  for (int t = 0; t < PB; ++t) { v[t] = S.hist[kFinNB - 1 - PB * tid - t]; s += v[t]; }
+  uint32_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) S.wcnt[w] = incl;
+  __syncthreads();
+  uint32_t wbefore = 0;
+  for (int u = 0; u < w; ++u) wbefore += S.wcnt[u];
+  const uint32_t before = wbefore + incl - s;
+  if (before < (uint32_t)K && (uint32_t)K <= before + s) {
+    uint32_t run = before;
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      if ((uint32_t)K <= run + v[t]) { S.bstar = kFinNB - 1 - PB * tid - t; S.above = (int)run; break; }
+      run += v[t];
+    }
+  }
+  __syncthreads();
+  const int bstar = S.bstar, above = S.above;
+  for (int c = tid; c < T; c += NT)
+    if (id[c] >= 0) {
+      const int b = bucket(ordered_u32(key[c]));
+      if (b > bstar) {
+        const int p = atomicAdd(&S.n_out, 1);
+        S.sel[p] = id[c]; S.selk[p] = key[c];
+      } else if (b == bstar) {
+        const int p = atomicAdd(&S.n_bnd, 1);
+        if (p < kFinBnd) { S.bkey[p] = key[c]; S.bid[p] = id[c]; }
+      }
+    }
+  __syncthreads();
+  const int nb = S.n_bnd;
+  if (nb > kFinBnd) return -1;   // (block-uniform)
+  const int rem = K - above;
+  for (int i = tid; i < nb; i += NT) {   // rank in the boundary bucket (key desc, id asc)
+    const float ki = S.bkey[i];
+    const int32_t ii = S.bid[i];
+    int r = 0;
+    for (int t = 0; t < nb; ++t) {
+      const float kt = S.bkey[t];
+      r += (kt > ki || (kt == ki && S.bid[t] < ii)) ? 1 : 0;
+    }
+    if (r < rem) { S.sel[above + r] = ii; S.selk[above + r] = ki; }
+  }
+  __syncthreads();
+  return K;
+}
+
+__global__ void __launch_bounds__(kFinBT, 1) finalize_block_kernel(FinalizeArgs a) {
+  TL_SCOPE(1);
+  extern __shared__ __align__(16) uint8_t fin_dyn[];
+  float *s_key = reinterpret_cast<float *>(fin_dyn);                 // [kFinStage]
+  int32_t *s_id = reinterpret_cast<int32_t *>(s_key + kFinStage);    // [kFinStage]; -1 = dropped
+  int32_t *s_off = s_id + kFinStage;                                 // [lists + 1] list offsets
+  __shared__ FinBlockShared S;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  constexpr int NW = kFinBT / 32;
+  const int64_t j = blockIdx.x;
+  pdl_wait();
+  TL_WAITED(1);
+  pdl_trigger();
+  const int L = a.lists;
+  const uint32_t thr = a.gtau ? __ldg(a.gtau + j) : 0u;
+  constexpr int PL = kFinBlockMaxLists / kFinBT;   // lists per thread (at most)
+  const int per = (L + kFinBT - 1) / kFinBT;
+  const int l0 = min(L, tid * per);
+  auto lbase = [&](int l) { return ((int64_t)l * a.q + j) * a.stride; };
+  // (1) counts (registers) -> block-wide exclusive prefix -> s_off
+  int cl[PL];
+  int mine = 0;
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    const int l = l0 + i;
+    cl[i] = (i < per && l < L) ? (a.cnt ? __ldg(a.cnt + (int64_t)l * a.q + j) : a.kread) : 0;
+    mine += cl[i];
+  }
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) S.wsum[w] = incl;
+  __syncthreads();
+  int off = incl - mine, total = 0;
+#pragma unroll
+  for (int v = 0; v < NW; ++v) {
+    const int x = S.wsum[v];
+    off += v < w ? x : 0;
+    total += x;
+  }
+  const bool staged = total <= (a.stage_cap > 0 ? min(a.stage_cap, kFinStage) : kFinStage);
+  // (2) stage (a thread per list, 8 loads in flight); s_off for the fallback's lookups
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    const int l = l0 + i;
+    if (i < per && l < L) {
+      s_off[l] = off;
+      if (staged) {
+        const int c = cl[i];
+        const int64_t b = lbase(l);
+        for (int r0 = 0; r0 < c; r0 += 8) {
+          float kv[8];
+          int32_t iv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (r0 + u < c) { kv[u] = __ldg(a.key + b + r0 + u); iv[u] = __ldg(a.id + b + r0 + u); }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (r0 + u < c) {
+              s_key[off + r0 + u] = kv[u];
+              s_id[off + r0 + u] = (iv[u] >= 0 && ordered_u32(kv[u]) >= thr) ? iv[u] : -1;
+            }
+        }
+      }
+      off += cl[i];
+    }
+  }
+  if (tid == 0) s_off[L] = total;
+  __syncthreads();
+  TL_STAMP(1, 2);
+  // (3) the k' best by key (ties -> lower id), unordered, in S.sel / S.selk
+  int m = staged && a.stage_cap >= 0 ? block_select_staged<kFinBT>(s_key, s_id, total, a.kprime, S) : -1;
+  if (m < 0) {
+    auto get = [&](int64_t c, float &k, int32_t &i) -> bool {
+      if (staged) {
+        i = s_id[c];
+        k = s_key[c];
+        return i >= 0;
+      }
+      int lo = 0, hi = L;   // the list holding entry c: s_off[lo] <= c < s_off[lo + 1]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= c) lo = mid; else hi = mid;
+      }
+      const int64_t o = lbase(lo) + (c - s_off[lo]);
+      k = __ldg(a.key + o);
+      i = __ldg(a.id + o);
+      return i >= 0 && ordered_u32(k) >= thr;
+    };
+    m = block_select_top<int32_t, kFinBT>(get, total, a.kprime, S.sel, S.selk);
+  }
+  TL_STAMP(1, 3);
+  // (4) exact re-score: every warp, 8 rows in flight
+  const double qq = fin_qq(a, j);
+  CertQ cq{0.0, 0.0, 1.0};
+  if (a.cert) cq = cert_setup(a, j, qq);
+  fin_rescore<8>(a, j, S.sel, m, w, NW, qq, S.sc, S.sid, a.stats ? S.selk : nullptr, &cq);
+  __syncthreads();
+  TL_STAMP(1, 4);
+  // (5) rank sort by exact score (ids unique: a strict order; NaN ranks as -inf), the
+  // certificate (thread 0), the k best written best-first with padding
+  for (int i = tid; i < m; i += kFinBT) {
+    const double ki = S.sc[i] == S.sc[i] ? S.sc[i] : -INFINITY;
+    const int64_t ii = S.sid[i];
+    int r = 0;
+    for (int t = 0; t < m; ++t) {
+      const double kt = S.sc[t] == S.sc[t] ? S.sc[t] : -INFINITY;
+      r += (kt > ki || (kt == ki && S.sid[t] < ii)) ? 1 : 0;
+    }
+    S.sc2[r] = ki;
+    S.sid2[r] = ii;
+  }
+  float km = INFINITY;
+  for (int i = tid; i < m; i += kFinBT) km = fminf(km, S.selk[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) km = fminf(km, __shfl_xor_sync(0xffffffffu, km, o));
+  if (lane == 0) S.wkmin[w] = km;
+  __syncthreads();
+  const bool zero_cos = a.metric == VRS_COSINE && !(qq > 0.0);
+  if (a.cert && tid == 0) {
+    float kmin = INFINITY;
+    for (int v = 0; v < NW; ++v) kmin = fminf(kmin, S.wkmin[v]);
+    fin_certify(a, j, m, qq, S.sc2[max(1, min(m, a.k)) - 1], kmin, cq);
+  }
+  const int mv = zero_cos ? 0 : min(m, a.k);
+  const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
+  for (int r = tid; r < a.k; r += kFinBT) {
+    const int64_t o = j * a.k + r;
+    if (r < mv) {
+      a.ids[o] = a.row_offset + S.sid2[r];
+      const double v = S.sc2[r];
+      a.dists[o] = (float)(a.metric == VRS_L2 ? -v : v);
+    } else {
+      a.ids[o] = -1;
+      a.dists[o] = pad;
+    }
+  }
+}
+
 // Per query (one CTA): the kth largest probe slot maximum (each the key of a
 // distinct row) -> gtau, a lower bound of the kth best key over all rows.  The
 // values are staged once in shared memory (ordered u32, 0 = no row) and a
@@ -1343,6 +1615,20 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
   if (launches) *launches += 1;
   // small batches: a CTA of 8 warps per query; large: a warp per query
   // (the refine's finalize: the CTA kernel -- its queries read F x the lists, refine_fold)
+  // (the block kernel for q <= 256 when k' >= 64: C3 s = 10 %, Q = 1 finalize 91 -> 49 us, C4 s = 5 %,
+  // Q = 256 -3 %; with C2's k' = 26 the CTA kernel is as fast at q = 1-16 and 10 us faster at
+  // q = 256 -- VRS_FIN_BLOCK_Q overrides)
+  static const int block_q_env = getenv("VRS_FIN_BLOCK_Q") ? atoi(getenv("VRS_FIN_BLOCK_Q")) : -1;
+  const int block_q = block_q_env >= 0 ? block_q_env : (a.kprime >= 64 ? 256 : 0);
+  if (a.q <= block_q && a.fold_qtiles == 0 && !a.sorted && a.lists <= kFinBlockMaxLists && a.kprime <= kFinMaxSel) {
+    static size_t attrb = 0;
+    const cudaError_t e = ensure_smem_attr(finalize_block_kernel, finalize_block_smem(kFinBlockMaxLists), attrb);
+    if (e != cudaSuccess) return e;
+    static const int stage_env = getenv("VRS_FIN_STAGE") ? atoi(getenv("VRS_FIN_STAGE")) : 0;
+    FinalizeArgs b = a;
+    b.stage_cap = stage_env;
+    return launch_k(finalize_block_kernel, dim3((unsigned)a.q), dim3(kFinBT), finalize_block_smem(a.lists), s, b);
+  }
   if (a.q < 4 * kSmCountB200 || a.fold_qtiles > 0) {
     // (16 warps per query for <= 64 queries with k' >= 64: C4 s = 5 %, Q = 1 finalize 93 -> 48 us;
     // k' = 32 (C2) gains nothing; 32 warps measured slower -- they spill at 64 registers,

@@ -185,6 +185,9 @@ struct FinalizeArgs {
   int32_t fold_qtiles = 0;         // the refine's finalize: level 0's query tiles (refine_fold)
   const float *rq2 = nullptr;
   int32_t *uncert_seen = nullptr;   // (mapped host flag) set to 1 when a level-0 certificate fails
+  // (A/B and tests only, VRS_FIN_STAGE: the small-batch finalize stages at most this many
+  // candidates (> 0), or skips its histogram selection for the radix select (< 0); 0 = default)
+  int32_t stage_cap = 0;
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches);
 

@@ -1,7 +1,8 @@
 """The opt-in variants of the tensor-core path (environment switches read once per
 process, so each runs in a subprocess): TMA gather4 late materialisation
 (VRS_GATHER4), cp.async gathering straight into the swizzled stages
-(VRS_CPGATHER), the one-launch selection + select_finish (VRS_SELECT_LOCAL) and the
+(VRS_CPGATHER), the one-launch selection + select_finish (VRS_SELECT_LOCAL), the
+small-batch finalize variants (VRS_FIN_STAGE, VRS_FIN_BLOCK_Q) and the
 warp-voted slow path (libvrs_exp.so, -DVRS_SLOW_GROUPS_VOTE, when built).  Each
 must meet the same parity rules as the default path."""
 import os
@@ -70,6 +71,23 @@ def test_cp_gather_adaptive_threshold(vrs_lib_built):
 
 def test_select_local(vrs_lib_built):
     _run({"VRS_SELECT_LOCAL": "1"})
+
+
+def test_finalize_block_radix(vrs_lib_built):
+    """The small-batch block finalize with its histogram selection skipped: the radix
+    select over the staged candidates (the path for one-valued keys / crowded buckets)."""
+    _run({"VRS_FIN_STAGE": "-1"})
+
+
+def test_finalize_block_unstaged(vrs_lib_built):
+    """The small-batch block finalize with staging capped at one candidate: the radix
+    select reads the lists in global memory (the path for > kFinStage candidates)."""
+    _run({"VRS_FIN_STAGE": "1"})
+
+
+def test_finalize_cta_small_q(vrs_lib_built):
+    """Small batches through the 8/16-warp CTA finalize instead of the block finalize."""
+    _run({"VRS_FIN_BLOCK_Q": "0"})
 
 
 def test_slow_path_vote_variant(vrs_lib_built):

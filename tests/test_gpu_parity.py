@@ -244,6 +244,24 @@ def test_exact_ties_go_to_lower_ids(vrs, dups, k):
         assert np.allclose(gd, rd, rtol=1e-6)
 
 
+@pytest.mark.parametrize("k", [10, 100], ids=["k10", "k100"])
+def test_exact_ties_crowd(vrs, k):
+    """One row duplicated 3000 times and queried by itself (q <= 2: the small-batch block
+    finalize): thousands of candidates share the k'-th key, so the selection resolves
+    them by id (one-valued key range / more ties than the tie buffer)."""
+    rng = np.random.default_rng(7 + k)
+    n, d = 20000, 64
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    X[rng.choice(n, 3000, replace=False)] = X[5]
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    Q = np.stack([X[5], X[5] + 1e-3 * rng.standard_normal(d).astype(np.float32)])
+    for metric in (oracle.L2, oracle.IP):
+        gi, gd = _run(vrs, X, attrs, [(0, 0, 949)], Q, k, metric)
+        ri, rd, _ = oracle.search(X, attrs, [(0, 0, 949)], Q, k, metric)
+        assert (gi == ri).all()
+        assert np.allclose(gd, rd, rtol=1e-6, atol=1e-30)
+
+
 def test_binding_rejects_bad_columns(vrs):
     """a short / misplaced attribute column would be read out of bounds by
     select_count_kernel -- the binding refuses it before vrs_load."""
