@@ -478,12 +478,31 @@ def main():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             run_cell(c)
             torch.cuda.synchronize()
-            reps = 3
+            # the cell alone as a CUDA graph (device time; eager launches of a tiny cell would
+            # time Python's launch loop), replayed `reps` times between two events
+            cg = None
+            if graph is not None:
+                try:
+                    cap_c = torch.cuda.Stream()
+                    cap_c.wait_stream(torch.cuda.current_stream())
+                    cg = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(cg, stream=cap_c):
+                        run_cell(c)
+                    cg.replay()
+                    torch.cuda.synchronize()
+                except Exception:   # noqa: BLE001 -- eager timing instead
+                    cg = None
+                    torch.cuda.synchronize()
+            reps = 5 if cg is not None else 3
             a.record(stream)
             for _ in range(reps):
-                run_cell(c)
+                if cg is not None:
+                    cg.replay()
+                else:
+                    run_cell(c)
             b.record(stream)
             torch.cuda.synchronize()
+            del cg
             t = a.elapsed_time(b) / reps / 1e3
             ns = nsel[s]
             fl = 2.0 * q * ns * d
@@ -491,9 +510,20 @@ def main():
             by = n_loc * sum(1 if cfg.attrs[i][0] == "u8" else 4 for i in range(len(cfg.attrs))) + ns * esz * d \
                 + q * 4.0 * d + q * k * 12
             tc_peak = pk["bf16_tflops"] * (1.0 if h16 else NOMINAL_TF32_OVER_BF16)
-            cell_out.append({"sel": s, "q": q, "n_sel": ns, "ms": t * 1e3, "qps": q / t,
-                             "path": "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan",
-                             "hbm_frac": by / t / 1e9 / pk["hbm_gbs"], "tensor_frac_burst": fl / t / 1e12 / tc_peak})
+            path = "gemm" if vrs.last_path() == vrs.PATH_GEMM else "scan"
+            # the cell's kernel split: one more call with per-kernel CUDA events (ProfScope)
+            vrs.profile(True)
+            vrs.profile_reset()
+            run_cell(c)
+            torch.cuda.synchronize()
+            kms = {kname: round(v[0], 4) for kname, v in vrs.profile_read().items()}
+            vrs.profile(False)
+            hf, tf = by / t / 1e9 / pk["hbm_gbs"], fl / t / 1e12 / tc_peak
+            cell_out.append({"sel": s, "q": q, "n_sel": ns, "ms": t * 1e3, "qps": q / t, "path": path,
+                             "timing": "graph replay" if reps == 5 else "eager",
+                             "hbm_frac": hf, "tensor_frac_burst": tf,
+                             "binding": "tensor" if fl / (tc_peak * 1e12) > by / (pk["hbm_gbs"] * 1e9) else "hbm",
+                             "kernels_ms": kms})
 
     # ---------------- e2e through the public API with host buffers
     h2d = sum(q * d * 4 for _, q in cells)
