@@ -9,7 +9,8 @@
 //     bitmap word and __popc its count; one block covers a contiguous chunk of
 //     8192 rows and publishes the chunk count.
 //   select_scatter_kernel: each block sums the counts of the chunks before it
-//     (a parallel reduction over <= a few thousand values), re-reads its 256
+//     (a parallel reduction over <= 4096 values; larger corpora get the
+//     prefix from one select_prefix_kernel block instead), re-reads its 256
 //     bitmap words (n/8 bytes in total, L2-resident) and scatters ascending row
 //     ids with a warp prefix of popcounts; the last block writes the count.
 // (A single-pass decoupled look-back was measured slower here: with the whole
@@ -117,8 +118,42 @@ __global__ void __launch_bounds__(kSelThreads) select_count_kernel(PredDev pred,
   }
 }
 
+// Corpora of more than kSelDirectChunks chunks: the exclusive prefix of the chunk counts
+// by one block (a contiguous segment per thread, a block scan of the segment sums), so
+// that select_scatter's prefix stays O(1) per block -- summing every earlier chunk in
+// each block is O(chunks^2) in total (fine at C3's 1221 chunks, not toward n ~ 2^31).
+constexpr uint32_t kSelDirectChunks = 4096;
+constexpr int kSelPrefixThreads = 1024;
+__global__ void __launch_bounds__(kSelPrefixThreads) select_prefix_kernel(const uint32_t *__restrict__ chunk_count,
+                                                                          uint32_t nchunks,
+                                                                          uint64_t *__restrict__ prefix) {
+  __shared__ uint64_t s_w[kSelPrefixThreads / 32];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (nchunks + kSelPrefixThreads - 1) / kSelPrefixThreads;
+  const uint32_t b0 = min(nchunks, tid * per), b1 = min(nchunks, b0 + per);
+  uint64_t mine = 0;
+  for (uint32_t b = b0; b < b1; ++b) mine += chunk_count[b];
+  uint64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint64_t run = incl - mine;
+  for (int i = 0; i < warp; ++i) run += s_w[i];
+  for (uint32_t b = b0; b < b1; ++b) {
+    prefix[b] = run;
+    run += chunk_count[b];
+  }
+}
+
 __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, const uint32_t *__restrict__ bitmap,
                                                                      const uint32_t *__restrict__ chunk_count,
+                                                                     const uint64_t *__restrict__ prefix,
                                                                      int32_t *__restrict__ ids,
                                                                      int64_t *__restrict__ count) {
   TL_SCOPE(1);
@@ -128,9 +163,12 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, 
   pdl_trigger();
   __shared__ uint32_t s_wsum[kSelWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // prefix over the chunks before this block
+  // prefix over the chunks before this block (select_prefix_kernel's, or summed here)
   uint64_t pre = 0;
-  for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kSelThreads) pre += chunk_count[b];
+  if (prefix == nullptr)
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kSelThreads) pre += chunk_count[b];
+  else if (threadIdx.x == 0)
+    pre = prefix[blockIdx.x];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
   if (lane == 0) s_red[warp] = pre;
@@ -165,6 +203,10 @@ __global__ void __launch_bounds__(kSelThreads) select_scatter_kernel(int64_t n, 
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kSelThreads - 1) *count = (int64_t)(base + wpre + incl);
 }
 
+// scratch: chunk counts uint32[nchunks] (+ 8), then the chunk prefix uint64[nchunks] (8-byte aligned)
+static size_t select_prefix_offset(int64_t n) { return ((size_t)((n + kSelRows - 1) / kSelRows) * 4 + 8 + 7) & ~size_t(7); }
+size_t select_scratch_bytes(int64_t n) { return select_prefix_offset(n) + (size_t)((n + kSelRows - 1) / kSelRows) * 8; }
+
 // Host launcher.  Scratch: chunk counts uint32[nchunks].  ids may be nullptr
 // (bitmap + count only).
 cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int32_t *ids, int64_t *count,
@@ -178,8 +220,18 @@ cudaError_t launch_select(const PredDev &pred, int64_t n, uint32_t *bitmap, int3
   if (launches) *launches += 1;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  static const uint32_t direct_max = getenv("VRS_SELECT_DIRECT_MAX") ? (uint32_t)atoi(getenv("VRS_SELECT_DIRECT_MAX"))
+                                                                     : kSelDirectChunks;   // (tests: force the prefix kernel)
+  uint64_t *prefix = nullptr;
+  if (nchunks > direct_max) {
+    prefix = reinterpret_cast<uint64_t *>(static_cast<char *>(scratch) + select_prefix_offset(n));
+    e = launch_k(select_prefix_kernel, dim3(1), dim3(kSelPrefixThreads), 0, stream, (const uint32_t *)chunk_count,
+                 nchunks, prefix);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+  }
   e = launch_k(select_scatter_kernel, dim3(nchunks), dim3(kSelThreads), 0, stream, n, (const uint32_t *)bitmap,
-               (const uint32_t *)chunk_count, ids, count);
+               (const uint32_t *)chunk_count, (const uint64_t *)prefix, ids, count);
   if (e != cudaSuccess) return e;
   if (launches) *launches += 1;
   return cudaGetLastError();
@@ -196,7 +248,6 @@ cudaError_t launch_select_local(const PredDev &pred, int64_t n, uint32_t *bitmap
   return cudaGetLastError();
 }
 
-size_t select_scratch_bytes(int64_t n) { return (size_t)((n + kSelRows - 1) / kSelRows) * 4 + 8; }
 
 }  // namespace vrs
 

@@ -273,3 +273,47 @@ def test_binding_rejects_bad_columns(vrs):
             vrs.Index(X, bad)
     with pytest.raises(ValueError):
         vrs.Index(X.double(), [])
+
+
+_SELECT_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_2403_15807_b200 as vrs
+from parity import check_select
+for n in (1, 8193, 250_001, 1_000_003):
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 4)).astype(np.float32)
+    attrs = [rng.integers(0, 1000, n).astype(np.int32), rng.integers(0, 64, n).astype(np.uint8)]
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
+    for pred in ([], [(0, -5, 99)], [(0, 500, 499)], [(0, 100, 899), (1, 3, 40)]):
+        bm, cnt, ids = ix.select(pred, with_ids=True)
+        torch.cuda.synchronize()
+        check_select(bm, cnt, ids, attrs, n, pred)
+print("OK")
+'''
+
+
+def test_select_prefix_kernel(vrs):
+    """The chunk-prefix kernel large corpora use (> 4096 chunks of 8192 rows), forced for
+    every size by VRS_SELECT_DIRECT_MAX=0 (read once per process: a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VRS_SELECT_DIRECT_MAX="0")
+    r = subprocess.run([sys.executable, "-c", _SELECT_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_select_large_corpus(vrs):
+    """n = 40M rows (4883 chunks > 4096): the chunk prefix by select_prefix_kernel."""
+    n = 40_000_000
+    rng = np.random.default_rng(11)
+    X = torch.randn((n, 4), dtype=torch.float32, device="cuda")
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    ix = vrs.Index(X, [torch.from_numpy(attrs[0]).cuda()])
+    for pred in ([(0, 0, 9)], [(0, 0, 499)]):
+        bm, cnt, ids = ix.select(pred, with_ids=True)
+        torch.cuda.synchronize()
+        check_select(bm, cnt, ids, attrs, n, pred)
