@@ -274,7 +274,16 @@ static int32_t tc_min_p(const GemmPlan &plan) {
   return off ? 1 : plan.min_p;
 }
 
-GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms) {
+// The main pass runs as CTA pairs (tc_kernel.cuh PAIR) for an even number of query tiles
+// on 16-bit operands with a streamed query tile (d > 256: nk > 4).  VRS_PAIR=0 disables.
+// (C4 bench 285.8 -> 297.8 k q/s: s = 50 %, Q = 256 3.24 -> 2.71 ms, Q = 8192 70.1 -> 68.1 ms;
+// r02_pair_ab.txt)
+bool pair_main(int64_t qtiles, int32_t d, bool h16) {
+  static const bool on = !getenv("VRS_PAIR") || atoi(getenv("VRS_PAIR")) > 0;
+  return on && h16 && qtiles % 2 == 0 && (d + 2 * tc::BK - 1) / (2 * tc::BK) > 4;
+}
+
+GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms, bool h16) {
   GemmPlan g{0, 0, 0, 1};
   if (d % 4 != 0 || d < 4 || q < 1 || n_upper < 1 || kprime > 256) return g;
   if (!encode_fn()) return g;
@@ -283,6 +292,8 @@ GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int nu
   // one CTA per SM; aim for up to 4 waves of (query tile, row split) items while keeping
   // items >= ~128 row tiles
   int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, row_tiles * qtiles / ((int64_t)num_sms * 128)));
+  // (two query tiles as one CTA pair per split: one wave -- C4 s = 5 %, Q = 256 0.433 -> 0.411 ms)
+  if (qtiles == 2 && pair_main(qtiles, d, h16)) waves = 1;
   int64_t P = std::max<int64_t>(1, (int64_t)num_sms * waves / qtiles);
   static const int p_env = getenv("VRS_P") ? atoi(getenv("VRS_P")) : 0;   // (experiments)
   if (p_env > 0) P = p_env;
@@ -474,6 +485,17 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     e = launch_threshold(ta, s);
     if (e != cudaSuccess) return e;
     if (launches) *launches += 2;
+  }
+  // CTA pairs (tc_kernel.cuh PAIR): an even number of query tiles, 16-bit operands streamed
+  // A, no gather4 -- every row tile is staged once per query-tile pair, half in each CTA
+  if (pair_main(plan.qtiles, a.d, L.bf) && !L.ar && p.g4 != 1 && p.nseg == 1) {
+    const int64_t xcap = a.ids ? a.xsel_cap : 0;
+    const bool by_id = xcap > 0 && a.xsel == nullptr;   // (rows by id: no X_sel map to resize)
+    if (!make_map(&L.mx, a.Xb, a.n, a.d, tc::BN / 2, true, a.fmt16) ||
+        (!by_id && !make_map(&L.mg, xcap > 0 ? a.xsel : a.Xb, xcap > 0 ? xcap : a.n, a.d, tc::BN / 2, true, a.fmt16)))
+      return cudaErrorInvalidValue;
+    L.pair = true;
+    p.idesc = mma_idesc(2 * tc::BM, tc::BN, (uint32_t)a.fmt16);
   }
   {
     ProfScope pf("gemm.main", s);

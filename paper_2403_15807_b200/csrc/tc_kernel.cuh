@@ -104,6 +104,67 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// ---- CTA pair (cta_group::2): cluster of two CTAs on one TPC --------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  // (default semantics, release at CTA scope, as CUTLASS's ClusterBarrier::arrive: a
+  // .release.cluster arrival compiles to a GPU-scope MEMBAR per call -- measured: the pair's
+  // main pass at 33 % tensor-pipe activity, membar / long-scoreboard stalls)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA load into this CTA's shared memory whose completion (bytes) is counted on the
+// barrier at cluster address `bar` -- the pair leader's stage barrier
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+// commit of the pair's MMAs: arrives on the barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+// D[tmem of both CTAs] (+)= A[smem, 128 rows per CTA] . B[smem, N / 2 rows per CTA]^T, M = 256
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -322,18 +383,27 @@ constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the li
 // ROWSCALE: per-row key scale (COSINE 1/|x|); otherwise a constant (L2: 2, IP: 1).
 // BF: operands are bf16 (shadow corpus, kind::f16) instead of fp32 (kind::tf32).
 #define TC_TL(slot) TL_STAMP(MODE & 3, slot)   // (thread-0-only stamps are filtered in TL_STAMP)
-template <bool AR, int MODE, bool ROWSCALE, bool BF>
+// PAIR: a cluster of two CTAs -- query tiles 2i and 2i + 1 of one row split -- runs
+// each tile's MMA as one cta_group::2 M = 256 MMA: each CTA stages its own 128 queries
+// and half (128) of the tile's rows, so every row is fetched once per query-tile pair
+// (the one-query-tile-per-CTA kernel fetches it per query tile); the leader (rank 0)
+// issues the MMAs, the accumulator (128 queries x 256 rows) lands in each CTA's TMEM
+// and each CTA's epilogue is unchanged.  MODE_MAIN, 16-bit operands, streamed A only.
+template <bool AR, int MODE, bool ROWSCALE, bool BF, bool PAIR>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
                    const __grid_constant__ CUtensorMap tmap_gl, TcParams p) {
   using namespace tc;
+  static_assert(!PAIR || (MODE == MODE_MAIN && !AR && BF), "CTA pairs: main pass, streamed 16-bit A");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
   // array itself, so the compiler keeps the shared address space (LDS, not LD)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // pipeline region: AR ? [A: nk x 16 KB][B stages of 32 KB] : [stages of (A 16 KB | B 32 KB)]
-  constexpr int SSTRIDE = AR ? B_BYTES : A_BYTES + B_BYTES;   // bytes per pipeline stage
+  constexpr int BROWS = PAIR ? BN / 2 : BN;               // rows of a tile this CTA stages
+  constexpr int BSTAGE = BROWS * BK * 4;                    // their bytes per K block
+  constexpr int SSTRIDE = AR ? B_BYTES : A_BYTES + BSTAGE;   // bytes per pipeline stage
   constexpr int NST = ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
                           ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
                           : MAX_STAGES;
@@ -359,11 +429,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int qtile = blockIdx.x % p.qtiles;
   int split = blockIdx.x / p.qtiles;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;   // (PAIR: qtile & 1)
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) TC_TL(0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    // (PAIR: the leader's stage barrier also counts the peer's relay, its accumulator-empty
+    // barrier both CTAs' epilogue warps)
+    for (int s = 0; s < NST; ++s) { mbar_init(&full_bar[s], PAIR && leader ? 2 : 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&afull_bar, 1);
-    for (int s = 0; s < ACC_STAGES; ++s) { mbar_init(&tfull_bar[s], 1); mbar_init(&tempty_bar[s], EPI_WARPS); }
+    for (int s = 0; s < ACC_STAGES; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], PAIR && leader ? 2 * EPI_WARPS : EPI_WARPS);
+    }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
       mbar_init(&bempty_bar[s], EPI_WARPS);
@@ -377,13 +454,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (p.nseg > 1) { prefetch_tmap(&tmap_xl); prefetch_tmap(&tmap_gl); }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
   // (the prologue above overlaps the predecessor kernel's tail; global memory from here on)
@@ -455,21 +540,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // each lane's cp.async.mbarrier.arrive adds a pending arrival that its copies
     // retire, and warp 0's lane 0 arrives only after both warps registered theirs)
     const bool lead = warp == 0;
-    const int hrow = lead ? 0 : BN / CPW;   // this warp's first row of the tile
+    const int hrow = lead ? 0 : BROWS / CPW;   // this warp's first row of the CTA's rows of the tile
     int stage = 0;
     uint32_t phase = 0;
     if (lead && AR && ntiles > 0 && lane == 0) {
       mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
       for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
     }
-    constexpr int GR = BN / (32 * CPW);   // rows per lane per warp
+    constexpr int GR = BROWS / (32 * CPW);   // rows per lane per warp
     const char *xb = static_cast<const char *>(p.xrows);
     const int64_t rb = p.row_bytes;
     const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;
     auto load_ids = [&](int t, int32_t (&r)[GR]) {
 #pragma unroll
       for (int u = 0; u < GR; ++u) {
-        const int64_t pos = tile_of(t) * BN + hrow + lane + 32 * u;
+        const int64_t pos = tile_of(t) * BN + rank * BROWS + hrow + lane + 32 * u;
         r[u] = pos < n_sel ? __ldg(p.ids + pos) : pad_row;
       }
     };
@@ -489,7 +574,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int c = lane & 7;
         const bool cvalid = koff + c * 16 < rb;
 #pragma unroll
-        for (int u = 0; u < BN / (4 * CPW); ++u) {
+        for (int u = 0; u < BROWS / (4 * CPW); ++u) {
           const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
           const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
           const int r = hrow + rl;
@@ -574,16 +659,40 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const int seg = kb / p.nk, kk = kb - seg * p.nk;   // (refine: 3 segments; else seg = 0)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *st = b_base + stage * SSTRIDE;
-          mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + B_BYTES);
-          if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
           // (refine: x_lo in segment 1 -- gathered into its own X_sel copy, or masked over the full x_lo)
           const CUtensorMap *bmap = seg == 1 ? (gather ? &tmap_gl : &tmap_xl) : (gather ? &tmap_g : &tmap_x);
-          tma_load_2d(st + BOFF, bmap, &full_bar[stage], kk * KE, row0);
+          if (PAIR) {   // both CTAs' loads complete on the leader's barrier; the peer adds one arrival
+            const uint32_t lbar = mapa_rank(&full_bar[stage], 0);
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * (A_BYTES + BSTAGE));
+            tma_load_2d_pair(st, &tmap_q, lbar, kk * KE, qtile * BM);
+            tma_load_2d_pair(st + BOFF, bmap, lbar, kk * KE, row0 + (int)rank * BROWS);   // (box BN / 2)
+            if (!leader) mbar_arrive_cluster(lbar);
+          } else {
+            mbar_expect_tx(&full_bar[stage], AR ? B_BYTES : A_BYTES + BSTAGE);
+            if (!AR) tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
+            tma_load_2d(st + BOFF, bmap, &full_bar[stage], kk * KE, row0);
+          }
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && PAIR && !leader && cpg) {
+    // ------------------------------------------------ the pair's peer: stage relay
+    // (cp.async rows: this CTA's half of a stage has landed -- A by TMA, rows by cp.async -- ->
+    // one arrival on the leader's barrier of that stage; the generic-proxy cp.async
+    // writes are fenced to the async proxy first, as the leader's MMA warp does for its own)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        if (cpg) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_rank(&full_bar[stage], 0));
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && (!PAIR || leader)) {
     // ------------------------------------------------ MMA issuer
     const uint32_t idesc = p.idesc;
     int stage = 0;
@@ -592,11 +701,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % ACC_STAGES;
       const uint32_t acc_phase = (t / ACC_STAGES) & 1;
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      if (PAIR) mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);   // (both CTAs' epilogues)
+      else mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+        if (PAIR) mbar_wait_cluster(&full_bar[stage], phase);   // (own half + the peer's relay)
+        else mbar_wait(&full_bar[stage], phase);
         if (t == 0 && kb == 0 && lane == 0) TL_STAMP_ANY(MODE & 3, 2);
         if (cpg) fence_proxy_async_smem();   // cp.async (generic proxy) writes -> the MMA's async-proxy reads
         tc_fence_after();
@@ -605,12 +716,19 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K = 8 tf32 / 16 bf16 = 32 bytes per instruction
-            if (BF) tc_mma_bf16(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            if (PAIR) tc_mma_f16_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else if (BF) tc_mma_bf16(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
             else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
           }
           // frees the smem slot when these MMAs finish; accumulator ready after the last K block
-          tc_commit(&empty_bar[stage]);
-          if (kb == nkb - 1) tc_commit(&tfull_bar[acc]);
+          // (PAIR: in both CTAs)
+          if (PAIR) {
+            tc_commit_pair(&empty_bar[stage]);
+            if (kb == nkb - 1) tc_commit_pair(&tfull_bar[acc]);
+          } else {
+            tc_commit(&empty_bar[stage]);
+            if (kb == nkb - 1) tc_commit(&tfull_bar[acc]);
+          }
         }
         __syncwarp();
         if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -1004,7 +1122,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&tempty_bar[acc]);
+        if (PAIR && !leader) mbar_arrive_cluster(mapa_rank(&tempty_bar[acc], 0));   // (the leader's MMA waits)
+        else mbar_arrive(&tempty_bar[acc]);
         mbar_arrive(&bempty_bar[bs]);
       }
     }
@@ -1028,6 +1147,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();   // no remote arrival / MMA into this CTA's smem or TMEM is pending
   if (threadIdx.x == 0) {
     TC_TL(5);
 #ifdef VRS_TC_TIMING
@@ -1038,7 +1158,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   }
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS) : "memory");
   }
 }
 
@@ -1056,20 +1177,24 @@ struct TcLaunch {
   CUtensorMap mq, mx, mg, ml, mlg;
   TcParams p;
   bool bf, ar, rowscale;
+  bool pair = false;   // main pass as CTA pairs (mx / mg then have boxes of BN / 2 rows)
 };
 // Queries -> bf16 (padded tiles), tensor maps, parameters, and the gather copy
 // when the selection is materialised (gemm_tc.cu).
 cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L);
 
 typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
-template <bool AR, int MODE, bool ROWSCALE, bool BF>
+template <bool AR, int MODE, bool ROWSCALE, bool BF, bool PAIR>
 __global__ void tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                                const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
                                const __grid_constant__ CUtensorMap tmap_gl, TcParams p);
 template <int MODE, bool BF>
-static TcKernel pick_kernel(bool ar, bool rowscale) {
-  return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF> : tc_topk_kernel<true, MODE, false, BF>)
-            : (rowscale ? tc_topk_kernel<false, MODE, true, BF> : tc_topk_kernel<false, MODE, false, BF>);
+static TcKernel pick_kernel(bool ar, bool rowscale, bool pair = false) {
+  if constexpr (MODE == MODE_MAIN && BF) {
+    if (pair) return rowscale ? tc_topk_kernel<false, MODE, true, BF, true> : tc_topk_kernel<false, MODE, false, BF, true>;
+  }
+  return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF, false> : tc_topk_kernel<true, MODE, false, BF, false>)
+            : (rowscale ? tc_topk_kernel<false, MODE, true, BF, false> : tc_topk_kernel<false, MODE, false, BF, false>);
 }
 
 // One launch of the pass in MODE (the kernels of a mode are instantiated in the
@@ -1077,19 +1202,20 @@ static TcKernel pick_kernel(bool ar, bool rowscale) {
 // builds with -DVRS_TC_STATS).
 template <int MODE>
 static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStream_t s) {
-  static size_t attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per variant (AR, ROWSCALE, BF)
-  cudaError_t e = ensure_smem_attr(L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale)
-                                        : pick_kernel<MODE, false>(L.ar, L.rowscale),
-                                   tc::SMEM_BYTES, attr[(L.ar ? 4 : 0) | (L.rowscale ? 2 : 0) | (L.bf ? 1 : 0)]);
+  static size_t attr[16] = {};   // per variant (PAIR, AR, ROWSCALE, BF)
+  const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale, L.pair)
+                             : pick_kernel<MODE, false>(L.ar, L.rowscale, L.pair);
+  cudaError_t e = ensure_smem_attr(kern, tc::SMEM_BYTES,
+                                   attr[(L.pair ? 8 : 0) | (L.ar ? 4 : 0) | (L.rowscale ? 2 : 0) | (L.bf ? 1 : 0)]);
   if (e != cudaSuccess) return e;
-  const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale) : pick_kernel<MODE, false>(L.ar, L.rowscale);
   static unsigned long long *stats = nullptr;
   static const bool want_stats = getenv("VRS_STATS") != nullptr;   // (debug counters, single-threaded use)
   if (want_stats && !stats) cudaMalloc(&stats, 64);
   TcParams p2 = pr;
   p2.stats = want_stats ? stats : nullptr;
   if (want_stats) cudaMemsetAsync(stats, 0, 64, s);
-  e = launch_k(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, L.mq, L.mx, L.mg, L.ml, L.mlg, p2);
+  e = launch_k_cluster(kern, dim3((unsigned)(pr.P * pr.qtiles)), dim3(tc::THREADS), tc::SMEM_BYTES, s, L.pair ? 2 : 1,
+                       L.mq, L.mx, L.mg, L.ml, L.mlg, p2);
   if (want_stats) {
     unsigned long long h[4];
     cudaMemcpyAsync(h, stats, 32, cudaMemcpyDeviceToHost, s);

@@ -645,7 +645,7 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   GemmPlan gp{0, 0, 0, 1};
   // the TMA paths need 16-byte aligned rows and bases
   const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
-  if (path != VRS_PATH_SCAN && tma_ok) gp = gemm_plan(q, d, n, kprime, ix->num_sms);
+  if (path != VRS_PATH_SCAN && tma_ok) gp = gemm_plan(q, d, n, kprime, ix->num_sms, use16);
   // (measured on C2: the tensor-core pass over the 16-bit shadow is HBM-bound and beats
   // the fp32 FFMA scan already at q = 1 -- it reads half the bytes)
   if (path == VRS_PATH_AUTO) path = gp.ok ? VRS_PATH_GEMM : VRS_PATH_SCAN;
@@ -902,7 +902,7 @@ vrs_status vrs_range_search(vrs_index *ix, const float *queries, int64_t q, int3
   const bool tma_ok = (((uintptr_t)queries | (uintptr_t)ix->X) & 15) == 0;
   const int64_t n = ix->n;
   GemmPlan gp{0, 0, 0, 1};
-  if (tma_ok) gp = gemm_plan(q, d, n, 32, ix->num_sms);
+  if (tma_ok) gp = gemm_plan(q, d, n, 32, ix->num_sms, false);   // (range passes: no CTA pairs)
   if (!gp.ok)
     return fail(VRS_EUNSUPPORTED, "range search runs on the tensor-core path: d %% 4 == 0 and 16-byte aligned rows");
   const bool identity = (pd.n == 0);

@@ -43,6 +43,29 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// launch_k with a thread-block cluster of `cluster_x` CTAs along x (1: none)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                    int cluster_x, Args &&...args) {
+  if (cluster_x <= 1) return launch_k(kern, grid, block, smem, s, std::forward<Args>(args)...);
+  static const bool pdl = getenv("VRS_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cluster_x;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---- debug timeline (compile-time only: -DVRS_TC_TIMING; tools/tc_timeline.py) --
 // Per translation unit: globaltimer stamps [region][cta][8] -- slot 0 kernel entry,
 // 1 after griddepcontrol.wait, 5 thread 0 leaving the kernel (the tensor-core

@@ -96,7 +96,8 @@ struct GemmPlan {
   int32_t ok;       // shape supported
   int32_t min_p;    // splits that keep ~every SM busy over the query tiles (used_splits)
 };
-GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms);
+GemmPlan gemm_plan(int64_t q, int32_t d, int64_t n_upper, int32_t kprime, int num_sms, bool h16);
+bool pair_main(int64_t qtiles, int32_t d, bool h16);
 
 struct GemmArgs {
   const float *X;
