@@ -574,12 +574,19 @@ static int pow2_at_least(int v) {
 // else the power of two >= k + 16 -- the lists keep that many per (list, query) anyway,
 // and the wider margin lets the certificate hold without the fallback (
 // C4 k = 100: 116 certified 99 %, 128 100 %; C5 k = 50 -> 128).
-static int kprime_of(int k) {
+// wide: the index has seen a level-0 certificate fail (its mapped flag) -- data whose
+// k-th and k'-th keys crowd within the fp16 bound (C5: clustered, cosine); twice the
+// over-fetch (<= 256) certifies most queries at level 0 instead of sending them through the
+// refine pass (C5: 89 -> 98 % certified at level 0, 3.44 -> 3.18 ms per step,
+// r02_kprime_c5_ab.txt); VRS_KPRIME_WIDE=0 disables
+static int kprime_of(int k, bool wide = false) {
   static const bool old = getenv("VRS_KPRIME_K16") != nullptr;   // (A/B only: r01's k + 16)
   static const int forced = getenv("VRS_KPRIME") ? atoi(getenv("VRS_KPRIME")) : 0;   // (A/B only)
+  static const bool wide_ok = !getenv("VRS_KPRIME_WIDE") || atoi(getenv("VRS_KPRIME_WIDE")) > 0;
   if (forced > 0) return std::max(k + 1, std::min(256, forced));
-  if (old || k <= 16) return k + 16;   // (small k: the margin of 16 already exceeds k; C2 k' = 26: +3 % vs 32)
-  return std::max(32, pow2_at_least(k + 16));
+  const int base = (old || k <= 16) ? k + 16   // (small k: the margin of 16 already exceeds k; C2 k' = 26: +3 % vs 32)
+                                    : std::max(32, pow2_at_least(k + 16));
+  return wide && wide_ok ? std::max(base, std::min(256, 2 * base)) : base;
 }
 
 static vrs_status check_precision(const vrs_index *ix, int prec_req) {
@@ -635,7 +642,10 @@ vrs_status vrs_search_ex(vrs_index *ix, const float *queries, int64_t q, int32_t
   if (dev != ix->device) return fail(VRS_EINVAL, "current device %d differs from the index device %d", dev, ix->device);
 
   cudaStream_t stream = (cudaStream_t)cuda_stream;
-  const int32_t kprime = kprime_of(k);  // over-fetch for the exact re-score
+  // over-fetch for the exact re-score; wider once the index has seen a
+  // level-0 certificate fail on the 16-bit path
+  const bool seen_uncert = ix->xb && prec_req != VRS_PREC_TF32 && ix->uncert_seen_host && *ix->uncert_seen_host != 0;
+  const int32_t kprime = kprime_of(k, seen_uncert);
   const int kpe = std::max(64, pow2_at_least(kprime));
   const bool identity = (pd.n == 0);
   const int64_t n = ix->n;

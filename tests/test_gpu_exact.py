@@ -190,7 +190,8 @@ def test_refine_pass_certifies_clustered(vrs, metric):
     pred = [(0, 7, 200)]
     ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs])
     Qd = torch.from_numpy(Q).cuda()
-    for call in range(2):   # the first failed certificate enables the refine pass for the index
+    first = None
+    for call in range(2):   # the first failed certificate enables the refine pass (and the wider k') for the index
         st = vrs.new_stats()
         ids, dists = ix.search(Qd, pred, k=50, metric={oracle.COS: "cos", oracle.IP: "ip", oracle.L2: "l2"}[metric],
                                stats=st)
@@ -200,11 +201,13 @@ def test_refine_pass_certifies_clustered(vrs, metric):
         assert s["max_key_error_over_bound"] < 1.0, s
         if metric != oracle.COS:   # (IP / L2 spread enough within a cluster: level 0 certifies them)
             continue
-        assert s["uncertified"] > 50, s
         if call == 0:
+            assert s["uncertified"] > 50, s
             assert s["exact_fallback"] == s["uncertified"], s     # (no refine yet)
-        else:
-            assert s["exact_fallback"] < s["uncertified"] / 4, s
+            first = s["uncertified"]
+        else:   # twice the over-fetch certifies more at level 0; the refine most of the rest
+            assert s["uncertified"] < first, (first, s)
+            assert s["exact_fallback"] <= s["uncertified"] / 4, s
 
 
 @pytest.mark.parametrize("nq,window,rows", [(2048, (0, 7, 200), None), (1024, (0, 7, 40), None),
