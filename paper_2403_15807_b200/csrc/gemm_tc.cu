@@ -435,6 +435,13 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
   p.cand_cnt = gs.cand_cnt;
   p.gtau = gs.gtau;
   p.probe_max = gs.probe_max;
+  // AR8 (tc_kernel.cuh): <= 8 queries held resident as 8 rows per K block -- the stages carry
+  // rows only (5 in flight instead of 4 stages of rows + query tile); probe and main pass
+  static const bool ar8_on = !getenv("VRS_AR8") || atoi(getenv("VRS_AR8")) > 0;
+  if (ar8_on && L.bf && !L.ar && plan.qtiles == 1 && a.q <= 8 && p.nk <= 32 && p.nseg == 1) {
+    if (!make_map(&L.mq, a.Qb, (int64_t)plan.qtiles * tc::BM, a.d, 8, true, a.fmt16)) return cudaErrorInvalidValue;
+    L.ar8 = true;
+  }
   static const bool no_probe = getenv("VRS_NO_PROBE") != nullptr;
   if (no_probe) {   // (otherwise threshold_kernel writes every query's gtau)
     e = cudaMemsetAsync(p.gtau, 0, (size_t)a.q * 4, s);

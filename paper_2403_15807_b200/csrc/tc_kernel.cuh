@@ -211,6 +211,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
+// The same with stride byte offset 0: every 8-row group of the operand reads the same
+// 8 rows (AR8: a query tile of <= 8 queries held as 8 rows per K block; accumulator rows
+// 8..127 repeat rows 0..7 and belong to no query)
+__device__ __forceinline__ uint64_t sw128_desc_rows8(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor: D fp32, A/B format ab (kind::f16: 0 fp16, 1 bf16;
 // kind::tf32: 2 tf32), both K-major, N = BN, M = BM.
 __host__ __device__ constexpr uint32_t mma_idesc(int M, int N, uint32_t ab) {
@@ -389,12 +401,19 @@ constexpr int MODE_RFILL = 3;   // range search: write those rows' ids to the li
 // (the one-query-tile-per-CTA kernel fetches it per query tile); the leader (rank 0)
 // issues the MMAs, the accumulator (128 queries x 256 rows) lands in each CTA's TMEM
 // and each CTA's epilogue is unchanged.  MODE_MAIN, 16-bit operands, streamed A only.
-template <bool AR, int MODE, bool ROWSCALE, bool BF, bool PAIR>
+// ARM: 0 the query tile streams with every stage; 1 (AR) it stays resident, 16 KB per K
+// block (nk <= 4); 2 (AR8) it stays resident as 8 rows per K block, 1 KB each (<= 8
+// queries, nk <= 32), read by the MMA with stride 0 -- the stages hold rows only, so a
+// small batch keeps 5 stages of rows in flight instead of 4 (A and B) per SM.
+template <int ARM, int MODE, bool ROWSCALE, bool BF, bool PAIR>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
                    const __grid_constant__ CUtensorMap tmap_gl, TcParams p) {
   using namespace tc;
+  constexpr bool AR = ARM != 0;
+  constexpr int ABLK = ARM == 2 ? 1024 : A_BYTES;           // resident bytes per K block
+  constexpr int ARES = ARM == 2 ? 32 * 1024 : 4 * A_BYTES;  // resident query region
   static_assert(!PAIR || (MODE == MODE_MAIN && !AR && BF), "CTA pairs: main pass, streamed 16-bit A");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by pointer arithmetic on the shared
@@ -404,13 +423,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   constexpr int BROWS = PAIR ? BN / 2 : BN;               // rows of a tile this CTA stages
   constexpr int BSTAGE = BROWS * BK * 4;                    // their bytes per K block
   constexpr int SSTRIDE = AR ? B_BYTES : A_BYTES + BSTAGE;   // bytes per pipeline stage
-  constexpr int NST = ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE) < MAX_STAGES
-                          ? ((PIPE_BYTES - (AR ? 4 * A_BYTES : 0)) / SSTRIDE)
+  constexpr int NST = ((PIPE_BYTES - (AR ? ARES : 0)) / SSTRIDE) < MAX_STAGES
+                          ? ((PIPE_BYTES - (AR ? ARES : 0)) / SSTRIDE)
                           : MAX_STAGES;
   constexpr int BOFF = AR ? 0 : A_BYTES;                 // B offset within a stage
   constexpr int KE = BF ? 2 * BK : BK;                   // elements per 128-byte K block
   uint8_t *a_res = smem;                                 // AR: resident query tile
-  uint8_t *b_base = AR ? smem + 4 * A_BYTES : smem;
+  uint8_t *b_base = AR ? smem + ARES : smem;
   float *bias_a = reinterpret_cast<float *>(smem + PIPE_BYTES);               // [BIAS_STAGES][BN]
   float *bias_b = bias_a + BIAS_STAGES * BN;                                    // [BIAS_STAGES][BN]
   int32_t *row_id = reinterpret_cast<int32_t *>(bias_b + BIAS_STAGES * BN);     // [BIAS_STAGES][BN]
@@ -544,8 +563,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     if (lead && AR && ntiles > 0 && lane == 0) {
-      mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
-      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+      mbar_expect_tx(&afull_bar, p.nk * ABLK);
+      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * ABLK, &tmap_q, &afull_bar, kb * KE, qtile * BM);
     }
     constexpr int GR = BROWS / (32 * CPW);   // rows per lane per warp
     const char *xb = static_cast<const char *>(p.xrows);
@@ -603,8 +622,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     if (AR && ntiles > 0 && lane == 0) {
-      mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
-      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+      mbar_expect_tx(&afull_bar, p.nk * ABLK);
+      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * ABLK, &tmap_q, &afull_bar, kb * KE, qtile * BM);
     }
     constexpr int GR = BN / 32;   // rows per lane (whole gather4 groups)
     static_assert(GR % 4 == 0, "gather4 groups per lane");
@@ -650,8 +669,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       if (AR && ntiles > 0) {
-        mbar_expect_tx(&afull_bar, p.nk * A_BYTES);
-        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * A_BYTES, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+        mbar_expect_tx(&afull_bar, p.nk * ABLK);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * ABLK, &tmap_q, &afull_bar, kb * KE, qtile * BM);
       }
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)(tile_of(t) * BN);
@@ -713,12 +732,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sb = smem_u32(b_base + stage * SSTRIDE + BOFF);
-          const uint32_t sa = AR ? smem_u32(a_res + kb * A_BYTES) : sb - A_BYTES;
+          const uint32_t sa = AR ? smem_u32(a_res + kb * ABLK) : sb - A_BYTES;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K = 8 tf32 / 16 bf16 = 32 bytes per instruction
-            if (PAIR) tc_mma_f16_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
-            else if (BF) tc_mma_bf16(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
-            else tc_mma_tf32(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            const uint64_t da = ARM == 2 ? sw128_desc_rows8(sa + k * 32) : sw128_desc(sa + k * 32);
+            if (PAIR) tc_mma_f16_pair(d_tmem, da, sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else if (BF) tc_mma_bf16(d_tmem, da, sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
+            else tc_mma_tf32(d_tmem, da, sw128_desc(sb + k * 32), idesc, (kb | k) != 0);
           }
           // frees the smem slot when these MMAs finish; accumulator ready after the last K block
           // (PAIR: in both CTAs)
@@ -1178,23 +1198,27 @@ struct TcLaunch {
   TcParams p;
   bool bf, ar, rowscale;
   bool pair = false;   // main pass as CTA pairs (mx / mg then have boxes of BN / 2 rows)
+  bool ar8 = false;    // <= 8 queries resident as 8 rows per K block (mq then has boxes of 8 rows)
 };
 // Queries -> bf16 (padded tiles), tensor maps, parameters, and the gather copy
 // when the selection is materialised (gemm_tc.cu).
 cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, int *launches, TcLaunch *L);
 
 typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
-template <bool AR, int MODE, bool ROWSCALE, bool BF, bool PAIR>
+template <int ARM, int MODE, bool ROWSCALE, bool BF, bool PAIR>
 __global__ void tc_topk_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_x,
                                const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_xl,
                                const __grid_constant__ CUtensorMap tmap_gl, TcParams p);
 template <int MODE, bool BF>
-static TcKernel pick_kernel(bool ar, bool rowscale, bool pair = false) {
+static TcKernel pick_kernel(bool ar, bool rowscale, bool pair = false, bool ar8 = false) {
   if constexpr (MODE == MODE_MAIN && BF) {
-    if (pair) return rowscale ? tc_topk_kernel<false, MODE, true, BF, true> : tc_topk_kernel<false, MODE, false, BF, true>;
+    if (pair) return rowscale ? tc_topk_kernel<0, MODE, true, BF, true> : tc_topk_kernel<0, MODE, false, BF, true>;
   }
-  return ar ? (rowscale ? tc_topk_kernel<true, MODE, true, BF, false> : tc_topk_kernel<true, MODE, false, BF, false>)
-            : (rowscale ? tc_topk_kernel<false, MODE, true, BF, false> : tc_topk_kernel<false, MODE, false, BF, false>);
+  if constexpr ((MODE == MODE_MAIN || MODE == MODE_PROBE) && BF) {
+    if (ar8) return rowscale ? tc_topk_kernel<2, MODE, true, BF, false> : tc_topk_kernel<2, MODE, false, BF, false>;
+  }
+  return ar ? (rowscale ? tc_topk_kernel<1, MODE, true, BF, false> : tc_topk_kernel<1, MODE, false, BF, false>)
+            : (rowscale ? tc_topk_kernel<0, MODE, true, BF, false> : tc_topk_kernel<0, MODE, false, BF, false>);
 }
 
 // One launch of the pass in MODE (the kernels of a mode are instantiated in the
@@ -1202,11 +1226,12 @@ static TcKernel pick_kernel(bool ar, bool rowscale, bool pair = false) {
 // builds with -DVRS_TC_STATS).
 template <int MODE>
 static cudaError_t tc_launch_mode(const TcLaunch &L, const TcParams &pr, cudaStream_t s) {
-  static size_t attr[16] = {};   // per variant (PAIR, AR, ROWSCALE, BF)
-  const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale, L.pair)
-                             : pick_kernel<MODE, false>(L.ar, L.rowscale, L.pair);
+  static size_t attr[32] = {};   // per variant (AR8, PAIR, AR, ROWSCALE, BF)
+  const TcKernel kern = L.bf ? pick_kernel<MODE, true>(L.ar, L.rowscale, L.pair, L.ar8)
+                             : pick_kernel<MODE, false>(L.ar, L.rowscale, L.pair, L.ar8);
   cudaError_t e = ensure_smem_attr(kern, tc::SMEM_BYTES,
-                                   attr[(L.pair ? 8 : 0) | (L.ar ? 4 : 0) | (L.rowscale ? 2 : 0) | (L.bf ? 1 : 0)]);
+                                   attr[(L.ar8 ? 16 : 0) | (L.pair ? 8 : 0) | (L.ar ? 4 : 0) | (L.rowscale ? 2 : 0) |
+                                        (L.bf ? 1 : 0)]);
   if (e != cudaSuccess) return e;
   static unsigned long long *stats = nullptr;
   static const bool want_stats = getenv("VRS_STATS") != nullptr;   // (debug counters, single-threaded use)
