@@ -18,11 +18,11 @@ def short(name):
     base = re.sub(r"\(.*", "", name).replace("void ", "").strip()
     mine = "vrs::" in name or any(base.split("<")[0].split("::")[-1] == k for k in OURS)
     if mine and "tc_topk_kernel" in base:
-        # template args <AR, MODE, ROWSCALE, BF>: name the mode
-        m = re.search(r"<(\d+), (\d+), (\d+), (\d+)>", base)
+        # template args <ARM, MODE, ROWSCALE, BF, PAIR>: name the mode (+ CTA pairs)
+        m = re.search(r"<(\d+), (\d+), (\d+), (\d+)(?:, (\d+))?>", base)
         if m:
             mode = {"0": "main", "1": "probe", "2": "range-count", "3": "range-fill"}[m.group(2)]
-            return f"vrs::tc_topk_kernel[{mode}]"
+            return f"vrs::tc_topk_kernel[{mode}{', pairs' if m.group(5) == '1' else ''}]"
     name = re.sub(r"\(.*", "", name)
     targs = re.search(r"<(.*)>", name)
     name = re.sub(r"<.*", "", name).replace("void ", "")
