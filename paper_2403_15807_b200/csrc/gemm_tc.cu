@@ -402,6 +402,8 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.xexp = bf ? a.xexp : 0;
   p.tile_step = 1;
   p.probe_div = 0;
+  static const bool no_helpers = getenv("VRS_NO_HELPERS") != nullptr;   // (A/B only)
+  p.no_helpers = no_helpers ? 1 : 0;
   p.min_span = tc_min_span();
   p.min_p = tc_min_p(plan);
   static const bool no_ar = getenv("VRS_NO_AR") != nullptr;

@@ -10,6 +10,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "vrs_kernels.cuh"
 
@@ -314,6 +315,7 @@ struct TcParams {
   int32_t a_lo_off = 0;
   const int32_t *qcount = nullptr;
   const void *xrows_lo = nullptr;   // cp.async gather, segment 1: x_lo's base
+  int32_t no_helpers = 0;           // (A/B, VRS_NO_HELPERS) no helper producer warps
 };
 
 // Warp-cooperative compaction of one lane's candidate buffer to its best KP
@@ -450,6 +452,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   int split = blockIdx.x / p.qtiles;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;   // (PAIR: qtile & 1)
   const bool leader = rank == 0;
+  // Helper producers: the epilogue warps of TMEM lane quadrants that hold no query of this
+  // tile (a batch of <= 96 queries) skip the epilogue; with cp.async row delivery they fetch
+  // rows beside warps 0 and 3 -- each warp keeps ~55 loads in flight, so two producer warps
+  // capped the by-id fetch near 40 GB/s per SM.  (Not in pairs / the refine / range passes.)
+  const int64_t q_tile = p.q - (int64_t)qtile * BM;   // queries of this tile (<= BM when not the last)
+  const int act_quads = (int)(((q_tile < BM ? q_tile : (int64_t)BM) + 31) / 32);
+  const bool hp_ok = !PAIR && p.qcount == nullptr && (MODE == MODE_MAIN || MODE == MODE_PROBE) && act_quads >= 1 &&
+                     act_quads < 4 && !p.no_helpers;
+  const int epi_arrivals = hp_ok ? LPS * act_quads : EPI_WARPS;   // epilogue warps releasing a tile
+  const bool helper = hp_ok && warp >= EPI_WARP0 && (warp & 3) >= act_quads;
   if (threadIdx.x == 0) TC_TL(0);
   if (threadIdx.x == 0) {
     // (PAIR: the leader's stage barrier also counts the peer's relay, its accumulator-empty
@@ -458,11 +470,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     mbar_init(&afull_bar, 1);
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], PAIR && leader ? 2 * EPI_WARPS : EPI_WARPS);
+      mbar_init(&tempty_bar[s], PAIR && leader ? 2 * EPI_WARPS : epi_arrivals);
     }
     for (int s = 0; s < BIAS_STAGES; ++s) {
       mbar_init(&bfull_bar[s], 32);
-      mbar_init(&bempty_bar[s], EPI_WARPS);
+      mbar_init(&bempty_bar[s], epi_arrivals);
     }
     fence_barrier_init();
   }
@@ -543,77 +555,92 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   auto tile_of = [&](int t) -> int64_t { return t_begin + (int64_t)t * step; };
 
 
-#ifndef VRS_CP_WARPS
-#define VRS_CP_WARPS 2
-#endif
-  // cp.async producer warps (1: warp 0; 2: warps 0 and 3).  With the coalesced producer two
-  // warps raise the per-SM fetch rate: C4 s = 50 % Q = 1 2.06 -> 1.89 ms, Q = 256 4.00 -> 3.33 ms,
-  // C3 s = 10 % Q = 1 0.51 -> 0.48 ms (r02_cp_warps_ab.txt; round 1's uncoalesced one: equal)
-  constexpr int CPW = VRS_CP_WARPS;
-  if ((warp == 0 || (CPW == 2 && warp == 3)) && cpg) {
+  // cp.async producer warps: warps 0 and 3, plus (helpers, above) 2 or 6 epilogue warps of
+  // query-less TMEM quadrants -- 2, 4 or 8 warps, each fetching a contiguous share of the
+  // tile's rows.  Two warps: C4 s = 50 % Q = 1 2.06 -> 1.89 ms (r02_cp_warps_ab.txt);
+  // the helpers: r02_helpers_ab.txt
+  const int n_help = hp_ok ? (act_quads == 1 ? 6 : 2) : 0;
+  int hidx = -1;   // helper index (epilogue warps of query-less quadrants, in warp order)
+  if (helper) {
+    hidx = 0;
+    for (int w2 = EPI_WARP0; w2 < warp; ++w2) hidx += (w2 & 3) >= act_quads ? 1 : 0;
+    if (hidx >= n_help) hidx = -1;   // (a third / fourth helper when two suffice: idle)
+  }
+  if ((warp == 0 || warp == 3 || hidx >= 0) && cpg) {
     // ------------------------------------------------ cp.async producers, gathered rows
-    // (late materialisation without a copy: warps 0 and 3 each fetch half of the tile's
-    // rows straight from X by id -- each row's 128-byte K-block segment as 8 x 16 B,
-    // placed in the 128B-swizzled layout the MMA descriptors expect (what a TMA box
-    // load would write); the stage's barrier completes when every lane's copies land:
-    // each lane's cp.async.mbarrier.arrive adds a pending arrival that its copies
-    // retire, and warp 0's lane 0 arrives only after both warps registered theirs)
+    // (late materialisation without a copy: NPW warps each fetch a contiguous share of the
+    // tile's rows straight from X by id -- each row's 128-byte K-block segment as 8 x 16 B,
+    // placed in the 128B-swizzled layout the MMA descriptors expect (what a TMA box load
+    // would write); the stage's barrier completes when every lane's copies land: each lane's
+    // cp.async.mbarrier.arrive adds a pending arrival that its copies retire, and warp 0's
+    // lane 0 arrives only after every producer warp registered its own)
     const bool lead = warp == 0;
-    const int hrow = lead ? 0 : BROWS / CPW;   // this warp's first row of the CTA's rows of the tile
-    int stage = 0;
-    uint32_t phase = 0;
-    if (lead && AR && ntiles > 0 && lane == 0) {
-      mbar_expect_tx(&afull_bar, p.nk * ABLK);
-      for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * ABLK, &tmap_q, &afull_bar, kb * KE, qtile * BM);
-    }
-    constexpr int GR = BROWS / (32 * CPW);   // rows per lane per warp
-    const char *xb = static_cast<const char *>(p.xrows);
-    const int64_t rb = p.row_bytes;
-    const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;
-    auto load_ids = [&](int t, int32_t (&r)[GR]) {
+    const int pidx = warp == 0 ? 0 : (warp == 3 ? 1 : 2 + hidx);
+    auto produce = [&](auto npw_c) {
+      constexpr int NPW = decltype(npw_c)::value;
+      const int hrow = pidx * (BROWS / NPW);   // this warp's first row of the CTA's rows of the tile
+      int stage = 0;
+      uint32_t phase = 0;
+      if (lead && AR && ntiles > 0 && lane == 0) {
+        mbar_expect_tx(&afull_bar, p.nk * ABLK);
+        for (int kb = 0; kb < p.nk; ++kb) tma_load_2d(a_res + kb * ABLK, &tmap_q, &afull_bar, kb * KE, qtile * BM);
+      }
+      constexpr int GR = BROWS / (32 * NPW);   // rows per lane per warp
+      static_assert(GR >= 1, "at least one row per lane");
+      const char *xb = static_cast<const char *>(p.xrows);
+      const int64_t rb = p.row_bytes;
+      const int32_t pad_row = n_sel > 0 ? __ldg(p.ids + n_sel - 1) : 0;
+      auto load_ids = [&](int t, int32_t (&r)[GR]) {
 #pragma unroll
-      for (int u = 0; u < GR; ++u) {
-        const int64_t pos = tile_of(t) * BN + rank * BROWS + hrow + lane + 32 * u;
-        r[u] = pos < n_sel ? __ldg(p.ids + pos) : pad_row;
+        for (int u = 0; u < GR; ++u) {
+          const int64_t pos = tile_of(t) * BN + rank * BROWS + hrow + lane + 32 * u;
+          r[u] = pos < n_sel ? __ldg(p.ids + pos) : pad_row;
+        }
+      };
+      int32_t rid[GR], rnext[GR];
+      if (ntiles > 0) load_ids(0, rid);
+      for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) load_ids(t + 1, rnext);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int seg = kb / p.nk, kk = kb - seg * p.nk;   // (refine: 3 segments, x_lo in segment 1)
+          const char *xs = seg == 1 ? static_cast<const char *>(p.xrows_lo) : xb;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t *st = b_base + stage * SSTRIDE;
+          const uint32_t bdst = smem_u32(st + BOFF);
+          const int64_t koff = (int64_t)kk * 128;
+          // coalesced: 8 lanes copy one row's 128-byte segment (16 B each), a warp
+          // instruction 4 whole rows; the row ids (lane j holds rows j + 32v) by shuffle
+          const int c = lane & 7;
+          const bool cvalid = koff + c * 16 < rb;
+#pragma unroll
+          for (int u = 0; u < BROWS / (4 * NPW); ++u) {
+            const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
+            const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
+            const int r = hrow + rl;
+            cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xs + (int64_t)id * rb + koff + c * 16, cvalid);
+          }
+          cpa_mbar_arrive(&full_bar[stage]);
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * NPW) : "memory");   // every producer warp registered its arrivals
+          if (lead && lane == 0) {
+            if (!AR) {
+              mbar_expect_tx(&full_bar[stage], A_BYTES);
+              tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
+            } else {
+              mbar_arrive(&full_bar[stage]);
+            }
+          }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+#pragma unroll
+        for (int u = 0; u < GR; ++u) rid[u] = rnext[u];
       }
     };
-    int32_t rid[GR], rnext[GR];
-    if (ntiles > 0) load_ids(0, rid);
-    for (int t = 0; t < ntiles; ++t) {
-      if (t + 1 < ntiles) load_ids(t + 1, rnext);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int seg = kb / p.nk, kk = kb - seg * p.nk;   // (refine: 3 segments, x_lo in segment 1)
-        const char *xs = seg == 1 ? static_cast<const char *>(p.xrows_lo) : xb;
-        mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t *st = b_base + stage * SSTRIDE;
-        const uint32_t bdst = smem_u32(st + BOFF);
-        const int64_t koff = (int64_t)kk * 128;
-        // coalesced: 8 lanes copy one row's 128-byte segment (16 B each), a warp
-        // instruction 4 whole rows; the row ids (lane j holds rows j + 32v) by shuffle
-        const int c = lane & 7;
-        const bool cvalid = koff + c * 16 < rb;
-#pragma unroll
-        for (int u = 0; u < BROWS / (4 * CPW); ++u) {
-          const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
-          const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
-          const int r = hrow + rl;
-          cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xs + (int64_t)id * rb + koff + c * 16, cvalid);
-        }
-        cpa_mbar_arrive(&full_bar[stage]);
-        if (CPW == 2) asm volatile("bar.sync 1, 64;" ::: "memory");   // both producer warps registered their arrivals
-        else __syncwarp();
-        if (lead && lane == 0) {
-          if (!AR) {
-            mbar_expect_tx(&full_bar[stage], A_BYTES);
-            tma_load_2d(st, &tmap_q, &full_bar[stage], (seg == 2 ? p.a_lo_off : 0) + kk * KE, qtile * BM);
-          } else {
-            mbar_arrive(&full_bar[stage]);
-          }
-        }
-        if (++stage == NST) { stage = 0; phase ^= 1; }
-      }
-#pragma unroll
-      for (int u = 0; u < GR; ++u) rid[u] = rnext[u];
+    if constexpr (PAIR) {   // (no helpers in pairs: half a tile per CTA)
+      produce(std::integral_constant<int, 2>{});
+    } else {
+      if (n_help == 6) produce(std::integral_constant<int, 8>{});
+      else if (n_help == 2) produce(std::integral_constant<int, 4>{});
+      else produce(std::integral_constant<int, 2>{});
     }
   } else if (warp == 0 && gather && p.g4 == 1) {
     // ------------------------------------------------ TMA producer, gathered rows
@@ -873,7 +900,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         fetch(t + PF, nv[u], iv[u], wv[u]);
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  } else if (warp >= EPI_WARP0 && !helper) {
     // ------------------------------------------------ epilogue
     const int ew = warp - EPI_WARP0;
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
