@@ -1578,6 +1578,104 @@ __global__ void __launch_bounds__(NW * 32) threshold_union_kernel(ThresholdArgs 
   }
 }
 
+// Small batches (q < 148, <= 32768 values per query): one CTA of 1024 threads per query,
+// few block-wide steps -- every value loaded in one round (<= 32 per thread, registers),
+// min / max, one 2048-bucket histogram over a monotone linear map of the values, the
+// bucket holding the K-th largest found from the top; gtau = the smallest value in that
+// bucket.  At least K values are >= it, so it is <= the K-th largest: a valid lower bound
+// of the K-th best key (within one bucket of the K-th value).  Replaces the per-lane top-E
+// union and its register sorts / merge tree (C3 / C4, Q = 1: 16-28 us on one SM).
+constexpr int kThrHT = 1024;
+constexpr int kThrHV = 32;      // values per thread
+constexpr int kThrHNB = 2048;   // buckets
+__global__ void __launch_bounds__(kThrHT, 1) threshold_hist_kernel(ThresholdArgs a) {
+  TL_SCOPE(0);
+  __shared__ uint32_t hist[kThrHNB];
+  __shared__ uint32_t s_lo[32], s_hi[32], s_cnt[32], s_w[32];
+  __shared__ uint32_t s_min;
+  __shared__ int s_bstar;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t j = blockIdx.x;
+  pdl_wait();
+  TL_WAITED(0);
+  pdl_trigger();
+  const float *v = a.vals + j * a.nvals;
+  TL_STAMP(0, 2);
+  uint32_t u[kThrHV];
+  uint32_t lo = 0xffffffffu, hi = 0u, cnt = 0;
+#pragma unroll
+  for (int i = 0; i < kThrHV; ++i) {
+    const int idx = tid + i * kThrHT;
+    const float f = idx < a.nvals ? __ldg(v + idx) : -INFINITY;
+    u[i] = f > -INFINITY ? ordered_u32(f) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < kThrHV; ++i)
+    if (u[i]) { lo = min(lo, u[i]); hi = max(hi, u[i]); ++cnt; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) { s_lo[w] = lo; s_hi[w] = hi; s_cnt[w] = cnt; }
+  for (int b = tid; b < kThrHNB; b += kThrHT) hist[b] = 0;
+  if (tid == 0) s_min = 0xffffffffu;
+  __syncthreads();
+  lo = 0xffffffffu; hi = 0u; cnt = 0;
+#pragma unroll
+  for (int x = 0; x < 32; ++x) { lo = min(lo, s_lo[x]); hi = max(hi, s_hi[x]); cnt += s_cnt[x]; }
+  if (cnt < (uint32_t)a.kth) {   // fewer than K probed rows: no bound
+    if (tid == 0) a.gtau[j] = 0u;
+    return;
+  }
+  if (hi == lo) {   // (block-uniform) one value: it is the K-th largest
+    if (tid == 0) a.gtau[j] = lo;
+    return;
+  }
+  const float scale = ((float)kThrHNB - 0.5f) / (float)(hi - lo);
+  auto bucket = [&](uint32_t x) { return min(kThrHNB - 1, (int)((float)(x - lo) * scale)); };   // monotone
+#pragma unroll
+  for (int i = 0; i < kThrHV; ++i)
+    if (u[i]) atomicAdd(&hist[bucket(u[i])], 1u);
+  __syncthreads();
+  // the bucket of the K-th largest: thread t sums buckets [NB-1-2t-1, NB-1-2t] (descending)
+  constexpr int PB = kThrHNB / kThrHT;
+  uint32_t hv[PB], sum = 0;
+#pragma unroll
+  for (int t = 0; t < PB; ++t) { hv[t] = hist[kThrHNB - 1 - PB * tid - t]; sum += hv[t]; }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  uint32_t before = incl - sum;
+  for (int x = 0; x < w; ++x) before += s_w[x];
+  if (before < (uint32_t)a.kth && (uint32_t)a.kth <= before + sum) {
+    uint32_t run = before;
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      if ((uint32_t)a.kth <= run + hv[t]) { s_bstar = kThrHNB - 1 - PB * tid - t; break; }
+      run += hv[t];
+    }
+  }
+  __syncthreads();
+  const int bstar = s_bstar;
+  uint32_t mn = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < kThrHV; ++i)
+    if (u[i] && bucket(u[i]) == bstar) mn = min(mn, u[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0 && mn != 0xffffffffu) atomicMin(&s_min, mn);
+  __syncthreads();
+  TL_STAMP(0, 3);
+  if (tid == 0) a.gtau[j] = s_min;
+}
+
 cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
   // large batches with short value lists: a warp per query (A/B: VRS_BLOCK_THRESHOLD forces the block kernel)
   static const bool block_thr = getenv("VRS_BLOCK_THRESHOLD") != nullptr;
@@ -1589,6 +1687,12 @@ cudaError_t launch_threshold(const ThresholdArgs &a, cudaStream_t s) {
     return launch_k(threshold_warp_kernel, dim3((unsigned)((a.q + kFinGroup - 1) / kFinGroup)), dim3(kFinGroup * 32),
                     wsmem, s, a);
   }
+  // (small batches with k' >= 64: the block histogram kernel -- C3 s = 10 %, Q = 1 threshold
+  // 16 -> 9 us, C4 s = 5 %, Q = 1 28 -> 12 us (cells -4-5 %); with C2's k' = 26 the union
+  // kernel is 4 us faster; VRS_THR_UNION=1 keeps the union kernels for A/B, r02_threshold_hist_ab.txt)
+  static const bool thr_union = getenv("VRS_THR_UNION") != nullptr;
+  if (!block_thr && !thr_union && a.q < kSmCountB200 && a.kth >= 64 && a.nvals <= kThrHT * kThrHV)
+    return launch_k(threshold_hist_kernel, dim3((unsigned)a.q), dim3(kThrHT), 0, s, a);
   if (!block_thr && a.kth <= 128) {
     // per lane E values, merged width 32M >= 2K (M = E): the K-th of the kept union stays
     // close to the K-th of all values (see threshold_warp_kernel)
