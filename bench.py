@@ -170,7 +170,7 @@ def workload_desc(cfg, world):
             "data": "synthetic, seeded (datagen): BASELINE.json configs shapes and distributions",
             "l2_flush": "inputs > L2 (corpus %.1f GB fp32 + %.1f GB fp16 shadow per GPU vs 126 MB L2)" % (
                 (r1 - r0) * cfg.d * 4 / 1e9, (r1 - r0) * cfg.d * 2 / 1e9),
-            "parallelism": (f"{world} GPUs, rows sharded, one NCCL all-gather of the step's candidates + vrs_merge"
+            "parallelism": (f"{world} GPUs, rows sharded, one exchange + merge of the step's candidates (vrs_merge_push over symmetric memory, else NCCL all-gather + vrs_merge)"
                             if world > 1 else "1 GPU")}
 
 
@@ -318,9 +318,23 @@ def main():
         bufs[c] = (ids_all[q0:q0 + c[1]], dists_all[q0:q0 + c[1]])
         offs[c] = q0
         q0 += c[1]
+    merge_path = None
     if world > 1:
         import torch.distributed as dist
-        from paper_2403_15807_b200.dist import gather_merge
+        from paper_2403_15807_b200.dist import PeerMerge, gather_merge
+        # the exchange + merge as one kernel over symmetric (NVLink peer) memory; NCCL
+        # all-gather + vrs_merge when symmetric memory is unavailable
+        try:
+            peer = PeerMerge(q_tot, k)
+            merge_path = "vrs_merge_push: one kernel, P2P pushes into torch symmetric memory + device-side wait + merge"
+        except Exception as e:   # noqa: BLE001 -- fall back to the collective
+            peer = None
+            merge_path = f"NCCL all_gather_into_tensor + vrs_merge (symmetric memory unavailable: {type(e).__name__})"
+
+        def exchange(ids_t, dists_t):
+            if peer is not None and ids_t.shape[0] == q_tot:
+                return peer.merge(ids_t, dists_t, metric)
+            return gather_merge(ids_t, dists_t, k, metric)
     launches = [0]
     merged = [None]
     cell_path = {}
@@ -335,8 +349,8 @@ def main():
     def step(stats=None):
         for c in cells:
             run_cell(c, stats)
-        if world > 1:   # the step's results: one NCCL all-gather per array + one vrs_merge
-            merged[0] = gather_merge(ids_all, dists_all, k, metric)
+        if world > 1:   # the step's results: one push-merge kernel (or all-gather + vrs_merge)
+            merged[0] = exchange(ids_all, dists_all)
             launches[0] += 1
 
     def barrier():
@@ -379,7 +393,7 @@ def main():
             torch.cuda.synchronize()
             barrier()
             timing = ("CUDA graph of the step (captured once, outside the timed region"
-                      + (", NCCL all-gather + merge inside" if world > 1 else "") + "), replayed K times")
+                      + (", the exchange + merge inside" if world > 1 else "") + "), replayed K times")
         except Exception as e:   # noqa: BLE001 -- report and time eagerly
             graph = None
             timing = f"eager launches (graph capture failed: {type(e).__name__})"
@@ -551,8 +565,8 @@ def main():
             else:
                 qd[q].copy_(qh[q], non_blocking=True)
                 ix.search(qd[q], preds[s], k=k, metric=metric, out=bufs[c])
-        if world > 1:   # one all-gather + merge for the step, results to the host
-            mi, md = gather_merge(ids_all, dists_all, k, metric)
+        if world > 1:   # one exchange + merge for the step, results to the host
+            mi, md = exchange(ids_all, dists_all)
             for c in cells:
                 hb[c][0].copy_(mi[offs[c]:offs[c] + c[1]], non_blocking=True)
                 hb[c][1].copy_(md[offs[c]:offs[c] + c[1]], non_blocking=True)
@@ -593,7 +607,7 @@ def main():
         for s, q in pcells:
             run_cell((s, q))
             torch.cuda.synchronize()
-            if world > 1:   # the merged result of this cell
+            if world > 1:   # the merged result of this cell (every rank runs the same merge)
                 gi_t, gd_t = gather_merge(*bufs[(s, q)], k, metric)
             else:
                 gi_t, gd_t = bufs[(s, q)]
@@ -643,6 +657,7 @@ def main():
                 "data": "synthetic", "config": workload_desc(cfg, world), "e2e": e2e,
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
                 "timing": timing, "certificate": cert, "parity": parity, "cells": cell_out,
+                "merge": merge_path,
                 "step_ms": [round(x, 4) for x in step_ms],
                 "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
         print(json.dumps(line), flush=True)

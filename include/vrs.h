@@ -280,6 +280,34 @@ VRS_API vrs_status vrs_select(vrs_index *ix, const vrs_predicate *pred, uint32_t
 VRS_API vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n_parts, int64_t q, int32_t k,
                      vrs_metric metric, int64_t *ids, float *dists, void *cuda_stream);
 
+/*
+ * vrs_merge_push -- the multi-GPU exchange and merge in ONE kernel over peer memory
+ * (north_star (4); SURVEY 8(e) mitigation 2: one-shot P2P stores, a device-side wait, the
+ * merge): every rank calls it on its own stream with its exact local vrs_search output; the
+ * kernel stores that [q x k] into this rank's slot of every rank's receive buffer (NVLink
+ * P2P), counts the push there with a system-scope atomic, waits until every rank's push of
+ * this call has arrived in its own buffer, and writes the top-k of the union -- the same
+ * result as vrs_merge over an all-gather.  No host synchronisation; CUDA-graph capturable
+ * (the call counter lives in `state`).
+ *   local_ids, local_dists : device [q x k], this rank's vrs_search output (global ids)
+ *   peer_bufs  : DEVICE array of n_parts pointers, rank p's receive buffer as mapped on this
+ *                GPU (e.g. torch symmetric memory's buffer_ptrs_dev); each buffer holds
+ *                buf_bytes >= vrs_push_buffer_bytes(n_parts, q, k) bytes, its first 256 bytes
+ *                zeroed before the first call (ownership: the caller's)
+ *   n_parts    : ranks, 1..64;  my_part : this rank, 0..n_parts-1
+ *   state      : this rank's device uint32[4], zeroed before the first call, then owned by
+ *                the calls (every rank must make the same sequence of calls)
+ *   ids, dists : device [q x k] outputs (may not alias the inputs)
+ * Errors: VRS_EINVAL (bad sizes, host pointers, buffer too small), VRS_EUNSUPPORTED
+ * (k > VRS_K_MAX, n_parts > 64).  All ranks' kernels must be able to run concurrently
+ * (one process per GPU): a rank whose peers never call waits forever.
+ */
+VRS_API vrs_status vrs_merge_push(const int64_t *local_ids, const float *local_dists, void *const *peer_bufs,
+                                  int64_t buf_bytes, int32_t n_parts, int32_t my_part, int64_t q, int32_t k,
+                                  vrs_metric metric, uint32_t *state, int64_t *ids, float *dists, void *cuda_stream);
+/* Bytes each rank's receive buffer needs for vrs_merge_push(n_parts, q, k). */
+VRS_API int64_t vrs_push_buffer_bytes(int32_t n_parts, int64_t q, int32_t k);
+
 /* Release the index's own memory (borrowed vectors / attrs are untouched). NULL is a no-op. */
 VRS_API vrs_status vrs_free(vrs_index *ix);
 

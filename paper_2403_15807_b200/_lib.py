@@ -27,7 +27,7 @@ MAX_CLAUSES = 8
 
 # every symbol include/vrs.h declares (tests check the library exports them)
 EXPORTS = ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_host_fence", "vrs_select", "vrs_merge", "vrs_free",
-           "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
+           "vrs_merge_push", "vrs_push_buffer_bytes", "vrs_last_error", "vrs_last_path", "vrs_last_precision", "vrs_index_precision", "vrs_last_launches", "vrs_index_rows", "vrs_index_dim",
            "vrs_profile_enable", "vrs_profile_read", "vrs_profile_reset", "vrs_pool_reserved_bytes")
 
 
@@ -91,6 +91,10 @@ def load_library():
     lib.vrs_host_fence.argtypes = [p, p]
     lib.vrs_select.argtypes = [p, p, p, p, p, p]
     lib.vrs_merge.argtypes = [p, p, i32, i64, i32, ctypes.c_int, p, p, p]
+    lib.vrs_merge_push.argtypes = [p, p, p, i64, i32, i32, i64, i32, ctypes.c_int, p, p, p, p]
+    lib.vrs_merge_push.restype = ctypes.c_int
+    lib.vrs_push_buffer_bytes.argtypes = [i32, i64, i32]
+    lib.vrs_push_buffer_bytes.restype = i64
     lib.vrs_free.argtypes = [p]
     for f in ("vrs_load", "vrs_load_ex", "vrs_search", "vrs_range_search", "vrs_search_ex", "vrs_search_host", "vrs_host_fence",
               "vrs_select", "vrs_merge", "vrs_free"):

@@ -1761,26 +1761,16 @@ cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s, int *launches
 
 // ------------------------------------------------------------------ K10' merge
 
-__global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
-  TL_SCOPE(2);
+// One query of the K10' merge (one CTA): the k best of C candidates by (dist, global id) --
+// block_select_top by key, then a warp sort -- written best-first with padding.
+template <typename Get>
+__device__ void merge_query(Get get, int64_t C, int k, int metric, int64_t j, int64_t *ids, float *dists) {
   __shared__ int64_t s_id[kFinMaxSel];
   __shared__ float s_key[kFinMaxSel];
   __shared__ double s_k2[kFinMaxSel];
   __shared__ int64_t s_i2[kFinMaxSel];
-  const int64_t j = blockIdx.x;
-  pdl_wait();
-  TL_WAITED(2);
-  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5;
-  auto get = [&](int64_t c, float &key, int64_t &id) -> bool {
-    const int64_t p = c / a.k, r = c - p * a.k;
-    const int64_t o = (p * a.q + j) * a.k + r;
-    id = a.cand_ids[o];
-    const float dv = a.cand_dists[o];
-    key = a.metric == VRS_L2 ? -dv : dv;
-    return id >= 0;
-  };
-  const int m = block_select_top<int64_t>(get, (int64_t)a.parts * a.k, a.k, s_id, s_key);
+  const int m = block_select_top<int64_t>(get, C, k, s_id, s_key);
   int np = 1;
   while (np < m) np <<= 1;
   for (int c = tid; c < np; c += kFinThreads) {
@@ -1790,18 +1780,120 @@ __global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
   __syncthreads();
   if (warp == 0 && m > 1) warp_sort_desc_d(s_k2, s_i2, np);
   __syncthreads();
-  const float pad = a.metric == VRS_L2 ? INFINITY : -INFINITY;
-  for (int r = tid; r < a.k; r += kFinThreads) {
-    const int64_t o = j * a.k + r;
+  const float pad = metric == VRS_L2 ? INFINITY : -INFINITY;
+  for (int r = tid; r < k; r += kFinThreads) {
+    const int64_t o = j * k + r;
     if (r < m) {
-      a.ids[o] = s_i2[r];
+      ids[o] = s_i2[r];
       const float kv = (float)s_k2[r];
-      a.dists[o] = a.metric == VRS_L2 ? -kv : kv;
+      dists[o] = metric == VRS_L2 ? -kv : kv;
     } else {
-      a.ids[o] = -1;
-      a.dists[o] = pad;
+      ids[o] = -1;
+      dists[o] = pad;
     }
   }
+  __syncthreads();   // (shared buffers reused by the CTA's next query)
+}
+
+__global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
+  TL_SCOPE(2);
+  const int64_t j = blockIdx.x;
+  pdl_wait();
+  TL_WAITED(2);
+  pdl_trigger();
+  auto get = [&](int64_t c, float &key, int64_t &id) -> bool {
+    const int64_t p = c / a.k, r = c - p * a.k;
+    const int64_t o = (p * a.q + j) * a.k + r;
+    id = a.cand_ids[o];
+    const float dv = a.cand_dists[o];
+    key = a.metric == VRS_L2 ? -dv : dv;
+    return id >= 0;
+  };
+  merge_query(get, (int64_t)a.parts * a.k, a.k, a.metric, j, a.ids, a.dists);
+}
+
+// ------------------------------------------------------------------ K10'' push-merge
+// The multi-GPU exchange + merge in one kernel over peer memory (NVLink P2P through
+// symmetric-memory buffers; SURVEY 8(e) mitigation 2): every rank pushes its exact local
+// [q x k] results into its slot of every rank's receive buffer (one-shot P2P stores), counts
+// the push on each peer with a system-scope atomic, waits until every source's pushes of
+// this call arrived, and merges its queries from its own buffer -- no all-gather launch, no
+// host involvement.  Receive buffer of rank p (peer_bufs[p]): uint32 counts[64] (pushes
+// received from each source, cumulative), then slots [2 parities][parts][q][k] of (int64 id)
+// followed by (fp32 dist).  The call's epoch e (device state, so CUDA-graph replays advance
+// it) picks the parity: a rank can run at most one call ahead of a peer (its merge waits for
+// the peer's push), so the slot a faster rank overwrites was read by the slower one a call
+// ago.  The grid (<= 2 CTAs per SM) is resident: every CTA's wait on all sources' pushes
+// cannot block a CTA it waits for.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void __launch_bounds__(kFinThreads) push_merge_kernel(PushMergeArgs a) {
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const uint32_t e = a.state[0] + 1u, par = e & 1u, base = a.state[2];
+  const uint32_t nblk = gridDim.x;
+  const int64_t qk = a.q * a.k;
+  auto slot = [&](const void *buf, uint32_t src) {
+    return reinterpret_cast<int64_t *>(static_cast<char *>(const_cast<void *>(buf)) + kPushHeader +
+                                       ((int64_t)(par * (uint32_t)a.parts + src) * qk) * 12);
+  };
+  // (1) push this CTA's queries to every rank (itself included)
+  for (int p = 0; p < a.parts; ++p) {
+    int64_t *di = slot(a.peer_bufs[p], (uint32_t)a.my_part);
+    float *dd = reinterpret_cast<float *>(di + qk);
+    for (int64_t j = blockIdx.x; j < a.q; j += nblk)
+      for (int r = tid; r < a.k; r += kFinThreads) {
+        const int64_t o = j * a.k + r;
+        di[o] = a.local_ids[o];
+        dd[o] = a.local_dists[o];
+      }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int p = 0; p < a.parts; ++p) atomicAdd_system(static_cast<uint32_t *>(a.peer_bufs[p]) + a.my_part, 1u);
+  }
+  // (2) every source's pushes of this call (all its CTAs) have landed in this rank's buffer
+  const uint32_t *cnt = static_cast<const uint32_t *>(a.peer_bufs[a.my_part]);
+  if (tid < a.parts)
+    while ((int32_t)(ld_acquire_sys(cnt + tid) - (base + nblk)) < 0) {
+    }
+  __syncthreads();
+  // (3) merge this CTA's queries from the parts' slots
+  const void *mine = a.peer_bufs[a.my_part];
+  for (int64_t j = blockIdx.x; j < a.q; j += nblk) {
+    auto get = [&](int64_t c, float &key, int64_t &id) -> bool {
+      const uint32_t src = (uint32_t)(c / a.k);
+      const int64_t r = c - (int64_t)src * a.k;
+      const int64_t *si = slot(mine, src);
+      const float *sd = reinterpret_cast<const float *>(si + qk);
+      id = si[j * a.k + r];
+      const float dv = sd[j * a.k + r];
+      key = a.metric == VRS_L2 ? -dv : dv;
+      return id >= 0;
+    };
+    merge_query(get, (int64_t)a.parts * a.k, a.k, a.metric, j, a.ids, a.dists);
+  }
+  // (4) the call's bookkeeping, by the last CTA to finish (every CTA read the state at its start)
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(a.state + 1, 1u);
+    if (t == nblk - 1) {
+      a.state[1] = 0;
+      a.state[2] = base + nblk;
+      a.state[0] = e;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t launch_push_merge(const PushMergeArgs &a, cudaStream_t s, int *launches) {
+  if (launches) *launches += 1;
+  const unsigned blocks = (unsigned)std::min<int64_t>(a.q, 2 * kSmCountB200);
+  return launch_k(push_merge_kernel, dim3(blocks), dim3(kFinThreads), 0, s, a);
 }
 
 cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s, int *launches) {

@@ -1122,6 +1122,37 @@ vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, int32_t n
   return VRS_OK;
 }
 
+vrs_status vrs_merge_push(const int64_t *local_ids, const float *local_dists, void *const *peer_bufs,
+                          int64_t buf_bytes, int32_t n_parts, int32_t my_part, int64_t q, int32_t k,
+                          vrs_metric metric, uint32_t *state, int64_t *ids, float *dists, void *cuda_stream) {
+  g_err[0] = 0;
+  if (n_parts < 1 || my_part < 0 || my_part >= n_parts || q < 0 || k < 1)
+    return fail(VRS_EINVAL, "n_parts %d, my_part %d, q %lld, k %d", n_parts, my_part, (long long)q, k);
+  if (n_parts > kPushMaxParts) return fail(VRS_EUNSUPPORTED, "n_parts = %d > %d", n_parts, kPushMaxParts);
+  if (metric != VRS_L2 && metric != VRS_IP && metric != VRS_COSINE)
+    return fail(VRS_EINVAL, "bad metric %d", (int)metric);
+  if (k > VRS_K_MAX) return fail(VRS_EUNSUPPORTED, "k = %d > VRS_K_MAX (%d)", k, VRS_K_MAX);
+  if (q == 0) return VRS_OK;
+  if (buf_bytes < push_buffer_bytes(n_parts, q, k))
+    return fail(VRS_EINVAL, "receive buffers of %lld bytes < %lld needed", (long long)buf_bytes,
+                (long long)push_buffer_bytes(n_parts, q, k));
+  if (!is_device_ptr(local_ids) || !is_device_ptr(local_dists) || !is_device_ptr(peer_bufs) || !is_device_ptr(state) ||
+      !is_device_ptr(ids) || !is_device_ptr(dists))
+    return fail(VRS_EINVAL, "vrs_merge_push buffers must be device pointers");
+  vrs_status st = check_device(nullptr, nullptr);
+  if (st != VRS_OK) return st;
+  int launches = 0;
+  PushMergeArgs a{local_ids, local_dists, peer_bufs, n_parts, my_part, q, k, (int32_t)metric, state, ids, dists};
+  {
+    ProfScope ps("merge", (cudaStream_t)cuda_stream);
+    CUDA_TRY(launch_push_merge(a, (cudaStream_t)cuda_stream, &launches));
+  }
+  g_last_launches = launches;
+  return VRS_OK;
+}
+
+int64_t vrs_push_buffer_bytes(int32_t n_parts, int64_t q, int32_t k) { return push_buffer_bytes(n_parts, q, k); }
+
 }  // extern "C"
 
 #ifdef VRS_TC_TIMING

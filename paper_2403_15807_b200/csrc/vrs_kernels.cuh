@@ -296,4 +296,21 @@ struct MergeArgs {
 };
 cudaError_t launch_merge(const MergeArgs &a, cudaStream_t s, int *launches);
 
+// the multi-GPU exchange + merge in one kernel over peer (symmetric) memory (finalize.cu)
+constexpr int64_t kPushHeader = 256;   // bytes before the slots: uint32 counts[64]
+constexpr int kPushMaxParts = 64;
+inline int64_t push_buffer_bytes(int32_t parts, int64_t q, int32_t k) { return kPushHeader + 2 * (int64_t)parts * q * k * 12; }
+struct PushMergeArgs {
+  const int64_t *local_ids;   // this rank's exact results [q][k] (device)
+  const float *local_dists;
+  void *const *peer_bufs;     // device array [parts]: every rank's receive buffer (peer-mapped)
+  int32_t parts, my_part;
+  int64_t q;
+  int32_t k, metric;
+  uint32_t *state;            // this rank's device state [4]: epoch, ticket, pushes expected so far, -
+  int64_t *ids;               // merged [q][k]
+  float *dists;
+};
+cudaError_t launch_push_merge(const PushMergeArgs &a, cudaStream_t s, int *launches);
+
 }  // namespace vrs

@@ -6,7 +6,8 @@ local id); the queries and the predicate are replicated.  Each rank runs the
 whole single-GPU path on its shard (vrs_search -> exact [Q x k] dists and
 global ids); one all-gather of each output array over NCCL (NVLink 5 /
 NVSwitch) and vrs_merge on every rank give the identical global top-k
-(top-k is decomposable under the (dist, id) total order).
+(top-k is decomposable under the (dist, id) total order).  PeerMerge does the exchange
+and the merge in one kernel over peer (symmetric) memory instead (vrs_merge_push).
 """
 from __future__ import annotations
 
@@ -40,6 +41,48 @@ def gather_merge(ids: torch.Tensor, dists: torch.Tensor, k: int, metric, group=N
     gi = all_gather_rows(ids, group)
     gd = all_gather_rows(dists, group)
     return merge_fn(gi, gd, k, metric)
+
+
+class PeerMerge:
+    """The exchange + merge as one kernel over peer memory (vrs_merge_push): every rank
+    allocates a receive buffer of vrs_push_buffer_bytes(world, q_max, k) in torch symmetric
+    memory (peer-mapped over NVLink), rendezvous once, then each merge() pushes the rank's
+    [q x k] results into every rank's buffer and merges its own -- one launch per call, no
+    NCCL collective, CUDA-graph capturable.  Raises if symmetric memory is unavailable
+    (callers fall back to gather_merge)."""
+
+    def __init__(self, q_max: int, k: int, group=None, device=None):
+        import ctypes
+
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import library
+        self.lib = library()
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.k, self.q_max = int(k), int(q_max)
+        self.bytes = int(self.lib.vrs_push_buffer_bytes(self.world, self.q_max, self.k))
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm_mem.empty((self.bytes + 7) // 8, dtype=torch.int64, device=dev)
+        self.buf.zero_()   # (the per-source push counts start at 0)
+        torch.cuda.synchronize(dev)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        self.peer_ptrs = ctypes.c_void_p(int(self.handle.buffer_ptrs_dev))
+        self.state = torch.zeros(4, dtype=torch.int32, device=dev)
+        dist.barrier(group=self.group)
+
+    def merge(self, ids: torch.Tensor, dists: torch.Tensor, metric, out=None, stream=None):
+        from . import _lib, _metric, _ptr, _stream
+        q, k = ids.shape
+        if k != self.k or q > self.q_max:
+            raise ValueError(f"PeerMerge sized for q <= {self.q_max}, k = {self.k}")
+        oi, od = out if out is not None else (torch.empty_like(ids), torch.empty_like(dists))
+        st = self.lib.vrs_merge_push(_ptr(ids.contiguous()), _ptr(dists.contiguous()), self.peer_ptrs, self.bytes,
+                                     self.world, self.rank, q, k, _metric(metric), _ptr(self.state), _ptr(oi),
+                                     _ptr(od), _stream(stream))
+        _lib.check(st, "vrs_merge_push")
+        return oi, od
 
 
 class ShardedIndex:
