@@ -72,3 +72,41 @@ def test_shard_ranges_cover_exactly():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(r1 - r0 for r0, r1 in rs) - min(r1 - r0 for r0, r1 in rs) <= 1
+
+
+def _fallback_worker(rank, port, out_dir):
+    """The bench's exchange at N > 1 without symmetric memory (here: gloo on CPU):
+    PeerMerge refuses, gather_merge carries the exchange."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_2403_15807_b200.dist import PeerMerge, gather_merge
+    ok = False
+    try:
+        PeerMerge(16, 10)
+    except Exception:   # noqa: BLE001 -- expected without CUDA symmetric memory
+        ok = True
+    rng = np.random.default_rng(rank)
+    d = np.sort(rng.standard_normal((4, 10)).astype(np.float32), axis=1)
+    i = (rank * 1000 + np.arange(40)).reshape(4, 10).astype(np.int64)
+    mi, md = gather_merge(torch.from_numpy(i), torch.from_numpy(d), 10, oracle.L2, merge_fn=_oracle_merge)
+    np.save(os.path.join(out_dir, f"fb{rank}.npy"), np.array([ok]))
+    np.save(os.path.join(out_dir, f"fi{rank}.npy"), mi.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_merge_falls_back_without_symmetric_memory():
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.start_processes(_fallback_worker, args=(_free_port(), tmp), nprocs=WORLD, start_method="spawn")
+        for r in range(WORLD):
+            assert np.load(os.path.join(tmp, f"fb{r}.npy"))[0]
+        assert np.array_equal(np.load(os.path.join(tmp, "fi0.npy")), np.load(os.path.join(tmp, "fi1.npy")))
+
+
+def test_push_buffer_layout():
+    """vrs_push_buffer_bytes: a 256-byte count header + 2 parities x parts x q x k x (8 + 4) bytes."""
+    import paper_2403_15807_b200 as vrs
+    lib = vrs.library()
+    for parts, q, k in ((1, 1, 1), (8, 25347, 100), (2, 4096, 10)):
+        assert lib.vrs_push_buffer_bytes(parts, q, k) == 256 + 2 * parts * q * k * 12
