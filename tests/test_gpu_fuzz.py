@@ -86,3 +86,36 @@ def test_fuzz_range(vrs, seed):
     assert o.cpu().numpy().tolist() == ro.tolist()
     assert ids.cpu().numpy().tolist() == rids.tolist()
     assert np.allclose(dists.cpu().numpy(), rd, rtol=1e-6, atol=1e-7)
+
+
+N_CASES_LARGE_D = 80
+
+
+def _case_large_d(seed):
+    """d > 256 (streamed query tile): CTA pairs (even tile counts), AR8 (q <= 8), helper
+    producer warps (<= 96 queries in a tile), the block finalize and the histogram threshold
+    (q < 148, k' >= 64) -- each with every row delivery."""
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.integers(1, 30000))
+    d = int(rng.choice([264, 320, 512, 768, 1032, 1536]))
+    q = int(rng.choice([1, 5, 8, 9, 33, 96, 97, 129, 200, 256, 257, 384, 512]))
+    k = int(rng.choice([1, 10, 50, 100, 150, 240]))
+    metric = int(rng.choice([oracle.L2, oracle.IP, oracle.COS]))
+    lo = int(rng.integers(0, 1000))
+    pred = [] if rng.integers(0, 4) == 0 else [(0, lo, int(rng.integers(lo - 3, 1000)))]
+    rows = [None, 1, 2][int(rng.integers(0, 3))]
+    off = int(rng.integers(0, 1 << 20))
+    return rng, n, d, q, k, metric, pred, rows, off
+
+
+@pytest.mark.parametrize("seed", range(N_CASES_LARGE_D))
+def test_fuzz_parity_large_d(vrs, seed):
+    rng, n, d, q, k, metric, pred, rows, off = _case_large_d(seed)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    attrs = [rng.integers(0, 1000, n).astype(np.int32)]
+    Q = rng.standard_normal((q, d)).astype(np.float32)
+    ix = vrs.Index(torch.from_numpy(X).cuda(), [torch.from_numpy(a).cuda() for a in attrs], row_offset=off)
+    ids, dists = ix.search(torch.from_numpy(Q).cuda(), pred, k=k, metric=METRICS[metric], path=vrs.PATH_GEMM,
+                           rows=rows)
+    torch.cuda.synchronize()
+    check_topk(ids.cpu().numpy(), dists.cpu().numpy(), X, attrs, pred, Q, k, metric, row_offset=off)
