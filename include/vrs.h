@@ -296,11 +296,14 @@ VRS_API vrs_status vrs_merge(const int64_t *cand_ids, const float *cand_dists, i
  *                zeroed before the first call (ownership: the caller's)
  *   n_parts    : ranks, 1..64;  my_part : this rank, 0..n_parts-1
  *   state      : this rank's device uint32[4], zeroed before the first call, then owned by
- *                the calls (every rank must make the same sequence of calls)
+ *                the calls (every rank must make the same sequence of calls); state[3] != 0
+ *                after a call: a peer's push did not arrive within the wait bound (20 s,
+ *                VRS_PUSH_TIMEOUT_MS) -- that call's and every later call's output is invalid
  *   ids, dists : device [q x k] outputs (may not alias the inputs)
  * Errors: VRS_EINVAL (bad sizes, host pointers, buffer too small), VRS_EUNSUPPORTED
  * (k > VRS_K_MAX, n_parts > 64).  All ranks' kernels must be able to run concurrently
- * (one process per GPU): a rank whose peers never call waits forever.
+ * (one process per GPU): a rank whose peers never call gives up after the wait bound and
+ * sets state[3] (the status of the launch is still VRS_OK: the host reads the flag).
  */
 VRS_API vrs_status vrs_merge_push(const int64_t *local_ids, const float *local_dists, void *const *peer_bufs,
                                   int64_t buf_bytes, int32_t n_parts, int32_t my_part, int64_t q, int32_t k,

@@ -1824,7 +1824,7 @@ __global__ void __launch_bounds__(kFinThreads) merge_kernel(MergeArgs a) {
 // it) picks the parity: a rank can run at most one call ahead of a peer (its merge waits for
 // the peer's push), so the slot a faster rank overwrites was read by the slower one a call
 // ago.  The grid (<= 2 CTAs per SM) is resident: every CTA's wait on all sources' pushes
-// cannot block a CTA it waits for.
+// cannot block a CTA it waits for.  The wait is bounded (wait_ns, VRS_PUSH_TIMEOUT_MS).
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1858,9 +1858,20 @@ __global__ void __launch_bounds__(kFinThreads) push_merge_kernel(PushMergeArgs a
   }
   // (2) every source's pushes of this call (all its CTAs) have landed in this rank's buffer
   const uint32_t *cnt = static_cast<const uint32_t *>(a.peer_bufs[a.my_part]);
-  if (tid < a.parts)
+  // (bounded: a peer that never calls -- a dead rank, a transport that does not deliver --
+  // must not hang the GPU; the flag in state[3] tells the host the results are invalid)
+  if (tid < a.parts) {
+    uint64_t t0 = 0;
     while ((int32_t)(ld_acquire_sys(cnt + tid) - (base + nblk)) < 0) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > a.wait_ns) {
+        atomicOr(a.state + 3, 1u);
+        break;
+      }
     }
+  }
   __syncthreads();
   // (3) merge this CTA's queries from the parts' slots
   const void *mine = a.peer_bufs[a.my_part];

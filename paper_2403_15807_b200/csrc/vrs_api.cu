@@ -1142,7 +1142,10 @@ vrs_status vrs_merge_push(const int64_t *local_ids, const float *local_dists, vo
   vrs_status st = check_device(nullptr, nullptr);
   if (st != VRS_OK) return st;
   int launches = 0;
-  PushMergeArgs a{local_ids, local_dists, peer_bufs, n_parts, my_part, q, k, (int32_t)metric, state, ids, dists};
+  // bound of the device-side wait for the peers' pushes (default 20 s; state[3] is set when it expires)
+  static const long wait_ms = getenv("VRS_PUSH_TIMEOUT_MS") ? atol(getenv("VRS_PUSH_TIMEOUT_MS")) : 20000;
+  PushMergeArgs a{local_ids, local_dists, peer_bufs, n_parts, my_part, q, k, (int32_t)metric, state, ids, dists,
+                  (uint64_t)(wait_ms > 0 ? wait_ms : 1) * 1000000ull};
   {
     ProfScope ps("merge", (cudaStream_t)cuda_stream);
     CUDA_TRY(launch_push_merge(a, (cudaStream_t)cuda_stream, &launches));

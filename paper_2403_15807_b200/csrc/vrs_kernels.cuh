@@ -307,9 +307,10 @@ struct PushMergeArgs {
   int32_t parts, my_part;
   int64_t q;
   int32_t k, metric;
-  uint32_t *state;            // this rank's device state [4]: epoch, ticket, pushes expected so far, -
+  uint32_t *state;            // this rank's device state [4]: epoch, ticket, pushes expected so far, timed-out flag
   int64_t *ids;               // merged [q][k]
   float *dists;
+  uint64_t wait_ns;           // bound of the wait for the peers' pushes (state[3] = 1 when it expires)
 };
 cudaError_t launch_push_merge(const PushMergeArgs &a, cudaStream_t s, int *launches);
 

@@ -9,6 +9,10 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__bytes_read.sum.per_second", "DRAM read rate"),
+    ("dram__bytes_write.sum.per_second", "DRAM write rate"),
+    ("l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_ld.ratio", "sectors / request (global loads)"),
+    ("l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_st.ratio", "sectors / request (global stores)"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
