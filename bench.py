@@ -324,12 +324,22 @@ def main():
         from paper_2403_15807_b200.dist import PeerMerge, gather_merge
         # the exchange + merge as one kernel over symmetric (NVLink peer) memory; NCCL
         # all-gather + vrs_merge when symmetric memory is unavailable
+        nccl_path = "NCCL all_gather_into_tensor + vrs_merge"
         try:
             peer = PeerMerge(q_tot, k)
             merge_path = "vrs_merge_push: one kernel, P2P pushes into torch symmetric memory + device-side wait + merge"
         except Exception as e:   # noqa: BLE001 -- fall back to the collective
             peer = None
-            merge_path = f"NCCL all_gather_into_tensor + vrs_merge (symmetric memory unavailable: {type(e).__name__})"
+            merge_path = f"{nccl_path} (symmetric memory unavailable: {type(e).__name__})"
+        # every rank must take the same path: the push kernel only if every rank built it AND one
+        # validation exchange equals the NCCL path's result on every rank with no expired wait
+        # (the kernel's wait is bounded, vrs.h: a transport that does not deliver cannot hang the run)
+        have = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(have, op=dist.ReduceOp.MIN)
+        if peer is not None and not have.item():
+            peer, merge_path = None, f"{nccl_path} (symmetric memory unavailable on another rank)"
+        if peer is not None and not peer.validate(metric):
+            peer, merge_path = None, f"{nccl_path} (vrs_merge_push failed its validation exchange against the NCCL path)"
 
         def exchange(ids_t, dists_t):
             if peer is not None and ids_t.shape[0] == q_tot:
@@ -658,6 +668,7 @@ def main():
                 "gpu_launches": gpu_launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
                 "timing": timing, "certificate": cert, "parity": parity, "cells": cell_out,
                 "merge": merge_path,
+                "merge_wait_expired": (bool(peer.timed_out()) if world > 1 and peer is not None else None),
                 "step_ms": [round(x, 4) for x in step_ms],
                 "kernels_ms_per_step": {kname: v[0] / nprof for kname, v in prof.items()}}
         print(json.dumps(line), flush=True)

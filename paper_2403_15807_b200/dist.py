@@ -84,6 +84,30 @@ class PeerMerge:
         _lib.check(st, "vrs_merge_push")
         return oi, od
 
+    def timed_out(self) -> bool:
+        """True once a call's wait for a peer's push expired (vrs.h: state[3]); synchronises.
+        Every output since is invalid -- the caller falls back to gather_merge."""
+        return bool(self.state[3].item() != 0)
+
+    def validate(self, metric="ip") -> bool:
+        """One exchange of a deterministic [q_max x k] pattern through the push kernel AND
+        through gather_merge (NCCL all-gather + vrs_merge); True iff every rank got identical
+        results and no wait expired.  Collective: every rank calls it.  Run once before trusting
+        the peer transport (e.g. a first multi-GPU box)."""
+        dev = self.state.device
+        q, k = self.q_max, self.k
+        g = torch.Generator(device="cpu").manual_seed(1234 + self.rank)
+        from . import _metric
+        best_first_desc = int(_metric(metric)) != 0   # (VRS_L2 = 0: smaller is better)
+        d = torch.randn(q, k, generator=g).sort(dim=1, descending=best_first_desc).values.to(dev)
+        i = (torch.arange(q * k, dtype=torch.int64).reshape(q, k) * self.world + self.rank).to(dev)
+        gi, gd = self.merge(i, d, metric)
+        ri, rd = gather_merge(i, d, k, metric, self.group)
+        ok = torch.equal(gi, ri) and torch.equal(gd, rd) and not self.timed_out()
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(flag.item())
+
 
 class ShardedIndex:
     """The calling rank's shard of a row-sharded corpus."""

@@ -60,6 +60,8 @@ for rep in range(5):
     ri, rd = vrs.merge(ids[None], dists[None], k, "ip")
     torch.cuda.synchronize()
     assert torch.equal(out[0], ri) and torch.equal(out[1], rd), rep
+assert not pm.timed_out()
+assert pm.validate("ip") and pm.validate("l2")     # push kernel == all-gather + vrs_merge, no expired wait
 dist.destroy_process_group()
 print("OK")
 '''
@@ -67,4 +69,42 @@ print("OK")
 
 def test_peer_merge_world1():
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
+TIMEOUT_SCRIPT = r'''
+import ctypes, sys, time, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2403_15807_b200 as vrs
+lib = vrs.library()
+torch.cuda.set_device(0)
+q, k, parts = 40, 10, 2
+nbytes = int(lib.vrs_push_buffer_bytes(parts, q, k))
+bufs = [torch.zeros((nbytes + 7) // 8, dtype=torch.int64, device="cuda") for _ in range(parts)]
+ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+state = torch.zeros(4, dtype=torch.int32, device="cuda")
+ids = torch.arange(q * k, dtype=torch.int64, device="cuda").reshape(q, k)
+dists = torch.randn(q, k, device="cuda").sort(dim=1, descending=True).values
+oi, od = torch.empty_like(ids), torch.empty_like(dists)
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+torch.cuda.synchronize()
+t0 = time.time()
+st = lib.vrs_merge_push(P(ids), P(dists), P(ptrs), nbytes, parts, 0, q, k, 1, P(state), P(oi), P(od),
+                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+assert st == 0, st
+torch.cuda.synchronize()
+dt = time.time() - t0
+# rank 1 never pushes: the wait for its pushes expires (VRS_PUSH_TIMEOUT_MS = 300) and the flag is set
+assert state[3].item() == 1, state.tolist()
+assert 0.25 < dt < 10.0, dt
+print("OK")
+'''
+
+
+def test_push_wait_is_bounded():
+    """A peer that never pushes: the kernel gives up after the wait bound and sets state[3]
+    (vrs.h) instead of hanging the GPU.  (One rank, two plain device buffers: no peer kernel
+    is waited for -- the point is that none arrives.)"""
+    env = dict(os.environ, VRS_PUSH_TIMEOUT_MS="300")
+    r = subprocess.run([sys.executable, "-c", TIMEOUT_SCRIPT, ROOT], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-4000:]
