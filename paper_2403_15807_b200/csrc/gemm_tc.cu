@@ -402,6 +402,7 @@ cudaError_t tc_prepare(const GemmArgs &a, const GemmPlan &plan, cudaStream_t s, 
   p.xexp = bf ? a.xexp : 0;
   p.tile_step = 1;
   p.probe_div = 0;
+  p.probe_rows = 0;
   static const bool no_helpers = getenv("VRS_NO_HELPERS") != nullptr;   // (A/B only)
   p.no_helpers = no_helpers ? 1 : 0;
   p.min_span = tc_min_span();
@@ -473,6 +474,10 @@ cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &plan, void *scratch, 
     // (C2 sweep, r01_cells_probe_step.txt: Q = 4096, s = 10 %: step 2 beats 8 by 18 %; Q = 256, s = 100 %: 4 beats 16)
     static const int div_env = getenv("VRS_PROBE_DIV") ? atoi(getenv("VRS_PROBE_DIV")) : -1;
     pp.probe_div = div_env >= 0 ? div_env : (a.q >= 64 && probe_env <= 0 && !hbm_bound ? 8 : 0);
+    // partial probe tiles (rows by cp.async only, decided on the device): VRS_PROBE_ROWS rows per probed tile
+    static const int prow_env = getenv("VRS_PROBE_ROWS") ? atoi(getenv("VRS_PROBE_ROWS")) : 0;
+    static const int prow_q = getenv("VRS_PROBE_ROWS_Q") ? atoi(getenv("VRS_PROBE_ROWS_Q")) : 8;
+    pp.probe_rows = prow_env > 0 && a.q <= prow_q ? (std::min(prow_env, 256) + 7) / 8 * 8 : 0;
     // one wave: the probe's CTAs are few-tile items, so fixed per-CTA costs (prologue,
     // pipeline fill / drain) dominate over several waves -- use at most 148 / qtiles
     // splits (the same density: the step follows the main pass's span)

@@ -287,6 +287,9 @@ struct TcParams {
   int32_t P;               // splits
   int32_t tile_step;       // 1: every tile; PROBE_STEP: probe pass
   int32_t probe_div;       // probe: > 0 => step = clamp(main span / probe_div, 2, tile_step) (device-side span)
+  int32_t probe_rows;      // probe with rows by cp.async: > 0 => only the first probe_rows (a multiple of 8) rows of
+                           // each probed tile are fetched and scored (the others: zero-filled, masked) -- a
+                           // one-tile-per-CTA probe lasts as long as one SM needs to fetch the tile
   int32_t P_main, min_p_main;   // probe: the main pass's splits (its span sets the density); 0 = P
   int32_t g4;              // gather mode: 1 = TMA gather4 from X by id (tmap_g), 2 = cp.async from X by id
                            // (xrows), 0 = TMA tiles from the X_sel copy
@@ -540,6 +543,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // the X_sel copy's extra pass costs more than cp.async's lower streaming rate
   const bool cpg = gather && p.g4 == 2 && cp_fetch(n_sel, p.row_bytes, p.cp_min_bytes, p.cp_min_rows);
   const bool direct = cpg || (gather && p.g4 == 1);   // rows by id from X (no X_sel)
+  const int prow_lim = cpg && p.probe_rows > 0 ? p.probe_rows : BN;   // rows of a tile that count (probe_rows)
   const int64_t n_space = gather ? n_sel : p.n_rows;
   const int64_t row_tiles = (n_space + BN - 1) / BN;
   // splits actually used (splits_used): >= 4 row tiles per item when the
@@ -624,7 +628,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const int rl = 4 * u + (lane >> 3);   // row within this warp's part of the tile
             const int32_t id = __shfl_sync(0xffffffffu, rid[(4 * u) >> 5], rl & 31);   // (rl >> 5 == 4u >> 5)
             const int r = hrow + rl;
-            cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xs + (int64_t)id * rb + koff + c * 16, cvalid);
+            cpa16(bdst + r * 128 + ((c ^ (r & 7)) << 4), xs + (int64_t)id * rb + koff + c * 16,
+                  cvalid && rank * BROWS + r < prow_lim);
           }
           cpa_mbar_arrive(&full_bar[stage]);
           asm volatile("bar.sync 1, %0;" ::"n"(32 * NPW) : "memory");   // every producer warp registered its arrivals
@@ -815,6 +820,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         } else {
 #pragma unroll
           for (int u = 0; u < RPL; ++u) i8[u] = pos0 + u < n_sel ? __ldg(p.ids + pos0 + u) : -1;
+        }
+        if (lane * RPL >= prow_lim) {   // (probe_rows: rows past the limit were not fetched)
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) i8[u] = -1;
         }
         if (need_norm && direct) {   // by row id (dependent loads; the bias warp runs PF tiles ahead)
 #pragma unroll

@@ -15,14 +15,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SCRIPT = r'''
-import sys, numpy as np, torch
+import os, sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
 import oracle, paper_2403_15807_b200 as vrs
 from parity import check_topk_exact
 M = {oracle.L2: "l2", oracle.IP: "ip", oracle.COS: "cos"}
 refined = 0
 for seed in range(int(sys.argv[2])):
-    rng = np.random.default_rng(4000 + seed)
+    rng = np.random.default_rng(int(os.environ.get('VRS_FUZZ_BASE', '0')) + 4000 + seed)   # (soak runs: fresh seeds)
     n = int(rng.integers(2000, 60000))
     d = int(rng.choice([8, 64, 72, 128, 256, 320]))
     q = int(rng.choice([1, 5, 64, 128, 130, 300, 700]))
